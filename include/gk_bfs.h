@@ -1,0 +1,159 @@
+/*
+ * gk_bfs.h -- C ABI of the B200-native direction-optimizing BFS.
+ *
+ * This is the drop-in boundary for the reference's BFS hot path.  The
+ * reference (gapkit, header-only C++20) has no plugin registry or FFI: its
+ * "operator API" is the function
+ *
+ *     ParentArray gapkit::Bfs(const CsrGraph& g, NodeId source,
+ *                             const BfsOptions& opts = {});
+ *                                 (proj/include/gapkit/kernels/bfs.hpp:117-118)
+ *
+ * plus the CsrGraph it reads (proj/include/gapkit/graph.hpp:26-183).  The
+ * entry points below replace that call; the C++ wrapper in
+ * paper_1508_03619_b200/host/gapkit/ restores the exact reference
+ * signature on top of them.
+ *
+ * Conventions: plain pointers and sizes only; no entry point throws or
+ * aborts; every failure returns a gk_status and leaves a thread-local
+ * message for gk_last_error().  There is no CPU fallback: without a CUDA
+ * device every compute entry point returns GK_ERR_NO_DEVICE.
+ */
+#ifndef GK_BFS_H_
+#define GK_BFS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GK_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define GK_API __attribute__((visibility("default")))
+#else
+#define GK_API
+#endif
+
+typedef enum {
+  GK_OK = 0,
+  GK_ERR_SOURCE_RANGE = 1, /* bfs.hpp:120-121 ConfigError("bfs source out of range") */
+  GK_ERR_BAD_PARAM = 2,    /* bfs.hpp:122-123 ConfigError("bfs alpha and beta must be positive") */
+  GK_ERR_CUDA = 3,
+  GK_ERR_NCCL = 4,
+  GK_ERR_OOM = 5,
+  GK_ERR_NO_DEVICE = 6,
+  GK_ERR_INVALID = 7,      /* malformed graph / null handle / bad generator spec */
+  GK_ERR_TIMEOUT = 8,      /* device-side watchdog fired (never expected) */
+  GK_ERR_NO_EDGES = 9      /* source_picker.hpp:27-28 "cannot pick sources: graph has no edges" */
+} gk_status;
+
+/* BfsStrategy (bfs.hpp:37) */
+typedef enum {
+  GK_BFS_DIRECTION_OPTIMIZING = 0,
+  GK_BFS_TOP_DOWN_ONLY = 1,
+  GK_BFS_TOP_DOWN_RESCAN = 2
+} gk_bfs_strategy;
+
+/* Host view of a CsrGraph (graph.hpp:26-45).  For undirected graphs the
+ * in_* arrays must be NULL (they alias the out arrays, graph.hpp:64-67). */
+typedef struct {
+  int64_t num_nodes;
+  int32_t directed;
+  int32_t reserved;
+  const int64_t* out_offsets;    /* n+1, out_offsets[n] = m arcs */
+  const uint32_t* out_neighbors; /* m, each list sorted, no dups/self-loops */
+  const int64_t* in_offsets;     /* directed only */
+  const uint32_t* in_neighbors;  /* directed only */
+} gk_csr_view;
+
+/* One executed step of the direction loop (bfs.hpp:142-169). */
+typedef struct {
+  int32_t dir;            /* 'T' top-down or 'B' bottom-up */
+  int32_t pad;
+  int64_t frontier;       /* frontier size entering the step */
+  int64_t result;         /* T: scout count after the step; B: awake count */
+  int64_t edges_to_check; /* heuristic's unexplored-arc budget */
+} gk_step;
+
+typedef struct {
+  /* in */
+  gk_step* steps;          /* optional caller buffer for the step log */
+  int32_t max_steps;       /* capacity of steps */
+  int32_t want_counts;     /* fill reached / component_edges (untimed pass) */
+  /* out */
+  float device_ms;         /* CUDA-event time of the traversal kernel */
+  int32_t num_steps;       /* steps executed (may exceed max_steps) */
+  int64_t reached;         /* vertices with parent >= 0 */
+  int64_t component_edges; /* sum of out-degree over reached / (directed?1:2) */
+} gk_bfs_stats;
+
+typedef struct gk_graph gk_graph;
+
+/* Human-readable description of the last failure on this thread. */
+GK_API const char* gk_last_error(void);
+GK_API int gk_abi_version(void);
+/* Number of CUDA devices visible (0 without a GPU). */
+GK_API int gk_device_count(void);
+
+/* Upload a host CSR into HBM on `device` (untimed, like the reference's
+ * untimed build, benchmark.hpp:29-34).  Host arrays are only borrowed. */
+GK_API gk_status gk_graph_upload(const gk_csr_view* csr, int device, gk_graph** out);
+
+/* Generate + build on the device: bit-identical to
+ * GenerateKronecker / GenerateUniform (generator.hpp:56-112) followed by the
+ * optional seeded ID permutation and BuildCsr(el, false, true)
+ * (builder.hpp:54-186).  kind: 0 = Kronecker (A,B,C = .57,.19,.19),
+ * 1 = uniform.  scale in [1, 31]. */
+GK_API gk_status gk_graph_generate(int kind, int scale, int degree, uint64_t seed,
+                            int permute, int device, gk_graph** out);
+/* Road-like grid (config 4): rows x cols 4-neighbour grid, each edge
+ * deleted with p_delete, per-cell diagonal shortcut with p_diag. */
+GK_API gk_status gk_graph_generate_grid(int64_t rows, int64_t cols, double p_delete,
+                                 double p_diag, uint64_t seed, int device,
+                                 gk_graph** out);
+GK_API void gk_graph_free(gk_graph* g);
+
+GK_API gk_status gk_graph_info(const gk_graph* g, int64_t* num_nodes,
+                        int64_t* num_arcs, int32_t* directed);
+/* Copy the device CSR to host arrays (any may be NULL). */
+GK_API gk_status gk_graph_download(const gk_graph* g, int64_t* out_offsets,
+                            uint32_t* out_neighbors, int64_t* in_offsets,
+                            uint32_t* in_neighbors);
+
+/* PickSources(g, count, seed) (source_picker.hpp:47-54). */
+GK_API gk_status gk_pick_sources(const gk_graph* g, int64_t count, uint64_t seed,
+                          uint32_t* out);
+
+/* Bfs(g, source, {alpha, beta, strategy}) (bfs.hpp:117-177).
+ * parent_out: host array of num_nodes int32 (the reference's ParentArray),
+ *             or NULL to leave the result resident in HBM.
+ * depth_out:  optional host array of num_nodes int32 BFS depths (-1 =
+ *             unreached); requesting it adds depth stores to the kernel.
+ * stats:      optional.
+ * Calls on one handle are serialized; the graph is never modified. */
+GK_API gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta,
+                 int32_t strategy, int32_t* parent_out, int32_t* depth_out,
+                 gk_bfs_stats* stats);
+
+/* Device pointer to the parent array of the last gk_bfs on this handle
+ * (valid until the next call / free). */
+GK_API const int32_t* gk_bfs_device_parent(const gk_graph* g);
+
+/* Sector-aware (B_sec) and element-granular (B_use) algorithmic byte model
+ * of the last gk_bfs on this handle; that call must have
+ * requested depth_out or GK_KEEP_DEPTH via gk_bfs_keep_depth(). */
+GK_API gk_status gk_bfs_byte_model(gk_graph* g, const gk_step* steps,
+                            int32_t num_steps, double* b_sec, double* b_use);
+/* Keep depths on the device for subsequent gk_bfs calls (for the model). */
+GK_API gk_status gk_bfs_keep_depth(gk_graph* g, int32_t keep);
+
+/* Pinned host buffers for end-to-end transfers. */
+GK_API void* gk_host_alloc(int64_t bytes);
+GK_API void gk_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GK_BFS_H_ */

@@ -1,0 +1,181 @@
+// gk_aux.cu -- untimed auxiliary kernels: reached/component-edge counts and
+// the algorithmic byte model of SURVEY.md §8(d) (the roofline numerator).
+// Neither runs inside the timed traversal.
+#include <vector>
+
+#include "gk_internal.cuh"
+
+namespace gk {
+namespace {
+
+constexpr int kAuxBlock = 256;
+constexpr int kLocalLevels = 64;
+
+__device__ __forceinline__ unsigned long long sec_bytes(long long k) {
+  return 32ull * (unsigned long long)((4 * k + 31) / 32);
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T x, T* sm) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = x;
+  __syncthreads();
+  T t = 0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kAuxBlock / 32; i++) t += sm[i];
+  __syncthreads();
+  return t;
+}
+
+__global__ void k_count_reached(const int32_t* __restrict__ parent, const int64_t* __restrict__ off,
+                                int64_t n, unsigned long long* out) {
+  __shared__ unsigned long long sm[kAuxBlock / 32];
+  unsigned long long r = 0, d = 0;
+  for (long long v = (long long)blockIdx.x * kAuxBlock + threadIdx.x; v < n;
+       v += (long long)gridDim.x * kAuxBlock) {
+    if (parent[v] >= 0) {
+      r++;
+      d += (unsigned long long)(off[v + 1] - off[v]);
+    }
+  }
+  r = block_sum(r, sm);
+  d = block_sum(d, sm);
+  if (threadIdx.x == 0) {
+    atomicAdd(out, r);
+    atomicAdd(out + 1, d);
+  }
+}
+
+// Per-depth TD terms: acc[3*d+0] = |{depth==d}|, acc[3*d+1] = sum(36 + sec(deg)),
+// acc[3*d+2] = sum(12 + 4 deg).  Levels < kLocalLevels are privatised in smem.
+__global__ void k_model_levels(const int32_t* __restrict__ depth, const int64_t* __restrict__ off,
+                               int64_t n, int32_t nlev, unsigned long long* acc) {
+  __shared__ unsigned long long loc[kLocalLevels * 3];
+  for (int i = threadIdx.x; i < kLocalLevels * 3; i += kAuxBlock) loc[i] = 0;
+  __syncthreads();
+  for (long long v = (long long)blockIdx.x * kAuxBlock + threadIdx.x; v < n;
+       v += (long long)gridDim.x * kAuxBlock) {
+    const int d = depth[v];
+    if (d < 0 || d >= nlev) continue;
+    const long long deg = off[v + 1] - off[v];
+    const unsigned long long a = 36ull + sec_bytes(deg), b = 12ull + 4ull * deg;
+    if (d < kLocalLevels) {
+      atomicAdd(&loc[3 * d], 1ull);
+      atomicAdd(&loc[3 * d + 1], a);
+      atomicAdd(&loc[3 * d + 2], b);
+    } else {
+      atomicAdd(&acc[3 * d], 1ull);
+      atomicAdd(&acc[3 * d + 1], a);
+      atomicAdd(&acc[3 * d + 2], b);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kLocalLevels * 3 && i < nlev * 3; i += kAuxBlock)
+    if (loc[i]) atomicAdd(&acc[i], loc[i]);
+}
+
+// BU step i terms: sum over unvisited (depth -1 or > i) vertices with in-arcs
+// of (8 + sec(s_v)) and (8 + 4 s_v), s_v = arcs scanned to the first
+// in-neighbour at depth i (all when none).
+__global__ void k_model_bu(const int32_t* __restrict__ depth, const int64_t* __restrict__ in_off,
+                           const uint32_t* __restrict__ in_nb, int64_t n, int32_t lvl,
+                           unsigned long long* out) {
+  __shared__ unsigned long long sm[kAuxBlock / 32];
+  unsigned long long bs = 0, bu = 0;
+  for (long long v = (long long)blockIdx.x * kAuxBlock + threadIdx.x; v < n;
+       v += (long long)gridDim.x * kAuxBlock) {
+    const int d = depth[v];
+    if (d >= 0 && d <= lvl) continue;
+    const long long b = in_off[v], e = in_off[v + 1];
+    if (b == e) continue;
+    long long sv = e - b;
+    for (long long j = b; j < e; j++)
+      if (depth[in_nb[j]] == lvl) {
+        sv = j - b + 1;
+        break;
+      }
+    bs += 8ull + sec_bytes(sv);
+    bu += 8ull + 4ull * (unsigned long long)sv;
+  }
+  bs = block_sum(bs, sm);
+  bu = block_sum(bu, sm);
+  if (threadIdx.x == 0) {
+    atomicAdd(out, bs);
+    atomicAdd(out + 1, bu);
+  }
+}
+
+int aux_grid(int64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long want = (n + kAuxBlock - 1) / kAuxBlock;
+  long long cap = (long long)sms * 8;
+  return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace
+
+cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
+                          unsigned long long* d_out2, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(d_out2, 0, 2 * sizeof(unsigned long long), s);
+  if (e) return e;
+  k_count_reached<<<aux_grid(n), kAuxBlock, 0, s>>>(parent, off, n, d_out2);
+  return cudaGetLastError();
+}
+
+cudaError_t byte_model(const BfsParams& p, const int32_t* depth, const char* dirs, int32_t nsteps,
+                       unsigned long long* /*unused*/, double* b_sec, double* b_use,
+                       cudaStream_t s) {
+  const int32_t nlev = nsteps + 2;
+  unsigned long long* acc = nullptr;
+  size_t bytes = sizeof(unsigned long long) * (3 * (size_t)nlev + 2);
+  cudaError_t e = cudaMallocAsync(&acc, bytes, s);
+  if (e) return e;
+  cudaMemsetAsync(acc, 0, bytes, s);
+  k_model_levels<<<aux_grid(p.n), kAuxBlock, 0, s>>>(depth, p.out_off, p.n, nlev, acc);
+  std::vector<unsigned long long> lev(3 * (size_t)nlev + 2);
+  const double W = (double)((p.n + 7) / 8);
+  double bs = 4.0 * (double)p.n, bu = 4.0 * (double)p.n;
+  std::vector<double> bu_sec(nsteps, 0.0), bu_use(nsteps, 0.0);
+  unsigned long long* tail = acc + 3 * (size_t)nlev;
+  for (int i = 0; i < nsteps; i++) {
+    if (dirs[i] != 'B') continue;
+    cudaMemsetAsync(tail, 0, 2 * sizeof(unsigned long long), s);
+    k_model_bu<<<aux_grid(p.n), kAuxBlock, 0, s>>>(depth, p.in_off, p.in_nb, p.n, i, tail);
+    unsigned long long two[2];
+    e = cudaMemcpyAsync(two, tail, sizeof(two), cudaMemcpyDeviceToHost, s);
+    if (e) break;
+    cudaStreamSynchronize(s);
+    bu_sec[i] = (double)two[0];
+    bu_use[i] = (double)two[1];
+  }
+  if (!e) e = cudaMemcpyAsync(lev.data(), acc, lev.size() * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(acc, s);
+  if (e) return e;
+  auto cnt = [&](int d) { return (double)lev[3 * (size_t)d]; };
+  for (int i = 0; i < nsteps; i++) {
+    if (dirs[i] == 'T') {
+      bs += (double)lev[3 * (size_t)i + 1] + 36.0 * cnt(i + 1);
+      bu += (double)lev[3 * (size_t)i + 2] + 4.0 * cnt(i + 1);
+    } else {
+      if (i == 0 || dirs[i - 1] != 'B') {
+        bs += W + 4.0 * cnt(i);
+        bu += W + 4.0 * cnt(i);
+      }
+      bs += 3.0 * W + bu_sec[i];
+      bu += 3.0 * W + bu_use[i];
+      if (i + 1 == nsteps || dirs[i + 1] != 'B') {
+        bs += W + 4.0 * cnt(i + 1);
+        bu += W + 4.0 * cnt(i + 1);
+      }
+    }
+  }
+  *b_sec = bs;
+  *b_use = bu;
+  return cudaSuccess;
+}
+
+}  // namespace gk

@@ -1,0 +1,589 @@
+// gk_bfs_kernel.cu -- direction-optimizing BFS as ONE persistent kernel.
+//
+// Restates gapkit::Bfs (proj/include/gapkit/kernels/bfs.hpp:117-177) for
+// sm_100a.  The whole level loop runs on the device: one cooperative launch
+// of 148 x k CTAs, grid barriers between phases, and the reference's
+// alpha/beta direction decision (bfs.hpp:143-144, 153-154, 156, 158)
+// evaluated redundantly by every thread from counters reduced in L2.  No
+// host round trip per level, so high-diameter graphs pay ~a grid barrier
+// per level instead of a launch + sync.
+//
+// Phases (each ends at a grid barrier):
+//   init      parent[:] = -1, visited[:] = 0, parent[src] = src, queue = [src]
+//             (replaces the degree-encoding init bfs.hpp:126-132: the
+//             claim test uses a 1-bit visited map in L2 instead of the
+//             parent sign, and the claimed vertex's degree -- what the
+//             encoding carries -- is read from the offsets at claim time;
+//             scout = sum(max(deg,1)) is identical to sum(-old) of
+//             bfs.hpp:83)
+//   TD light  frontier tiles of 512 vertices, CTA-wide scan of degrees,
+//             load-balanced edge gather (bfs.hpp:68-91); vertices of degree
+//             > kHeavy are cut into kChunk-edge chunks instead
+//   TD heavy  chunks spread over all warps (hub expansion)
+//   q2b       QueueToBitmap (bfs.hpp:93-97)
+//   BU        one warp per 32-vertex bitmap word: visited-word skip, per-lane
+//             scan of the first 4 in-neighbours, then warp-ballot scans of
+//             the remaining lists; the first hit in ascending order is the
+//             parent exactly as bfs.hpp:55-60 picks it
+//   b2q       BitmapToQueue (bfs.hpp:99-113), CTA-aggregated appends
+//   rescan    kTopDownRescan's extra degree pass (bfs.hpp:161-167)
+#include <cooperative_groups.h>
+
+#include "gk_internal.cuh"
+
+namespace gk {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kQBuf = 256;         // per-warp queue staging (QueueBuffer analogue)
+constexpr int64_t kHeavy = 1024;   // degree above which a vertex is chunked
+constexpr int kChunk = 1024;       // edges per heavy chunk
+
+struct __align__(16) SmemT {
+  uint32_t qbuf[kWarps][kQBuf];
+  int64_t t_b[kBlock];
+  int64_t t_pre[kBlock];
+  uint32_t t_u[kBlock];
+  long long red[kWarps + 2];
+  unsigned long long bcast[4];
+  int ok;
+};
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// Sense-counting grid barrier with a watchdog.  The gpu-scope fences
+// order this CTA's stores before the arrival and invalidate the SM's L1
+// after the release, so plain loads after the barrier see every store made
+// before it.
+__device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& gen, unsigned& ph) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Ctrl* c = P.ctrl;
+    int ok = 1;
+    __threadfence();
+    if (blockIdx.x < 2048) c->cta_ph[blockIdx.x] = ph + 1;
+    unsigned arrived = atomicAdd(&c->bar_count, 1u);
+    if (arrived == gridDim.x - 1) {
+      atomicExch(&c->bar_count, 0u);
+      __threadfence();
+      c->cnt[(ph + 1) & 3][kTailSnap] = ld_volatile(&c->tail);
+      __threadfence();
+      atomicAdd(&c->bar_gen, 1u);
+    } else {
+      unsigned long long t0 = globaltimer();
+      while (ld_acquire(&c->bar_gen) == gen) {
+        __nanosleep(32);
+        if (*reinterpret_cast<volatile int*>(&c->error)) { ok = 0; break; }
+        if (globaltimer() - t0 > P.timeout_ns) {
+          atomicExch(&c->error, 2);
+          ok = 0;
+          break;
+        }
+      }
+    }
+    __threadfence();
+    if (*reinterpret_cast<volatile int*>(&c->error)) ok = 0;
+    s.ok = ok;
+    if (blockIdx.x == 0) {  // recycle the counter set two phases ahead
+      unsigned long long* z = c->cnt[(ph + 3) & 3];
+#pragma unroll
+      for (int i = 0; i < kSlots; i++) z[i] = 0;
+    }
+  }
+  __syncthreads();
+  gen++;
+  ph++;
+  return s.ok != 0;
+}
+
+// Exclusive scan of one int64 per thread across the CTA; *total gets the sum.
+__device__ int64_t block_exscan(int64_t x, int64_t* total, SmemT& s) {
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  int64_t incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= (unsigned)o) incl += y;
+  }
+  if (lane == 31) s.red[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < (unsigned)kWarps ? s.red[lane] : 0;
+    int64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(kFull, wi, o);
+      if (lane >= (unsigned)o) wi += y;
+    }
+    if (lane < (unsigned)kWarps) s.red[lane] = wi - w;
+    if (lane == kWarps - 1) s.red[kWarps] = wi;
+  }
+  __syncthreads();
+  int64_t r = s.red[warp] + incl - x;
+  *total = s.red[kWarps];
+  __syncthreads();
+  return r;
+}
+
+// CTA sum; one atomicAdd into the counter ring by thread 0.
+__device__ void block_add(long long x, unsigned long long* dst, SmemT& s) {
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(kFull, x, o);
+  if (lane == 0) s.red[warp] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int i = 0; i < kWarps; i++) t += s.red[i];
+    if (t) atomicAdd(dst, (unsigned long long)t);
+  }
+  __syncthreads();
+}
+
+// Per-warp staging buffer flushed with one fetch-add (QueueBuffer,
+// sliding_queue.hpp:62-86).  Must be called by all 32 lanes.
+__device__ __forceinline__ void wq_flush(const BfsParams& P, uint32_t* buf, int& qcnt) {
+  __syncwarp();
+  if (qcnt == 0) return;
+  unsigned long long base = 0;
+  if (lane_id() == 0) base = atomicAdd(&P.ctrl->tail, (unsigned long long)qcnt);
+  base = __shfl_sync(kFull, base, 0);
+  for (int i = lane_id(); i < qcnt; i += 32) P.queue[base + i] = buf[i];
+  __syncwarp();
+  qcnt = 0;
+}
+
+__device__ __forceinline__ void wq_push(const BfsParams& P, bool claim, uint32_t v,
+                                        uint32_t* buf, int& qcnt) {
+  unsigned mask = __ballot_sync(kFull, claim);
+  if (!mask) return;
+  if (claim) buf[qcnt + __popc(mask & lanemask_lt())] = v;
+  qcnt += __popc(mask);
+  if (qcnt > kQBuf - 32) wq_flush(P, buf, qcnt);
+}
+
+// Claim v for parent u (bfs.hpp:78-84).  The visited word is read from L2
+// first so already-visited targets cost no atomic.
+__device__ __forceinline__ bool try_claim(const BfsParams& P, uint32_t v) {
+  const uint32_t bit = 1u << (v & 31u);
+  uint32_t* w = P.visited + (v >> 5);
+  if (__ldcg(w) & bit) return false;
+  return (atomicOr(w, bit) & bit) == 0;
+}
+
+__device__ __forceinline__ void on_claim(const BfsParams& P, uint32_t u, uint32_t v, int lvl,
+                                         bool encode, long long& scout) {
+  P.parent[v] = (int32_t)u;
+  if (P.want_depth) P.depth[v] = lvl + 1;
+  if (encode) {
+    long long d = P.out_off[v + 1] - P.out_off[v];
+    scout += d ? d : 1;  // -old of the degree-encoded slot (bfs.hpp:83,130)
+  } else {
+    scout += 1;  // unencoded slot is -1 (bfs.hpp:129-130 with encode off)
+  }
+}
+
+// ---- top-down, light vertices + chunk registration ------------------------
+__device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, unsigned long long qs,
+                         unsigned long long qe, int lvl, bool encode, long long& scout,
+                         int& qcnt) {
+  uint32_t* buf = s.qbuf[threadIdx.x >> 5];
+  unsigned long long* cnt = P.ctrl->cnt[ph & 3];
+  for (;;) {
+    if (threadIdx.x == 0) s.bcast[1] = atomicAdd(&cnt[kTile], 1ull);
+    __syncthreads();
+    const unsigned long long start = qs + s.bcast[1] * (unsigned long long)kBlock;
+    __syncthreads();
+    if (start >= qe) break;
+    const unsigned long long i = start + threadIdx.x;
+    uint32_t u = 0;
+    int64_t b = 0, dl = 0;
+    if (i < qe) {
+      u = __ldcg(P.queue + i);
+      b = P.out_off[u];
+      const int64_t d = P.out_off[u + 1] - b;
+      if (d > kHeavy) {
+        const int64_t nch = (d + kChunk - 1) / kChunk;
+        const unsigned long long base = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
+        if ((int64_t)(base + nch) <= P.chunk_cap) {
+          for (int64_t c = 0; c < nch; c++) {
+            Chunk ch;
+            ch.u = u;
+            ch.start = b + c * kChunk;
+            ch.len = (uint32_t)((d - c * kChunk) < kChunk ? (d - c * kChunk) : kChunk);
+            P.chunks[base + c] = ch;
+          }
+        } else {
+          atomicExch(&P.ctrl->error, 3);
+        }
+      } else {
+        dl = d;
+      }
+    }
+    s.t_u[threadIdx.x] = u;
+    s.t_b[threadIdx.x] = b;
+    int64_t tot;
+    const int64_t pre = block_exscan(dl, &tot, s);
+    s.t_pre[threadIdx.x] = pre;
+    __syncthreads();
+    for (int64_t eb = 0; eb < tot; eb += kBlock) {
+      const int64_t ei = eb + threadIdx.x;
+      bool claim = false;
+      uint32_t v = 0;
+      if (ei < tot) {
+        int lo = 0, hi = kBlock - 1;  // last k with t_pre[k] <= ei
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s.t_pre[mid] <= ei) lo = mid;
+          else hi = mid - 1;
+        }
+        const uint32_t uu = s.t_u[lo];
+        v = __ldg(P.out_nb + s.t_b[lo] + (ei - s.t_pre[lo]));
+        claim = try_claim(P, v);
+        if (claim) on_claim(P, uu, v, lvl, encode, scout);
+      }
+      wq_push(P, claim, v, buf, qcnt);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- top-down, heavy chunks: one warp per chunk, 4 loads in flight --------
+__device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, unsigned long long nch,
+                         int lvl, bool encode, long long& scout, int& qcnt) {
+  uint32_t* buf = s.qbuf[threadIdx.x >> 5];
+  unsigned long long* cnt = P.ctrl->cnt[ph & 3];
+  const unsigned lane = lane_id();
+  for (;;) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(&cnt[kChunkNext], 1ull);
+    c = __shfl_sync(kFull, c, 0);
+    if (c >= nch) break;
+    const Chunk ch = P.chunks[c];
+    for (uint32_t o = 0; o < ch.len; o += 128) {
+      uint32_t v[4];
+      bool ok[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint32_t j = o + lane + 32u * k;
+        ok[k] = j < ch.len;
+        v[k] = ok[k] ? __ldg(P.out_nb + ch.start + j) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        bool claim = ok[k] && try_claim(P, v[k]);
+        if (claim) on_claim(P, ch.u, v[k], lvl, encode, scout);
+        wq_push(P, claim, v[k], buf, qcnt);
+      }
+    }
+  }
+}
+
+// ---- bottom-up sweep (bfs.hpp:47-66) ---------------------------------------
+__device__ void bu_step(const BfsParams& P, const uint32_t* front, uint32_t* next, int lvl,
+                        long long& awake) {
+  const unsigned lane = lane_id();
+  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  for (long long w = gw; w < P.w32; w += nw) {
+    const uint32_t vis = __ldcg(P.visited + w);
+    const uint32_t v = (uint32_t)(w * 32 + lane);
+    bool pend = ((int64_t)v < P.n) && !((vis >> lane) & 1u);
+    if (__ballot_sync(kFull, pend) == 0) {
+      if (lane == 0) next[w] = 0;
+      continue;
+    }
+    bool found = false, dead = false;
+    uint32_t par = 0;
+    int64_t b = 0, e = 0;
+    if (pend) {
+      b = P.in_off[v];
+      e = P.in_off[v + 1];
+      if (b == e) {  // no in-edges: can never be reached; skip it from now on
+        dead = true;
+        pend = false;
+      }
+    }
+    if (pend) {  // first <= 4 in-neighbours, loads issued together
+      const int64_t k = e - b;
+      uint32_t u0 = __ldg(P.in_nb + b);
+      uint32_t u1 = k > 1 ? __ldg(P.in_nb + b + 1) : 0u;
+      uint32_t u2 = k > 2 ? __ldg(P.in_nb + b + 2) : 0u;
+      uint32_t u3 = k > 3 ? __ldg(P.in_nb + b + 3) : 0u;
+      const bool h0 = (front[u0 >> 5] >> (u0 & 31u)) & 1u;
+      const bool h1 = k > 1 && ((front[u1 >> 5] >> (u1 & 31u)) & 1u);
+      const bool h2 = k > 2 && ((front[u2 >> 5] >> (u2 & 31u)) & 1u);
+      const bool h3 = k > 3 && ((front[u3 >> 5] >> (u3 & 31u)) & 1u);
+      if (h0) { found = true; par = u0; }
+      else if (h1) { found = true; par = u1; }
+      else if (h2) { found = true; par = u2; }
+      else if (h3) { found = true; par = u3; }
+      if (found) {
+        pend = false;
+      } else {
+        b += k < 4 ? k : 4;
+        pend = b < e;
+      }
+    }
+    unsigned pm = __ballot_sync(kFull, pend);
+    while (pm) {  // warp-cooperative scan of one long list at a time
+      const int l = __ffs(pm) - 1;
+      pm &= pm - 1;
+      const int64_t lb = __shfl_sync(kFull, b, l);
+      const int64_t le = __shfl_sync(kFull, e, l);
+      for (int64_t j = lb; j < le; j += 32) {
+        const int64_t jj = j + lane;
+        bool h = false;
+        uint32_t u = 0;
+        if (jj < le) {
+          u = __ldg(P.in_nb + jj);
+          h = (front[u >> 5] >> (u & 31u)) & 1u;
+        }
+        const unsigned bal = __ballot_sync(kFull, h);
+        if (bal) {
+          const uint32_t hu = __shfl_sync(kFull, u, __ffs(bal) - 1);
+          if ((int)lane == l) {
+            found = true;
+            par = hu;
+          }
+          break;
+        }
+      }
+    }
+    if (found) {
+      P.parent[v] = (int32_t)par;
+      if (P.want_depth) P.depth[v] = lvl + 1;
+    }
+    const unsigned nbits = __ballot_sync(kFull, found);
+    const unsigned dbits = __ballot_sync(kFull, dead);
+    if (lane == 0) {
+      next[w] = nbits;
+      if (nbits | dbits) P.visited[w] = vis | nbits | dbits;
+      awake += __popc(nbits);
+    }
+  }
+}
+
+// ---- BitmapToQueue (bfs.hpp:99-113) ----------------------------------------
+__device__ void b2q(const BfsParams& P, const uint32_t* front, SmemT& s) {
+  for (long long base = (long long)blockIdx.x * kBlock; base < P.w32;
+       base += (long long)gridDim.x * kBlock) {
+    const long long w = base + threadIdx.x;
+    uint32_t word = w < P.w32 ? __ldcg(front + w) : 0u;
+    int64_t tot;
+    const int64_t pre = block_exscan(__popc(word), &tot, s);
+    if (tot == 0) continue;
+    if (threadIdx.x == 0) s.bcast[0] = atomicAdd(&P.ctrl->tail, (unsigned long long)tot);
+    __syncthreads();
+    unsigned long long q = s.bcast[0] + pre;
+    while (word) {
+      const int bp = __ffs(word) - 1;
+      word &= word - 1;
+      P.queue[q++] = (uint32_t)(w * 32 + bp);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void log_step(const BfsParams& P, long long idx, int dir, long long frontier,
+                         long long result, long long etc) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && idx < P.step_cap) {
+    gk_step st;
+    st.dir = dir;
+    st.pad = 0;
+    st.frontier = frontier;
+    st.result = result;
+    st.edges_to_check = etc;
+    P.steps[idx] = st;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
+  extern __shared__ uint4 dyn_smem[];
+  __shared__ SmemT s;
+  unsigned gen = 0, ph = 0;
+  const long long gtid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long gthreads = (long long)gridDim.x * kBlock;
+  const uint32_t src = P.src;
+
+  // ---- init (timed; replaces bfs.hpp:126-138) ----
+  {
+    const long long n4 = P.n >> 2;
+    int4* p4 = reinterpret_cast<int4*>(P.parent);
+    int4* d4 = reinterpret_cast<int4*>(P.depth);
+    for (long long i = gtid; i < n4; i += gthreads) {
+      int4 val = make_int4(-1, -1, -1, -1);
+      int4 dv = val;
+      if ((long long)(src >> 2) == i) {
+        reinterpret_cast<int*>(&val)[src & 3] = (int)src;
+        reinterpret_cast<int*>(&dv)[src & 3] = 0;
+      }
+      p4[i] = val;
+      if (P.want_depth) d4[i] = dv;
+    }
+    for (long long i = (n4 << 2) + gtid; i < P.n; i += gthreads) {
+      P.parent[i] = i == (long long)src ? (int)src : -1;
+      if (P.want_depth) P.depth[i] = i == (long long)src ? 0 : -1;
+    }
+    for (long long i = gtid; i < P.w32; i += gthreads)
+      P.visited[i] = (long long)(src >> 5) == i ? (1u << (src & 31u)) : 0u;
+    if (gtid == 0) {
+      P.queue[0] = src;
+      P.ctrl->tail = 1;
+    }
+  }
+  if (!grid_sync(P, s, gen, ph)) return;
+
+  const bool encode = P.strategy != GK_BFS_TOP_DOWN_RESCAN;
+  unsigned long long qs = 0, qe = 1;
+  long long etc = P.m;                                  // bfs.hpp:139
+  long long scout = P.out_off[src + 1] - P.out_off[src];  // bfs.hpp:140
+  long long nsteps = 0;
+  int lvl = 0;
+  int qcnt = 0;
+  uint32_t* frontg = P.bm0;
+  uint32_t* nextg = P.bm1;
+  uint32_t* sfront = reinterpret_cast<uint32_t*>(dyn_smem);
+
+  while (qe > qs) {
+    if (P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha) {
+      // QueueToBitmap into a cleared front (bfs.hpp:145)
+      for (long long i = gtid; i < P.w32; i += gthreads) frontg[i] = 0u;
+      if (!grid_sync(P, s, gen, ph)) return;
+      for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
+        const uint32_t v = __ldcg(P.queue + i);
+        atomicOr(frontg + (v >> 5), 1u << (v & 31u));
+      }
+      if (!grid_sync(P, s, gen, ph)) return;
+      long long awake = (long long)(qe - qs);  // bfs.hpp:146
+      qs = qe;                                 // bfs.hpp:147
+      long long old_awake;
+      do {  // bfs.hpp:149-154
+        old_awake = awake;
+        const uint32_t* fr = frontg;
+        if (P.front_in_smem) {
+          for (long long i = threadIdx.x; i < P.w32; i += kBlock) sfront[i] = __ldcg(frontg + i);
+          __syncthreads();
+          fr = sfront;
+        }
+        long long acc = 0;
+        bu_step(P, fr, nextg, lvl, acc);
+        const unsigned set = ph & 3;
+        block_add(acc, &P.ctrl->cnt[set][kSum], s);
+        if (!grid_sync(P, s, gen, ph)) return;
+        awake = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        log_step(P, nsteps++, 'B', old_awake, awake, etc);
+        lvl++;
+        uint32_t* t = frontg;
+        frontg = nextg;
+        nextg = t;
+      } while (awake >= old_awake || awake > P.n / P.beta);
+      b2q(P, frontg, s);  // bfs.hpp:155
+      if (!grid_sync(P, s, gen, ph)) return;
+      qe = ld_volatile(&P.ctrl->cnt[ph & 3][kTailSnap]);
+      scout = 1;  // bfs.hpp:156
+    } else {
+      etc -= scout;  // bfs.hpp:158
+      const long long fsize = (long long)(qe - qs);
+      long long sacc = 0;
+      td_light(P, s, ph, qs, qe, lvl, encode, sacc, qcnt);
+      wq_flush(P, s.qbuf[threadIdx.x >> 5], qcnt);
+      unsigned set = ph & 3;
+      block_add(sacc, &P.ctrl->cnt[set][kSum], s);
+      if (!grid_sync(P, s, gen, ph)) return;
+      scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+      const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
+      if (nch) {
+        sacc = 0;
+        td_heavy(P, s, ph, nch, lvl, encode, sacc, qcnt);
+        wq_flush(P, s.qbuf[threadIdx.x >> 5], qcnt);
+        set = ph & 3;
+        block_add(sacc, &P.ctrl->cnt[set][kSum], s);
+        if (!grid_sync(P, s, gen, ph)) return;
+        scout += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+      }
+      qs = qe;  // SlideWindow (bfs.hpp:160)
+      qe = ld_volatile(&P.ctrl->cnt[ph & 3][kTailSnap]);
+      if (P.strategy == GK_BFS_TOP_DOWN_RESCAN) {  // bfs.hpp:161-167
+        long long tot = 0;
+        for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
+          const uint32_t u = __ldcg(P.queue + i);
+          tot += P.out_off[u + 1] - P.out_off[u];
+        }
+        set = ph & 3;
+        block_add(tot, &P.ctrl->cnt[set][kSum], s);
+        if (!grid_sync(P, s, gen, ph)) return;
+        scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+      }
+      log_step(P, nsteps++, 'T', fsize, scout, etc);
+      lvl++;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->num_steps = nsteps;
+  // bfs.hpp:171-175's final sweep is unnecessary: unreached slots were
+  // written -1 by init and never touched.
+}
+
+}  // namespace
+
+cudaError_t bfs_configure(int device, BfsLaunch* cfg) {
+  cudaError_t e;
+  int sms = 0, optin = 0, coop = 0;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device))) return e;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device))) return e;
+  if ((e = cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device))) return e;
+  if (!coop) return cudaErrorNotSupported;
+  cfg->smem_static = sizeof(SmemT);
+  // Stage the front bitmap in shared memory when it fits next to the
+  // static part at 1 CTA/SM; otherwise it is read through L1/L2.
+  const size_t budget = (size_t)optin > cfg->smem_static + 1024 ? optin - cfg->smem_static - 1024 : 0;
+  cfg->smem_front_max = budget & ~size_t(15);
+  if ((e = cudaFuncSetAttribute(bfs_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)cfg->smem_front_max)))
+    return e;
+  int occ = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bfs_persistent, kBlock, 0))) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  cfg->grid = sms * occ;
+  cfg->block = kBlock;
+  return cudaSuccess;
+}
+
+cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st) {
+  size_t dyn = 0;
+  int grid = cfg.grid;
+  if (p.front_in_smem) {
+    dyn = ((size_t)p.w32 * 4 + 15) & ~size_t(15);
+    int occ = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bfs_persistent, kBlock, dyn);
+    if (e) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    grid = sms * occ;
+  }
+  BfsParams local = p;
+  void* args[] = {&local};
+  return cudaLaunchCooperativeKernel((const void*)bfs_persistent, dim3(grid), dim3(cfg.block), args,
+                                     dyn, st);
+}
+
+}  // namespace gk

@@ -1,0 +1,397 @@
+// gk_capi.cu -- the C ABI of include/gk_bfs.h.
+//
+// Every entry point catches failures and returns a gk_status with a
+// thread-local message; nothing throws across the boundary.  There is no
+// CPU path: without a device, compute entry points fail with
+// GK_ERR_NO_DEVICE.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gk_internal.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+gk_status fail(gk_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+gk_status cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation)
+    return fail(GK_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+    return fail(GK_ERR_NO_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+  return fail(GK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call, what)                       \
+  do {                                       \
+    cudaError_t e_ = (call);                 \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+gk_status need_device(int device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(GK_ERR_NO_DEVICE, "no CUDA device available (libgk_bfs has no CPU fallback)");
+  if (device < 0 || device >= n) return fail(GK_ERR_INVALID, "device index out of range");
+  CK(cudaSetDevice(device), "cudaSetDevice");
+  return GK_OK;
+}
+
+void free_graph(gk_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  if (g->in_off && g->in_off != g->out_off) cudaFree(g->in_off);
+  if (g->in_nb && g->in_nb != g->out_nb) cudaFree(g->in_nb);
+  cudaFree(g->out_off);
+  cudaFree(g->out_nb);
+  cudaFree(g->parent);
+  cudaFree(g->depth);
+  cudaFree(g->visited);
+  cudaFree(g->bm0);
+  cudaFree(g->bm1);
+  cudaFree(g->queue);
+  cudaFree(g->chunks);
+  cudaFree(g->ctrl);
+  cudaFree(g->steps);
+  cudaFree(g->acc);
+  if (g->ev0) cudaEventDestroy(g->ev0);
+  if (g->ev1) cudaEventDestroy(g->ev1);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+// Workspace sized for n vertices / m arcs; reused across trials and
+// re-initialised inside the timed kernel.
+gk_status alloc_workspace(gk_graph* g) {
+  const int64_t n = g->n;
+  const int64_t w32 = (n + 31) / 32;
+  const size_t wbytes = ((size_t)w32 * 4 + 15) & ~size_t(15);
+  CK(cudaMalloc(&g->parent, sizeof(int32_t) * std::max<int64_t>(n, 4) + 16), "alloc parent");
+  CK(cudaMalloc(&g->visited, wbytes + 16), "alloc visited");
+  CK(cudaMalloc(&g->bm0, wbytes + 16), "alloc bitmap");
+  CK(cudaMalloc(&g->bm1, wbytes + 16), "alloc bitmap");
+  CK(cudaMalloc(&g->queue, sizeof(uint32_t) * (n + 1)), "alloc queue");
+  g->chunk_cap = 2 * (g->m / 1024) + 64;
+  CK(cudaMalloc(&g->chunks, sizeof(gk::Chunk) * g->chunk_cap), "alloc chunks");
+  CK(cudaMalloc(&g->ctrl, sizeof(gk::Ctrl)), "alloc ctrl");
+  g->step_cap = std::min<int64_t>(n + 2, int64_t(1) << 20);
+  CK(cudaMalloc(&g->steps, sizeof(gk_step) * g->step_cap), "alloc step log");
+  CK(cudaMalloc(&g->acc, sizeof(unsigned long long) * 8), "alloc acc");
+  CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking), "stream");
+  CK(cudaEventCreate(&g->ev0), "event");
+  CK(cudaEventCreate(&g->ev1), "event");
+  CK(gk::bfs_configure(g->device, &g->launch), "configure bfs kernel");
+  return GK_OK;
+}
+
+gk_status finish_graph(gk_graph* g, gk_graph** out) {
+  gk_status st = alloc_workspace(g);
+  if (st != GK_OK) {
+    free_graph(g);
+    return st;
+  }
+  *out = g;
+  return GK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gk_last_error(void) { return g_last_error.c_str(); }
+int gk_abi_version(void) { return GK_ABI_VERSION; }
+
+int gk_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+gk_status gk_graph_upload(const gk_csr_view* csr, int device, gk_graph** out) {
+  if (!csr || !out || !csr->out_offsets || csr->num_nodes < 0)
+    return fail(GK_ERR_INVALID, "gk_graph_upload: null argument");
+  if (csr->num_nodes > (int64_t(1) << 32))
+    return fail(GK_ERR_INVALID, "gk_graph_upload: more than 2^32 vertices (NodeId is 32-bit)");
+  if (csr->directed && (!csr->in_offsets || (!csr->in_neighbors && csr->out_offsets[csr->num_nodes])))
+    return fail(GK_ERR_INVALID, "gk_graph_upload: directed graph needs in_* arrays");
+  gk_status st = need_device(device);
+  if (st != GK_OK) return st;
+  auto* g = new gk_graph;
+  g->device = device;
+  g->n = csr->num_nodes;
+  g->m = csr->out_offsets[csr->num_nodes];
+  g->directed = csr->directed ? 1 : 0;
+  const size_t ob = sizeof(int64_t) * (g->n + 1), nbb = sizeof(uint32_t) * std::max<int64_t>(g->m, 1);
+  cudaError_t e;
+  if ((e = cudaMalloc(&g->out_off, ob)) || (e = cudaMalloc(&g->out_nb, nbb)) ||
+      (e = cudaMemcpy(g->out_off, csr->out_offsets, ob, cudaMemcpyHostToDevice)) ||
+      (g->m && (e = cudaMemcpy(g->out_nb, csr->out_neighbors, sizeof(uint32_t) * g->m,
+                               cudaMemcpyHostToDevice)))) {
+    free_graph(g);
+    return cuda_fail(e, "upload CSR");
+  }
+  if (g->directed) {
+    if ((e = cudaMalloc(&g->in_off, ob)) || (e = cudaMalloc(&g->in_nb, nbb)) ||
+        (e = cudaMemcpy(g->in_off, csr->in_offsets, ob, cudaMemcpyHostToDevice)) ||
+        (g->m && (e = cudaMemcpy(g->in_nb, csr->in_neighbors, sizeof(uint32_t) * g->m,
+                                 cudaMemcpyHostToDevice)))) {
+      free_graph(g);
+      return cuda_fail(e, "upload in-CSR");
+    }
+  } else {
+    g->in_off = g->out_off;  // graph.hpp:64-67: in aliases out when undirected
+    g->in_nb = g->out_nb;
+  }
+  return finish_graph(g, out);
+}
+
+gk_status gk_graph_generate(int kind, int scale, int degree, uint64_t seed, int permute,
+                            int device, gk_graph** out) {
+  if (!out) return fail(GK_ERR_INVALID, "gk_graph_generate: null out");
+  if (kind != 0 && kind != 1) return fail(GK_ERR_INVALID, "generator kind must be 0 (kron) or 1 (urand)");
+  if (scale < 1 || scale > 31) return fail(GK_ERR_INVALID, "generator scale must be in [1, 31]");
+  if (degree < 1) return fail(GK_ERR_INVALID, "generator avg_degree must be >= 1");
+  gk_status st = need_device(device);
+  if (st != GK_OK) return st;
+  gk::DevCsr csr;
+  std::string err;
+  cudaError_t e = gk::build_generated(kind, scale, degree, seed, permute, &csr, &err);
+  if (e != cudaSuccess) return cuda_fail(e, err.empty() ? "device graph build" : err.c_str());
+  auto* g = new gk_graph;
+  g->device = device;
+  g->n = csr.n;
+  g->m = csr.m;
+  g->out_off = g->in_off = csr.off;
+  g->out_nb = g->in_nb = csr.nb;
+  return finish_graph(g, out);
+}
+
+gk_status gk_graph_generate_grid(int64_t rows, int64_t cols, double p_delete, double p_diag,
+                                 uint64_t seed, int device, gk_graph** out) {
+  if (!out) return fail(GK_ERR_INVALID, "gk_graph_generate_grid: null out");
+  if (rows < 1 || cols < 1 || rows * cols > (int64_t(1) << 31))
+    return fail(GK_ERR_INVALID, "grid dimensions out of range");
+  if (!(p_delete >= 0 && p_delete <= 1 && p_diag >= 0 && p_diag <= 1))
+    return fail(GK_ERR_INVALID, "grid probabilities must be in [0, 1]");
+  gk_status st = need_device(device);
+  if (st != GK_OK) return st;
+  gk::DevCsr csr;
+  std::string err;
+  cudaError_t e = gk::build_grid(rows, cols, p_delete, p_diag, seed, &csr, &err);
+  if (e != cudaSuccess) return cuda_fail(e, err.empty() ? "device grid build" : err.c_str());
+  auto* g = new gk_graph;
+  g->device = device;
+  g->n = csr.n;
+  g->m = csr.m;
+  g->out_off = g->in_off = csr.off;
+  g->out_nb = g->in_nb = csr.nb;
+  return finish_graph(g, out);
+}
+
+void gk_graph_free(gk_graph* g) { free_graph(g); }
+
+gk_status gk_graph_info(const gk_graph* g, int64_t* n, int64_t* m, int32_t* directed) {
+  if (!g) return fail(GK_ERR_INVALID, "null graph");
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (directed) *directed = g->directed;
+  return GK_OK;
+}
+
+gk_status gk_graph_download(const gk_graph* g, int64_t* out_offsets, uint32_t* out_neighbors,
+                            int64_t* in_offsets, uint32_t* in_neighbors) {
+  if (!g) return fail(GK_ERR_INVALID, "null graph");
+  CK(cudaSetDevice(g->device), "cudaSetDevice");
+  const size_t ob = sizeof(int64_t) * (g->n + 1), nbb = sizeof(uint32_t) * g->m;
+  if (out_offsets) CK(cudaMemcpy(out_offsets, g->out_off, ob, cudaMemcpyDeviceToHost), "download");
+  if (out_neighbors && g->m) CK(cudaMemcpy(out_neighbors, g->out_nb, nbb, cudaMemcpyDeviceToHost), "download");
+  if (in_offsets) CK(cudaMemcpy(in_offsets, g->in_off, ob, cudaMemcpyDeviceToHost), "download");
+  if (in_neighbors && g->m) CK(cudaMemcpy(in_neighbors, g->in_nb, nbb, cudaMemcpyDeviceToHost), "download");
+  return GK_OK;
+}
+
+// source_picker.hpp:22-54: Rng(seed) draws NextBounded(n), rejecting
+// zero out-degree candidates; degrees are read from the device offsets.
+gk_status gk_pick_sources(const gk_graph* g, int64_t count, uint64_t seed, uint32_t* out) {
+  if (!g || (!out && count > 0)) return fail(GK_ERR_INVALID, "null argument");
+  if (g->m == 0) return fail(GK_ERR_NO_EDGES, "cannot pick sources: graph has no edges");
+  CK(cudaSetDevice(g->device), "cudaSetDevice");
+  auto mix = [](uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+  };
+  uint64_t state = mix(seed) ^ mix(~0ULL);
+  auto next = [&]() {
+    state += 0x9e3779b97f4a7c15ULL;
+    return mix(state - 0x9e3779b97f4a7c15ULL);
+  };
+  const uint32_t bound = (uint32_t)g->n;
+  uint32_t mask = bound - 1;
+  mask |= mask >> 1;
+  mask |= mask >> 2;
+  mask |= mask >> 4;
+  mask |= mask >> 8;
+  mask |= mask >> 16;
+  for (int64_t i = 0; i < count; i++) {
+    for (;;) {
+      uint32_t c;
+      do {
+        c = (uint32_t)(next() >> 32) & mask;
+      } while (c >= bound);
+      int64_t o[2];
+      CK(cudaMemcpy(o, g->out_off + c, sizeof(o), cudaMemcpyDeviceToHost), "read degree");
+      if (o[1] != o[0]) {
+        out[i] = c;
+        break;
+      }
+    }
+  }
+  return GK_OK;
+}
+
+gk_status gk_bfs_keep_depth(gk_graph* g, int32_t keep) {
+  if (!g) return fail(GK_ERR_INVALID, "null graph");
+  g->keep_depth = keep ? 1 : 0;
+  return GK_OK;
+}
+
+gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int32_t strategy,
+                 int32_t* parent_out, int32_t* depth_out, gk_bfs_stats* stats) {
+  if (!g) return fail(GK_ERR_INVALID, "null graph");
+  // bfs.hpp:120-123, same order and messages
+  if ((int64_t)source >= g->n) return fail(GK_ERR_SOURCE_RANGE, "bfs source out of range");
+  if (alpha <= 0 || beta <= 0) return fail(GK_ERR_BAD_PARAM, "bfs alpha and beta must be positive");
+  if (strategy < 0 || strategy > 2) return fail(GK_ERR_BAD_PARAM, "unknown bfs strategy");
+  std::lock_guard<std::mutex> lock(g->mu);
+  CK(cudaSetDevice(g->device), "cudaSetDevice");
+  const int want_depth = (depth_out != nullptr) || g->keep_depth;
+  if (want_depth && !g->depth)
+    CK(cudaMalloc(&g->depth, sizeof(int32_t) * std::max<int64_t>(g->n, 4) + 16), "alloc depth");
+
+  gk::BfsParams p{};
+  p.n = g->n;
+  p.m = g->m;
+  p.w32 = (g->n + 31) / 32;
+  p.out_off = g->out_off;
+  p.out_nb = g->out_nb;
+  p.in_off = g->in_off;
+  p.in_nb = g->in_nb;
+  p.src = source;
+  p.strategy = strategy;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.want_depth = want_depth;
+  p.front_in_smem = ((size_t)p.w32 * 4 <= g->launch.smem_front_max) ? 1 : 0;
+  p.parent = g->parent;
+  p.depth = g->depth;
+  p.visited = g->visited;
+  p.bm0 = g->bm0;
+  p.bm1 = g->bm1;
+  p.queue = g->queue;
+  p.chunks = g->chunks;
+  p.chunk_cap = g->chunk_cap;
+  p.ctrl = g->ctrl;
+  p.steps = g->steps;
+  p.step_cap = g->step_cap;
+  p.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
+
+  cudaStream_t s = g->stream;
+  CK(cudaEventRecord(g->ev0, s), "event record");
+  CK(cudaMemsetAsync(g->ctrl, 0, sizeof(gk::Ctrl), s), "reset ctrl");
+  CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
+  CK(cudaEventRecord(g->ev1, s), "event record");
+  gk::Ctrl ctrl;
+  CK(cudaMemcpyAsync(&ctrl, g->ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
+  CK(cudaStreamSynchronize(s), "bfs kernel");
+  g->depth_valid = want_depth;
+  if (ctrl.error) {
+    if (ctrl.error == 2) {
+      unsigned lo = ~0u, hi = 0;
+      for (int i = 0; i < 2048; i++) {
+        if (ctrl.cta_ph[i] == 0) continue;
+        lo = std::min(lo, ctrl.cta_ph[i]);
+        hi = std::max(hi, ctrl.cta_ph[i]);
+      }
+      char buf[256];
+      snprintf(buf, sizeof(buf),
+               "bfs kernel watchdog fired (grid barrier timeout): CTA barrier counts min %u max %u, "
+               "arrived %u, gen %u, tail %llu",
+               lo, hi, ctrl.bar_count, ctrl.bar_gen, (unsigned long long)ctrl.tail);
+      return fail(GK_ERR_TIMEOUT, buf);
+    }
+    return fail(GK_ERR_CUDA, "bfs kernel: heavy-chunk buffer overflow");
+  }
+  if (stats) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1), "event time");
+    stats->device_ms = ms;
+    stats->num_steps = (int32_t)ctrl.num_steps;
+    if (stats->steps && stats->max_steps > 0) {
+      int64_t k = std::min<int64_t>({(int64_t)stats->max_steps, ctrl.num_steps, g->step_cap});
+      if (k > 0)
+        CK(cudaMemcpy(stats->steps, g->steps, sizeof(gk_step) * k, cudaMemcpyDeviceToHost), "read steps");
+    }
+    if (stats->want_counts) {
+      CK(gk::count_reached(g->parent, g->out_off, g->n, g->acc, s), "count reached");
+      unsigned long long two[2];
+      CK(cudaMemcpyAsync(two, g->acc, sizeof(two), cudaMemcpyDeviceToHost, s), "read counts");
+      CK(cudaStreamSynchronize(s), "count reached");
+      stats->reached = (int64_t)two[0];
+      stats->component_edges = (int64_t)(g->directed ? two[1] : two[1] / 2);
+    }
+  }
+  if (parent_out && g->n)
+    CK(cudaMemcpyAsync(parent_out, g->parent, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, s), "D2H parent");
+  if (depth_out && g->n)
+    CK(cudaMemcpyAsync(depth_out, g->depth, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, s), "D2H depth");
+  if (parent_out || depth_out) CK(cudaStreamSynchronize(s), "D2H");
+  return GK_OK;
+}
+
+const int32_t* gk_bfs_device_parent(const gk_graph* g) { return g ? g->parent : nullptr; }
+
+gk_status gk_bfs_byte_model(gk_graph* g, const gk_step* steps, int32_t num_steps, double* b_sec,
+                            double* b_use) {
+  if (!g || !b_sec || !b_use || (num_steps > 0 && !steps)) return fail(GK_ERR_INVALID, "null argument");
+  if (!g->depth || !g->depth_valid)
+    return fail(GK_ERR_INVALID, "byte model needs the last gk_bfs to record depths");
+  std::lock_guard<std::mutex> lock(g->mu);
+  CK(cudaSetDevice(g->device), "cudaSetDevice");
+  std::vector<char> dirs(std::max(num_steps, 1));
+  for (int i = 0; i < num_steps; i++) dirs[i] = (char)steps[i].dir;
+  gk::BfsParams p{};
+  p.n = g->n;
+  p.out_off = g->out_off;
+  p.out_nb = g->out_nb;
+  p.in_off = g->in_off;
+  p.in_nb = g->in_nb;
+  CK(gk::byte_model(p, g->depth, dirs.data(), num_steps, nullptr, b_sec, b_use, g->stream), "byte model");
+  return GK_OK;
+}
+
+void* gk_host_alloc(int64_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocDefault) != cudaSuccess) {
+    g_last_error = "cudaHostAlloc failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void gk_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+}  // extern "C"

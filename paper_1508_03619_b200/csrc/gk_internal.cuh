@@ -1,0 +1,145 @@
+// gk_internal.cuh -- shared device/host internals of libgk_bfs.so.
+//
+// Layout in HBM (one gk_graph per device):
+//   graph     : out_off int64[n+1], out_nb uint32[m]; in_* alias out_* when
+//               undirected (graph.hpp:64-67), separate arrays when directed.
+//   per-trial : parent int32[n]           -- the result (ParentArray)
+//   scratch     visited/bm0/bm1 uint32[ceil(n/32)] -- 1 bit per vertex
+//               queue uint32[n+1]        -- sliding frontier queue
+//                                           (sliding_queue.hpp:24-57)
+//               chunks                   -- heavy-vertex edge chunks
+//               ctrl                     -- grid barrier + counter ring
+//   Scratch is re-initialised inside the timed kernel each trial
+//   (GAP rule: only the graph is reused between trials).
+#ifndef GK_INTERNAL_CUH_
+#define GK_INTERNAL_CUH_
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "../../include/gk_bfs.h"
+
+namespace gk {
+
+// Counter ring: a phase (the interval between two grid barriers) that
+// accumulates counters uses set ph&3; set (ph+2)&3 is zeroed by CTA 0
+// during phase ph (its last reader finished before barrier ph).
+// kTailSnap: queue tail as of the barrier that starts the phase, written by
+// the last CTA to arrive (the live tail moves as soon as fast CTAs append).
+enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kTailSnap = 4, kSlots = 8 };
+
+struct Ctrl {
+  unsigned int bar_count;
+  unsigned int bar_gen;
+  int error;
+  int pad0;
+  unsigned long long tail;  // sliding-queue append cursor
+  long long num_steps;
+  long long pad1;
+  unsigned long long cnt[4][kSlots];
+  unsigned int cta_ph[2048];  // per-CTA barrier count (watchdog diagnostics)
+};
+
+struct Chunk {
+  uint32_t u;
+  uint32_t len;
+  int64_t start;
+};
+
+struct BfsParams {
+  int64_t n;
+  int64_t m;
+  int64_t w32;  // ceil(n/32)
+  const int64_t* out_off;
+  const uint32_t* out_nb;
+  const int64_t* in_off;
+  const uint32_t* in_nb;
+  uint32_t src;
+  int32_t strategy;
+  int64_t alpha;
+  int64_t beta;
+  int32_t want_depth;
+  int32_t front_in_smem;
+  int32_t* parent;
+  int32_t* depth;
+  uint32_t* visited;
+  uint32_t* bm0;
+  uint32_t* bm1;
+  uint32_t* queue;
+  Chunk* chunks;
+  int64_t chunk_cap;
+  Ctrl* ctrl;
+  gk_step* steps;
+  int64_t step_cap;
+  unsigned long long timeout_ns;
+};
+
+constexpr int kBlock = 512;
+constexpr int kWarps = kBlock / 32;
+
+// Host-side launch of the persistent traversal kernel.
+struct BfsLaunch {
+  int grid = 0;
+  int block = kBlock;
+  size_t smem_static = 0;
+  size_t smem_front_max = 0;  // largest front bitmap (bytes) staged in smem
+};
+cudaError_t bfs_configure(int device, BfsLaunch* cfg);
+cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t s);
+
+// Auxiliary (untimed) kernels.
+cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
+                          unsigned long long* d_out2, cudaStream_t s);
+cudaError_t byte_model(const BfsParams& p, const int32_t* depth, const char* dirs,
+                       int32_t nsteps, unsigned long long* d_acc, double* b_sec,
+                       double* b_use, cudaStream_t s);
+
+// Device graph construction (gk_graph_build.cu).
+struct DevCsr {
+  int64_t n = 0;
+  int64_t m = 0;
+  int64_t* off = nullptr;
+  uint32_t* nb = nullptr;
+};
+cudaError_t build_generated(int kind, int scale, int degree, uint64_t seed, int permute,
+                            DevCsr* out, std::string* err);
+cudaError_t build_grid(int64_t rows, int64_t cols, double p_delete, double p_diag,
+                       uint64_t seed, DevCsr* out, std::string* err);
+
+}  // namespace gk
+
+struct gk_graph {
+  int device = 0;
+  int64_t n = 0;
+  int64_t m = 0;
+  int32_t directed = 0;
+  int64_t* out_off = nullptr;
+  uint32_t* out_nb = nullptr;
+  int64_t* in_off = nullptr;  // == out_off when undirected
+  uint32_t* in_nb = nullptr;
+  // workspace
+  int32_t* parent = nullptr;
+  int32_t* depth = nullptr;
+  uint32_t* visited = nullptr;
+  uint32_t* bm0 = nullptr;
+  uint32_t* bm1 = nullptr;
+  uint32_t* queue = nullptr;
+  gk::Chunk* chunks = nullptr;
+  int64_t chunk_cap = 0;
+  gk::Ctrl* ctrl = nullptr;
+  gk_step* steps = nullptr;
+  int64_t step_cap = 0;
+  unsigned long long* acc = nullptr;  // aux accumulators
+  int32_t keep_depth = 0;
+  int32_t depth_valid = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr;
+  cudaEvent_t ev1 = nullptr;
+  gk::BfsLaunch launch;
+  std::mutex mu;
+};
+
+#endif  // GK_INTERNAL_CUH_

@@ -1,0 +1,245 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle.
+
+Bar (north_star): per-vertex depth bit-exact; every parent valid as
+VerifyBfs checks it (verify.hpp:62-98); plus schedule parity -- the
+direction sequence and per-step counters equal the reference's
+(gkr_bfs_schedule / golden.json), and bottom-up parents equal the
+reference's deterministic choice (bfs.hpp:55-60).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1508_03619_b200 import Bfs, BfsOptions, BfsStrategy, ConfigError, DeviceGraph
+
+from test_oracle import build_case, small_graph
+
+pytestmark = pytest.mark.gpu
+SEED = 24601
+
+
+def fnv(a):
+    return f"{O.fnv1a(np.ascontiguousarray(a)):016x}"
+
+
+@pytest.fixture(scope="module")
+def hosts(golden):
+    out = {}
+    for name, ent in golden["graphs"].items():
+        out[name] = build_case(name, ent) if ent["kind"] != "edges" else small_graph(name)
+    return out
+
+
+@pytest.fixture(scope="module")
+def devs(hosts):
+    return {name: DeviceGraph.from_csr(g) for name, g in hosts.items()}
+
+
+def test_upload_roundtrip(hosts, devs):
+    for name, g in hosts.items():
+        off, nb, io, inb = devs[name].download()
+        assert (off == g.off).all() and (nb == g.nb).all(), name
+        if g.directed:
+            assert (io == g.in_off).all() and (inb == g.in_nb).all()
+
+
+@pytest.mark.parametrize("name,make", [
+    ("kron10", lambda: DeviceGraph.generate("kron", 10, 16, SEED, permute=False)),
+    ("urand10", lambda: DeviceGraph.generate("urand", 10, 16, SEED)),
+    ("kron12_s7", lambda: DeviceGraph.generate("kron", 12, 16, 7, permute=False)),
+    ("urand14", lambda: DeviceGraph.generate("urand", 14, 16, SEED)),
+    ("kron16p", lambda: DeviceGraph.generate("kron", 16, 16, SEED, permute=True)),
+    ("grid60x70", lambda: DeviceGraph.grid(60, 70, 0.15, 0.02, SEED)),
+])
+def test_device_generator_matches_reference(golden, name, make):
+    ent = golden["graphs"][name]
+    g = make()
+    off, nb, _, _ = g.download()
+    assert g.n == ent["n"] and g.m == ent["m"]
+    assert fnv(off) == ent["off_fnv"] and fnv(nb) == ent["nb_fnv"]
+
+
+def test_device_generator_larger_scales():
+    for kind, scale, perm in (("kron", 18, True), ("urand", 17, False), ("kron", 17, False)):
+        g = DeviceGraph.generate(kind, scale, 16, SEED, permute=perm)
+        e = O.gen_kron(scale) if kind == "kron" else O.gen_urand(scale)
+        if perm:
+            e = O.permute_edges(e, scale, SEED)
+        h = O.build_csr(1 << scale, e)
+        off, nb, _, _ = g.download()
+        assert (off == h.off).all() and (nb == h.nb).all(), (kind, scale)
+    g = DeviceGraph.grid(300, 257, 0.15, 0.02, 99)
+    h = O.make_graph("grid", rows=300, cols=257, seed=99)
+    off, nb, _, _ = g.download()
+    assert (off == h.off).all() and (nb == h.nb).all()
+
+
+def test_pick_sources(golden, devs):
+    for name, ent in golden["graphs"].items():
+        assert devs[name].pick_sources(64, SEED).tolist() == ent["sources"], name
+
+
+def test_bfs_parity_against_reference(golden, hosts, devs):
+    """Every golden run: depths, parents, schedule and counters."""
+    for name, ent in golden["graphs"].items():
+        g, dg = hosts[name], devs[name]
+        for r in ent["runs"]:
+            s = r["source"]
+            res = dg.bfs(s, r["alpha"], r["beta"], r["strategy"], depth=True, counts=True)
+            key = (name, s, r["strategy"])
+            assert fnv(res.depth) == r["depth_fnv"], key
+            ok, msg = O.verify_bfs(g, s, res.parent)
+            assert ok, (key, msg)
+            assert res.schedule == r["dirs"], (key, res.schedule, r["dirs"])
+            assert [x[1] for x in res.steps] == r["frontier"], key
+            assert [x[2] for x in res.steps] == r["result"], key
+            assert [x[3] for x in res.steps] == r["edges_to_check"], key
+            assert res.reached == r["reached"], key
+            rp = O.bfs_replay(g, s, r["alpha"], r["beta"], r["strategy"])
+            for i, c in enumerate(res.schedule):
+                if c == "B":
+                    sel = res.depth == i + 1
+                    assert (res.parent[sel] == rp.parent[sel]).all(), (key, "bottom-up parent", i)
+
+
+def test_known_answers():
+    # test_kernels_source.cc:13-29
+    path = DeviceGraph.from_csr(O.build_csr(3, np.array([0, 1, 1, 2], np.uint32)))
+    assert Bfs(path, 0).tolist() == [0, 0, 1]
+    iso = DeviceGraph.from_csr(O.build_csr(4, np.array([0, 1, 1, 2], np.uint32)))
+    assert Bfs(iso, 0)[3] == -1
+    with pytest.raises(ConfigError, match="bfs source out of range"):
+        Bfs(path, 17)
+    with pytest.raises(ConfigError, match="bfs alpha and beta must be positive"):
+        Bfs(path, 0, BfsOptions(alpha=0))
+    with pytest.raises(ConfigError, match="bfs alpha and beta must be positive"):
+        Bfs(path, 0, BfsOptions(beta=-1))
+
+
+def test_single_vertex_and_edgeless():
+    one = DeviceGraph.upload(1, np.zeros(2, np.int64), np.zeros(0, np.uint32))
+    assert Bfs(one, 0).tolist() == [0]
+    none = DeviceGraph.upload(5, np.zeros(6, np.int64), np.zeros(0, np.uint32))
+    assert Bfs(none, 3).tolist() == [-1, -1, -1, 3, -1]
+    with pytest.raises(ConfigError, match="no edges"):
+        none.pick_sources(1)
+
+
+def test_strategies_agree(hosts, devs):
+    # test_kernels_source.cc:42-53 on a larger graph
+    g, dg = hosts["kron16p"], devs["kron16p"]
+    for s in O.pick_sources(g, 6, 3):
+        d = O.bfs_depths(g, int(s))
+        for st in BfsStrategy:
+            res = dg.bfs(int(s), strategy=int(st), depth=True)
+            assert (res.depth == d).all(), st
+            assert O.verify_bfs(g, int(s), res.parent)[0], st
+            rp = O.bfs_replay(g, int(s), strategy=int(st))
+            assert res.schedule == rp.dirs and [x[2] for x in res.steps] == rp.result
+
+
+def test_directed_bottom_up_uses_in_edges():
+    # test_kernels_source.cc:55-67 (alpha = beta = 1)
+    e = O.gen_kron(12, 16, 11)
+    g = O.build_csr(1 << 12, e, symmetrize=False, directed=True)
+    dg = DeviceGraph.from_csr(g)
+    seen_b = False
+    for s in O.pick_sources(g, 16):
+        s = int(s)
+        for a, b in ((1, 1), (2, 1), (15, 18)):
+            res = dg.bfs(s, a, b, depth=True)
+            assert (res.depth == O.bfs_depths(g, s)).all()
+            assert O.verify_bfs(g, s, res.parent)[0]
+            rp = O.bfs_replay(g, s, a, b)
+            assert res.schedule == rp.dirs and [x[2] for x in res.steps] == rp.result
+            seen_b |= "B" in res.schedule
+    assert seen_b
+
+
+def test_graph_untouched_and_repeatable(hosts, devs):
+    # test_kernels_source.cc:69-85 + acceptance criterion 3 (determinism)
+    g, dg = hosts["kron16p"], devs["kron16p"]
+    s = int(O.pick_sources(g, 1)[0])
+    a = dg.bfs(s, depth=True)
+    b = dg.bfs(s, depth=True)
+    off, nb, _, _ = dg.download()
+    assert (off == g.off).all() and (nb == g.nb).all()
+    assert (a.depth == b.depth).all() and a.steps == b.steps
+
+
+def test_byte_model_matches_oracle(hosts, devs):
+    for name in ("kron16p", "urand14", "grid60x70", "kron12_s7"):
+        g, dg = hosts[name], devs[name]
+        for s in O.pick_sources(g, 3):
+            s = int(s)
+            res = dg.bfs(s, depth=True)
+            bs, bu = dg.byte_model(res.steps)
+            obs, obu = O.byte_model(g, res.depth, res.schedule)
+            assert bs == obs and bu == obu, (name, s)
+
+
+def test_component_edges(hosts, devs):
+    g, dg = hosts["kron16p"], devs["kron16p"]
+    for s in O.pick_sources(g, 4):
+        res = dg.bfs(int(s), counts=True, depth=True)
+        assert res.component_edges == O.component_edges(g, res.depth)
+
+
+def _check_bfs_properties(off, nb, src, depth, parent):
+    """Size-independent certificate that depth is the exact BFS distance and
+    parent a valid BFS tree: d(src)=0; every reached v != src has an edge
+    (parent, v) with d(parent) = d(v)-1; every arc joins two reached or two
+    unreached vertices and changes depth by at most 1."""
+    n = off.size - 1
+    reached = depth >= 0
+    assert depth[src] == 0 and parent[src] == src
+    assert ((parent >= 0) == reached).all()
+    src_of = np.repeat(np.arange(n, dtype=np.int64), np.diff(off))
+    du, dw = depth[src_of], depth[nb]
+    assert (reached[src_of] == reached[nb]).all()
+    both = reached[src_of]
+    assert (np.abs(du[both].astype(np.int64) - dw[both]) <= 1).all()
+    v = np.nonzero(reached)[0]
+    v = v[v != src]
+    p = parent[v].astype(np.int64)
+    assert (depth[p] == depth[v] - 1).all()
+    key = src_of * n + nb.astype(np.int64)  # CSR order is sorted by (u, w)
+    q = p * n + v
+    pos = np.searchsorted(key, q)
+    assert (pos < key.size).all() and (key[np.minimum(pos, key.size - 1)] == q).all()
+
+
+@pytest.mark.parametrize("kind,scale", [("kron", 21), ("urand", 20)])
+def test_medium_scale_against_oracle(kind, scale):
+    dg = DeviceGraph.generate(kind, scale, 16, SEED)
+    off, nb, _, _ = dg.download()
+    g = O.Csr(dg.n, off, nb)
+    for s in dg.pick_sources(4, SEED):
+        s = int(s)
+        res = dg.bfs(s, depth=True)
+        assert (res.depth == O.bfs_depths(g, s)).all()
+        assert O.verify_bfs(g, s, res.parent)[0]
+        rp = O.bfs_replay(g, s)
+        assert res.schedule == rp.dirs and [x[2] for x in res.steps] == rp.result
+
+
+def test_large_scale_properties():
+    dg = DeviceGraph.generate("kron", 23, 16, SEED)
+    off, nb, _, _ = dg.download()
+    for s in dg.pick_sources(2, SEED):
+        s = int(s)
+        res = dg.bfs(s, depth=True, counts=True)
+        _check_bfs_properties(off, nb, s, res.depth, res.parent)
+        assert res.reached == int((res.depth >= 0).sum())
+
+
+def test_grid_high_diameter():
+    dg = DeviceGraph.grid(700, 650, 0.15, 0.02, SEED)
+    off, nb, _, _ = dg.download()
+    g = O.Csr(dg.n, off, nb)
+    for s in dg.pick_sources(2, SEED):
+        s = int(s)
+        res = dg.bfs(s, depth=True)
+        assert (res.depth == O.bfs_depths(g, s)).all()
+        assert O.verify_bfs(g, s, res.parent)[0]
+        assert res.schedule == O.bfs_replay(g, s).dirs
