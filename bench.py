@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py -- BFS GTEPS (harmonic mean over sources) + % of HBM roofline.
+
+Default workload = BASELINE config 3 (the north_star's 1-GPU target): a
+Kronecker graph of 2^27 vertices, edge factor 16, initiator .57/.19/.19,
+seeded (24601), vertex IDs permuted, symmetrized/deduplicated, generated and
+built on the device bit-identically to the reference generator + BuildCsr.
+A "step" is one BFS (gk_bfs, the C-ABI replacement of gapkit::Bfs,
+bfs.hpp:117) from the next of PickSources(g, K, seed) (source_picker.hpp:47).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config kron27|urand27|kron16|grid4900|kronS|urandS]
+
+value     : harmonic mean over the K steps of m_cc(s)/t_dev(s) (GTEPS), t_dev the
+            CUDA-event time of the traversal kernel, graph resident in HBM.
+e2e       : same metric through the C ABI with the parent array returned to a
+            pinned host buffer (D2H inside the timed region), host wall clock.
+roofline  : algorithmic bytes B_sec (evaluated per source from
+            exact depths + the executed direction schedule) / t_dev vs the
+            measured HBM copy bandwidth (MEASURED_PEAKS.json).
+cpu_baseline : the reference's own OpenMP Bfs (oracle/_ref/libgapref.so, the
+            unmodified headers) on the box's host cores, bounded sample.
+N > 1     : one process per GPU (torchrun), independent replicas of the whole
+            job (1D-partitioned sharding is not built yet); per-step time is the
+            max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "kron27": dict(kind="kron", scale=27, degree=16, permute=True,
+                   workload="BASELINE config 3: Kronecker 2^27 vertices, edge factor 16, A/B/C=.57/.19/.19, "
+                            "permuted IDs, symmetrized+deduplicated, int32 IDs, CSR"),
+    "urand27": dict(kind="urand", scale=27, degree=16, permute=False,
+                    workload="BASELINE config 2: uniform random 2^27 vertices, 2^31 generated edges, "
+                             "symmetrized+deduplicated, CSR"),
+    "kron16": dict(kind="kron", scale=16, degree=16, permute=True,
+                   workload="BASELINE config 1: Kronecker 2^16 vertices, edge factor 16, permuted"),
+    "grid4900": dict(kind="grid", rows=4900, cols=4900, p_delete=0.15, p_diag=0.02,
+                     workload="BASELINE config 4: 4900x4900 4-neighbour grid, 15% edges deleted, "
+                              "2% diagonal shortcuts"),
+}
+SEED = 24601
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def parse_config(name: str) -> dict:
+    if name in CONFIGS:
+        return dict(CONFIGS[name], name=name)
+    for kind in ("kron", "urand"):
+        if name.startswith(kind) and name[len(kind):].isdigit():
+            sc = int(name[len(kind):])
+            return dict(kind=kind, scale=sc, degree=16, permute=(kind == "kron"), name=name,
+                        workload=f"{kind} 2^{sc} vertices, edge factor 16" + (", permuted" if kind == "kron" else ""))
+    raise SystemExit(f"unknown config {name}")
+
+
+def hmean(xs):
+    xs = [x for x in xs if x > 0]
+    return len(xs) / sum(1.0 / x for x in xs) if xs else 0.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join("/tmp", f"gk_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                r = int(parts[2], 16) if parts[2].startswith("0x") else int(parts[2])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx.append(m)
+            for bit, name in REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def build_graph(cfg, device):
+    from paper_1508_03619_b200 import DeviceGraph
+    t0 = time.time()
+    if cfg["kind"] == "grid":
+        g = DeviceGraph.grid(cfg["rows"], cfg["cols"], cfg["p_delete"], cfg["p_diag"], SEED, device=device)
+    else:
+        g = DeviceGraph.generate(cfg["kind"], cfg["scale"], cfg["degree"], SEED, permute=cfg["permute"],
+                                 device=device)
+    return g, time.time() - t0
+
+
+def host_ref_graph(g):
+    """Download the device CSR straight into the reference's CsrGraph vectors
+    (public constructor, graph.hpp:30-45)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import oracle as O
+    R = O.RefLib()
+    po, pn, pio, pin = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+    h = R.L.gkr_graph_alloc(g.n, g.m, 0, C.byref(po), C.byref(pn), C.byref(pio), C.byref(pin))
+    g.download_into(po.value, pn.value)
+    off = np.frombuffer((C.c_int64 * (g.n + 1)).from_address(po.value), np.int64).copy()
+    err = C.create_string_buffer(256)
+    R.L.gkr_graph_seal(h, 0, err, 256)
+    return O.RefGraph(R, h), off
+
+
+def cpu_reference(g, sources, warmup, budget_s, label, m_of=None):
+    """Time gapkit::Bfs (the reference) on the host cores; bounded by budget_s."""
+    import numpy as np
+    t0 = time.time()
+    rg, off = host_ref_graph(g)
+    deg = np.diff(off)
+    threads = rg.ref.L.gkr_max_threads()
+    for s in sources[:warmup]:
+        rg.bfs_timed([int(s)])
+    secs, gteps, done = [], [], 0
+    tstart = time.time()
+    for s in sources:
+        sec = float(rg.bfs_timed([int(s)])[0])
+        if m_of is not None and int(s) in m_of:
+            m = m_of[int(s)]
+        else:
+            p = rg.bfs(int(s))
+            m = int(deg[p >= 0].sum()) // 2
+        secs.append(sec)
+        gteps.append(m / sec / 1e9)
+        done += 1
+        if time.time() - tstart > budget_s:
+            break
+    return {"value": hmean(gteps), "unit": "GTEPS", "cores": threads, "kind": "reference",
+            "sample": f"{label}: first {done} of the {len(sources)} picked sources, gapkit::Bfs "
+                      f"(oracle/_ref, unmodified reference headers, OpenMP {threads} threads, "
+                      f"OMP_WAIT_POLICY=active, OMP_PROC_BIND=spread), steady_clock per call incl. allocation",
+            "mean_ms": 1e3 * sum(secs) / max(len(secs), 1), "setup_s": round(tstart - t0, 2)}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="kron27")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of reference CPU BFS work")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-model", action="store_true")
+    args = ap.parse_args()
+    # OpenMP settings for the reference CPU legs (must precede libgomp init).
+    os.environ.setdefault("OMP_WAIT_POLICY", "active")
+    os.environ.setdefault("OMP_PROC_BIND", "spread")
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = parse_config(args.config)
+    K, W = args.steps, max(args.warmup, 0)
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1508_03619_b200 import PinnedBuffer
+
+    if args.impl == "reference":
+        if rank != 0:
+            if dist:
+                dist.destroy_process_group()
+            return
+        g, build_s = build_graph(cfg, local)
+        sources = g.pick_sources(K, SEED)
+        res = cpu_reference(g, sources, W, budget_s=1e9, label=cfg["name"])
+        line = {"impl": "reference", "metric": "BFS GTEPS (harmonic mean over sources)", "value": res["value"],
+                "unit": "GTEPS", "n_gpus": args.gpus, "steps": K, "warmup": W,
+                "ms_per_step": res["mean_ms"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generator, no dataset)",
+                "config": {"workload": cfg["workload"], "name": cfg["name"], "n": g.n, "arcs": g.m,
+                           "host_cpu": cpu_model(), "nproc": os.cpu_count()},
+                "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": res["value"], "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- our arm ----------------
+    g, build_s = build_graph(cfg, local)
+    sources = [int(s) for s in g.pick_sources(K, SEED + rank)]
+    warm = sources[: max(W, 0)] if W <= K else (sources * (W // K + 1))[:W]
+    for s in warm:
+        g.bfs(s, parent=False)
+    # untimed pre-pass: exact depths -> m_cc and the B_sec/B_use byte model
+    m_of, bsec_of, buse_of, sched_of = {}, {}, {}, {}
+    if not args.no_model:
+        g.keep_depth(True)
+    for s in sources:
+        r = g.bfs(s, parent=False, counts=True)
+        m_of[s] = r.component_edges
+        sched_of[s] = r.schedule
+        if not args.no_model:
+            bsec_of[s], buse_of[s] = g.byte_model(r.steps)
+    g.keep_depth(False)
+
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.2)
+    if dist:
+        dist.barrier()
+    tw0 = time.time()
+    dev_ms = []
+    for s in sources:
+        r = g.bfs(s, parent=False)
+        dev_ms.append(r.device_ms)
+    wall = time.time() - tw0
+    clocks = clk.stop()
+
+    # e2e: the C-ABI call with the ParentArray returned to host memory
+    pin = PinnedBuffer(g.n)
+    e2e_s = []
+    for s in sources:
+        t0 = time.perf_counter()
+        g.bfs(s, parent=pin.array)
+        e2e_s.append(time.perf_counter() - t0)
+
+    if dist:
+        import torch
+        t = torch.tensor(dev_ms, dtype=torch.float64, device="cuda")
+        m = torch.tensor([m_of[s] for s in sources], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(m, op=dist.ReduceOp.SUM)
+        step_ms, step_m = t.tolist(), m.tolist()
+        e = torch.tensor(e2e_s, dtype=torch.float64, device="cuda")
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+        e2e_step = e.tolist()
+    else:
+        step_ms, step_m, e2e_step = dev_ms, [m_of[s] for s in sources], e2e_s
+
+    gteps = [m / (t * 1e-3) / 1e9 for m, t in zip(step_m, step_ms)]
+    value = hmean(gteps)
+    e2e_val = hmean([m / t / 1e9 for m, t in zip(step_m, e2e_step)])
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    roof = None
+    if bsec_of:
+        tot_b = sum(bsec_of[s] for s in sources)
+        tot_t = sum(dev_ms) * 1e-3
+        ach = tot_b / tot_t / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                tj = json.load(f)
+            if tj.get("config") == cfg["name"]:
+                traffic = tj.get("dram_bytes_per_launch")
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": tot_b / len(sources),
+                "b_use_frac": (sum(buse_of[s] for s in sources) / tot_t / 1e9) / peak,
+                "frac_of_8TBs_nominal": ach / 8000.0,
+                "kernel": "bfs_persistent (one launch per BFS)"}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_reference(g, sources, 1, args.cpu_budget, cfg["name"], m_of)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
+
+    scheds = sorted(set(sched_of.values()), key=len)
+    line = {
+        "metric": "BFS GTEPS (harmonic mean over sources) and % of HBM roofline",
+        "value": value, "unit": "GTEPS", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": statistics.mean(step_ms), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generator, no dataset)",
+        "config": {"workload": cfg["workload"], "name": cfg["name"], "n": g.n, "arcs": g.m, "seed": SEED,
+                   "sources": K, "alpha": 15, "beta": 18,
+                   "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % ((g.m * 4 + g.n * 8) / 1e9),
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "device_build_s": round(build_s, 2), "timed_region_wall_s": round(wall, 4),
+                   "schedules": scheds[:4], "mean_m_cc": statistics.mean(step_m)},
+        "e2e": {"value": e2e_val, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * g.n,
+                "note": "gk_bfs with the parent array copied to a pinned host buffer; graph resident "
+                        "(uploaded once, untimed, as the reference harness builds it untimed); per-step "
+                        "input is the source id passed by value"},
+        "gpu_launches": K,
+        "clocks": clocks,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

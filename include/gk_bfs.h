@@ -141,6 +141,13 @@ GK_API gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t bet
  * (valid until the next call / free). */
 GK_API const int32_t* gk_bfs_device_parent(const gk_graph* g);
 
+/* Phase trace of the last gk_bfs: ts_ns[0] = kernel start, ts_ns[i] = release
+ * of grid barrier i (globaltimer ns) and tags[i] the phase it ended: 'I' init,
+ * 'T' top-down, 'H' heavy-vertex chunks, 'Z' front clear, 'Q' queue->bitmap,
+ * 'B' bottom-up, 'C' bitmap->queue, 'R' rescan.  Up to 511 barriers. */
+GK_API gk_status gk_bfs_trace(const gk_graph* g, uint64_t* ts_ns, char* tags,
+                              int32_t cap, int32_t* count);
+
 /* Sector-aware (B_sec) and element-granular (B_use) algorithmic byte model
  * of the last gk_bfs on this handle; that call must have
  * requested depth_out or GK_KEEP_DEPTH via gk_bfs_keep_depth(). */

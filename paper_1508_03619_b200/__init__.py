@@ -224,6 +224,16 @@ class DeviceGraph:
                "gk_bfs_byte_model")
         return bs.value, bu.value
 
+    def trace(self):
+        """[(tag, t_ms_since_kernel_start)] for the phases of the last bfs."""
+        cap = 4096
+        ts = (C.c_uint64 * cap)()
+        tags = C.create_string_buffer(cap)
+        cnt = C.c_int32()
+        _check(_lib.load().gk_bfs_trace(self._h, ts, tags, cap, C.byref(cnt)), "gk_bfs_trace")
+        k = min(cnt.value, cap)
+        return [(tags.raw[i:i + 1].decode(), (ts[i] - ts[0]) * 1e-6) for i in range(k)]
+
     def device_parent_ptr(self) -> int:
         return int(_lib.load().gk_bfs_device_parent(self._h) or 0)
 

@@ -28,7 +28,7 @@ EXPORTED = (
     "gk_last_error", "gk_abi_version", "gk_device_count", "gk_graph_upload",
     "gk_graph_generate", "gk_graph_generate_grid", "gk_graph_free", "gk_graph_info",
     "gk_graph_download", "gk_pick_sources", "gk_bfs", "gk_bfs_device_parent",
-    "gk_bfs_byte_model", "gk_bfs_keep_depth", "gk_host_alloc", "gk_host_free",
+    "gk_bfs_byte_model", "gk_bfs_keep_depth", "gk_host_alloc", "gk_host_free", "gk_bfs_trace",
 )
 
 
@@ -78,6 +78,7 @@ def load() -> C.CDLL:
     L.gk_bfs_device_parent.restype = vp
     L.gk_bfs_byte_model.argtypes = [vp, C.POINTER(Step), i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.gk_bfs_keep_depth.argtypes = [vp, i32]
+    L.gk_bfs_trace.argtypes = [vp, C.POINTER(C.c_uint64), C.c_char_p, i32, C.POINTER(i32)]
     L.gk_host_alloc.argtypes = [i64]
     L.gk_host_alloc.restype = vp
     L.gk_host_free.argtypes = [vp]

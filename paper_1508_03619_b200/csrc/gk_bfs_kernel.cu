@@ -39,11 +39,15 @@ constexpr int kQBuf = 256;         // per-warp queue staging (QueueBuffer analog
 constexpr int64_t kHeavy = 1024;   // degree above which a vertex is chunked
 constexpr int kChunk = 1024;       // edges per heavy chunk
 
+constexpr int kBW = 4;  // bottom-up: 32-vertex words per warp iteration
+
 struct __align__(16) SmemT {
-  uint32_t qbuf[kWarps][kQBuf];
-  int64_t t_b[kBlock];
-  int64_t t_pre[kBlock];
-  uint32_t t_u[kBlock];
+  struct {  // top-down phases
+    uint32_t qbuf[kWarps][kQBuf];
+    int64_t t_b[kBlock];
+    int64_t t_pre[kBlock];
+    uint32_t t_u[kBlock];
+  } td;
   long long red[kWarps + 2];
   unsigned long long bcast[4];
   int ok;
@@ -73,7 +77,7 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 // order this CTA's stores before the arrival and invalidate the SM's L1
 // after the release, so plain loads after the barrier see every store made
 // before it.
-__device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& gen, unsigned& ph) {
+__device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& gen, unsigned& ph, unsigned char tag) {
   __syncthreads();
   if (threadIdx.x == 0) {
     Ctrl* c = P.ctrl;
@@ -85,6 +89,10 @@ __device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& gen, unsigned&
       atomicExch(&c->bar_count, 0u);
       __threadfence();
       c->cnt[(ph + 1) & 3][kTailSnap] = ld_volatile(&c->tail);
+      if (ph + 1 < (unsigned)kTraceCap) {
+        c->ts[ph + 1] = globaltimer();
+        c->tag[ph + 1] = tag;
+      }
       __threadfence();
       atomicAdd(&c->bar_gen, 1u);
     } else {
@@ -201,11 +209,51 @@ __device__ __forceinline__ void on_claim(const BfsParams& P, uint32_t u, uint32_
   }
 }
 
+// Claim up to 4 edges (u_k -> v_k) per thread with their loads and atomics
+// issued together (bfs.hpp:77-84).  The visited word is read from L2 first
+// so already-visited targets cost no atomic.  kBig (large frontiers):
+// claimed vertices are also OR-ed into the next-frontier bitmap (so a
+// following bottom-up step needs no QueueToBitmap) and their degrees are
+// summed afterwards by td_scout instead of inline.
+template <bool kBig>
+__device__ __forceinline__ void claim4(const BfsParams& P, const uint32_t (&u)[4],
+                                       const uint32_t (&v)[4], const bool (&ok)[4],
+                                       uint32_t* nextbm, int lvl, bool encode, long long& scout,
+                                       uint32_t* buf, int& qcnt) {
+  uint32_t w[4];
+  bool c[4];
+#pragma unroll
+  for (int k = 0; k < 4; k++) w[k] = ok[k] ? __ldcg(P.visited + (v[k] >> 5)) : 0xffffffffu;
+#pragma unroll
+  for (int k = 0; k < 4; k++) c[k] = !((w[k] >> (v[k] & 31u)) & 1u);
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    if (c[k]) {
+      const uint32_t bit = 1u << (v[k] & 31u);
+      c[k] = (atomicOr(P.visited + (v[k] >> 5), bit) & bit) == 0;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    if (c[k]) {
+      P.parent[v[k]] = (int32_t)u[k];
+      if (kBig) {
+        atomicOr(nextbm + (v[k] >> 5), 1u << (v[k] & 31u));  // result unused -> RED
+      } else {
+        on_claim(P, u[k], v[k], lvl, encode, scout);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; k++) wq_push(P, c[k], v[k], buf, qcnt);
+}
+
 // ---- top-down, light vertices + chunk registration ------------------------
+template <bool kBig>
 __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, unsigned long long qs,
-                         unsigned long long qe, int lvl, bool encode, long long& scout,
-                         int& qcnt) {
-  uint32_t* buf = s.qbuf[threadIdx.x >> 5];
+                         unsigned long long qe, uint32_t* nextbm, int lvl, bool encode,
+                         long long& scout, int& qcnt) {
+  uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
   for (;;) {
     if (threadIdx.x == 0) s.bcast[1] = atomicAdd(&cnt[kTile], 1ull);
@@ -238,38 +286,43 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, unsigned lon
         dl = d;
       }
     }
-    s.t_u[threadIdx.x] = u;
-    s.t_b[threadIdx.x] = b;
+    s.td.t_u[threadIdx.x] = u;
+    s.td.t_b[threadIdx.x] = b;
     int64_t tot;
     const int64_t pre = block_exscan(dl, &tot, s);
-    s.t_pre[threadIdx.x] = pre;
+    s.td.t_pre[threadIdx.x] = pre;
     __syncthreads();
-    for (int64_t eb = 0; eb < tot; eb += kBlock) {
-      const int64_t ei = eb + threadIdx.x;
-      bool claim = false;
-      uint32_t v = 0;
-      if (ei < tot) {
-        int lo = 0, hi = kBlock - 1;  // last k with t_pre[k] <= ei
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (s.t_pre[mid] <= ei) lo = mid;
-          else hi = mid - 1;
+    for (int64_t eb = 0; eb < tot; eb += 4 * kBlock) {
+      uint32_t uu[4], v[4];
+      bool ok[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int64_t ei = eb + k * kBlock + threadIdx.x;
+        ok[k] = ei < tot;
+        uu[k] = 0;
+        v[k] = 0;
+        if (ok[k]) {
+          int lo = 0, hi = kBlock - 1;  // last item with t_pre <= ei
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s.td.t_pre[mid] <= ei) lo = mid;
+            else hi = mid - 1;
+          }
+          uu[k] = s.td.t_u[lo];
+          v[k] = __ldg(P.out_nb + s.td.t_b[lo] + (ei - s.td.t_pre[lo]));
         }
-        const uint32_t uu = s.t_u[lo];
-        v = __ldg(P.out_nb + s.t_b[lo] + (ei - s.t_pre[lo]));
-        claim = try_claim(P, v);
-        if (claim) on_claim(P, uu, v, lvl, encode, scout);
       }
-      wq_push(P, claim, v, buf, qcnt);
+      claim4<kBig>(P, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
     }
     __syncthreads();
   }
 }
 
-// ---- top-down, heavy chunks: one warp per chunk, 4 loads in flight --------
+// ---- top-down, heavy chunks: one warp per chunk, 4 edges per lane ---------
+template <bool kBig>
 __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, unsigned long long nch,
-                         int lvl, bool encode, long long& scout, int& qcnt) {
-  uint32_t* buf = s.qbuf[threadIdx.x >> 5];
+                         uint32_t* nextbm, int lvl, bool encode, long long& scout, int& qcnt) {
+  uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
   const unsigned lane = lane_id();
   for (;;) {
@@ -278,6 +331,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, unsigned lon
     c = __shfl_sync(kFull, c, 0);
     if (c >= nch) break;
     const Chunk ch = P.chunks[c];
+    const uint32_t uu[4] = {ch.u, ch.u, ch.u, ch.u};
     for (uint32_t o = 0; o < ch.len; o += 128) {
       uint32_t v[4];
       bool ok[4];
@@ -287,97 +341,158 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, unsigned lon
         ok[k] = j < ch.len;
         v[k] = ok[k] ? __ldg(P.out_nb + ch.start + j) : 0u;
       }
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        bool claim = ok[k] && try_claim(P, v[k]);
-        if (claim) on_claim(P, ch.u, v[k], lvl, encode, scout);
-        wq_push(P, claim, v[k], buf, qcnt);
-      }
+      claim4<kBig>(P, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
+    }
+  }
+}
+
+// ---- degrees of the vertices a large top-down step claimed ----------------
+// scout = sum of -old over the claims (bfs.hpp:83) = sum of max(deg, 1)
+// with the degree encoding, or the claim count without it (bfs.hpp:129).
+__device__ void td_scout(const BfsParams& P, unsigned long long q0, unsigned long long q1, int lvl,
+                         bool encode, long long& scout) {
+  const long long gtid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long gthreads = (long long)gridDim.x * kBlock;
+#pragma unroll 4
+  for (unsigned long long i = q0 + gtid; i < q1; i += gthreads) {
+    const uint32_t v = __ldcg(P.queue + i);
+    if (P.want_depth) P.depth[v] = lvl + 1;
+    if (encode) {
+      const long long d = P.out_off[v + 1] - P.out_off[v];
+      scout += d ? d : 1;
+    } else {
+      scout += 1;
     }
   }
 }
 
 // ---- bottom-up sweep (bfs.hpp:47-66) ---------------------------------------
+// One warp handles kBW consecutive 32-vertex words per iteration so that
+// kBW independent load chains (visited word -> offsets -> in-neighbours ->
+// front bits) are in flight per warp.  Each lane then walks its own vertex's
+// in-list 2 neighbours per round for up to kLaneRounds rounds; lists still
+// unresolved after that are scanned by the whole warp with a ballot per 32
+// neighbours.  The chosen parent is the first in-neighbour (ascending) whose
+// front bit is set, as in bfs.hpp:55-60.  Vertices without in-edges are
+// marked visited ("dead") the first time they are seen.
+constexpr int kLaneRounds = 4;
+
+__device__ __forceinline__ bool front_bit(const uint32_t* front, uint32_t u) {
+  return (front[u >> 5] >> (u & 31u)) & 1u;
+}
+
 __device__ void bu_step(const BfsParams& P, const uint32_t* front, uint32_t* next, int lvl,
                         long long& awake) {
   const unsigned lane = lane_id();
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
-  for (long long w = gw; w < P.w32; w += nw) {
-    const uint32_t vis = __ldcg(P.visited + w);
-    const uint32_t v = (uint32_t)(w * 32 + lane);
-    bool pend = ((int64_t)v < P.n) && !((vis >> lane) & 1u);
-    if (__ballot_sync(kFull, pend) == 0) {
-      if (lane == 0) next[w] = 0;
+  for (long long w0 = gw * kBW; w0 < P.w32; w0 += nw * kBW) {
+    uint32_t vis[kBW];
+    bool pend[kBW], found[kBW], dead[kBW];
+    int64_t b[kBW];
+    uint32_t d[kBW], par[kBW];
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < kBW; k++) {
+      vis[k] = (w0 + k < P.w32) ? __ldcg(P.visited + w0 + k) : 0xffffffffu;
+      const int64_t v = (w0 + k) * 32 + lane;
+      pend[k] = v < P.n && !((vis[k] >> lane) & 1u);
+      found[k] = dead[k] = false;
+      b[k] = 0;
+      d[k] = 0;
+      par[k] = 0;
+      any |= pend[k];
+    }
+    if (__ballot_sync(kFull, any) == 0) {
+      if (lane < kBW && w0 + lane < P.w32) next[w0 + lane] = 0u;
       continue;
     }
-    bool found = false, dead = false;
-    uint32_t par = 0;
-    int64_t b = 0, e = 0;
-    if (pend) {
-      b = P.in_off[v];
-      e = P.in_off[v + 1];
-      if (b == e) {  // no in-edges: can never be reached; skip it from now on
-        dead = true;
-        pend = false;
-      }
-    }
-    if (pend) {  // first <= 4 in-neighbours, loads issued together
-      const int64_t k = e - b;
-      uint32_t u0 = __ldg(P.in_nb + b);
-      uint32_t u1 = k > 1 ? __ldg(P.in_nb + b + 1) : 0u;
-      uint32_t u2 = k > 2 ? __ldg(P.in_nb + b + 2) : 0u;
-      uint32_t u3 = k > 3 ? __ldg(P.in_nb + b + 3) : 0u;
-      const bool h0 = (front[u0 >> 5] >> (u0 & 31u)) & 1u;
-      const bool h1 = k > 1 && ((front[u1 >> 5] >> (u1 & 31u)) & 1u);
-      const bool h2 = k > 2 && ((front[u2 >> 5] >> (u2 & 31u)) & 1u);
-      const bool h3 = k > 3 && ((front[u3 >> 5] >> (u3 & 31u)) & 1u);
-      if (h0) { found = true; par = u0; }
-      else if (h1) { found = true; par = u1; }
-      else if (h2) { found = true; par = u2; }
-      else if (h3) { found = true; par = u3; }
-      if (found) {
-        pend = false;
-      } else {
-        b += k < 4 ? k : 4;
-        pend = b < e;
-      }
-    }
-    unsigned pm = __ballot_sync(kFull, pend);
-    while (pm) {  // warp-cooperative scan of one long list at a time
-      const int l = __ffs(pm) - 1;
-      pm &= pm - 1;
-      const int64_t lb = __shfl_sync(kFull, b, l);
-      const int64_t le = __shfl_sync(kFull, e, l);
-      for (int64_t j = lb; j < le; j += 32) {
-        const int64_t jj = j + lane;
-        bool h = false;
-        uint32_t u = 0;
-        if (jj < le) {
-          u = __ldg(P.in_nb + jj);
-          h = (front[u >> 5] >> (u & 31u)) & 1u;
+#pragma unroll
+    for (int k = 0; k < kBW; k++) {
+      if (pend[k]) {
+        const int64_t v = (w0 + k) * 32 + lane;
+        b[k] = P.in_off[v];
+        d[k] = (uint32_t)(P.in_off[v + 1] - b[k]);
+        if (d[k] == 0) {  // no in-edges: never reachable; skip it from now on
+          dead[k] = true;
+          pend[k] = false;
         }
-        const unsigned bal = __ballot_sync(kFull, h);
-        if (bal) {
-          const uint32_t hu = __shfl_sync(kFull, u, __ffs(bal) - 1);
-          if ((int)lane == l) {
-            found = true;
-            par = hu;
+      }
+    }
+#pragma unroll 1
+    for (int round = 0; round < kLaneRounds; round++) {
+      bool more = false;
+#pragma unroll
+      for (int k = 0; k < kBW; k++) more |= pend[k];
+      if (__ballot_sync(kFull, more) == 0) break;
+      uint32_t u0[kBW], u1[kBW];
+#pragma unroll
+      for (int k = 0; k < kBW; k++) {
+        u0[k] = pend[k] ? __ldg(P.in_nb + b[k]) : 0u;
+        u1[k] = (pend[k] && d[k] > 1) ? __ldg(P.in_nb + b[k] + 1) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kBW; k++) {
+        if (!pend[k]) continue;
+        if (front_bit(front, u0[k])) {
+          found[k] = true;
+          par[k] = u0[k];
+        } else if (d[k] > 1 && front_bit(front, u1[k])) {
+          found[k] = true;
+          par[k] = u1[k];
+        }
+        if (found[k]) {
+          pend[k] = false;
+        } else {
+          const uint32_t t = d[k] < 2 ? d[k] : 2u;
+          b[k] += t;
+          d[k] -= t;
+          pend[k] = d[k] > 0;
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kBW; k++) {
+      unsigned pm = __ballot_sync(kFull, pend[k]);
+      while (pm) {  // warp-cooperative scan of one long list at a time
+        const int l = __ffs(pm) - 1;
+        pm &= pm - 1;
+        const int64_t lb = __shfl_sync(kFull, b[k], l);
+        const int64_t le = lb + __shfl_sync(kFull, d[k], l);
+        for (int64_t j = lb; j < le; j += 32) {
+          const int64_t jj = j + lane;
+          bool h = false;
+          uint32_t u = 0;
+          if (jj < le) {
+            u = __ldg(P.in_nb + jj);
+            h = front_bit(front, u);
           }
-          break;
+          const unsigned bal = __ballot_sync(kFull, h);
+          if (bal) {
+            const uint32_t hu = __shfl_sync(kFull, u, __ffs(bal) - 1);
+            if ((int)lane == l) {
+              found[k] = true;
+              par[k] = hu;
+            }
+            break;
+          }
         }
       }
     }
-    if (found) {
-      P.parent[v] = (int32_t)par;
-      if (P.want_depth) P.depth[v] = lvl + 1;
-    }
-    const unsigned nbits = __ballot_sync(kFull, found);
-    const unsigned dbits = __ballot_sync(kFull, dead);
-    if (lane == 0) {
-      next[w] = nbits;
-      if (nbits | dbits) P.visited[w] = vis | nbits | dbits;
-      awake += __popc(nbits);
+#pragma unroll
+    for (int k = 0; k < kBW; k++) {
+      const int64_t v = (w0 + k) * 32 + lane;
+      if (found[k]) {
+        P.parent[v] = (int32_t)par[k];
+        if (P.want_depth) P.depth[v] = lvl + 1;
+      }
+      const unsigned nbits = __ballot_sync(kFull, found[k]);
+      const unsigned dbits = __ballot_sync(kFull, dead[k]);
+      if (lane == 0 && w0 + k < P.w32) {
+        next[w0 + k] = nbits;
+        if (nbits | dbits) P.visited[w0 + k] = vis[k] | nbits | dbits;
+        awake += __popc(nbits);
+      }
     }
   }
 }
@@ -425,32 +540,39 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   const uint32_t src = P.src;
 
   // ---- init (timed; replaces bfs.hpp:126-138) ----
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->ts[0] = globaltimer();
   {
     const long long n4 = P.n >> 2;
     int4* p4 = reinterpret_cast<int4*>(P.parent);
     int4* d4 = reinterpret_cast<int4*>(P.depth);
+    const int4 m1 = make_int4(-1, -1, -1, -1);
+#pragma unroll 4
     for (long long i = gtid; i < n4; i += gthreads) {
-      int4 val = make_int4(-1, -1, -1, -1);
-      int4 dv = val;
-      if ((long long)(src >> 2) == i) {
-        reinterpret_cast<int*>(&val)[src & 3] = (int)src;
-        reinterpret_cast<int*>(&dv)[src & 3] = 0;
-      }
-      p4[i] = val;
-      if (P.want_depth) d4[i] = dv;
+      p4[i] = m1;
+      if (P.want_depth) d4[i] = m1;
     }
     for (long long i = (n4 << 2) + gtid; i < P.n; i += gthreads) {
-      P.parent[i] = i == (long long)src ? (int)src : -1;
-      if (P.want_depth) P.depth[i] = i == (long long)src ? 0 : -1;
+      P.parent[i] = -1;
+      if (P.want_depth) P.depth[i] = -1;
     }
-    for (long long i = gtid; i < P.w32; i += gthreads)
-      P.visited[i] = (long long)(src >> 5) == i ? (1u << (src & 31u)) : 0u;
-    if (gtid == 0) {
-      P.queue[0] = src;
-      P.ctrl->tail = 1;
+    const long long w4 = P.w32 >> 2;
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+    for (long long i = gtid; i < w4; i += gthreads) {
+      reinterpret_cast<uint4*>(P.visited)[i] = z4;
+    }
+    for (long long i = (w4 << 2) + gtid; i < P.w32; i += gthreads) {
+      P.visited[i] = 0u;
     }
   }
-  if (!grid_sync(P, s, gen, ph)) return;
+  if (!grid_sync(P, s, gen, ph, kTagInit)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // bfs.hpp:132-136
+    P.parent[src] = (int32_t)src;
+    if (P.want_depth) P.depth[src] = 0;
+    P.visited[src >> 5] = 1u << (src & 31u);
+    P.queue[0] = src;
+    P.ctrl->tail = 1;
+  }
+  if (!grid_sync(P, s, gen, ph, kTagInit)) return;
 
   const bool encode = P.strategy != GK_BFS_TOP_DOWN_RESCAN;
   unsigned long long qs = 0, qe = 1;
@@ -459,20 +581,22 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   long long nsteps = 0;
   int lvl = 0;
   int qcnt = 0;
+  bool front_ready = false;  // frontg holds exactly the current frontier
   uint32_t* frontg = P.bm0;
   uint32_t* nextg = P.bm1;
   uint32_t* sfront = reinterpret_cast<uint32_t*>(dyn_smem);
 
   while (qe > qs) {
     if (P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha) {
-      // QueueToBitmap into a cleared front (bfs.hpp:145)
-      for (long long i = gtid; i < P.w32; i += gthreads) frontg[i] = 0u;
-      if (!grid_sync(P, s, gen, ph)) return;
-      for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
-        const uint32_t v = __ldcg(P.queue + i);
-        atomicOr(frontg + (v >> 5), 1u << (v & 31u));
+      if (!front_ready) {  // QueueToBitmap into a cleared front (bfs.hpp:145)
+        for (long long i = gtid; i < P.w32; i += gthreads) frontg[i] = 0u;
+        if (!grid_sync(P, s, gen, ph, kTagZero)) return;
+        for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
+          const uint32_t v = __ldcg(P.queue + i);
+          atomicOr(frontg + (v >> 5), 1u << (v & 31u));
+        }
+        if (!grid_sync(P, s, gen, ph, kTagQ2B)) return;
       }
-      if (!grid_sync(P, s, gen, ph)) return;
       long long awake = (long long)(qe - qs);  // bfs.hpp:146
       qs = qe;                                 // bfs.hpp:147
       long long old_awake;
@@ -488,7 +612,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         bu_step(P, fr, nextg, lvl, acc);
         const unsigned set = ph & 3;
         block_add(acc, &P.ctrl->cnt[set][kSum], s);
-        if (!grid_sync(P, s, gen, ph)) return;
+        if (!grid_sync(P, s, gen, ph, kTagBU)) return;
         awake = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
         log_step(P, nsteps++, 'B', old_awake, awake, etc);
         lvl++;
@@ -497,28 +621,57 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         nextg = t;
       } while (awake >= old_awake || awake > P.n / P.beta);
       b2q(P, frontg, s);  // bfs.hpp:155
-      if (!grid_sync(P, s, gen, ph)) return;
+      if (!grid_sync(P, s, gen, ph, kTagB2Q)) return;
       qe = ld_volatile(&P.ctrl->cnt[ph & 3][kTailSnap]);
       scout = 1;  // bfs.hpp:156
+      front_ready = true;
     } else {
       etc -= scout;  // bfs.hpp:158
       const long long fsize = (long long)(qe - qs);
+      // Large frontiers (by the degree total the heuristic already holds)
+      // also build the next-frontier bitmap and sum degrees in a separate
+      // high-MLP pass; small ones keep everything inline, so a long chain of
+      // tiny levels costs one grid barrier each.
+      const bool big = scout > P.bitmap_td_min;
       long long sacc = 0;
-      td_light(P, s, ph, qs, qe, lvl, encode, sacc, qcnt);
-      wq_flush(P, s.qbuf[threadIdx.x >> 5], qcnt);
-      unsigned set = ph & 3;
+      unsigned set;
+      if (big) {
+        for (long long i = gtid; i < P.w32; i += gthreads) nextg[i] = 0u;
+        if (!grid_sync(P, s, gen, ph, kTagZero)) return;
+        td_light<true>(P, s, ph, qs, qe, nextg, lvl, encode, sacc, qcnt);
+      } else {
+        td_light<false>(P, s, ph, qs, qe, nextg, lvl, encode, sacc, qcnt);
+      }
+      wq_flush(P, s.td.qbuf[threadIdx.x >> 5], qcnt);
+      set = ph & 3;
       block_add(sacc, &P.ctrl->cnt[set][kSum], s);
-      if (!grid_sync(P, s, gen, ph)) return;
+      if (!grid_sync(P, s, gen, ph, kTagTD)) return;
       scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
       const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
       if (nch) {
         sacc = 0;
-        td_heavy(P, s, ph, nch, lvl, encode, sacc, qcnt);
-        wq_flush(P, s.qbuf[threadIdx.x >> 5], qcnt);
         set = ph & 3;
+        if (big) td_heavy<true>(P, s, ph, nch, nextg, lvl, encode, sacc, qcnt);
+        else td_heavy<false>(P, s, ph, nch, nextg, lvl, encode, sacc, qcnt);
+        wq_flush(P, s.td.qbuf[threadIdx.x >> 5], qcnt);
         block_add(sacc, &P.ctrl->cnt[set][kSum], s);
-        if (!grid_sync(P, s, gen, ph)) return;
+        if (!grid_sync(P, s, gen, ph, kTagHeavy)) return;
         scout += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+      }
+      if (big) {
+        const unsigned long long q1 = ld_volatile(&P.ctrl->cnt[ph & 3][kTailSnap]);
+        sacc = 0;
+        set = ph & 3;
+        td_scout(P, qe, q1, lvl, encode, sacc);
+        block_add(sacc, &P.ctrl->cnt[set][kSum], s);
+        if (!grid_sync(P, s, gen, ph, kTagSweep)) return;
+        scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        uint32_t* t = frontg;
+        frontg = nextg;
+        nextg = t;
+        front_ready = true;
+      } else {
+        front_ready = false;
       }
       qs = qe;  // SlideWindow (bfs.hpp:160)
       qe = ld_volatile(&P.ctrl->cnt[ph & 3][kTailSnap]);
@@ -530,7 +683,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         }
         set = ph & 3;
         block_add(tot, &P.ctrl->cnt[set][kSum], s);
-        if (!grid_sync(P, s, gen, ph)) return;
+        if (!grid_sync(P, s, gen, ph, kTagRescan)) return;
         scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
       }
       log_step(P, nsteps++, 'T', fsize, scout, etc);

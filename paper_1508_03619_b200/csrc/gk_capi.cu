@@ -55,9 +55,7 @@ void free_graph(gk_graph* g) {
   cudaFree(g->out_nb);
   cudaFree(g->parent);
   cudaFree(g->depth);
-  cudaFree(g->visited);
-  cudaFree(g->bm0);
-  cudaFree(g->bm1);
+  cudaFree(g->bits);
   cudaFree(g->queue);
   cudaFree(g->chunks);
   cudaFree(g->ctrl);
@@ -76,9 +74,12 @@ gk_status alloc_workspace(gk_graph* g) {
   const int64_t w32 = (n + 31) / 32;
   const size_t wbytes = ((size_t)w32 * 4 + 15) & ~size_t(15);
   CK(cudaMalloc(&g->parent, sizeof(int32_t) * std::max<int64_t>(n, 4) + 16), "alloc parent");
-  CK(cudaMalloc(&g->visited, wbytes + 16), "alloc visited");
-  CK(cudaMalloc(&g->bm0, wbytes + 16), "alloc bitmap");
-  CK(cudaMalloc(&g->bm1, wbytes + 16), "alloc bitmap");
+  // visited | front | next bitmaps in one block so one L2 access-policy
+  // window can keep them resident while the graph streams past.
+  CK(cudaMalloc(&g->bits, 3 * wbytes + 64), "alloc bitmaps");
+  g->visited = g->bits;
+  g->bm0 = g->bits + wbytes / 4;
+  g->bm1 = g->bits + 2 * (wbytes / 4);
   CK(cudaMalloc(&g->queue, sizeof(uint32_t) * (n + 1)), "alloc queue");
   g->chunk_cap = 2 * (g->m / 1024) + 64;
   CK(cudaMalloc(&g->chunks, sizeof(gk::Chunk) * g->chunk_cap), "alloc chunks");
@@ -90,6 +91,26 @@ gk_status alloc_workspace(gk_graph* g) {
   CK(cudaEventCreate(&g->ev0), "event");
   CK(cudaEventCreate(&g->ev1), "event");
   CK(gk::bfs_configure(g->device, &g->launch), "configure bfs kernel");
+  const char* pers = getenv("GK_L2_PERSIST");
+  if (!pers || atoi(pers) != 0) {
+    int max_win = 0, max_pers = 0;
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
+    cudaDeviceGetAttribute(&max_pers, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+    const size_t want = std::min<size_t>({3 * wbytes, (size_t)max_win, (size_t)max_pers});
+    if (want > 0) {
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+      cudaStreamAttrValue a{};
+      a.accessPolicyWindow.base_ptr = g->bits;
+      a.accessPolicyWindow.num_bytes = want;
+      a.accessPolicyWindow.hitRatio = 1.0f;
+      a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &a);
+      cudaGetLastError();  // best effort: persistence is an optimisation only
+    }
+  }
   return GK_OK;
 }
 
@@ -132,7 +153,7 @@ gk_status gk_graph_upload(const gk_csr_view* csr, int device, gk_graph** out) {
   g->directed = csr->directed ? 1 : 0;
   const size_t ob = sizeof(int64_t) * (g->n + 1), nbb = sizeof(uint32_t) * std::max<int64_t>(g->m, 1);
   cudaError_t e;
-  if ((e = cudaMalloc(&g->out_off, ob)) || (e = cudaMalloc(&g->out_nb, nbb)) ||
+  if ((e = cudaMalloc(&g->out_off, ob + 16)) || (e = cudaMalloc(&g->out_nb, nbb)) ||
       (e = cudaMemcpy(g->out_off, csr->out_offsets, ob, cudaMemcpyHostToDevice)) ||
       (g->m && (e = cudaMemcpy(g->out_nb, csr->out_neighbors, sizeof(uint32_t) * g->m,
                                cudaMemcpyHostToDevice)))) {
@@ -140,7 +161,7 @@ gk_status gk_graph_upload(const gk_csr_view* csr, int device, gk_graph** out) {
     return cuda_fail(e, "upload CSR");
   }
   if (g->directed) {
-    if ((e = cudaMalloc(&g->in_off, ob)) || (e = cudaMalloc(&g->in_nb, nbb)) ||
+    if ((e = cudaMalloc(&g->in_off, ob + 16)) || (e = cudaMalloc(&g->in_nb, nbb)) ||
         (e = cudaMemcpy(g->in_off, csr->in_offsets, ob, cudaMemcpyHostToDevice)) ||
         (g->m && (e = cudaMemcpy(g->in_nb, csr->in_neighbors, sizeof(uint32_t) * g->m,
                                  cudaMemcpyHostToDevice)))) {
@@ -298,6 +319,10 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   p.visited = g->visited;
   p.bm0 = g->bm0;
   p.bm1 = g->bm1;
+  // Large top-down steps additionally clear and fill the n/8-byte next
+  // bitmap and sum degrees in a separate pass; worth it above ~n/16 edges.
+  p.bitmap_td_min = std::max<int64_t>(4096, g->n / 16);
+  if (const char* bt = getenv("GK_BITMAP_TD_MIN")) p.bitmap_td_min = strtoll(bt, nullptr, 10);
   p.queue = g->queue;
   p.chunks = g->chunks;
   p.chunk_cap = g->chunk_cap;
@@ -312,9 +337,11 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   CK(cudaMemsetAsync(g->ctrl, 0, sizeof(gk::Ctrl), s), "reset ctrl");
   CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
   CK(cudaEventRecord(g->ev1, s), "event record");
-  gk::Ctrl ctrl;
+  gk::Ctrl& ctrl = g->last_ctrl;
+  g->last_valid = 0;
   CK(cudaMemcpyAsync(&ctrl, g->ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
   CK(cudaStreamSynchronize(s), "bfs kernel");
+  g->last_valid = 1;
   g->depth_valid = want_depth;
   if (ctrl.error) {
     if (ctrl.error == 2) {
@@ -361,6 +388,22 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
 }
 
 const int32_t* gk_bfs_device_parent(const gk_graph* g) { return g ? g->parent : nullptr; }
+
+gk_status gk_bfs_trace(const gk_graph* g, uint64_t* ts_ns, char* tags, int32_t cap, int32_t* count) {
+  if (!g || !count) return fail(GK_ERR_INVALID, "null argument");
+  if (!g->last_valid) return fail(GK_ERR_INVALID, "no completed gk_bfs on this handle");
+  int32_t k = 0;
+  for (int32_t i = 0; i < gk::kTraceCap; i++) {
+    if (i > 0 && g->last_ctrl.tag[i] == 0) break;
+    if (k < cap) {
+      if (ts_ns) ts_ns[k] = g->last_ctrl.ts[i];
+      if (tags) tags[k] = i == 0 ? 'S' : (char)g->last_ctrl.tag[i];
+    }
+    k++;
+  }
+  *count = k;
+  return GK_OK;
+}
 
 gk_status gk_bfs_byte_model(gk_graph* g, const gk_step* steps, int32_t num_steps, double* b_sec,
                             double* b_use) {

@@ -29,6 +29,9 @@ namespace gk {
 // during phase ph (its last reader finished before barrier ph).
 // kTailSnap: queue tail as of the barrier that starts the phase, written by
 // the last CTA to arrive (the live tail moves as soon as fast CTAs append).
+constexpr int kTraceCap = 512;
+enum PhaseTag : unsigned char { kTagInit = 'I', kTagTD = 'T', kTagHeavy = 'H', kTagZero = 'Z', kTagQ2B = 'Q',
+                                kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S' };
 enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kTailSnap = 4, kSlots = 8 };
 
 struct Ctrl {
@@ -41,6 +44,11 @@ struct Ctrl {
   long long pad1;
   unsigned long long cnt[4][kSlots];
   unsigned int cta_ph[2048];  // per-CTA barrier count (watchdog diagnostics)
+  // Trace: globaltimer at kernel start (ts[0]) and at the release of each
+  // of the first kTraceCap-1 grid barriers; tag[i] names the phase that
+  // barrier i ended (see PhaseTag).
+  unsigned long long ts[kTraceCap];
+  unsigned char tag[kTraceCap];
 };
 
 struct Chunk {
@@ -63,6 +71,7 @@ struct BfsParams {
   int64_t beta;
   int32_t want_depth;
   int32_t front_in_smem;
+  int64_t bitmap_td_min;  // scout above which a top-down step is 'large'
   int32_t* parent;
   int32_t* depth;
   uint32_t* visited;
@@ -123,6 +132,7 @@ struct gk_graph {
   // workspace
   int32_t* parent = nullptr;
   int32_t* depth = nullptr;
+  uint32_t* bits = nullptr;  // one block: visited | bm0 | bm1
   uint32_t* visited = nullptr;
   uint32_t* bm0 = nullptr;
   uint32_t* bm1 = nullptr;
@@ -139,6 +149,8 @@ struct gk_graph {
   cudaEvent_t ev0 = nullptr;
   cudaEvent_t ev1 = nullptr;
   gk::BfsLaunch launch;
+  gk::Ctrl last_ctrl;  // host copy of the last traversal's control block
+  int32_t last_valid = 0;
   std::mutex mu;
 };
 
