@@ -39,7 +39,6 @@ constexpr int kQBuf = 256;         // per-warp queue staging (QueueBuffer analog
 constexpr int64_t kHeavy = 1024;   // degree above which a vertex is chunked
 constexpr int kChunk = 1024;       // edges per heavy chunk
 
-constexpr int kBW = 4;  // bottom-up: 32-vertex words per warp iteration
 
 struct __align__(16) SmemT {
   struct {  // top-down phases
@@ -48,6 +47,7 @@ struct __align__(16) SmemT {
     int64_t t_pre[kBlock];
     uint32_t t_u[kBlock];
   } td;
+  uint32_t bu_acc[kWarps][2][32];  // bottom-up: per-warp next/dead bits of a task
   long long red[kWarps + 2];
   unsigned long long bcast[4];
   int ok;
@@ -367,131 +367,175 @@ __device__ void td_scout(const BfsParams& P, unsigned long long q0, unsigned lon
 }
 
 // ---- bottom-up sweep (bfs.hpp:47-66) ---------------------------------------
-// One warp handles kBW consecutive 32-vertex words per iteration so that
-// kBW independent load chains (visited word -> offsets -> in-neighbours ->
-// front bits) are in flight per warp.  Each lane then walks its own vertex's
-// in-list 2 neighbours per round for up to kLaneRounds rounds; lists still
-// unresolved after that are scanned by the whole warp with a ballot per 32
-// neighbours.  The chosen parent is the first in-neighbour (ascending) whose
-// front bit is set, as in bfs.hpp:55-60.  Vertices without in-edges are
+// A warp takes a task of 32 consecutive bitmap words (1024 vertices): lane l
+// loads word l and the task's unvisited vertices are numbered by a warp
+// prefix sum.  Every lane keeps kBuSlots vertices in flight and refills a slot
+// (select-the-c-th-pending-vertex: shuffle binary search + __fns) as soon as
+// its vertex resolves, so one slow list never idles the other lanes.  Per
+// round a slot tests the next 2 in-neighbours of its vertex; after
+// kLaneRounds rounds a still-unresolved vertex is deferred to the long list,
+// scanned after the sweep by whole warps with a ballot per 32 neighbours.
+// The chosen parent is the first in-neighbour (ascending) whose front bit is
+// set, as in bfs.hpp:55-60.  Results are OR-ed into per-warp shared-memory
+// words and written back once per task; vertices without in-edges are
 // marked visited ("dead") the first time they are seen.
-constexpr int kLaneRounds = 4;
+constexpr int kBuSlots = 2;
+constexpr int kLaneRounds = 3;
 
 __device__ __forceinline__ bool front_bit(const uint32_t* front, uint32_t u) {
   return (front[u >> 5] >> (u & 31u)) & 1u;
 }
 
-__device__ void bu_step(const BfsParams& P, const uint32_t* front, uint32_t* next, int lvl,
-                        long long& awake) {
+__device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_t* front, uint32_t* next,
+                        int lvl, unsigned long long long_base, long long& awake) {
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t* acc_n = s.bu_acc[warp][0];
+  uint32_t* acc_d = s.bu_acc[warp][1];
+  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  const long long ntasks = (P.w32 + 31) >> 5;
+  for (long long t = gw; t < ntasks; t += nw) {
+    const long long w = (t << 5) + lane;
+    uint32_t vis = 0xffffffffu, pad = 0u;
+    if (w < P.w32) {
+      vis = __ldcg(P.visited + w);
+      const int64_t rem = P.n - w * 32;  // mask off ids >= n in the last word
+      if (rem < 32) pad = 0xffffffffu << rem;
+    }
+    const uint32_t pm = ~(vis | pad);
+    const int cnt = __popc(pm);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(kFull, incl, 31);
+    acc_n[lane] = 0u;
+    acc_d[lane] = 0u;
+    __syncwarp();
+    int next_c = 0;
+    uint32_t v[kBuSlots], d[kBuSlots], rounds[kBuSlots];
+    int64_t b[kBuSlots];
+    int st[kBuSlots];  // 0 empty, 1 scanning
+#pragma unroll
+    for (int k = 0; k < kBuSlots; k++) {
+      st[k] = 0;
+      v[k] = d[k] = rounds[k] = 0;
+      b[k] = 0;
+    }
+    for (;;) {
+      // refill empty slots with the next pending vertices of the task
+#pragma unroll
+      for (int k = 0; k < kBuSlots; k++) {
+        const bool need = st[k] == 0;
+        const unsigned nm = __ballot_sync(kFull, need);
+        const int c = next_c + __popc(nm & lanemask_lt());
+        next_c += __popc(nm);
+        int lo = 0;  // word holding the c-th pending vertex: last lane with excl <= c
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int e = __shfl_sync(kFull, excl, lo + step);
+          if (e <= c) lo += step;
+        }
+        const uint32_t m = __shfl_sync(kFull, pm, lo);
+        const int ex = __shfl_sync(kFull, excl, lo);
+        if (need && c < total) {
+          v[k] = (uint32_t)(((t << 5) + lo) * 32 + (int)__fns(m, 0, c - ex + 1));
+          b[k] = P.in_off[v[k]];
+          d[k] = (uint32_t)(P.in_off[v[k] + 1] - b[k]);
+          rounds[k] = 0;
+          st[k] = 1;
+          if (d[k] == 0) {  // no in-edges: never reachable; skip it from now on
+            atomicOr(&acc_d[(v[k] >> 5) & 31u], 1u << (v[k] & 31u));
+            st[k] = 0;
+          }
+        }
+      }
+      bool active = false;
+#pragma unroll
+      for (int k = 0; k < kBuSlots; k++) active |= st[k] != 0;
+      if (__ballot_sync(kFull, active) == 0) {
+        if (next_c >= total) break;
+        continue;
+      }
+      uint32_t u0[kBuSlots], u1[kBuSlots];
+#pragma unroll
+      for (int k = 0; k < kBuSlots; k++) {
+        u0[k] = st[k] ? __ldg(P.in_nb + b[k]) : 0u;
+        u1[k] = (st[k] && d[k] > 1) ? __ldg(P.in_nb + b[k] + 1) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kBuSlots; k++) {
+        if (!st[k]) continue;
+        bool hit = false;
+        uint32_t par = 0;
+        if (front_bit(front, u0[k])) {
+          hit = true;
+          par = u0[k];
+        } else if (d[k] > 1 && front_bit(front, u1[k])) {
+          hit = true;
+          par = u1[k];
+        }
+        if (hit) {
+          P.parent[v[k]] = (int32_t)par;
+          if (P.want_depth) P.depth[v[k]] = lvl + 1;
+          atomicOr(&acc_n[(v[k] >> 5) & 31u], 1u << (v[k] & 31u));
+          st[k] = 0;
+        } else {
+          const uint32_t tk = d[k] < 2 ? d[k] : 2u;
+          b[k] += tk;
+          d[k] -= tk;
+          if (d[k] == 0) {
+            st[k] = 0;  // exhausted: not reached at this level
+          } else if (++rounds[k] >= kLaneRounds) {
+            P.queue[long_base + atomicAdd(&P.ctrl->cnt[ph & 3][kLongCount], 1ull)] = v[k];
+            st[k] = 0;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (w < P.w32) {
+      const uint32_t nbits = acc_n[lane], dbits = acc_d[lane];
+      next[w] = nbits;
+      if (nbits | dbits) P.visited[w] = vis | nbits | dbits;
+      awake += __popc(nbits);
+    }
+    __syncwarp();
+  }
+}
+
+// Long in-lists deferred by bu_step: one warp per vertex, ballot over 32
+// neighbours at a time, resuming after the 2*kLaneRounds already tested.
+__device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* next,
+                        unsigned long long base, unsigned long long count, int lvl, long long& awake) {
   const unsigned lane = lane_id();
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
-  for (long long w0 = gw * kBW; w0 < P.w32; w0 += nw * kBW) {
-    uint32_t vis[kBW];
-    bool pend[kBW], found[kBW], dead[kBW];
-    int64_t b[kBW];
-    uint32_t d[kBW], par[kBW];
-    bool any = false;
-#pragma unroll
-    for (int k = 0; k < kBW; k++) {
-      vis[k] = (w0 + k < P.w32) ? __ldcg(P.visited + w0 + k) : 0xffffffffu;
-      const int64_t v = (w0 + k) * 32 + lane;
-      pend[k] = v < P.n && !((vis[k] >> lane) & 1u);
-      found[k] = dead[k] = false;
-      b[k] = 0;
-      d[k] = 0;
-      par[k] = 0;
-      any |= pend[k];
-    }
-    if (__ballot_sync(kFull, any) == 0) {
-      if (lane < kBW && w0 + lane < P.w32) next[w0 + lane] = 0u;
-      continue;
-    }
-#pragma unroll
-    for (int k = 0; k < kBW; k++) {
-      if (pend[k]) {
-        const int64_t v = (w0 + k) * 32 + lane;
-        b[k] = P.in_off[v];
-        d[k] = (uint32_t)(P.in_off[v + 1] - b[k]);
-        if (d[k] == 0) {  // no in-edges: never reachable; skip it from now on
-          dead[k] = true;
-          pend[k] = false;
+  for (long long i = gw; i < (long long)count; i += nw) {
+    const uint32_t v = __ldcg(P.queue + base + i);
+    const int64_t le = P.in_off[v + 1];
+    for (int64_t j = P.in_off[v] + 2 * kLaneRounds; j < le; j += 32) {
+      const int64_t jj = j + lane;
+      bool h = false;
+      uint32_t u = 0;
+      if (jj < le) {
+        u = __ldg(P.in_nb + jj);
+        h = front_bit(front, u);
+      }
+      const unsigned bal = __ballot_sync(kFull, h);
+      if (bal) {
+        const uint32_t hu = __shfl_sync(kFull, u, __ffs(bal) - 1);
+        if (lane == 0) {
+          P.parent[v] = (int32_t)hu;
+          if (P.want_depth) P.depth[v] = lvl + 1;
+          atomicOr(next + (v >> 5), 1u << (v & 31u));
+          atomicOr(P.visited + (v >> 5), 1u << (v & 31u));
+          awake++;
         }
-      }
-    }
-#pragma unroll 1
-    for (int round = 0; round < kLaneRounds; round++) {
-      bool more = false;
-#pragma unroll
-      for (int k = 0; k < kBW; k++) more |= pend[k];
-      if (__ballot_sync(kFull, more) == 0) break;
-      uint32_t u0[kBW], u1[kBW];
-#pragma unroll
-      for (int k = 0; k < kBW; k++) {
-        u0[k] = pend[k] ? __ldg(P.in_nb + b[k]) : 0u;
-        u1[k] = (pend[k] && d[k] > 1) ? __ldg(P.in_nb + b[k] + 1) : 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < kBW; k++) {
-        if (!pend[k]) continue;
-        if (front_bit(front, u0[k])) {
-          found[k] = true;
-          par[k] = u0[k];
-        } else if (d[k] > 1 && front_bit(front, u1[k])) {
-          found[k] = true;
-          par[k] = u1[k];
-        }
-        if (found[k]) {
-          pend[k] = false;
-        } else {
-          const uint32_t t = d[k] < 2 ? d[k] : 2u;
-          b[k] += t;
-          d[k] -= t;
-          pend[k] = d[k] > 0;
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kBW; k++) {
-      unsigned pm = __ballot_sync(kFull, pend[k]);
-      while (pm) {  // warp-cooperative scan of one long list at a time
-        const int l = __ffs(pm) - 1;
-        pm &= pm - 1;
-        const int64_t lb = __shfl_sync(kFull, b[k], l);
-        const int64_t le = lb + __shfl_sync(kFull, d[k], l);
-        for (int64_t j = lb; j < le; j += 32) {
-          const int64_t jj = j + lane;
-          bool h = false;
-          uint32_t u = 0;
-          if (jj < le) {
-            u = __ldg(P.in_nb + jj);
-            h = front_bit(front, u);
-          }
-          const unsigned bal = __ballot_sync(kFull, h);
-          if (bal) {
-            const uint32_t hu = __shfl_sync(kFull, u, __ffs(bal) - 1);
-            if ((int)lane == l) {
-              found[k] = true;
-              par[k] = hu;
-            }
-            break;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < kBW; k++) {
-      const int64_t v = (w0 + k) * 32 + lane;
-      if (found[k]) {
-        P.parent[v] = (int32_t)par[k];
-        if (P.want_depth) P.depth[v] = lvl + 1;
-      }
-      const unsigned nbits = __ballot_sync(kFull, found[k]);
-      const unsigned dbits = __ballot_sync(kFull, dead[k]);
-      if (lane == 0 && w0 + k < P.w32) {
-        next[w0 + k] = nbits;
-        if (nbits | dbits) P.visited[w0 + k] = vis[k] | nbits | dbits;
-        awake += __popc(nbits);
+        break;
       }
     }
   }
@@ -609,11 +653,23 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
           fr = sfront;
         }
         long long acc = 0;
-        bu_step(P, fr, nextg, lvl, acc);
-        const unsigned set = ph & 3;
+        // long-list scratch: queue slots past the tail are unused during bottom-up
+        const unsigned long long lbase = qe;
+        bu_step(P, s, ph, fr, nextg, lvl, lbase, acc);
+        unsigned set = ph & 3;
         block_add(acc, &P.ctrl->cnt[set][kSum], s);
         if (!grid_sync(P, s, gen, ph, kTagBU)) return;
-        awake = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        const unsigned long long nlong = ld_volatile(&P.ctrl->cnt[set][kLongCount]);
+        long long awake_bu = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        if (nlong) {
+          acc = 0;
+          bu_long(P, fr, nextg, lbase, nlong, lvl, acc);
+          set = ph & 3;
+          block_add(acc, &P.ctrl->cnt[set][kSum], s);
+          if (!grid_sync(P, s, gen, ph, kTagLong)) return;
+          awake_bu += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        }
+        awake = awake_bu;
         log_step(P, nsteps++, 'B', old_awake, awake, etc);
         lvl++;
         uint32_t* t = frontg;

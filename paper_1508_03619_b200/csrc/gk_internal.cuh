@@ -31,8 +31,8 @@ namespace gk {
 // the last CTA to arrive (the live tail moves as soon as fast CTAs append).
 constexpr int kTraceCap = 512;
 enum PhaseTag : unsigned char { kTagInit = 'I', kTagTD = 'T', kTagHeavy = 'H', kTagZero = 'Z', kTagQ2B = 'Q',
-                                kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S' };
-enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kTailSnap = 4, kSlots = 8 };
+                                kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S', kTagLong = 'L' };
+enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kTailSnap = 4, kLongCount = 5, kSlots = 8 };
 
 struct Ctrl {
   unsigned int bar_count;
