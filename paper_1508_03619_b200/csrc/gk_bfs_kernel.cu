@@ -73,51 +73,58 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
-// Sense-counting grid barrier with a watchdog.  The gpu-scope fences
-// order this CTA's stores before the arrival and invalidate the SM's L1
-// after the release, so plain loads after the barrier see every store made
-// before it.
-__device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& gen, unsigned& ph, unsigned char tag) {
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Grid barrier on a monotonic arrival counter: barrier k completes when the
+// counter reaches k * gridDim.x.  The release-add publishes this CTA's
+// stores (ordered before it by __syncthreads); the acquire spin orders the
+// CTA's later loads after every other CTA's stores.  A watchdog turns a hang
+// into an error instead of a stuck GPU.  Measured ~1.3 us per barrier at
+// 296 CTAs on B200 (tools/bench_mem/barbench.cu).
+__device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& ph, unsigned char tag) {
   __syncthreads();
   if (threadIdx.x == 0) {
     Ctrl* c = P.ctrl;
     int ok = 1;
-    __threadfence();
     if (blockIdx.x < 2048) c->cta_ph[blockIdx.x] = ph + 1;
-    unsigned arrived = atomicAdd(&c->bar_count, 1u);
-    if (arrived == gridDim.x - 1) {
-      atomicExch(&c->bar_count, 0u);
-      __threadfence();
-      c->cnt[(ph + 1) & 3][kTailSnap] = ld_volatile(&c->tail);
-      if (ph + 1 < (unsigned)kTraceCap) {
-        c->ts[ph + 1] = globaltimer();
-        c->tag[ph + 1] = tag;
-      }
-      __threadfence();
-      atomicAdd(&c->bar_gen, 1u);
-    } else {
-      unsigned long long t0 = globaltimer();
-      while (ld_acquire(&c->bar_gen) == gen) {
-        __nanosleep(32);
-        if (*reinterpret_cast<volatile int*>(&c->error)) { ok = 0; break; }
-        if (globaltimer() - t0 > P.timeout_ns) {
+    red_release_add(&c->bar_count, 1ull);
+    const unsigned long long target = (unsigned long long)(ph + 1) * gridDim.x;
+    unsigned spins = 0;
+    unsigned long long t0 = 0;
+    while (ld_acquire_u64(&c->bar_count) < target) {
+      if ((++spins & 255u) == 0) {
+        if (*reinterpret_cast<volatile int*>(&c->error) == 2) {
+          ok = 0;
+          break;
+        }
+        const unsigned long long now = globaltimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > P.timeout_ns) {
           atomicExch(&c->error, 2);
           ok = 0;
           break;
         }
       }
     }
-    __threadfence();
-    if (*reinterpret_cast<volatile int*>(&c->error)) ok = 0;
     s.ok = ok;
-    if (blockIdx.x == 0) {  // recycle the counter set two phases ahead
+    if (blockIdx.x == 0) {  // recycle the counter set two phases ahead; trace
       unsigned long long* z = c->cnt[(ph + 3) & 3];
 #pragma unroll
       for (int i = 0; i < kSlots; i++) z[i] = 0;
+      if (ph + 1 < (unsigned)kTraceCap) {
+        c->ts[ph + 1] = globaltimer();
+        c->tag[ph + 1] = tag;
+      }
     }
   }
   __syncthreads();
-  gen++;
   ph++;
   return s.ok != 0;
 }
@@ -166,26 +173,37 @@ __device__ void block_add(long long x, unsigned long long* dst, SmemT& s) {
   __syncthreads();
 }
 
+// Queue appends of one phase land at base + fetch-add on that phase's ring
+// counter; after the barrier every thread advances its copy of the tail by
+// the counter (a single live tail would race with the next phase's appends).
+struct QApp {
+  unsigned long long base;
+  unsigned long long* ctr;
+};
+__device__ __forceinline__ QApp qapp(const BfsParams& P, unsigned ph, unsigned long long base) {
+  return QApp{base, &P.ctrl->cnt[ph & 3][kAppend]};
+}
+
 // Per-warp staging buffer flushed with one fetch-add (QueueBuffer,
 // sliding_queue.hpp:62-86).  Must be called by all 32 lanes.
-__device__ __forceinline__ void wq_flush(const BfsParams& P, uint32_t* buf, int& qcnt) {
+__device__ __forceinline__ void wq_flush(const BfsParams& P, const QApp& qa, uint32_t* buf, int& qcnt) {
   __syncwarp();
   if (qcnt == 0) return;
   unsigned long long base = 0;
-  if (lane_id() == 0) base = atomicAdd(&P.ctrl->tail, (unsigned long long)qcnt);
+  if (lane_id() == 0) base = qa.base + atomicAdd(qa.ctr, (unsigned long long)qcnt);
   base = __shfl_sync(kFull, base, 0);
   for (int i = lane_id(); i < qcnt; i += 32) P.queue[base + i] = buf[i];
   __syncwarp();
   qcnt = 0;
 }
 
-__device__ __forceinline__ void wq_push(const BfsParams& P, bool claim, uint32_t v,
+__device__ __forceinline__ void wq_push(const BfsParams& P, const QApp& qa, bool claim, uint32_t v,
                                         uint32_t* buf, int& qcnt) {
   unsigned mask = __ballot_sync(kFull, claim);
   if (!mask) return;
   if (claim) buf[qcnt + __popc(mask & lanemask_lt())] = v;
   qcnt += __popc(mask);
-  if (qcnt > kQBuf - 32) wq_flush(P, buf, qcnt);
+  if (qcnt > kQBuf - 32) wq_flush(P, qa, buf, qcnt);
 }
 
 // Claim v for parent u (bfs.hpp:78-84).  The visited word is read from L2
@@ -216,7 +234,7 @@ __device__ __forceinline__ void on_claim(const BfsParams& P, uint32_t u, uint32_
 // following bottom-up step needs no QueueToBitmap) and their degrees are
 // summed afterwards by td_scout instead of inline.
 template <bool kBig>
-__device__ __forceinline__ void claim4(const BfsParams& P, const uint32_t (&u)[4],
+__device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const uint32_t (&u)[4],
                                        const uint32_t (&v)[4], const bool (&ok)[4],
                                        uint32_t* nextbm, int lvl, bool encode, long long& scout,
                                        uint32_t* buf, int& qcnt) {
@@ -245,21 +263,21 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const uint32_t (&u)[4
     }
   }
 #pragma unroll
-  for (int k = 0; k < 4; k++) wq_push(P, c[k], v[k], buf, qcnt);
+  for (int k = 0; k < 4; k++) wq_push(P, qa, c[k], v[k], buf, qcnt);
 }
 
 // ---- top-down, light vertices + chunk registration ------------------------
 template <bool kBig>
-__device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, unsigned long long qs,
+__device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, unsigned long long qs,
                          unsigned long long qe, uint32_t* nextbm, int lvl, bool encode,
                          long long& scout, int& qcnt) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
+  // First tile of each CTA is static (no atomic on the latency chain of
+  // small levels); the rest are handed out dynamically.
+  unsigned long long tile = blockIdx.x;
   for (;;) {
-    if (threadIdx.x == 0) s.bcast[1] = atomicAdd(&cnt[kTile], 1ull);
-    __syncthreads();
-    const unsigned long long start = qs + s.bcast[1] * (unsigned long long)kBlock;
-    __syncthreads();
+    const unsigned long long start = qs + tile * (unsigned long long)kBlock;
     if (start >= qe) break;
     const unsigned long long i = start + threadIdx.x;
     uint32_t u = 0;
@@ -312,15 +330,19 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, unsigned lon
           v[k] = __ldg(P.out_nb + s.td.t_b[lo] + (ei - s.td.t_pre[lo]));
         }
       }
-      claim4<kBig>(P, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
+      claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
     }
+    if (threadIdx.x == 0 && start + kBlock < qe) s.bcast[1] = gridDim.x + atomicAdd(&cnt[kTile], 1ull);
+    __syncthreads();
+    if (start + kBlock >= qe) break;  // every later tile starts past qe too
+    tile = s.bcast[1];
     __syncthreads();
   }
 }
 
 // ---- top-down, heavy chunks: one warp per chunk, 4 edges per lane ---------
 template <bool kBig>
-__device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, unsigned long long nch,
+__device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, unsigned long long nch,
                          uint32_t* nextbm, int lvl, bool encode, long long& scout, int& qcnt) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
@@ -341,7 +363,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, unsigned lon
         ok[k] = j < ch.len;
         v[k] = ok[k] ? __ldg(P.out_nb + ch.start + j) : 0u;
       }
-      claim4<kBig>(P, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
+      claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
     }
   }
 }
@@ -372,7 +394,7 @@ __device__ void td_scout(const BfsParams& P, unsigned long long q0, unsigned lon
 // prefix sum.  Every lane keeps kBuSlots vertices in flight and refills a slot
 // (select-the-c-th-pending-vertex: shuffle binary search + __fns) as soon as
 // its vertex resolves, so one slow list never idles the other lanes.  Per
-// round a slot tests the next 2 in-neighbours of its vertex; after
+// round a slot tests the next kPerRound in-neighbours of its vertex; after
 // kLaneRounds rounds a still-unresolved vertex is deferred to the long list,
 // scanned after the sweep by whole warps with a ballot per 32 neighbours.
 // The chosen parent is the first in-neighbour (ascending) whose front bit is
@@ -380,7 +402,8 @@ __device__ void td_scout(const BfsParams& P, unsigned long long q0, unsigned lon
 // words and written back once per task; vertices without in-edges are
 // marked visited ("dead") the first time they are seen.
 constexpr int kBuSlots = 2;
-constexpr int kLaneRounds = 3;
+constexpr int kPerRound = 4;    // in-neighbours tested per slot per round
+constexpr int kLaneRounds = 8;  // rounds before a list is deferred to the long list
 
 __device__ __forceinline__ bool front_bit(const uint32_t* front, uint32_t u) {
   return (front[u >> 5] >> (u & 31u)) & 1u;
@@ -460,23 +483,24 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         if (next_c >= total) break;
         continue;
       }
-      uint32_t u0[kBuSlots], u1[kBuSlots];
+      uint32_t u[kBuSlots][kPerRound];
 #pragma unroll
       for (int k = 0; k < kBuSlots; k++) {
-        u0[k] = st[k] ? __ldg(P.in_nb + b[k]) : 0u;
-        u1[k] = (st[k] && d[k] > 1) ? __ldg(P.in_nb + b[k] + 1) : 0u;
+#pragma unroll
+        for (int j = 0; j < kPerRound; j++)
+          u[k][j] = (st[k] && d[k] > (uint32_t)j) ? __ldg(P.in_nb + b[k] + j) : 0u;
       }
 #pragma unroll
       for (int k = 0; k < kBuSlots; k++) {
         if (!st[k]) continue;
         bool hit = false;
         uint32_t par = 0;
-        if (front_bit(front, u0[k])) {
-          hit = true;
-          par = u0[k];
-        } else if (d[k] > 1 && front_bit(front, u1[k])) {
-          hit = true;
-          par = u1[k];
+#pragma unroll
+        for (int j = 0; j < kPerRound; j++) {
+          if (!hit && d[k] > (uint32_t)j && front_bit(front, u[k][j])) {
+            hit = true;
+            par = u[k][j];
+          }
         }
         if (hit) {
           P.parent[v[k]] = (int32_t)par;
@@ -484,7 +508,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
           atomicOr(&acc_n[(v[k] >> 5) & 31u], 1u << (v[k] & 31u));
           st[k] = 0;
         } else {
-          const uint32_t tk = d[k] < 2 ? d[k] : 2u;
+          const uint32_t tk = d[k] < (uint32_t)kPerRound ? d[k] : (uint32_t)kPerRound;
           b[k] += tk;
           d[k] -= tk;
           if (d[k] == 0) {
@@ -508,7 +532,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
 }
 
 // Long in-lists deferred by bu_step: one warp per vertex, ballot over 32
-// neighbours at a time, resuming after the 2*kLaneRounds already tested.
+// neighbours at a time, resuming after the kPerRound*kLaneRounds tested.
 __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* next,
                         unsigned long long base, unsigned long long count, int lvl, long long& awake) {
   const unsigned lane = lane_id();
@@ -517,7 +541,7 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
   for (long long i = gw; i < (long long)count; i += nw) {
     const uint32_t v = __ldcg(P.queue + base + i);
     const int64_t le = P.in_off[v + 1];
-    for (int64_t j = P.in_off[v] + 2 * kLaneRounds; j < le; j += 32) {
+    for (int64_t j = P.in_off[v] + kPerRound * kLaneRounds; j < le; j += 32) {
       const int64_t jj = j + lane;
       bool h = false;
       uint32_t u = 0;
@@ -542,7 +566,7 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
 }
 
 // ---- BitmapToQueue (bfs.hpp:99-113) ----------------------------------------
-__device__ void b2q(const BfsParams& P, const uint32_t* front, SmemT& s) {
+__device__ void b2q(const BfsParams& P, const QApp& qa, const uint32_t* front, SmemT& s) {
   for (long long base = (long long)blockIdx.x * kBlock; base < P.w32;
        base += (long long)gridDim.x * kBlock) {
     const long long w = base + threadIdx.x;
@@ -550,7 +574,7 @@ __device__ void b2q(const BfsParams& P, const uint32_t* front, SmemT& s) {
     int64_t tot;
     const int64_t pre = block_exscan(__popc(word), &tot, s);
     if (tot == 0) continue;
-    if (threadIdx.x == 0) s.bcast[0] = atomicAdd(&P.ctrl->tail, (unsigned long long)tot);
+    if (threadIdx.x == 0) s.bcast[0] = qa.base + atomicAdd(qa.ctr, (unsigned long long)tot);
     __syncthreads();
     unsigned long long q = s.bcast[0] + pre;
     while (word) {
@@ -578,7 +602,7 @@ __device__ void log_step(const BfsParams& P, long long idx, int dir, long long f
 __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   extern __shared__ uint4 dyn_smem[];
   __shared__ SmemT s;
-  unsigned gen = 0, ph = 0;
+  unsigned ph = 0;
   const long long gtid = (long long)blockIdx.x * kBlock + threadIdx.x;
   const long long gthreads = (long long)gridDim.x * kBlock;
   const uint32_t src = P.src;
@@ -608,18 +632,18 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       P.visited[i] = 0u;
     }
   }
-  if (!grid_sync(P, s, gen, ph, kTagInit)) return;
+  if (!grid_sync(P, s, ph, kTagInit)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // bfs.hpp:132-136
     P.parent[src] = (int32_t)src;
     if (P.want_depth) P.depth[src] = 0;
     P.visited[src >> 5] = 1u << (src & 31u);
     P.queue[0] = src;
-    P.ctrl->tail = 1;
   }
-  if (!grid_sync(P, s, gen, ph, kTagInit)) return;
+  if (!grid_sync(P, s, ph, kTagInit)) return;
 
   const bool encode = P.strategy != GK_BFS_TOP_DOWN_RESCAN;
   unsigned long long qs = 0, qe = 1;
+  unsigned long long qtail = 1;  // queue entries written so far (uniform)
   long long etc = P.m;                                  // bfs.hpp:139
   long long scout = P.out_off[src + 1] - P.out_off[src];  // bfs.hpp:140
   long long nsteps = 0;
@@ -634,12 +658,12 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
     if (P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha) {
       if (!front_ready) {  // QueueToBitmap into a cleared front (bfs.hpp:145)
         for (long long i = gtid; i < P.w32; i += gthreads) frontg[i] = 0u;
-        if (!grid_sync(P, s, gen, ph, kTagZero)) return;
+        if (!grid_sync(P, s, ph, kTagZero)) return;
         for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
           const uint32_t v = __ldcg(P.queue + i);
           atomicOr(frontg + (v >> 5), 1u << (v & 31u));
         }
-        if (!grid_sync(P, s, gen, ph, kTagQ2B)) return;
+        if (!grid_sync(P, s, ph, kTagQ2B)) return;
       }
       long long awake = (long long)(qe - qs);  // bfs.hpp:146
       qs = qe;                                 // bfs.hpp:147
@@ -658,7 +682,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         bu_step(P, s, ph, fr, nextg, lvl, lbase, acc);
         unsigned set = ph & 3;
         block_add(acc, &P.ctrl->cnt[set][kSum], s);
-        if (!grid_sync(P, s, gen, ph, kTagBU)) return;
+        if (!grid_sync(P, s, ph, kTagBU)) return;
         const unsigned long long nlong = ld_volatile(&P.ctrl->cnt[set][kLongCount]);
         long long awake_bu = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
         if (nlong) {
@@ -666,7 +690,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
           bu_long(P, fr, nextg, lbase, nlong, lvl, acc);
           set = ph & 3;
           block_add(acc, &P.ctrl->cnt[set][kSum], s);
-          if (!grid_sync(P, s, gen, ph, kTagLong)) return;
+          if (!grid_sync(P, s, ph, kTagLong)) return;
           awake_bu += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
         }
         awake = awake_bu;
@@ -676,9 +700,11 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         frontg = nextg;
         nextg = t;
       } while (awake >= old_awake || awake > P.n / P.beta);
-      b2q(P, frontg, s);  // bfs.hpp:155
-      if (!grid_sync(P, s, gen, ph, kTagB2Q)) return;
-      qe = ld_volatile(&P.ctrl->cnt[ph & 3][kTailSnap]);
+      const unsigned bset = ph & 3;
+      b2q(P, qapp(P, ph, qtail), frontg, s);  // bfs.hpp:155
+      if (!grid_sync(P, s, ph, kTagB2Q)) return;
+      qtail += ld_volatile(&P.ctrl->cnt[bset][kAppend]);
+      qe = qtail;
       scout = 1;  // bfs.hpp:156
       front_ready = true;
     } else {
@@ -693,34 +719,38 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       unsigned set;
       if (big) {
         for (long long i = gtid; i < P.w32; i += gthreads) nextg[i] = 0u;
-        if (!grid_sync(P, s, gen, ph, kTagZero)) return;
-        td_light<true>(P, s, ph, qs, qe, nextg, lvl, encode, sacc, qcnt);
-      } else {
-        td_light<false>(P, s, ph, qs, qe, nextg, lvl, encode, sacc, qcnt);
+        if (!grid_sync(P, s, ph, kTagZero)) return;
       }
-      wq_flush(P, s.td.qbuf[threadIdx.x >> 5], qcnt);
       set = ph & 3;
+      {
+        const QApp qa = qapp(P, ph, qtail);
+        if (big) td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt);
+        else td_light<false>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt);
+        wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+      }
       block_add(sacc, &P.ctrl->cnt[set][kSum], s);
-      if (!grid_sync(P, s, gen, ph, kTagTD)) return;
+      if (!grid_sync(P, s, ph, kTagTD)) return;
       scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+      qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
       const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
       if (nch) {
         sacc = 0;
         set = ph & 3;
-        if (big) td_heavy<true>(P, s, ph, nch, nextg, lvl, encode, sacc, qcnt);
-        else td_heavy<false>(P, s, ph, nch, nextg, lvl, encode, sacc, qcnt);
-        wq_flush(P, s.td.qbuf[threadIdx.x >> 5], qcnt);
+        const QApp qa = qapp(P, ph, qtail);
+        if (big) td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt);
+        else td_heavy<false>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt);
+        wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
         block_add(sacc, &P.ctrl->cnt[set][kSum], s);
-        if (!grid_sync(P, s, gen, ph, kTagHeavy)) return;
+        if (!grid_sync(P, s, ph, kTagHeavy)) return;
         scout += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
       }
       if (big) {
-        const unsigned long long q1 = ld_volatile(&P.ctrl->cnt[ph & 3][kTailSnap]);
         sacc = 0;
         set = ph & 3;
-        td_scout(P, qe, q1, lvl, encode, sacc);
+        td_scout(P, qe, qtail, lvl, encode, sacc);
         block_add(sacc, &P.ctrl->cnt[set][kSum], s);
-        if (!grid_sync(P, s, gen, ph, kTagSweep)) return;
+        if (!grid_sync(P, s, ph, kTagSweep)) return;
         scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
         uint32_t* t = frontg;
         frontg = nextg;
@@ -730,7 +760,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         front_ready = false;
       }
       qs = qe;  // SlideWindow (bfs.hpp:160)
-      qe = ld_volatile(&P.ctrl->cnt[ph & 3][kTailSnap]);
+      qe = qtail;
       if (P.strategy == GK_BFS_TOP_DOWN_RESCAN) {  // bfs.hpp:161-167
         long long tot = 0;
         for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
@@ -739,7 +769,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         }
         set = ph & 3;
         block_add(tot, &P.ctrl->cnt[set][kSum], s);
-        if (!grid_sync(P, s, gen, ph, kTagRescan)) return;
+        if (!grid_sync(P, s, ph, kTagRescan)) return;
         scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
       }
       log_step(P, nsteps++, 'T', fsize, scout, etc);

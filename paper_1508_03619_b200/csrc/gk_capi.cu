@@ -354,8 +354,8 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
       char buf[256];
       snprintf(buf, sizeof(buf),
                "bfs kernel watchdog fired (grid barrier timeout): CTA barrier counts min %u max %u, "
-               "arrived %u, gen %u, tail %llu",
-               lo, hi, ctrl.bar_count, ctrl.bar_gen, (unsigned long long)ctrl.tail);
+               "arrivals %llu",
+               lo, hi, (unsigned long long)ctrl.bar_count);
       return fail(GK_ERR_TIMEOUT, buf);
     }
     return fail(GK_ERR_CUDA, "bfs kernel: heavy-chunk buffer overflow");

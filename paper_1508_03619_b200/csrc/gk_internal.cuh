@@ -27,19 +27,18 @@ namespace gk {
 // Counter ring: a phase (the interval between two grid barriers) that
 // accumulates counters uses set ph&3; set (ph+2)&3 is zeroed by CTA 0
 // during phase ph (its last reader finished before barrier ph).
-// kTailSnap: queue tail as of the barrier that starts the phase, written by
-// the last CTA to arrive (the live tail moves as soon as fast CTAs append).
+// kAppend: queue entries appended during the phase (appends of a phase go
+// to tail + fetch-add on it; one live tail would race with the next phase's
+// appends).  kLongCount: bottom-up vertices deferred to the long list.
 constexpr int kTraceCap = 512;
 enum PhaseTag : unsigned char { kTagInit = 'I', kTagTD = 'T', kTagHeavy = 'H', kTagZero = 'Z', kTagQ2B = 'Q',
                                 kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S', kTagLong = 'L' };
-enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kTailSnap = 4, kLongCount = 5, kSlots = 8 };
+enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend = 4, kLongCount = 5, kSlots = 8 };
 
 struct Ctrl {
-  unsigned int bar_count;
-  unsigned int bar_gen;
+  unsigned long long bar_count;  // monotonic grid-barrier arrivals
   int error;
   int pad0;
-  unsigned long long tail;  // sliding-queue append cursor
   long long num_steps;
   long long pad1;
   unsigned long long cnt[4][kSlots];
