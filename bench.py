@@ -208,6 +208,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of reference CPU BFS work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-model", action="store_true")
+    ap.add_argument("--verbose", action="store_true", help="per-source times on stderr")
     args = ap.parse_args()
     # OpenMP settings for the reference CPU legs (must precede libgomp init).
     os.environ.setdefault("OMP_WAIT_POLICY", "active")
@@ -279,6 +280,9 @@ def main():
         dev_ms.append(r.device_ms)
     wall = time.time() - tw0
     clocks = clk.stop()
+    if args.verbose:
+        for s, t in zip(sources, dev_ms):
+            print(f"rank {rank} src {s}: {t:.3f} ms  m_cc {m_of[s]}  {sched_of[s][:40]}", file=sys.stderr)
 
     # e2e: the C-ABI call with the ParentArray returned to host memory
     pin = PinnedBuffer(g.n)
@@ -337,7 +341,8 @@ def main():
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
 
-    scheds = sorted(set(sched_of.values()), key=len)
+    scheds = sorted(set(v if len(v) <= 48 else f"{v[:40]}...({len(v)} steps)" for v in sched_of.values()),
+                    key=len)
     line = {
         "metric": "BFS GTEPS (harmonic mean over sources) and % of HBM roofline",
         "value": value, "unit": "GTEPS", "n_gpus": world, "steps": K, "warmup": W,

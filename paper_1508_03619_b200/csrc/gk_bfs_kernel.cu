@@ -73,6 +73,30 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
   return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
+// L2 cache policy hints: the bitmaps (visited / front, n/8 bytes each) are
+// the only reused working set, the graph arrays stream past them.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Bitmap word, bypassing L1 (other SMs update bitmaps within a phase), kept in L2.
+__device__ __forceinline__ uint32_t ld_bits(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+  return v;
+}
+// Read-only front bitmap word within a bottom-up phase: L1-cacheable, kept in L2.
+__device__ __forceinline__ uint32_t ld_front(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+  return v;
+}
+// Graph data: read-only path, default L2 policy (an evict-first hint made
+// bottom-up slower: the next round re-reads the same neighbour sector).
+__device__ __forceinline__ uint32_t ld_nb(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ int64_t ld_off(const int64_t* p) { return __ldg(p); }
+
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -229,10 +253,11 @@ __device__ __forceinline__ void on_claim(const BfsParams& P, uint32_t u, uint32_
 
 // Claim up to 4 edges (u_k -> v_k) per thread with their loads and atomics
 // issued together (bfs.hpp:77-84).  The visited word is read from L2 first
-// so already-visited targets cost no atomic.  kBig (large frontiers):
-// claimed vertices are also OR-ed into the next-frontier bitmap (so a
-// following bottom-up step needs no QueueToBitmap) and their degrees are
-// summed afterwards by td_scout instead of inline.
+// so already-visited targets cost no atomic.  kBig (large frontiers): the
+// claims go only into the next-frontier bitmap (a following bottom-up step
+// needs no QueueToBitmap, a following top-down step converts it with
+// BitmapToQueue), and their degrees are summed afterwards by td_scout_bits
+// in vertex order instead of by random reads at claim time.
 template <bool kBig>
 __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const uint32_t (&u)[4],
                                        const uint32_t (&v)[4], const bool (&ok)[4],
@@ -241,7 +266,7 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
   uint32_t w[4];
   bool c[4];
 #pragma unroll
-  for (int k = 0; k < 4; k++) w[k] = ok[k] ? __ldcg(P.visited + (v[k] >> 5)) : 0xffffffffu;
+  for (int k = 0; k < 4; k++) w[k] = ok[k] ? ld_bits(P.visited + (v[k] >> 5)) : 0xffffffffu;
 #pragma unroll
   for (int k = 0; k < 4; k++) c[k] = !((w[k] >> (v[k] & 31u)) & 1u);
 #pragma unroll
@@ -262,8 +287,10 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
       }
     }
   }
+  if (!kBig) {
 #pragma unroll
-  for (int k = 0; k < 4; k++) wq_push(P, qa, c[k], v[k], buf, qcnt);
+    for (int k = 0; k < 4; k++) wq_push(P, qa, c[k], v[k], buf, qcnt);
+  }
 }
 
 // ---- top-down, light vertices + chunk registration ------------------------
@@ -327,7 +354,7 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
             else hi = mid - 1;
           }
           uu[k] = s.td.t_u[lo];
-          v[k] = __ldg(P.out_nb + s.td.t_b[lo] + (ei - s.td.t_pre[lo]));
+          v[k] = ld_nb(P.out_nb + s.td.t_b[lo] + (ei - s.td.t_pre[lo]));
         }
       }
       claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
@@ -361,7 +388,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       for (int k = 0; k < 4; k++) {
         const uint32_t j = o + lane + 32u * k;
         ok[k] = j < ch.len;
-        v[k] = ok[k] ? __ldg(P.out_nb + ch.start + j) : 0u;
+        v[k] = ok[k] ? ld_nb(P.out_nb + ch.start + j) : 0u;
       }
       claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
     }
@@ -371,19 +398,36 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
 // ---- degrees of the vertices a large top-down step claimed ----------------
 // scout = sum of -old over the claims (bfs.hpp:83) = sum of max(deg, 1)
 // with the degree encoding, or the claim count without it (bfs.hpp:129).
-__device__ void td_scout(const BfsParams& P, unsigned long long q0, unsigned long long q1, int lvl,
-                         bool encode, long long& scout) {
-  const long long gtid = (long long)blockIdx.x * kBlock + threadIdx.x;
-  const long long gthreads = (long long)gridDim.x * kBlock;
-#pragma unroll 4
-  for (unsigned long long i = q0 + gtid; i < q1; i += gthreads) {
-    const uint32_t v = __ldcg(P.queue + i);
-    if (P.want_depth) P.depth[v] = lvl + 1;
-    if (encode) {
-      const long long d = P.out_off[v + 1] - P.out_off[v];
-      scout += d ? d : 1;
-    } else {
-      scout += 1;
+// Walks the claim bitmap in vertex order, kSW words per warp iteration, so
+// the degree reads are coalesced offset runs instead of random gathers.
+constexpr int kSW = 4;
+__device__ void td_scout_bits(const BfsParams& P, const uint32_t* bm, int lvl, bool encode,
+                              long long& scout, long long& count) {
+  const unsigned lane = lane_id();
+  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  for (long long w0 = gw * kSW; w0 < P.w32; w0 += nw * kSW) {
+    uint32_t wd[kSW];
+    int64_t o0[kSW], o1[kSW];
+#pragma unroll
+    for (int k = 0; k < kSW; k++) wd[k] = (w0 + k < P.w32) ? ld_bits(bm + w0 + k) : 0u;
+#pragma unroll
+    for (int k = 0; k < kSW; k++) {
+      o0[k] = o1[k] = 0;
+      if ((wd[k] >> lane) & 1u) {
+        const int64_t v = (w0 + k) * 32 + lane;
+        o0[k] = __ldg(P.out_off + v);
+        o1[k] = __ldg(P.out_off + v + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kSW; k++) {
+      if ((wd[k] >> lane) & 1u) {
+        const long long d = o1[k] - o0[k];
+        scout += encode ? (d ? d : 1) : 1;
+        if (P.want_depth) P.depth[(w0 + k) * 32 + lane] = lvl + 1;
+      }
+      if (lane == 0) count += __popc(wd[k]);
     }
   }
 }
@@ -405,10 +449,14 @@ constexpr int kBuSlots = 2;
 constexpr int kPerRound = 4;    // in-neighbours tested per slot per round
 constexpr int kLaneRounds = 8;  // rounds before a list is deferred to the long list
 
+// front is either the global bitmap or its shared-memory copy (small graphs).
+template <bool kSmem>
 __device__ __forceinline__ bool front_bit(const uint32_t* front, uint32_t u) {
-  return (front[u >> 5] >> (u & 31u)) & 1u;
+  const uint32_t w = kSmem ? front[u >> 5] : ld_front(front + (u >> 5));
+  return (w >> (u & 31u)) & 1u;
 }
 
+template <bool kSmem>
 __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_t* front, uint32_t* next,
                         int lvl, unsigned long long long_base, long long& awake) {
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -421,7 +469,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
     const long long w = (t << 5) + lane;
     uint32_t vis = 0xffffffffu, pad = 0u;
     if (w < P.w32) {
-      vis = __ldcg(P.visited + w);
+      vis = ld_bits(P.visited + w);
       const int64_t rem = P.n - w * 32;  // mask off ids >= n in the last word
       if (rem < 32) pad = 0xffffffffu << rem;
     }
@@ -466,8 +514,8 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         const int ex = __shfl_sync(kFull, excl, lo);
         if (need && c < total) {
           v[k] = (uint32_t)(((t << 5) + lo) * 32 + (int)__fns(m, 0, c - ex + 1));
-          b[k] = P.in_off[v[k]];
-          d[k] = (uint32_t)(P.in_off[v[k] + 1] - b[k]);
+          b[k] = ld_off(P.in_off + v[k]);
+          d[k] = (uint32_t)(ld_off(P.in_off + v[k] + 1) - b[k]);
           rounds[k] = 0;
           st[k] = 1;
           if (d[k] == 0) {  // no in-edges: never reachable; skip it from now on
@@ -488,7 +536,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
       for (int k = 0; k < kBuSlots; k++) {
 #pragma unroll
         for (int j = 0; j < kPerRound; j++)
-          u[k][j] = (st[k] && d[k] > (uint32_t)j) ? __ldg(P.in_nb + b[k] + j) : 0u;
+          u[k][j] = (st[k] && d[k] > (uint32_t)j) ? ld_nb(P.in_nb + b[k] + j) : 0u;
       }
 #pragma unroll
       for (int k = 0; k < kBuSlots; k++) {
@@ -497,7 +545,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         uint32_t par = 0;
 #pragma unroll
         for (int j = 0; j < kPerRound; j++) {
-          if (!hit && d[k] > (uint32_t)j && front_bit(front, u[k][j])) {
+          if (!hit && d[k] > (uint32_t)j && front_bit<kSmem>(front, u[k][j])) {
             hit = true;
             par = u[k][j];
           }
@@ -533,6 +581,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
 
 // Long in-lists deferred by bu_step: one warp per vertex, ballot over 32
 // neighbours at a time, resuming after the kPerRound*kLaneRounds tested.
+template <bool kSmem>
 __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* next,
                         unsigned long long base, unsigned long long count, int lvl, long long& awake) {
   const unsigned lane = lane_id();
@@ -546,8 +595,8 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
       bool h = false;
       uint32_t u = 0;
       if (jj < le) {
-        u = __ldg(P.in_nb + jj);
-        h = front_bit(front, u);
+        u = ld_nb(P.in_nb + jj);
+        h = front_bit<kSmem>(front, u);
       }
       const unsigned bal = __ballot_sync(kFull, h);
       if (bal) {
@@ -650,12 +699,21 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   int lvl = 0;
   int qcnt = 0;
   bool front_ready = false;  // frontg holds exactly the current frontier
+  bool queue_stale = false;  // the current frontier's queue window is not written yet
   uint32_t* frontg = P.bm0;
   uint32_t* nextg = P.bm1;
   uint32_t* sfront = reinterpret_cast<uint32_t*>(dyn_smem);
 
   while (qe > qs) {
-    if (P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha) {
+    const bool go_bu = P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha;
+    if (!go_bu && queue_stale) {  // BitmapToQueue for the coming top-down step
+      const unsigned bset = ph & 3;
+      b2q(P, qapp(P, ph, qtail), frontg, s);
+      if (!grid_sync(P, s, ph, kTagB2Q)) return;
+      qtail += ld_volatile(&P.ctrl->cnt[bset][kAppend]);
+      queue_stale = false;
+    }
+    if (go_bu) {
       if (!front_ready) {  // QueueToBitmap into a cleared front (bfs.hpp:145)
         for (long long i = gtid; i < P.w32; i += gthreads) frontg[i] = 0u;
         if (!grid_sync(P, s, ph, kTagZero)) return;
@@ -666,7 +724,11 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         if (!grid_sync(P, s, ph, kTagQ2B)) return;
       }
       long long awake = (long long)(qe - qs);  // bfs.hpp:146
-      qs = qe;                                 // bfs.hpp:147
+      if (queue_stale) {  // the bitmap-only frontier's queue window is never written
+        qe = qtail;
+        queue_stale = false;
+      }
+      qs = qe;  // bfs.hpp:147
       long long old_awake;
       do {  // bfs.hpp:149-154
         old_awake = awake;
@@ -679,7 +741,8 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         long long acc = 0;
         // long-list scratch: queue slots past the tail are unused during bottom-up
         const unsigned long long lbase = qe;
-        bu_step(P, s, ph, fr, nextg, lvl, lbase, acc);
+        if (P.front_in_smem) bu_step<true>(P, s, ph, fr, nextg, lvl, lbase, acc);
+        else bu_step<false>(P, s, ph, fr, nextg, lvl, lbase, acc);
         unsigned set = ph & 3;
         block_add(acc, &P.ctrl->cnt[set][kSum], s);
         if (!grid_sync(P, s, ph, kTagBU)) return;
@@ -687,7 +750,8 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         long long awake_bu = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
         if (nlong) {
           acc = 0;
-          bu_long(P, fr, nextg, lbase, nlong, lvl, acc);
+          if (P.front_in_smem) bu_long<true>(P, fr, nextg, lbase, nlong, lvl, acc);
+          else bu_long<false>(P, fr, nextg, lbase, nlong, lvl, acc);
           set = ph & 3;
           block_add(acc, &P.ctrl->cnt[set][kSum], s);
           if (!grid_sync(P, s, ph, kTagLong)) return;
@@ -724,9 +788,12 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       set = ph & 3;
       {
         const QApp qa = qapp(P, ph, qtail);
-        if (big) td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt);
-        else td_light<false>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt);
-        wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+        if (big) {
+          td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt);
+        } else {
+          td_light<false>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt);
+          wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+        }
       }
       block_add(sacc, &P.ctrl->cnt[set][kSum], s);
       if (!grid_sync(P, s, ph, kTagTD)) return;
@@ -737,30 +804,42 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         sacc = 0;
         set = ph & 3;
         const QApp qa = qapp(P, ph, qtail);
-        if (big) td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt);
-        else td_heavy<false>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt);
-        wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+        if (big) {
+          td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt);
+        } else {
+          td_heavy<false>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt);
+          wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+        }
         block_add(sacc, &P.ctrl->cnt[set][kSum], s);
         if (!grid_sync(P, s, ph, kTagHeavy)) return;
         scout += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
         qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
       }
       if (big) {
+        long long cacc = 0;
         sacc = 0;
         set = ph & 3;
-        td_scout(P, qe, qtail, lvl, encode, sacc);
+        td_scout_bits(P, nextg, lvl, encode, sacc, cacc);
         block_add(sacc, &P.ctrl->cnt[set][kSum], s);
+        block_add(cacc, &P.ctrl->cnt[set][kCount], s);
         if (!grid_sync(P, s, ph, kTagSweep)) return;
         scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        const unsigned long long claimed = ld_volatile(&P.ctrl->cnt[set][kCount]);
         uint32_t* t = frontg;
         frontg = nextg;
         nextg = t;
         front_ready = true;
+        // The new frontier exists only as a bitmap; its queue window is
+        // [qtail, qtail + claimed), materialised by BitmapToQueue only if a
+        // top-down step follows.
+        qs = qtail;
+        qe = qtail + claimed;
+        queue_stale = true;
       } else {
         front_ready = false;
+        qs = qe;  // SlideWindow (bfs.hpp:160)
+        qe = qtail;
       }
-      qs = qe;  // SlideWindow (bfs.hpp:160)
-      qe = qtail;
       if (P.strategy == GK_BFS_TOP_DOWN_RESCAN) {  // bfs.hpp:161-167
         long long tot = 0;
         for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {

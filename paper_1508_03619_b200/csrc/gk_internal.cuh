@@ -33,7 +33,7 @@ namespace gk {
 constexpr int kTraceCap = 512;
 enum PhaseTag : unsigned char { kTagInit = 'I', kTagTD = 'T', kTagHeavy = 'H', kTagZero = 'Z', kTagQ2B = 'Q',
                                 kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S', kTagLong = 'L' };
-enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend = 4, kLongCount = 5, kSlots = 8 };
+enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend = 4, kLongCount = 5, kCount = 6, kSlots = 8 };
 
 struct Ctrl {
   unsigned long long bar_count;  // monotonic grid-barrier arrivals
