@@ -86,6 +86,13 @@ __device__ __forceinline__ uint32_t ld_bits(const uint32_t* p) {
   asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
   return v;
 }
+// Visited word for a claim pre-check: may be served stale from L1 (bits
+// are only ever set, so a stale 0 merely costs the atomic that follows).
+__device__ __forceinline__ uint32_t ld_bits_l1(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.ca.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+  return v;
+}
 // Read-only front bitmap word within a bottom-up phase: L1-cacheable, kept in L2.
 __device__ __forceinline__ uint32_t ld_front(const uint32_t* p) {
   uint32_t v;
@@ -266,7 +273,7 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
   uint32_t w[4];
   bool c[4];
 #pragma unroll
-  for (int k = 0; k < 4; k++) w[k] = ok[k] ? ld_bits(P.visited + (v[k] >> 5)) : 0xffffffffu;
+  for (int k = 0; k < 4; k++) w[k] = ok[k] ? ld_bits_l1(P.visited + (v[k] >> 5)) : 0xffffffffu;
 #pragma unroll
   for (int k = 0; k < 4; k++) c[k] = !((w[k] >> (v[k] & 31u)) & 1u);
 #pragma unroll
