@@ -102,6 +102,21 @@ __device__ __forceinline__ uint32_t ld_front(const uint32_t* p) {
 // Graph data: read-only path, default L2 policy (an evict-first hint made
 // bottom-up slower: the next round re-reads the same neighbour sector).
 __device__ __forceinline__ uint32_t ld_nb(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Top-down edge lists are read exactly once per step: stream them.
+__device__ __forceinline__ uint32_t ld_nb_once(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_first()));
+  return v;
+}
+// Random parent writes: do not let them displace the bitmaps in L2.
+__device__ __forceinline__ void st_parent(int32_t* p, int32_t v) {
+  asm volatile("st.global.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(policy_evict_first()) : "memory");
+}
 __device__ __forceinline__ int64_t ld_off(const int64_t* p) { return __ldg(p); }
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -157,7 +172,8 @@ __device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& ph, unsigned c
   }
   __syncthreads();
   ph++;
-  return s.ok != 0;
+  // Profiling aid (GK_STOP_AFTER): every CTA leaves after the same barrier.
+  return s.ok != 0 && ph < P.stop_after;
 }
 
 // Exclusive scan of one int64 per thread across the CTA; *total gets the sum.
@@ -272,6 +288,28 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
                                        uint32_t* buf, int& qcnt) {
   uint32_t w[4];
   bool c[4];
+  if (kBig) {
+    // Fire-and-forget claims: a target is taken when neither its visited
+    // bit nor its next-frontier bit is set; racing writers all store a valid
+    // parent (any frontier neighbour) and OR the same next bit.  visited is
+    // folded in afterwards by td_scout_bits.  No atomic round trip sits on
+    // the chain, and the next-bit pre-check filters repeat targets once the
+    // first RED lands.
+    uint32_t x[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      w[k] = ok[k] ? ld_bits_l1(P.visited + (v[k] >> 5)) : 0xffffffffu;
+      x[k] = ok[k] ? ld_bits(nextbm + (v[k] >> 5)) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      if (!(((w[k] | x[k]) >> (v[k] & 31u)) & 1u)) {
+        st_parent(P.parent + v[k], (int32_t)u[k]);
+        atomicOr(nextbm + (v[k] >> 5), 1u << (v[k] & 31u));  // result unused -> RED
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < 4; k++) w[k] = ok[k] ? ld_bits_l1(P.visited + (v[k] >> 5)) : 0xffffffffu;
 #pragma unroll
@@ -284,20 +322,10 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
     }
   }
 #pragma unroll
-  for (int k = 0; k < 4; k++) {
-    if (c[k]) {
-      P.parent[v[k]] = (int32_t)u[k];
-      if (kBig) {
-        atomicOr(nextbm + (v[k] >> 5), 1u << (v[k] & 31u));  // result unused -> RED
-      } else {
-        on_claim(P, u[k], v[k], lvl, encode, scout);
-      }
-    }
-  }
-  if (!kBig) {
+  for (int k = 0; k < 4; k++)
+    if (c[k]) on_claim(P, u[k], v[k], lvl, encode, scout);
 #pragma unroll
-    for (int k = 0; k < 4; k++) wq_push(P, qa, c[k], v[k], buf, qcnt);
-  }
+  for (int k = 0; k < 4; k++) wq_push(P, qa, c[k], v[k], buf, qcnt);
 }
 
 // ---- top-down, light vertices + chunk registration ------------------------
@@ -361,7 +389,7 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
             else hi = mid - 1;
           }
           uu[k] = s.td.t_u[lo];
-          v[k] = ld_nb(P.out_nb + s.td.t_b[lo] + (ei - s.td.t_pre[lo]));
+          v[k] = ld_nb_once(P.out_nb + s.td.t_b[lo] + (ei - s.td.t_pre[lo]));
         }
       }
       claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
@@ -374,18 +402,17 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
   }
 }
 
-// ---- top-down, heavy chunks: one warp per chunk, 4 edges per lane ---------
+// ---- top-down, heavy chunks: one warp per chunk, 4 edges per lane in flight --
 template <bool kBig>
 __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, unsigned long long nch,
                          uint32_t* nextbm, int lvl, bool encode, long long& scout, int& qcnt) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
-  unsigned long long* cnt = P.ctrl->cnt[ph & 3];
   const unsigned lane = lane_id();
-  for (;;) {
-    unsigned long long c = 0;
-    if (lane == 0) c = atomicAdd(&cnt[kChunkNext], 1ull);
-    c = __shfl_sync(kFull, c, 0);
-    if (c >= nch) break;
+  // Chunks are equal-sized (kChunk edges but the tails), so a static
+  // round-robin over warps balances without a contended grab counter.
+  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  for (unsigned long long c = gw; c < nch; c += nw) {
     const Chunk ch = P.chunks[c];
     const uint32_t uu[4] = {ch.u, ch.u, ch.u, ch.u};
     for (uint32_t o = 0; o < ch.len; o += 128) {
@@ -395,7 +422,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       for (int k = 0; k < 4; k++) {
         const uint32_t j = o + lane + 32u * k;
         ok[k] = j < ch.len;
-        v[k] = ok[k] ? ld_nb(P.out_nb + ch.start + j) : 0u;
+        v[k] = ok[k] ? ld_nb_once(P.out_nb + ch.start + j) : 0u;
       }
       claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
     }
@@ -418,6 +445,14 @@ __device__ void td_scout_bits(const BfsParams& P, const uint32_t* bm, int lvl, b
     int64_t o0[kSW], o1[kSW];
 #pragma unroll
     for (int k = 0; k < kSW; k++) wd[k] = (w0 + k < P.w32) ? ld_bits(bm + w0 + k) : 0u;
+    // fold the claims into visited (one owner per word)
+    if (lane < kSW && w0 + lane < P.w32) {
+      uint32_t mine = wd[0];
+#pragma unroll
+      for (int k = 1; k < kSW; k++)
+        if ((int)lane == k) mine = wd[k];
+      if (mine) P.visited[w0 + lane] |= mine;
+    }
 #pragma unroll
     for (int k = 0; k < kSW; k++) {
       o0[k] = o1[k] = 0;

@@ -331,6 +331,8 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   p.step_cap = g->step_cap;
   p.timeout_ns = 20ull * 1000 * 1000 * 1000;
   if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
+  p.stop_after = 0xffffffffu;
+  if (const char* sa = getenv("GK_STOP_AFTER")) p.stop_after = (unsigned)strtoul(sa, nullptr, 10);
 
   cudaStream_t s = g->stream;
   CK(cudaEventRecord(g->ev0, s), "event record");

@@ -83,6 +83,7 @@ struct BfsParams {
   gk_step* steps;
   int64_t step_cap;
   unsigned long long timeout_ns;
+  unsigned stop_after;  // leave after this many grid barriers (profiling only)
 };
 
 constexpr int kBlock = 512;
