@@ -156,6 +156,57 @@ GK_API gk_status gk_bfs_byte_model(gk_graph* g, const gk_step* steps,
 /* Keep depths on the device for subsequent gk_bfs calls (for the model). */
 GK_API gk_status gk_bfs_keep_depth(gk_graph* g, int32_t keep);
 
+/* ---- Sharded (1D-partitioned) traversal, SURVEY.md §8(e) ----------------
+ * Rank r of P owns vertices [r*block, min(n, (r+1)*block)), block =
+ * ceil(n/P) rounded up to a multiple of 32.  A gk_shard holds the owned CSR
+ * rows (global neighbour ids) and owned BFS state.  The level loop of
+ * bfs.hpp:139-169 and the exchanges between these calls (all-reduce of
+ * counters, all-to-all of (v,u) claim pairs, all-gather of bitmap slices)
+ * are run by the host orchestrator (paper_1508_03619_b200/dist.py).  All
+ * kernels run on the stream set with gk_shard_set_stream. */
+typedef struct gk_shard gk_shard;
+GK_API const char* gk_shard_last_error(void);
+/* This rank's rows of the device-generated graph (same graph as
+ * gk_graph_generate). */
+GK_API gk_status gk_shard_generate(int kind, int scale, int degree, uint64_t seed,
+                                   int permute, int rank, int nranks, int device,
+                                   gk_shard** out);
+/* This rank's rows from host arrays: local_offsets has (hi-lo+1) entries
+ * starting at 0; neighbours are global ids (undirected graphs). */
+GK_API gk_status gk_shard_upload(int64_t num_nodes, int rank, int nranks,
+                                 const int64_t* local_offsets,
+                                 const uint32_t* neighbors, int device,
+                                 gk_shard** out);
+GK_API void gk_shard_free(gk_shard* s);
+GK_API gk_status gk_shard_info(const gk_shard* s, int64_t* num_nodes, int64_t* lo,
+                               int64_t* hi, int64_t* local_arcs, int64_t* block);
+GK_API gk_status gk_shard_set_stream(gk_shard* s, void* cuda_stream);
+GK_API gk_status gk_shard_degree(const gk_shard* s, uint32_t v, int64_t* degree);
+GK_API gk_status gk_shard_begin(gk_shard* s, uint32_t source, int32_t strategy,
+                                int32_t want_depth);
+/* Top-down over the owned queue window [qs, qe): local[0..1] = claims made
+ * in place and their scout; dest_counts[r] = claim pairs (v<<32|u) for rank
+ * r, written contiguously by rank into pairs_out_dev (device, capacity
+ * pairs_cap >= local arcs suffices).  dedup: send each remote target at most
+ * once this level (clears an n-bit sent map; worth it for large frontiers). */
+GK_API gk_status gk_shard_td_expand(gk_shard* s, uint64_t qs, uint64_t qe,
+                                    int32_t level, int32_t dedup, int64_t* local,
+                                    int64_t* dest_counts, uint64_t* pairs_out_dev,
+                                    int64_t pairs_cap);
+GK_API gk_status gk_shard_td_apply(gk_shard* s, const uint64_t* pairs_dev,
+                                   int64_t npairs, int32_t level, int64_t* out);
+GK_API gk_status gk_shard_tail(gk_shard* s, uint64_t* tail);
+GK_API gk_status gk_shard_rescan(gk_shard* s, uint64_t qs, uint64_t qe,
+                                 int64_t* degree_total);
+GK_API gk_status gk_shard_q2b(gk_shard* s, uint64_t qs, uint64_t qe,
+                              uint32_t* slice_dev);
+GK_API gk_status gk_shard_bu(gk_shard* s, const uint32_t* front_dev,
+                             uint32_t* next_slice_dev, int32_t level,
+                             int64_t* awake);
+GK_API gk_status gk_shard_b2q(gk_shard* s, const uint32_t* slice_dev);
+GK_API gk_status gk_shard_result(gk_shard* s, int32_t* parent_out,
+                                 int32_t* depth_out, int64_t* counts);
+
 /* Pinned host buffers for end-to-end transfers. */
 GK_API void* gk_host_alloc(int64_t bytes);
 GK_API void gk_host_free(void* p);

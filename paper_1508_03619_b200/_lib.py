@@ -29,6 +29,9 @@ EXPORTED = (
     "gk_graph_generate", "gk_graph_generate_grid", "gk_graph_free", "gk_graph_info",
     "gk_graph_download", "gk_pick_sources", "gk_bfs", "gk_bfs_device_parent",
     "gk_bfs_byte_model", "gk_bfs_keep_depth", "gk_host_alloc", "gk_host_free", "gk_bfs_trace",
+    "gk_shard_last_error", "gk_shard_generate", "gk_shard_upload", "gk_shard_free", "gk_shard_info",
+    "gk_shard_set_stream", "gk_shard_degree", "gk_shard_begin", "gk_shard_td_expand", "gk_shard_td_apply",
+    "gk_shard_tail", "gk_shard_rescan", "gk_shard_q2b", "gk_shard_bu", "gk_shard_b2q", "gk_shard_result",
 )
 
 
@@ -79,13 +82,32 @@ def load() -> C.CDLL:
     L.gk_bfs_byte_model.argtypes = [vp, C.POINTER(Step), i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.gk_bfs_keep_depth.argtypes = [vp, i32]
     L.gk_bfs_trace.argtypes = [vp, C.POINTER(C.c_uint64), C.c_char_p, i32, C.POINTER(i32)]
+    L.gk_shard_last_error.restype = C.c_char_p
+    L.gk_shard_generate.argtypes = [C.c_int, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.POINTER(vp)]
+    L.gk_shard_upload.argtypes = [i64, C.c_int, C.c_int, vp, vp, C.c_int, C.POINTER(vp)]
+    L.gk_shard_free.argtypes = [vp]
+    L.gk_shard_free.restype = None
+    L.gk_shard_info.argtypes = [vp] + [C.POINTER(i64)] * 5
+    L.gk_shard_set_stream.argtypes = [vp, vp]
+    L.gk_shard_degree.argtypes = [vp, u32, C.POINTER(i64)]
+    L.gk_shard_begin.argtypes = [vp, u32, i32, i32]
+    L.gk_shard_td_expand.argtypes = [vp, u64, u64, i32, i32, vp, vp, vp, i64]
+    L.gk_shard_td_apply.argtypes = [vp, vp, i64, i32, vp]
+    L.gk_shard_tail.argtypes = [vp, C.POINTER(u64)]
+    L.gk_shard_rescan.argtypes = [vp, u64, u64, C.POINTER(i64)]
+    L.gk_shard_q2b.argtypes = [vp, u64, u64, vp]
+    L.gk_shard_bu.argtypes = [vp, vp, vp, i32, C.POINTER(i64)]
+    L.gk_shard_b2q.argtypes = [vp, vp]
+    L.gk_shard_result.argtypes = [vp, vp, vp, vp]
     L.gk_host_alloc.argtypes = [i64]
     L.gk_host_alloc.restype = vp
     L.gk_host_free.argtypes = [vp]
     L.gk_host_free.restype = None
     for f in EXPORTED:
         if f not in ("gk_last_error", "gk_abi_version", "gk_device_count", "gk_graph_free",
-                     "gk_bfs_device_parent", "gk_host_alloc", "gk_host_free"):
+                     "gk_bfs_device_parent", "gk_host_alloc", "gk_host_free", "gk_shard_last_error",
+                     "gk_shard_free"):
             getattr(L, f).restype = C.c_int
     _lib = L
     return L

@@ -185,7 +185,7 @@ gk_status gk_graph_generate(int kind, int scale, int degree, uint64_t seed, int 
   if (st != GK_OK) return st;
   gk::DevCsr csr;
   std::string err;
-  cudaError_t e = gk::build_generated(kind, scale, degree, seed, permute, &csr, &err);
+  cudaError_t e = gk::build_generated(kind, scale, degree, seed, permute, 0, -1, &csr, &err);
   if (e != cudaSuccess) return cuda_fail(e, err.empty() ? "device graph build" : err.c_str());
   auto* g = new gk_graph;
   g->device = device;

@@ -108,13 +108,15 @@ cudaError_t byte_model(const BfsParams& p, const int32_t* depth, const char* dir
 
 // Device graph construction (gk_graph_build.cu).
 struct DevCsr {
-  int64_t n = 0;
-  int64_t m = 0;
+  int64_t n = 0;   // global vertex count
+  int64_t lo = 0;  // rows [lo, hi) are stored; offsets are local to lo
+  int64_t hi = 0;
+  int64_t m = 0;   // stored arcs
   int64_t* off = nullptr;
   uint32_t* nb = nullptr;
 };
-cudaError_t build_generated(int kind, int scale, int degree, uint64_t seed, int permute,
-                            DevCsr* out, std::string* err);
+cudaError_t build_generated(int kind, int scale, int degree, uint64_t seed, int permute, int64_t klo,
+                            int64_t khi, DevCsr* out, std::string* err);
 cudaError_t build_grid(int64_t rows, int64_t cols, double p_delete, double p_diag,
                        uint64_t seed, DevCsr* out, std::string* err);
 

@@ -1,0 +1,841 @@
+// gk_shard.cu -- one rank's part of the 1D-partitioned BFS.
+//
+// Vertex v is owned by rank v / block (block = ceil(n/P) rounded up to a
+// multiple of 32 so every rank's slice of a bitmap is whole words).  A rank
+// stores the CSR rows of its owned vertices (global neighbour ids), their
+// parent / visited state, and its local frontier queue.  The host
+// orchestrator (paper_1508_03619_b200/dist.py) runs the reference's level
+// loop (bfs.hpp:139-169) and performs the exchanges between these kernels:
+//   top-down  : expand the owned frontier; owned targets are claimed in place,
+//               remote targets become (v, u) pairs bucketed by owner (deduped
+//               per level with a sent-bitmap) -> all-to-all -> td_apply
+//   bottom-up : owned unvisited vertices scan their in-lists against the
+//               replicated n-bit front bitmap; the owned slice of `next` is
+//               then all-gathered
+// The single-GPU path is the persistent kernel in gk_bfs_kernel.cu; this file
+// is the multi-GPU path, launched per phase on a caller-provided stream so
+// the exchanges (NCCL through torch.distributed) order with the kernels.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "gk_internal.cuh"
+
+namespace gk {
+namespace {
+
+constexpr int kSB = 512;             // block size of the shard kernels
+constexpr int64_t kShHeavy = 1024;   // degree above which a vertex is chunked
+constexpr int kShChunk = 1024;
+constexpr unsigned kFullMask = 0xffffffffu;
+
+// device counter slots
+enum : int { cTail = 0, cPairs = 1, cScout = 2, cClaims = 3, cAwake = 4, cChunks = 5, cDest = 8 };
+
+struct ShardParams {
+  int64_t n, lo, hi, nloc, block;
+  int rank, nranks;
+  const int64_t* off;
+  const uint32_t* nb;
+  int32_t* parent;
+  int32_t* depth;
+  uint32_t* visited;  // local, nloc bits
+  uint32_t* sent;     // global n bits: remote targets already sent this level
+  uint32_t* queue;
+  uint64_t* pairs;    // outbox (unsorted)
+  uint64_t* pairs_out;
+  int64_t pair_cap;
+  Chunk* chunks;
+  int64_t chunk_cap;
+  unsigned long long* ctr;
+  int want_depth;
+  int encode;
+  int dedup;  // use (and set) the sent bitmap this level
+};
+
+__device__ __forceinline__ unsigned lmask_lt() {
+  unsigned r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// Warp-aggregated append of one value per active lane into arr at *cursor.
+template <typename T>
+__device__ __forceinline__ void warp_append(bool want, T val, T* arr, unsigned long long* cursor,
+                                            int64_t cap, int* overflow) {
+  const unsigned m = __ballot_sync(kFullMask, want);
+  if (!m) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(cursor, (unsigned long long)__popc(m));
+  base = __shfl_sync(kFullMask, base, leader);
+  if (want) {
+    const unsigned long long pos = base + __popc(m & lmask_lt());
+    if ((int64_t)pos < cap) arr[pos] = val;
+    else *overflow = 1;
+  }
+}
+
+__device__ __forceinline__ long long local_degree(const ShardParams& P, uint32_t v) {
+  const int64_t r = (int64_t)v - P.lo;
+  return P.off[r + 1] - P.off[r];
+}
+
+// Claim owned v for parent u; returns true if this thread won.
+__device__ __forceinline__ bool claim_local(const ShardParams& P, uint32_t v, uint32_t u, int lvl,
+                                            long long& scout) {
+  const uint32_t r = (uint32_t)((int64_t)v - P.lo);
+  const uint32_t bit = 1u << (r & 31u);
+  uint32_t* w = P.visited + (r >> 5);
+  if (__ldcg(w) & bit) return false;
+  if (atomicOr(w, bit) & bit) return false;
+  P.parent[r] = (int32_t)u;
+  if (P.want_depth) P.depth[r] = lvl + 1;
+  if (P.encode) {
+    const long long d = local_degree(P, v);
+    scout += d ? d : 1;  // -old of the degree-encoded slot (bfs.hpp:83)
+  } else {
+    scout += 1;
+  }
+  return true;
+}
+
+// One edge (u -> v) of the owned frontier: claim in place or post a pair.
+__device__ __forceinline__ void td_edge(const ShardParams& P, bool ok, uint32_t u, uint32_t v, int lvl,
+                                        long long& scout, long long& claims, int* overflow) {
+  bool local = false, remote = false;
+  if (ok) {
+    const int owner = (int)((int64_t)v / P.block);
+    if (owner == P.rank) {
+      local = claim_local(P, v, u, lvl, scout);
+    } else {
+      if (P.dedup) {
+        const uint32_t bit = 1u << (v & 31u);
+        uint32_t* w = P.sent + (v >> 5);
+        remote = !(__ldcg(w) & bit) && !(atomicOr(w, bit) & bit);
+      } else {
+        remote = true;
+      }
+    }
+  }
+  claims += local;
+  warp_append<uint32_t>(local, v, P.queue, &P.ctr[cTail], P.nloc + 1, overflow);
+  warp_append<uint64_t>(remote, ((uint64_t)v << 32) | u, P.pairs, &P.ctr[cPairs], P.pair_cap, overflow);
+}
+
+__device__ void block_sum2(long long a, long long b, unsigned long long* da, unsigned long long* db) {
+  __shared__ long long red[2][kSB / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(kFullMask, a, o);
+    b += __shfl_down_sync(kFullMask, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = a;
+    red[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long ta = 0, tb = 0;
+    for (int i = 0; i < kSB / 32; i++) {
+      ta += red[0][i];
+      tb += red[1][i];
+    }
+    if (ta) atomicAdd(da, (unsigned long long)ta);
+    if (tb) atomicAdd(db, (unsigned long long)tb);
+  }
+}
+
+__global__ void k_sh_init(ShardParams P) {
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gs = (long long)gridDim.x * blockDim.x;
+  for (long long i = gt; i < P.nloc; i += gs) {
+    P.parent[i] = -1;
+    if (P.want_depth) P.depth[i] = -1;
+  }
+  for (long long i = gt; i < (P.nloc + 31) / 32; i += gs) P.visited[i] = 0u;
+}
+
+__global__ void k_sh_set_source(ShardParams P, uint32_t src) {
+  const uint32_t r = (uint32_t)((int64_t)src - P.lo);
+  P.parent[r] = (int32_t)src;
+  if (P.want_depth) P.depth[r] = 0;
+  P.visited[r >> 5] |= 1u << (r & 31u);
+  P.queue[0] = src;
+  P.ctr[cTail] = 1;
+}
+
+// Top-down expansion of queue[qs, qe): tiles of kSB frontier vertices, CTA
+// scan of degrees, load-balanced edge gather; vertices of degree > kShHeavy
+// become kShChunk-edge chunks handled by k_sh_td_heavy.
+__global__ void __launch_bounds__(kSB) k_sh_td_light(ShardParams P, unsigned long long qs, unsigned long long qe,
+                                                     int lvl) {
+  __shared__ int64_t t_b[kSB];
+  __shared__ int64_t t_pre[kSB + 1];
+  __shared__ uint32_t t_u[kSB];
+  __shared__ int64_t wsum[kSB / 32 + 1];
+  __shared__ int overflow;
+  if (threadIdx.x == 0) overflow = 0;
+  __syncthreads();
+  long long scout = 0, claims = 0;
+  for (unsigned long long tile = blockIdx.x; qs + tile * kSB < qe; tile += gridDim.x) {
+    const unsigned long long i = qs + tile * kSB + threadIdx.x;
+    uint32_t u = 0;
+    int64_t b = 0, dl = 0;
+    if (i < qe) {
+      u = __ldcg(P.queue + i);
+      const int64_t r = (int64_t)u - P.lo;
+      b = P.off[r];
+      const int64_t d = P.off[r + 1] - b;
+      if (d > kShHeavy) {
+        const int64_t nch = (d + kShChunk - 1) / kShChunk;
+        const unsigned long long base = atomicAdd(&P.ctr[cChunks], (unsigned long long)nch);
+        if ((int64_t)(base + nch) <= P.chunk_cap) {
+          for (int64_t c = 0; c < nch; c++) {
+            Chunk ch;
+            ch.u = u;
+            ch.start = b + c * kShChunk;
+            ch.len = (uint32_t)((d - c * kShChunk) < kShChunk ? (d - c * kShChunk) : kShChunk);
+            P.chunks[base + c] = ch;
+          }
+        } else {
+          overflow = 1;
+        }
+      } else {
+        dl = d;
+      }
+    }
+    // CTA exclusive scan of dl
+    int64_t incl = dl;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(kFullMask, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t run = 0;
+      for (int w = 0; w < kSB / 32; w++) {
+        const int64_t t = wsum[w];
+        wsum[w] = run;
+        run += t;
+      }
+      wsum[kSB / 32] = run;
+    }
+    __syncthreads();
+    t_pre[threadIdx.x] = wsum[warp] + incl - dl;
+    t_u[threadIdx.x] = u;
+    t_b[threadIdx.x] = b;
+    const int64_t tot = wsum[kSB / 32];
+    __syncthreads();
+    for (int64_t eb = 0; eb < tot; eb += kSB) {
+      const int64_t ei = eb + threadIdx.x;
+      bool ok = ei < tot;
+      uint32_t uu = 0, v = 0;
+      if (ok) {
+        int lo = 0, hi = kSB - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (t_pre[mid] <= ei) lo = mid;
+          else hi = mid - 1;
+        }
+        uu = t_u[lo];
+        v = __ldg(P.nb + t_b[lo] + (ei - t_pre[lo]));
+      }
+      td_edge(P, ok, uu, v, lvl, scout, claims, &overflow);
+    }
+    __syncthreads();
+  }
+  block_sum2(scout, claims, &P.ctr[cScout], &P.ctr[cClaims]);
+  if (threadIdx.x == 0 && overflow) atomicExch((unsigned*)&P.ctr[7], 1u);
+}
+
+__global__ void __launch_bounds__(kSB) k_sh_td_heavy(ShardParams P, unsigned long long nch, int lvl) {
+  __shared__ int overflow;
+  if (threadIdx.x == 0) overflow = 0;
+  __syncthreads();
+  long long scout = 0, claims = 0;
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (unsigned long long c = gw; c < nch; c += nw) {
+    const Chunk ch = P.chunks[c];
+    for (uint32_t o = 0; o < ch.len; o += 32) {
+      const uint32_t j = o + lane;
+      const bool ok = j < ch.len;
+      const uint32_t v = ok ? __ldg(P.nb + ch.start + j) : 0u;
+      td_edge(P, ok, ch.u, v, lvl, scout, claims, &overflow);
+    }
+  }
+  block_sum2(scout, claims, &P.ctr[cScout], &P.ctr[cClaims]);
+  if (threadIdx.x == 0 && overflow) atomicExch((unsigned*)&P.ctr[7], 1u);
+}
+
+// Bucket the outbox by owner rank: count, then scatter into pairs_out at
+// per-destination offsets (exclusive scan done on the host, P is small).
+__global__ void k_sh_count_dest(ShardParams P, unsigned long long npairs) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < npairs;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t v = (uint32_t)(P.pairs[i] >> 32);
+    atomicAdd(&P.ctr[cDest + (int)((int64_t)v / P.block)], 1ull);
+  }
+}
+__global__ void k_sh_scatter_dest(ShardParams P, unsigned long long npairs, unsigned long long* cursor) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < npairs;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint64_t pr = P.pairs[i];
+    const int d = (int)((int64_t)(pr >> 32) / P.block);
+    P.pairs_out[atomicAdd(&cursor[d], 1ull)] = pr;
+  }
+}
+
+// Received (v, u) pairs: claim owned v.
+__global__ void __launch_bounds__(kSB) k_sh_td_apply(ShardParams P, const uint64_t* in, unsigned long long npairs,
+                                                     int lvl) {
+  __shared__ int overflow;
+  if (threadIdx.x == 0) overflow = 0;
+  __syncthreads();
+  long long scout = 0, claims = 0;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x;
+  for (unsigned long long i0 = 0; i0 < npairs; i0 += stride) {
+    const unsigned long long i = i0 + base + threadIdx.x;
+    bool won = false;
+    uint32_t v = 0;
+    if (i < npairs) {
+      const uint64_t pr = in[i];
+      v = (uint32_t)(pr >> 32);
+      won = claim_local(P, v, (uint32_t)pr, lvl, scout);
+    }
+    claims += won;
+    warp_append<uint32_t>(won, v, P.queue, &P.ctr[cTail], P.nloc + 1, &overflow);
+  }
+  block_sum2(scout, claims, &P.ctr[cScout], &P.ctr[cClaims]);
+  if (threadIdx.x == 0 && overflow) atomicExch((unsigned*)&P.ctr[7], 1u);
+}
+
+// Owned slice of the front bitmap from queue[qs, qe) (QueueToBitmap).
+__global__ void k_sh_q2b(ShardParams P, unsigned long long qs, unsigned long long qe, uint32_t* slice) {
+  for (unsigned long long i = qs + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < qe;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)((int64_t)__ldcg(P.queue + i) - P.lo);
+    atomicOr(slice + (r >> 5), 1u << (r & 31u));
+  }
+}
+
+// Bottom-up sweep of the owned vertices against the replicated front
+// (bfs.hpp:47-66): lane per vertex, 4 in-neighbours per round, then
+// warp-cooperative ballots; parent = first in-neighbour (ascending) with its
+// front bit, as the reference picks.
+__global__ void __launch_bounds__(kSB) k_sh_bu(ShardParams P, const uint32_t* front, uint32_t* next_slice, int lvl) {
+  long long awake = 0;
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long w32 = (P.nloc + 31) / 32;
+  for (long long w = gw; w < w32; w += nw) {
+    const uint32_t vis = __ldcg(P.visited + w);
+    const int64_t r = w * 32 + lane;
+    bool pend = r < P.nloc && !((vis >> lane) & 1u);
+    if (__ballot_sync(kFullMask, pend) == 0) {
+      if (lane == 0) next_slice[w] = 0u;
+      continue;
+    }
+    bool found = false, dead = false;
+    uint32_t par = 0;
+    int64_t b = 0, e = 0;
+    if (pend) {
+      b = P.off[r];
+      e = P.off[r + 1];
+      if (b == e) {
+        dead = true;
+        pend = false;
+      }
+    }
+    for (int round = 0; round < 4 && __ballot_sync(kFullMask, pend); round++) {
+      if (pend) {
+        uint32_t u[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) u[j] = (b + j < e) ? __ldg(P.nb + b + j) : 0u;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          if (!found && b + j < e && ((front[u[j] >> 5] >> (u[j] & 31u)) & 1u)) {
+            found = true;
+            par = u[j];
+          }
+        }
+        if (found) pend = false;
+        else {
+          b += 4;
+          pend = b < e;
+        }
+      }
+    }
+    unsigned pm = __ballot_sync(kFullMask, pend);
+    while (pm) {
+      const int l = __ffs(pm) - 1;
+      pm &= pm - 1;
+      const int64_t lb = __shfl_sync(kFullMask, b, l), le = __shfl_sync(kFullMask, e, l);
+      for (int64_t j = lb; j < le; j += 32) {
+        const int64_t jj = j + lane;
+        uint32_t u = 0;
+        bool h = false;
+        if (jj < le) {
+          u = __ldg(P.nb + jj);
+          h = (front[u >> 5] >> (u & 31u)) & 1u;
+        }
+        const unsigned bal = __ballot_sync(kFullMask, h);
+        if (bal) {
+          const uint32_t hu = __shfl_sync(kFullMask, u, __ffs(bal) - 1);
+          if (lane == l) {
+            found = true;
+            par = hu;
+          }
+          break;
+        }
+      }
+    }
+    if (found) {
+      P.parent[r] = (int32_t)par;
+      if (P.want_depth) P.depth[r] = lvl + 1;
+    }
+    const unsigned nbits = __ballot_sync(kFullMask, found), dbits = __ballot_sync(kFullMask, dead);
+    if (lane == 0) {
+      next_slice[w] = nbits;
+      if (nbits | dbits) P.visited[w] = vis | nbits | dbits;
+      awake += __popc(nbits);
+    }
+  }
+  block_sum2(awake, 0, &P.ctr[cAwake], &P.ctr[cAwake]);
+}
+
+// Queue from the owned slice of the front (BitmapToQueue, bfs.hpp:99-113).
+__global__ void k_sh_b2q(ShardParams P, const uint32_t* slice) {
+  const long long w32 = (P.nloc + 31) / 32;
+  int overflow = 0;
+  for (long long w0 = (long long)blockIdx.x * blockDim.x; w0 < w32; w0 += (long long)gridDim.x * blockDim.x) {
+    const long long w = w0 + threadIdx.x;
+    uint32_t word = w < w32 ? __ldcg(slice + w) : 0u;
+    // one warp-aggregated append per set bit round
+    while (__ballot_sync(kFullMask, word != 0)) {
+      const bool has = word != 0;
+      uint32_t v = 0;
+      if (has) {
+        const int bp = __ffs(word) - 1;
+        word &= word - 1;
+        v = (uint32_t)(P.lo + w * 32 + bp);
+      }
+      warp_append<uint32_t>(has, v, P.queue, &P.ctr[cTail], P.nloc + 1, &overflow);
+    }
+  }
+}
+
+// m_cc contribution: (reached, sum of degrees of reached owned vertices).
+__global__ void k_sh_count(ShardParams P, unsigned long long* out) {
+  long long r = 0, d = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P.nloc;
+       i += (long long)gridDim.x * blockDim.x)
+    if (P.parent[i] >= 0) {
+      r++;
+      d += P.off[i + 1] - P.off[i];
+    }
+  block_sum2(r, d, out, out + 1);
+}
+
+int grid_of(int64_t work) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long want = (work + kSB - 1) / kSB;
+  return (int)std::max<long long>(1, std::min<long long>(want, (long long)sms * 4));
+}
+
+}  // namespace
+}  // namespace gk
+
+// ---------------------------------------------------------------- C ABI
+struct gk_shard {
+  int device = 0;
+  int rank = 0, nranks = 1;
+  int64_t n = 0, lo = 0, hi = 0, nloc = 0, block = 0, m = 0;
+  int64_t* off = nullptr;
+  uint32_t* nb = nullptr;
+  int32_t* parent = nullptr;
+  int32_t* depth = nullptr;
+  uint32_t* visited = nullptr;
+  uint32_t* sent = nullptr;
+  uint32_t* queue = nullptr;
+  uint64_t* pairs = nullptr;
+  int64_t pair_cap = 0;
+  gk::Chunk* chunks = nullptr;
+  int64_t chunk_cap = 0;
+  unsigned long long* ctr = nullptr;  // device counters
+  unsigned long long* acc = nullptr;
+  cudaStream_t stream = nullptr;  // caller's stream (e.g. torch's current stream)
+  int want_depth = 0;
+  int encode = 1;
+};
+
+namespace {
+thread_local std::string g_shard_err;
+gk_status shard_fail(gk_status st, const std::string& m) {
+  g_shard_err = m;
+  return st;
+}
+#define SCK(call, what)                                                                        \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return shard_fail(e_ == cudaErrorMemoryAllocation ? GK_ERR_OOM : GK_ERR_CUDA,            \
+                        std::string(what) + ": " + cudaGetErrorString(e_));                   \
+  } while (0)
+
+gk::ShardParams params(const gk_shard* s) {
+  gk::ShardParams p{};
+  p.n = s->n;
+  p.lo = s->lo;
+  p.hi = s->hi;
+  p.nloc = s->nloc;
+  p.block = s->block;
+  p.rank = s->rank;
+  p.nranks = s->nranks;
+  p.off = s->off;
+  p.nb = s->nb;
+  p.parent = s->parent;
+  p.depth = s->depth;
+  p.visited = s->visited;
+  p.sent = s->sent;
+  p.queue = s->queue;
+  p.pairs = s->pairs;
+  p.pair_cap = s->pair_cap;
+  p.chunks = s->chunks;
+  p.chunk_cap = s->chunk_cap;
+  p.ctr = s->ctr;
+  p.want_depth = s->want_depth;
+  p.encode = s->encode;
+  return p;
+}
+
+gk_status shard_alloc(gk_shard* s) {
+  const int64_t wl = (s->nloc + 31) / 32 + 4, wg = (s->n + 31) / 32 + 4;
+  SCK(cudaMalloc(&s->parent, sizeof(int32_t) * std::max<int64_t>(s->nloc, 1)), "alloc parent");
+  SCK(cudaMalloc(&s->depth, sizeof(int32_t) * std::max<int64_t>(s->nloc, 1)), "alloc depth");
+  SCK(cudaMalloc(&s->visited, sizeof(uint32_t) * wl), "alloc visited");
+  SCK(cudaMalloc(&s->sent, sizeof(uint32_t) * wg), "alloc sent");
+  SCK(cudaMalloc(&s->queue, sizeof(uint32_t) * (s->nloc + 2)), "alloc queue");
+  s->pair_cap = std::max<int64_t>(s->m, 1024);
+  SCK(cudaMalloc(&s->pairs, sizeof(uint64_t) * s->pair_cap), "alloc pairs");
+  s->chunk_cap = 2 * (s->m / 1024) + 64;
+  SCK(cudaMalloc(&s->chunks, sizeof(gk::Chunk) * s->chunk_cap), "alloc chunks");
+  SCK(cudaMalloc(&s->ctr, sizeof(unsigned long long) * (gk::cDest + s->nranks + 8)), "alloc counters");
+  SCK(cudaMalloc(&s->acc, sizeof(unsigned long long) * 4), "alloc acc");
+  return GK_OK;
+}
+
+void shard_free(gk_shard* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  for (void* p : {(void*)s->off, (void*)s->nb, (void*)s->parent, (void*)s->depth, (void*)s->visited,
+                  (void*)s->sent, (void*)s->queue, (void*)s->pairs, (void*)s->chunks,
+                  (void*)s->ctr, (void*)s->acc})
+    cudaFree(p);
+  delete s;
+}
+
+int64_t block_of(int64_t n, int nranks) {
+  int64_t b = (n + nranks - 1) / nranks;
+  return (b + 31) / 32 * 32;
+}
+
+gk_status read_ctr(gk_shard* s, unsigned long long* h, int count) {
+  SCK(cudaMemcpyAsync(h, s->ctr, sizeof(unsigned long long) * count, cudaMemcpyDeviceToHost, s->stream), "D2H");
+  SCK(cudaStreamSynchronize(s->stream), "sync");
+  if (h[7]) return shard_fail(GK_ERR_CUDA, "shard buffer overflow");
+  return GK_OK;
+}
+}  // namespace
+
+extern "C" {
+
+GK_API const char* gk_shard_last_error(void) { return g_shard_err.c_str(); }
+
+GK_API gk_status gk_shard_generate(int kind, int scale, int degree, uint64_t seed, int permute, int rank,
+                                   int nranks, int device, gk_shard** out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return shard_fail(GK_ERR_INVALID, "bad shard spec");
+  if (kind != 0 && kind != 1) return shard_fail(GK_ERR_INVALID, "generator kind must be 0 or 1");
+  if (scale < 5 || scale > 31) return shard_fail(GK_ERR_INVALID, "sharded generator scale must be in [5, 31]");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return shard_fail(GK_ERR_NO_DEVICE, "no CUDA device available (no CPU fallback)");
+  SCK(cudaSetDevice(device), "cudaSetDevice");
+  auto* s = new gk_shard;
+  s->device = device;
+  s->rank = rank;
+  s->nranks = nranks;
+  s->n = int64_t{1} << scale;
+  s->block = block_of(s->n, nranks);
+  s->lo = std::min<int64_t>(s->n, rank * s->block);
+  s->hi = std::min<int64_t>(s->n, s->lo + s->block);
+  s->nloc = s->hi - s->lo;
+  gk::DevCsr csr;
+  std::string err;
+  cudaError_t e = gk::build_generated(kind, scale, degree, seed, permute, s->lo, s->hi, &csr, &err);
+  if (e != cudaSuccess) {
+    delete s;
+    return shard_fail(GK_ERR_CUDA, err.empty() ? cudaGetErrorString(e) : err);
+  }
+  s->off = csr.off;
+  s->nb = csr.nb;
+  s->m = csr.m;
+  gk_status st = shard_alloc(s);
+  if (st != GK_OK) {
+    shard_free(s);
+    return st;
+  }
+  *out = s;
+  return GK_OK;
+}
+
+GK_API gk_status gk_shard_upload(int64_t n, int rank, int nranks, const int64_t* local_offsets,
+                                 const uint32_t* neighbors, int device, gk_shard** out) {
+  if (!out || !local_offsets || nranks < 1 || rank < 0 || rank >= nranks || n < 1)
+    return shard_fail(GK_ERR_INVALID, "bad shard spec");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return shard_fail(GK_ERR_NO_DEVICE, "no CUDA device available (no CPU fallback)");
+  SCK(cudaSetDevice(device), "cudaSetDevice");
+  auto* s = new gk_shard;
+  s->device = device;
+  s->rank = rank;
+  s->nranks = nranks;
+  s->n = n;
+  s->block = block_of(n, nranks);
+  s->lo = std::min<int64_t>(n, rank * s->block);
+  s->hi = std::min<int64_t>(n, s->lo + s->block);
+  s->nloc = s->hi - s->lo;
+  s->m = local_offsets[s->nloc];
+  cudaError_t e;
+  if ((e = cudaMalloc(&s->off, sizeof(int64_t) * (s->nloc + 3))) ||
+      (e = cudaMalloc(&s->nb, sizeof(uint32_t) * std::max<int64_t>(s->m, 1))) ||
+      (e = cudaMemcpy(s->off, local_offsets, sizeof(int64_t) * (s->nloc + 1), cudaMemcpyHostToDevice)) ||
+      (s->m && (e = cudaMemcpy(s->nb, neighbors, sizeof(uint32_t) * s->m, cudaMemcpyHostToDevice)))) {
+    shard_free(s);
+    return shard_fail(GK_ERR_CUDA, cudaGetErrorString(e));
+  }
+  gk_status st = shard_alloc(s);
+  if (st != GK_OK) {
+    shard_free(s);
+    return st;
+  }
+  *out = s;
+  return GK_OK;
+}
+
+GK_API void gk_shard_free(gk_shard* s) { shard_free(s); }
+
+GK_API gk_status gk_shard_info(const gk_shard* s, int64_t* n, int64_t* lo, int64_t* hi, int64_t* arcs,
+                               int64_t* block) {
+  if (!s) return shard_fail(GK_ERR_INVALID, "null shard");
+  if (n) *n = s->n;
+  if (lo) *lo = s->lo;
+  if (hi) *hi = s->hi;
+  if (arcs) *arcs = s->m;
+  if (block) *block = s->block;
+  return GK_OK;
+}
+
+GK_API gk_status gk_shard_set_stream(gk_shard* s, void* stream) {
+  if (!s) return shard_fail(GK_ERR_INVALID, "null shard");
+  s->stream = (cudaStream_t)stream;
+  return GK_OK;
+}
+
+GK_API gk_status gk_shard_degree(const gk_shard* s, uint32_t v, int64_t* deg) {
+  if (!s || !deg || (int64_t)v < s->lo || (int64_t)v >= s->hi) return shard_fail(GK_ERR_INVALID, "vertex not owned");
+  int64_t o[2];
+  SCK(cudaSetDevice(s->device), "cudaSetDevice");
+  SCK(cudaMemcpy(o, s->off + (v - s->lo), sizeof(o), cudaMemcpyDeviceToHost), "D2H");
+  *deg = o[1] - o[0];
+  return GK_OK;
+}
+
+// Start a traversal: reset owned state; the owner of src claims it.
+GK_API gk_status gk_shard_begin(gk_shard* s, uint32_t src, int32_t strategy, int32_t want_depth) {
+  if (!s) return shard_fail(GK_ERR_INVALID, "null shard");
+  if ((int64_t)src >= s->n) return shard_fail(GK_ERR_SOURCE_RANGE, "bfs source out of range");
+  SCK(cudaSetDevice(s->device), "cudaSetDevice");
+  s->want_depth = want_depth ? 1 : 0;
+  s->encode = strategy != GK_BFS_TOP_DOWN_RESCAN;
+  gk::ShardParams p = params(s);
+  SCK(cudaMemsetAsync(s->ctr, 0, sizeof(unsigned long long) * (gk::cDest + s->nranks + 8), s->stream), "memset");
+  gk::k_sh_init<<<gk::grid_of(s->nloc), gk::kSB, 0, s->stream>>>(p);
+  if ((int64_t)src >= s->lo && (int64_t)src < s->hi) gk::k_sh_set_source<<<1, 1, 0, s->stream>>>(p, src);
+  SCK(cudaGetLastError(), "begin");
+  return GK_OK;
+}
+
+// Top-down expansion of the owned window [qs, qe).  Outputs (host):
+//   local[0] = claims made in place, local[1] = their scout,
+//   dest_counts[r] = pairs for rank r, laid out by rank in *pairs_dev.
+GK_API gk_status gk_shard_td_expand(gk_shard* s, uint64_t qs, uint64_t qe, int32_t lvl, int32_t dedup,
+                                    int64_t* local, int64_t* dest_counts, uint64_t* pairs_out_dev,
+                                    int64_t pairs_cap) {
+  if (!s || !local || !dest_counts || (!pairs_out_dev && s->nranks > 1))
+    return shard_fail(GK_ERR_INVALID, "null argument");
+  SCK(cudaSetDevice(s->device), "cudaSetDevice");
+  gk::ShardParams p = params(s);
+  p.dedup = dedup ? 1 : 0;
+  p.pairs_out = pairs_out_dev;
+  const int P = s->nranks;
+  SCK(cudaMemsetAsync(s->ctr + gk::cPairs, 0, sizeof(unsigned long long), s->stream), "memset");
+  SCK(cudaMemsetAsync(s->ctr + gk::cScout, 0, sizeof(unsigned long long) * 2, s->stream), "memset");
+  SCK(cudaMemsetAsync(s->ctr + gk::cChunks, 0, sizeof(unsigned long long), s->stream), "memset");
+  SCK(cudaMemsetAsync(s->ctr + gk::cDest, 0, sizeof(unsigned long long) * P, s->stream), "memset");
+  if (dedup) SCK(cudaMemsetAsync(s->sent, 0, sizeof(uint32_t) * ((s->n + 31) / 32), s->stream), "memset");
+  gk::k_sh_td_light<<<gk::grid_of((int64_t)(qe - qs)), gk::kSB, 0, s->stream>>>(p, qs, qe, lvl);
+  SCK(cudaGetLastError(), "td_light");
+  unsigned long long h[gk::cDest + 64];
+  gk_status st = read_ctr(s, h, gk::cDest);
+  if (st != GK_OK) return st;
+  if (h[gk::cChunks]) {
+    gk::k_sh_td_heavy<<<gk::grid_of((int64_t)h[gk::cChunks] * 32), gk::kSB, 0, s->stream>>>(p, h[gk::cChunks], lvl);
+    SCK(cudaGetLastError(), "td_heavy");
+    st = read_ctr(s, h, gk::cDest);
+    if (st != GK_OK) return st;
+  }
+  const unsigned long long npairs = h[gk::cPairs];
+  if ((int64_t)npairs > pairs_cap) return shard_fail(GK_ERR_INVALID, "pairs buffer too small");
+  std::vector<unsigned long long> cursor(P, 0);
+  if (npairs) {
+    gk::k_sh_count_dest<<<gk::grid_of((int64_t)npairs), gk::kSB, 0, s->stream>>>(p, npairs);
+    SCK(cudaGetLastError(), "count_dest");
+    st = read_ctr(s, h, gk::cDest + P);
+    if (st != GK_OK) return st;
+    unsigned long long run = 0;
+    for (int r = 0; r < P; r++) {
+      cursor[r] = run;
+      run += h[gk::cDest + r];
+    }
+    SCK(cudaMemcpyAsync(s->ctr + gk::cDest, cursor.data(), sizeof(unsigned long long) * P, cudaMemcpyHostToDevice,
+                        s->stream),
+        "H2D");
+    gk::k_sh_scatter_dest<<<gk::grid_of((int64_t)npairs), gk::kSB, 0, s->stream>>>(p, npairs, s->ctr + gk::cDest);
+    SCK(cudaGetLastError(), "scatter_dest");
+  } else {
+    for (int r = 0; r < P; r++) h[gk::cDest + r] = 0;
+  }
+  for (int r = 0; r < P; r++) dest_counts[r] = npairs ? (int64_t)h[gk::cDest + r] : 0;
+  local[0] = (int64_t)h[gk::cClaims];
+  local[1] = (int64_t)h[gk::cScout];
+  SCK(cudaStreamSynchronize(s->stream), "td_expand");
+  return GK_OK;
+}
+
+// Claims from received pairs (device array, npairs entries).  out[0] =
+// claims, out[1] = scout; new queue entries are appended after the local ones.
+GK_API gk_status gk_shard_td_apply(gk_shard* s, const uint64_t* pairs_in, int64_t npairs, int32_t lvl,
+                                   int64_t* out) {
+  if (!s || !out) return shard_fail(GK_ERR_INVALID, "null argument");
+  SCK(cudaSetDevice(s->device), "cudaSetDevice");
+  gk::ShardParams p = params(s);
+  SCK(cudaMemsetAsync(s->ctr + gk::cScout, 0, sizeof(unsigned long long) * 2, s->stream), "memset");
+  if (npairs > 0) {
+    gk::k_sh_td_apply<<<gk::grid_of(npairs), gk::kSB, 0, s->stream>>>(p, pairs_in, (unsigned long long)npairs, lvl);
+    SCK(cudaGetLastError(), "td_apply");
+  }
+  unsigned long long h[gk::cDest];
+  gk_status st = read_ctr(s, h, gk::cDest);
+  if (st != GK_OK) return st;
+  out[0] = (int64_t)h[gk::cClaims];
+  out[1] = (int64_t)h[gk::cScout];
+  return GK_OK;
+}
+
+GK_API gk_status gk_shard_tail(gk_shard* s, uint64_t* tail) {
+  if (!s || !tail) return shard_fail(GK_ERR_INVALID, "null argument");
+  unsigned long long h[gk::cDest];
+  gk_status st = read_ctr(s, h, gk::cDest);
+  if (st != GK_OK) return st;
+  *tail = h[gk::cTail];
+  return GK_OK;
+}
+
+// Sum of degrees of the owned queue window (kTopDownRescan, bfs.hpp:161-167).
+GK_API gk_status gk_shard_rescan(gk_shard* s, uint64_t qs, uint64_t qe, int64_t* total) {
+  if (!s || !total) return shard_fail(GK_ERR_INVALID, "null argument");
+  std::vector<uint32_t> q(qe - qs);
+  std::vector<int64_t> off(s->nloc + 1);
+  SCK(cudaStreamSynchronize(s->stream), "sync");
+  if (qe > qs) SCK(cudaMemcpy(q.data(), s->queue + qs, sizeof(uint32_t) * (qe - qs), cudaMemcpyDeviceToHost), "D2H");
+  SCK(cudaMemcpy(off.data(), s->off, sizeof(int64_t) * (s->nloc + 1), cudaMemcpyDeviceToHost), "D2H");
+  int64_t t = 0;
+  for (uint32_t v : q) t += off[v - s->lo + 1] - off[v - s->lo];
+  *total = t;
+  return GK_OK;
+}
+
+// Owned slice (words) of the front bitmap from the queue window [qs, qe).
+GK_API gk_status gk_shard_q2b(gk_shard* s, uint64_t qs, uint64_t qe, uint32_t* slice_dev) {
+  if (!s || !slice_dev) return shard_fail(GK_ERR_INVALID, "null argument");
+  SCK(cudaSetDevice(s->device), "cudaSetDevice");
+  gk::ShardParams p = params(s);
+  SCK(cudaMemsetAsync(slice_dev, 0, sizeof(uint32_t) * (s->block / 32), s->stream), "memset");
+  if (qe > qs) gk::k_sh_q2b<<<gk::grid_of((int64_t)(qe - qs)), gk::kSB, 0, s->stream>>>(p, qs, qe, slice_dev);
+  SCK(cudaGetLastError(), "q2b");
+  return GK_OK;
+}
+
+// Bottom-up step: front_dev = replicated n-bit bitmap (block*nranks bits);
+// writes the owned slice of next; *awake = vertices found here.
+GK_API gk_status gk_shard_bu(gk_shard* s, const uint32_t* front_dev, uint32_t* next_slice_dev, int32_t lvl,
+                             int64_t* awake) {
+  if (!s || !front_dev || !next_slice_dev || !awake) return shard_fail(GK_ERR_INVALID, "null argument");
+  SCK(cudaSetDevice(s->device), "cudaSetDevice");
+  gk::ShardParams p = params(s);
+  SCK(cudaMemsetAsync(s->ctr + gk::cAwake, 0, sizeof(unsigned long long), s->stream), "memset");
+  SCK(cudaMemsetAsync(next_slice_dev, 0, sizeof(uint32_t) * (s->block / 32), s->stream), "memset");
+  gk::k_sh_bu<<<gk::grid_of(s->nloc), gk::kSB, 0, s->stream>>>(p, front_dev, next_slice_dev, lvl);
+  SCK(cudaGetLastError(), "bu");
+  unsigned long long h[gk::cDest];
+  gk_status st = read_ctr(s, h, gk::cDest);
+  if (st != GK_OK) return st;
+  *awake = (int64_t)h[gk::cAwake];
+  return GK_OK;
+}
+
+// Queue entries from the owned slice of the front (appended at the tail).
+GK_API gk_status gk_shard_b2q(gk_shard* s, const uint32_t* slice_dev) {
+  if (!s || !slice_dev) return shard_fail(GK_ERR_INVALID, "null argument");
+  SCK(cudaSetDevice(s->device), "cudaSetDevice");
+  gk::ShardParams p = params(s);
+  gk::k_sh_b2q<<<gk::grid_of((s->nloc + 31) / 32), gk::kSB, 0, s->stream>>>(p, slice_dev);
+  SCK(cudaGetLastError(), "b2q");
+  return GK_OK;
+}
+
+// Owned results: parent (and depth when requested) for [lo, hi), plus
+// counts[0] = reached, counts[1] = sum of degrees of reached owned vertices.
+GK_API gk_status gk_shard_result(gk_shard* s, int32_t* parent_out, int32_t* depth_out, int64_t* counts) {
+  if (!s) return shard_fail(GK_ERR_INVALID, "null shard");
+  SCK(cudaSetDevice(s->device), "cudaSetDevice");
+  if (counts) {
+    gk::ShardParams p = params(s);
+    SCK(cudaMemsetAsync(s->acc, 0, sizeof(unsigned long long) * 2, s->stream), "memset");
+    gk::k_sh_count<<<gk::grid_of(s->nloc), gk::kSB, 0, s->stream>>>(p, s->acc);
+    unsigned long long two[2];
+    SCK(cudaMemcpyAsync(two, s->acc, sizeof(two), cudaMemcpyDeviceToHost, s->stream), "D2H");
+    SCK(cudaStreamSynchronize(s->stream), "sync");
+    counts[0] = (int64_t)two[0];
+    counts[1] = (int64_t)two[1];
+  }
+  if (parent_out && s->nloc)
+    SCK(cudaMemcpyAsync(parent_out, s->parent, sizeof(int32_t) * s->nloc, cudaMemcpyDeviceToHost, s->stream), "D2H");
+  if (depth_out && s->nloc && s->want_depth)
+    SCK(cudaMemcpyAsync(depth_out, s->depth, sizeof(int32_t) * s->nloc, cudaMemcpyDeviceToHost, s->stream), "D2H");
+  SCK(cudaStreamSynchronize(s->stream), "sync");
+  return GK_OK;
+}
+
+}  // extern "C"
