@@ -181,6 +181,8 @@ GK_API void gk_shard_free(gk_shard* s);
 GK_API gk_status gk_shard_info(const gk_shard* s, int64_t* num_nodes, int64_t* lo,
                                int64_t* hi, int64_t* local_arcs, int64_t* block);
 GK_API gk_status gk_shard_set_stream(gk_shard* s, void* cuda_stream);
+/* Kernels this shard has launched so far (telemetry for the bench line). */
+GK_API int64_t gk_shard_launches(const gk_shard* s);
 GK_API gk_status gk_shard_degree(const gk_shard* s, uint32_t v, int64_t* degree);
 GK_API gk_status gk_shard_begin(gk_shard* s, uint32_t source, int32_t strategy,
                                 int32_t want_depth);

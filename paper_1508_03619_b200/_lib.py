@@ -32,6 +32,7 @@ EXPORTED = (
     "gk_shard_last_error", "gk_shard_generate", "gk_shard_upload", "gk_shard_free", "gk_shard_info",
     "gk_shard_set_stream", "gk_shard_degree", "gk_shard_begin", "gk_shard_td_expand", "gk_shard_td_apply",
     "gk_shard_tail", "gk_shard_rescan", "gk_shard_q2b", "gk_shard_bu", "gk_shard_b2q", "gk_shard_result",
+    "gk_shard_launches",
 )
 
 
@@ -90,6 +91,8 @@ def load() -> C.CDLL:
     L.gk_shard_free.restype = None
     L.gk_shard_info.argtypes = [vp] + [C.POINTER(i64)] * 5
     L.gk_shard_set_stream.argtypes = [vp, vp]
+    L.gk_shard_launches.argtypes = [vp]
+    L.gk_shard_launches.restype = i64
     L.gk_shard_degree.argtypes = [vp, u32, C.POINTER(i64)]
     L.gk_shard_begin.argtypes = [vp, u32, i32, i32]
     L.gk_shard_td_expand.argtypes = [vp, u64, u64, i32, i32, vp, vp, vp, i64]
@@ -107,7 +110,7 @@ def load() -> C.CDLL:
     for f in EXPORTED:
         if f not in ("gk_last_error", "gk_abi_version", "gk_device_count", "gk_graph_free",
                      "gk_bfs_device_parent", "gk_host_alloc", "gk_host_free", "gk_shard_last_error",
-                     "gk_shard_free"):
+                     "gk_shard_free", "gk_shard_launches"):
             getattr(L, f).restype = C.c_int
     _lib = L
     return L

@@ -476,6 +476,7 @@ struct gk_shard {
   cudaStream_t stream = nullptr;  // caller's stream (e.g. torch's current stream)
   int want_depth = 0;
   int encode = 1;
+  long long launches = 0;  // kernels launched on this shard (telemetry)
 };
 
 namespace {
@@ -646,6 +647,8 @@ GK_API gk_status gk_shard_info(const gk_shard* s, int64_t* n, int64_t* lo, int64
   return GK_OK;
 }
 
+GK_API int64_t gk_shard_launches(const gk_shard* s) { return s ? s->launches : 0; }
+
 GK_API gk_status gk_shard_set_stream(gk_shard* s, void* stream) {
   if (!s) return shard_fail(GK_ERR_INVALID, "null shard");
   s->stream = (cudaStream_t)stream;
@@ -670,8 +673,12 @@ GK_API gk_status gk_shard_begin(gk_shard* s, uint32_t src, int32_t strategy, int
   s->encode = strategy != GK_BFS_TOP_DOWN_RESCAN;
   gk::ShardParams p = params(s);
   SCK(cudaMemsetAsync(s->ctr, 0, sizeof(unsigned long long) * (gk::cDest + s->nranks + 8), s->stream), "memset");
+  s->launches++;
   gk::k_sh_init<<<gk::grid_of(s->nloc), gk::kSB, 0, s->stream>>>(p);
-  if ((int64_t)src >= s->lo && (int64_t)src < s->hi) gk::k_sh_set_source<<<1, 1, 0, s->stream>>>(p, src);
+  if ((int64_t)src >= s->lo && (int64_t)src < s->hi) {
+    s->launches++;
+    gk::k_sh_set_source<<<1, 1, 0, s->stream>>>(p, src);
+  }
   SCK(cudaGetLastError(), "begin");
   return GK_OK;
 }
@@ -694,12 +701,14 @@ GK_API gk_status gk_shard_td_expand(gk_shard* s, uint64_t qs, uint64_t qe, int32
   SCK(cudaMemsetAsync(s->ctr + gk::cChunks, 0, sizeof(unsigned long long), s->stream), "memset");
   SCK(cudaMemsetAsync(s->ctr + gk::cDest, 0, sizeof(unsigned long long) * P, s->stream), "memset");
   if (dedup) SCK(cudaMemsetAsync(s->sent, 0, sizeof(uint32_t) * ((s->n + 31) / 32), s->stream), "memset");
+  s->launches++;
   gk::k_sh_td_light<<<gk::grid_of((int64_t)(qe - qs)), gk::kSB, 0, s->stream>>>(p, qs, qe, lvl);
   SCK(cudaGetLastError(), "td_light");
   unsigned long long h[gk::cDest + 64];
   gk_status st = read_ctr(s, h, gk::cDest);
   if (st != GK_OK) return st;
   if (h[gk::cChunks]) {
+    s->launches++;
     gk::k_sh_td_heavy<<<gk::grid_of((int64_t)h[gk::cChunks] * 32), gk::kSB, 0, s->stream>>>(p, h[gk::cChunks], lvl);
     SCK(cudaGetLastError(), "td_heavy");
     st = read_ctr(s, h, gk::cDest);
@@ -709,6 +718,7 @@ GK_API gk_status gk_shard_td_expand(gk_shard* s, uint64_t qs, uint64_t qe, int32
   if ((int64_t)npairs > pairs_cap) return shard_fail(GK_ERR_INVALID, "pairs buffer too small");
   std::vector<unsigned long long> cursor(P, 0);
   if (npairs) {
+    s->launches += 2;
     gk::k_sh_count_dest<<<gk::grid_of((int64_t)npairs), gk::kSB, 0, s->stream>>>(p, npairs);
     SCK(cudaGetLastError(), "count_dest");
     st = read_ctr(s, h, gk::cDest + P);
@@ -742,6 +752,7 @@ GK_API gk_status gk_shard_td_apply(gk_shard* s, const uint64_t* pairs_in, int64_
   gk::ShardParams p = params(s);
   SCK(cudaMemsetAsync(s->ctr + gk::cScout, 0, sizeof(unsigned long long) * 2, s->stream), "memset");
   if (npairs > 0) {
+    s->launches++;
     gk::k_sh_td_apply<<<gk::grid_of(npairs), gk::kSB, 0, s->stream>>>(p, pairs_in, (unsigned long long)npairs, lvl);
     SCK(cudaGetLastError(), "td_apply");
   }
@@ -782,6 +793,7 @@ GK_API gk_status gk_shard_q2b(gk_shard* s, uint64_t qs, uint64_t qe, uint32_t* s
   SCK(cudaSetDevice(s->device), "cudaSetDevice");
   gk::ShardParams p = params(s);
   SCK(cudaMemsetAsync(slice_dev, 0, sizeof(uint32_t) * (s->block / 32), s->stream), "memset");
+  if (qe > qs) s->launches++;
   if (qe > qs) gk::k_sh_q2b<<<gk::grid_of((int64_t)(qe - qs)), gk::kSB, 0, s->stream>>>(p, qs, qe, slice_dev);
   SCK(cudaGetLastError(), "q2b");
   return GK_OK;
@@ -796,6 +808,7 @@ GK_API gk_status gk_shard_bu(gk_shard* s, const uint32_t* front_dev, uint32_t* n
   gk::ShardParams p = params(s);
   SCK(cudaMemsetAsync(s->ctr + gk::cAwake, 0, sizeof(unsigned long long), s->stream), "memset");
   SCK(cudaMemsetAsync(next_slice_dev, 0, sizeof(uint32_t) * (s->block / 32), s->stream), "memset");
+  s->launches++;
   gk::k_sh_bu<<<gk::grid_of(s->nloc), gk::kSB, 0, s->stream>>>(p, front_dev, next_slice_dev, lvl);
   SCK(cudaGetLastError(), "bu");
   unsigned long long h[gk::cDest];
@@ -810,6 +823,7 @@ GK_API gk_status gk_shard_b2q(gk_shard* s, const uint32_t* slice_dev) {
   if (!s || !slice_dev) return shard_fail(GK_ERR_INVALID, "null argument");
   SCK(cudaSetDevice(s->device), "cudaSetDevice");
   gk::ShardParams p = params(s);
+  s->launches++;
   gk::k_sh_b2q<<<gk::grid_of((s->nloc + 31) / 32), gk::kSB, 0, s->stream>>>(p, slice_dev);
   SCK(cudaGetLastError(), "b2q");
   return GK_OK;
@@ -823,6 +837,7 @@ GK_API gk_status gk_shard_result(gk_shard* s, int32_t* parent_out, int32_t* dept
   if (counts) {
     gk::ShardParams p = params(s);
     SCK(cudaMemsetAsync(s->acc, 0, sizeof(unsigned long long) * 2, s->stream), "memset");
+    s->launches++;
     gk::k_sh_count<<<gk::grid_of(s->nloc), gk::kSB, 0, s->stream>>>(p, s->acc);
     unsigned long long two[2];
     SCK(cudaMemcpyAsync(two, s->acc, sizeof(two), cudaMemcpyDeviceToHost, s->stream), "D2H");

@@ -156,7 +156,13 @@ class GpuEngine:
         _check(_lib.load().gk_shard_b2q(self._h, C.c_void_p(own_slice.data_ptr())), "b2q")
 
     def result(self, want_parent: bool = True, want_depth: bool = False):
-        parent = np.empty(max(self.nloc, 1), np.int32) if want_parent else None
+        if want_parent:
+            if getattr(self, "_pin", None) is None:  # page-locked: the D2H runs at link speed
+                from . import PinnedBuffer
+                self._pin = PinnedBuffer(max(self.nloc, 1))
+            parent = self._pin.array
+        else:
+            parent = None
         depth = np.empty(max(self.nloc, 1), np.int32) if want_depth else None
         counts = (C.c_int64 * 2)()
         _check(_lib.load().gk_shard_result(self._h, parent.ctypes.data if parent is not None else None,
@@ -168,6 +174,9 @@ class GpuEngine:
     def own_slice_of(self, full, rank: int):
         w = self.block // 32
         return full[rank * w:(rank + 1) * w]
+
+    def launches(self) -> int:
+        return int(_lib.load().gk_shard_launches(self._h))
 
 
 # ----------------------------------------------------------------- communicators
@@ -261,6 +270,7 @@ class ShardedResult:
     depth: np.ndarray | None = None
     reached: int = 0
     component_edges: int = 0
+    bytes_in: int = 0  # bytes received by this process's engines from other ranks
 
     @property
     def schedule(self) -> str:
@@ -278,10 +288,26 @@ class ShardedBfs:
         self.n, self.block, self.P = e0.n, e0.block, comm.size
         self.alpha, self.beta = alpha, beta
         self.like = e0.slice
+        import os
+        self.profile = os.environ.get("GK_DIST_PROFILE") == "1"
+        self.prof = {}
         self.m = comm.allreduce([[e.m] for e in engines], self.like)[0]
 
     def _ar(self, vals):
-        return self.comm.allreduce(vals, self.like)
+        return self._t("allreduce", self.comm.allreduce, vals, self.like)
+
+    def _t(self, key, fn, *a):
+        """Call fn(*a); with GK_DIST_PROFILE=1 accumulate its synchronized wall time."""
+        if not self.profile:
+            return fn(*a)
+        import time
+        import torch
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = fn(*a)
+        torch.cuda.synchronize()
+        self.prof[key] = self.prof.get(key, 0.0) + time.perf_counter() - t0
+        return out
 
     def run(self, src: int, strategy: int = BfsStrategy.kDirectionOptimizing, want_depth: bool = False,
             gather: bool = False) -> ShardedResult:
@@ -300,23 +326,25 @@ class ShardedBfs:
         big_edges = max(4096, self.n // 16)
         front, front_valid, lvl = None, False, 0
         res = ShardedResult()
+        slice_bytes = (P - 1) * (self.block // 8) * len(E)  # all-gather: every other rank's slice
         while frontier > 0:
             if strategy == BfsStrategy.kDirectionOptimizing and scout > _tdiv(etc, self.alpha):
                 if not front_valid:                                        # QueueToBitmap
-                    front = self.comm.allgather([e.q2b(a, b) for e, a, b in zip(E, qs, qe)])
+                    front = self._t("q2b+gather", lambda: self.comm.allgather([e.q2b(a, b) for e, a, b in zip(E, qs, qe)]))
+                    res.bytes_in += slice_bytes
                 awake = frontier
                 qs = list(qe)
                 while True:                                                # bfs.hpp:149-154
                     old = awake
-                    outs = [e.bu(front, lvl) for e in E]
+                    outs = self._t("bu", lambda: [e.bu(front, lvl) for e in E])
                     awake = self._ar([[a] for a, _ in outs])[0]
-                    front = self.comm.allgather([sl for _, sl in outs])
+                    front = self._t("allgather", lambda: self.comm.allgather([sl for _, sl in outs]))
+                    res.bytes_in += slice_bytes
                     res.steps.append(("B", old, awake, etc))
                     lvl += 1
                     if not (awake >= old or awake > _tdiv(self.n, self.beta)):
                         break
-                for e, r in zip(E, self.ranks):                            # BitmapToQueue
-                    e.b2q(e.own_slice_of(front, r))
+                self._t("b2q", lambda: [e.b2q(e.own_slice_of(front, r)) for e, r in zip(E, self.ranks)])  # BitmapToQueue
                 qe = [e.tail() for e in E]
                 frontier = awake
                 scout = 1                                                  # bfs.hpp:156
@@ -325,9 +353,11 @@ class ShardedBfs:
                 etc -= scout                                               # bfs.hpp:158
                 fsize = frontier
                 dedup = scout > big_edges
-                outs = [e.td_expand(a, b, lvl, dedup, P) for e, a, b in zip(E, qs, qe)]
-                recvs, nrecv = self.comm.alltoall([o[3] for o in outs], [o[2] for o in outs], self.like)
-                applied = [e.td_apply(r, k, lvl) for e, r, k in zip(E, recvs, nrecv)]
+                outs = self._t("td_expand", lambda: [e.td_expand(a, b, lvl, dedup, P) for e, a, b in zip(E, qs, qe)])
+                recvs, nrecv = self._t("alltoall", self.comm.alltoall, [o[3] for o in outs], [o[2] for o in outs],
+                                       self.like)
+                res.bytes_in += 8 * sum(k - o[2][r] for k, o, r in zip(nrecv, outs, self.ranks))
+                applied = self._t("td_apply", lambda: [e.td_apply(r, k, lvl) for e, r, k in zip(E, recvs, nrecv)])
                 qs = list(qe)
                 qe = [e.tail() for e in E]
                 scout, frontier = self._ar([[o[1] + a[1], o[0] + a[0]] for o, a in zip(outs, applied)])
@@ -344,3 +374,33 @@ class ShardedBfs:
             if want_depth:
                 res.depth = np.concatenate([o[1] for o in outs]) if len(E) == P else None
         return res
+
+
+# ----------------------------------------------------------------- sources
+def _mix64(x: int) -> int:
+    M = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & M
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+    return x ^ (x >> 31)
+
+
+def pick_sources_sharded(sb: ShardedBfs, count: int, seed: int = 24601) -> list[int]:
+    """PickSources (source_picker.hpp:22-54) over a sharded graph: every rank
+    draws the same Rng(seed) candidates; the owner reports the degree."""
+    M = (1 << 64) - 1
+    state = _mix64(seed) ^ _mix64(M)  # Rng(seed, stream=0): Mix64(seed) ^ Mix64(~0)
+    n = sb.n
+    mask = n - 1
+    for sh in (1, 2, 4, 8, 16):
+        mask |= mask >> sh
+    out = []
+    while len(out) < count:
+        while True:
+            state = (state + 0x9E3779B97F4A7C15) & M
+            c = (_mix64((state - 0x9E3779B97F4A7C15) & M) >> 32) & mask
+            if c < n:
+                break
+        if sb._ar([[e.owned_degree(c)] for e in sb.engines])[0] > 0:
+            out.append(c)
+    return out
