@@ -363,12 +363,14 @@ def main():
     m_of, bsec_of, buse_of, sched_of = {}, {}, {}, {}
     if not args.no_model:
         g.keep_depth(True)
+    verified = 0
     for s in sources:
         r = g.bfs(s, parent=False, counts=True)
         m_of[s] = r.component_edges
         sched_of[s] = r.schedule
         if not args.no_model:
             bsec_of[s], buse_of[s] = g.byte_model(r.steps)
+            verified += bool(g.verify(s)["ok"])  # device BFS certificate (untimed)
     g.keep_depth(False)
 
     clk = ClockSampler(local)
@@ -456,7 +458,9 @@ def main():
                    "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % ((g.m * 4 + g.n * 8) / 1e9),
                    "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
                    "device_build_s": round(build_s, 2), "timed_region_wall_s": round(wall, 4),
-                   "schedules": scheds[:4], "mean_m_cc": statistics.mean(step_m)},
+                   "schedules": scheds[:4], "mean_m_cc": statistics.mean(step_m),
+                   "verified": (f"{verified}/{len(sources)} sources pass the device BFS certificate "
+                                "(depths exact, parents valid)") if not args.no_model else "not run"},
         "e2e": {"value": e2e_val, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * g.n,
                 "note": "gk_bfs with the parent array copied to a pinned host buffer; graph resident "
                         "(uploaded once, untimed, as the reference harness builds it untimed); per-step "

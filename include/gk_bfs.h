@@ -153,6 +153,14 @@ GK_API gk_status gk_bfs_trace(const gk_graph* g, uint64_t* ts_ns, char* tags,
  * requested depth_out or GK_KEEP_DEPTH via gk_bfs_keep_depth(). */
 GK_API gk_status gk_bfs_byte_model(gk_graph* g, const gk_step* steps,
                             int32_t num_steps, double* b_sec, double* b_use);
+/* Device-side BFS certificate of the last gk_bfs (which must have recorded
+ * depths): checks verify.hpp:62-98's conditions plus "every arc v->w with v
+ * reached has w reached at depth <= depth[v]+1", which together prove the
+ * depths are exact BFS distances -- at full size, without a serial BFS.
+ * errors[0..6] = violation counts (source, unreached-with-parent, parent
+ * range, parent depth, missing parent edge, arc reachability, arc level),
+ * errors[7] = smallest offending vertex or -1. */
+GK_API gk_status gk_bfs_verify(gk_graph* g, uint32_t source, int64_t* errors);
 /* Keep depths on the device for subsequent gk_bfs calls (for the model). */
 GK_API gk_status gk_bfs_keep_depth(gk_graph* g, int32_t keep);
 

@@ -224,6 +224,14 @@ class DeviceGraph:
                "gk_bfs_byte_model")
         return bs.value, bu.value
 
+    def verify(self, source: int) -> dict:
+        """Device certificate of the last bfs (needs keep_depth or depth=...).
+        Returns {'ok': bool, 'errors': [...7 counts], 'first_bad': v or -1}."""
+        errs = (C.c_int64 * 8)()
+        _check(_lib.load().gk_bfs_verify(self._h, int(source), errs), "gk_bfs_verify")
+        e = list(errs)
+        return {"ok": sum(e[:7]) == 0, "errors": e[:7], "first_bad": e[7]}
+
     def trace(self):
         """[(tag, t_ms_since_kernel_start)] for the phases of the last bfs."""
         cap = 4096

@@ -1,6 +1,6 @@
-// gk_aux.cu -- untimed auxiliary kernels: reached/component-edge counts and
-// the algorithmic byte model of SURVEY.md §8(d) (the roofline numerator).
-// Neither runs inside the timed traversal.
+// gk_aux.cu -- untimed auxiliary kernels: reached/component-edge counts, the
+// algorithmic byte model of SURVEY.md §8(d) (the roofline numerator) and the
+// device BFS certificate (§8(f)-2).  None runs inside the timed traversal.
 #include <vector>
 
 #include "gk_internal.cuh"
@@ -105,6 +105,80 @@ __global__ void k_model_bu(const int32_t* __restrict__ depth, const int64_t* __r
   }
 }
 
+// ---- device BFS certificate ---------------------------
+// depth/parent of a finished BFS are a valid BFS iff
+//   (1) depth[src] = 0, parent[src] = src;
+//   (2) every reached v != src has parent p with an edge p->v and
+//       depth[p] = depth[v]-1; every unreached v has parent -1;
+//   (3) every arc v->w with v reached has w reached and depth[w] <= depth[v]+1.
+// (2) gives depth >= true distance along the parent chain, (3) gives <= by
+// induction along a shortest path, so the depths are exactly the BFS
+// distances (the verify.hpp:62-98 conditions, without a serial BFS).
+// errs: [0] source, [1] unreached-with-parent, [2] parent range, [3] parent
+// depth, [4] missing parent edge, [5] arc reachability, [6] arc level,
+// [7] first offending vertex (min).
+__global__ void k_verify_vertices(const int64_t* __restrict__ off, const uint32_t* __restrict__ nb,
+                                  const int32_t* __restrict__ parent, const int32_t* __restrict__ depth,
+                                  int64_t n, uint32_t src, unsigned long long* errs) {
+  for (long long v = (long long)blockIdx.x * kAuxBlock + threadIdx.x; v < n;
+       v += (long long)gridDim.x * kAuxBlock) {
+    const int d = depth[v], p = parent[v];
+    int bad = -1;
+    if (v == (long long)src) {
+      if (p != (int)src || d != 0) bad = 0;
+    } else if (d < 0) {
+      if (p != -1) bad = 1;
+    } else if (p < 0 || (int64_t)p >= n) {
+      bad = 2;
+    } else if (depth[p] != d - 1) {
+      bad = 3;
+    } else {
+      int64_t lo = off[p], hi = off[p + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (nb[mid] < (uint32_t)v) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo >= off[p + 1] || nb[lo] != (uint32_t)v) bad = 4;
+    }
+    if (bad >= 0) {
+      atomicAdd(&errs[bad], 1ull);
+      atomicMin(&errs[7], (unsigned long long)v);
+    }
+  }
+}
+
+// Arc rule (3): a warp per 32 vertices, each list scanned 32 arcs at a time.
+__global__ void k_verify_arcs(const int64_t* __restrict__ off, const uint32_t* __restrict__ nb,
+                              const int32_t* __restrict__ depth, int64_t n, unsigned long long* errs) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * kAuxBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kAuxBlock) >> 5;
+  for (long long base = gw * 32; base < n; base += nw * 32) {
+    const long long mine = base + lane;
+    const int dmine = mine < n ? depth[mine] : -1;
+    unsigned todo = __ballot_sync(0xffffffffu, dmine >= 0);
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const long long v = base + l;
+      const int dv = __shfl_sync(0xffffffffu, dmine, l);
+      const int64_t b = off[v], e = off[v + 1];
+      unsigned long long reach = 0, level = 0;
+      for (int64_t j = b + lane; j < e; j += 32) {
+        const int dw = depth[nb[j]];
+        if (dw < 0) reach++;
+        else if (dw > dv + 1) level++;
+      }
+      if (reach | level) {
+        atomicAdd(&errs[5], reach);
+        atomicAdd(&errs[6], level);
+        atomicMin(&errs[7], (unsigned long long)v);
+      }
+    }
+  }
+}
+
 int aux_grid(int64_t n) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -122,6 +196,24 @@ cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
   if (e) return e;
   k_count_reached<<<aux_grid(n), kAuxBlock, 0, s>>>(parent, off, n, d_out2);
   return cudaGetLastError();
+}
+
+cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
+                       int64_t n, uint32_t src, long long* errs8, cudaStream_t s) {
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMallocAsync(&d, 8 * sizeof(unsigned long long), s);
+  if (e) return e;
+  unsigned long long init[8] = {0, 0, 0, 0, 0, 0, 0, ~0ull};
+  cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, s);
+  k_verify_vertices<<<aux_grid(n), kAuxBlock, 0, s>>>(off, nb, parent, depth, n, src, d);
+  k_verify_arcs<<<aux_grid(n), kAuxBlock, 0, s>>>(off, nb, depth, n, d);
+  unsigned long long h[8];
+  e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(d, s);
+  for (int i = 0; i < 8; i++) errs8[i] = (long long)h[i];
+  if (h[7] == ~0ull) errs8[7] = -1;
+  return e;
 }
 
 cudaError_t byte_model(const BfsParams& p, const int32_t* depth, const char* dirs, int32_t nsteps,

@@ -426,6 +426,19 @@ gk_status gk_bfs_byte_model(gk_graph* g, const gk_step* steps, int32_t num_steps
   return GK_OK;
 }
 
+gk_status gk_bfs_verify(gk_graph* g, uint32_t source, int64_t* errors) {
+  if (!g || !errors) return fail(GK_ERR_INVALID, "null argument");
+  if (!g->depth || !g->depth_valid)
+    return fail(GK_ERR_INVALID, "verification needs the last gk_bfs to record depths");
+  if ((int64_t)source >= g->n) return fail(GK_ERR_SOURCE_RANGE, "bfs source out of range");
+  std::lock_guard<std::mutex> lock(g->mu);
+  CK(cudaSetDevice(g->device), "cudaSetDevice");
+  long long e8[8];
+  CK(gk::verify_bfs(g->out_off, g->out_nb, g->parent, g->depth, g->n, source, e8, g->stream), "verify");
+  for (int i = 0; i < 8; i++) errors[i] = e8[i];
+  return GK_OK;
+}
+
 void* gk_host_alloc(int64_t bytes) {
   void* p = nullptr;
   if (cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocDefault) != cudaSuccess) {

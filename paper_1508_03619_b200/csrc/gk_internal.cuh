@@ -102,6 +102,8 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t s)
 // Auxiliary (untimed) kernels.
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s);
+cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
+                       int64_t n, uint32_t src, long long* errs8, cudaStream_t s);
 cudaError_t byte_model(const BfsParams& p, const int32_t* depth, const char* dirs,
                        int32_t nsteps, unsigned long long* d_acc, double* b_sec,
                        double* b_use, cudaStream_t s);

@@ -243,3 +243,69 @@ def test_grid_high_diameter():
         assert (res.depth == O.bfs_depths(g, s)).all()
         assert O.verify_bfs(g, s, res.parent)[0]
         assert res.schedule == O.bfs_replay(g, s).dirs
+
+
+# ---------------------------------------------------------------- certificate
+def _cuda_memcpy_h2d(dst_ptr, arr):
+    """Tamper with a device array (test only) through the system CUDA runtime."""
+    import ctypes
+    import glob
+    libs = glob.glob("/usr/local/cuda/lib64/libcudart.so*")
+    rt = ctypes.CDLL(sorted(libs)[0])
+    rt.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    assert rt.cudaMemcpy(dst_ptr, arr.ctypes.data, arr.nbytes, 1) == 0  # cudaMemcpyHostToDevice
+
+
+def test_device_certificate_accepts(hosts, devs):
+    for name in ("kron16p", "urand14", "grid60x70", "dkron10_s11", "star9", "path8"):
+        g, dg = hosts[name], devs[name]
+        dg.keep_depth(True)
+        for s in O.pick_sources(g, 4):
+            dg.bfs(int(s), parent=False)
+            v = dg.verify(int(s))
+            assert v["ok"], (name, s, v)
+        dg.keep_depth(False)
+
+
+def test_device_certificate_rejects_tampering():
+    # acceptance.cc:392-405 / test_verify.cc:13-57 on the device checker
+    g = O.build_csr(4, np.array([0, 1, 1, 2, 2, 3, 3, 0], np.uint32))  # square 0-1-2-3-0
+    dg = DeviceGraph.from_csr(g)
+    dg.keep_depth(True)
+    dg.bfs(0, parent=False)
+    assert dg.verify(0)["ok"]
+    ptr = dg.device_parent_ptr()
+    good = dg.bfs(0).parent.copy()
+    for idx, val, slot in ((2, 0, 4), (1, 2, 3), (0, 1, 0), (2, -1, 1)):  # no edge / depth / source / unreached
+        dg.bfs(0, parent=False)
+        bad = good.copy()
+        bad[idx] = val
+        _cuda_memcpy_h2d(ptr, bad)
+        v = dg.verify(0)
+        assert not v["ok"], (idx, val)
+    iso = DeviceGraph.from_csr(O.build_csr(3, np.array([0, 1], np.uint32)))
+    iso.keep_depth(True)
+    iso.bfs(0, parent=False)
+    _cuda_memcpy_h2d(iso.device_parent_ptr(), np.array([0, 0, 1], np.int32))
+    v = iso.verify(0)
+    assert not v["ok"] and v["errors"][1] == 1 and v["first_bad"] == 2
+
+
+@pytest.mark.parametrize("cfg", ["kron27", "urand27", "grid4900"])
+def test_full_size_configs_certificate(cfg):
+    """BASELINE configs 2-4 at full size: the size-independent certificate
+    for several picked sources + schedule sanity."""
+    if cfg == "grid4900":
+        dg = DeviceGraph.grid(4900, 4900, 0.15, 0.02, SEED)
+        nsrc = 2
+    else:
+        dg = DeviceGraph.generate(cfg[:-2], 27, 16, SEED)
+        nsrc = 4
+    dg.keep_depth(True)
+    for s in dg.pick_sources(nsrc, SEED):
+        r = dg.bfs(int(s), parent=False, counts=True)
+        v = dg.verify(int(s))
+        assert v["ok"], (cfg, s, v)
+        assert r.reached > 0 and r.component_edges > 0
+        if cfg != "grid4900":
+            assert "B" in r.schedule
