@@ -46,7 +46,8 @@ typedef enum {
   GK_ERR_NO_DEVICE = 6,
   GK_ERR_INVALID = 7,      /* malformed graph / null handle / bad generator spec */
   GK_ERR_TIMEOUT = 8,      /* device-side watchdog fired (never expected) */
-  GK_ERR_NO_EDGES = 9      /* source_picker.hpp:27-28 "cannot pick sources: graph has no edges" */
+  GK_ERR_NO_EDGES = 9,     /* source_picker.hpp:27-28 "cannot pick sources: graph has no edges" */
+  GK_ERR_LOAD = 10         /* errors.hpp:35-46 LoadError family (bad magic / version / truncated) */
 } gk_status;
 
 /* BfsStrategy (bfs.hpp:37) */
@@ -113,6 +114,15 @@ GK_API gk_status gk_graph_generate(int kind, int scale, int degree, uint64_t see
 GK_API gk_status gk_graph_generate_grid(int64_t rows, int64_t cols, double p_delete,
                                  double p_diag, uint64_t seed, int device,
                                  gk_graph** out);
+/* Serialized-graph cache: the reference's ".sg"/".wsg"
+ * binary layout (io.hpp:328-456), streamed file -> pinned -> HBM without a
+ * host copy of the graph; weights are skipped.  Errors follow ReadSerialized:
+ * GK_ERR_LOAD with "...not a serialized graph (bad magic)", "...unsupported
+ * version N", "...file shorter than its declared arrays"; GK_ERR_INVALID when
+ * the file cannot be opened. */
+GK_API gk_status gk_graph_load_sg(const char* path, int device, gk_graph** out);
+/* WriteSerialized (io.hpp:364-389) of an unweighted graph from HBM. */
+GK_API gk_status gk_graph_save_sg(const gk_graph* g, const char* path);
 GK_API void gk_graph_free(gk_graph* g);
 
 GK_API gk_status gk_graph_info(const gk_graph* g, int64_t* num_nodes,

@@ -281,6 +281,10 @@ class RefLib:
                                        C.c_int64, _I32P]
         L.gkr_bfs_schedule.restype = C.c_int64
         L.gkr_bfs_depths.argtypes = [vp, C.c_uint32, _I32P]
+        L.gkr_write_sg.argtypes = [vp, C.c_char_p, C.c_int, C.c_char_p, C.c_int]
+        L.gkr_write_sg.restype = C.c_int
+        L.gkr_read_sg.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        L.gkr_read_sg.restype = vp
         L.gkr_verify_bfs.argtypes = [vp, C.c_uint32, _I32P, C.c_char_p, C.c_int]
         L.gkr_verify_bfs.restype = C.c_int
         self.L = L
@@ -295,6 +299,13 @@ class RefLib:
         e = np.ascontiguousarray(edges, np.uint32)
         h = self.L.gkr_build(n, e if e.size else np.zeros(2, np.uint32), e.size // 2,
                              int(directed), int(symmetrize), err, 256)
+        if not h:
+            raise RuntimeError(err.value.decode())
+        return RefGraph(self, h)
+
+    def read_sg(self, path: str) -> "RefGraph":
+        err = C.create_string_buffer(256)
+        h = self.L.gkr_read_sg(str(path).encode(), err, 256)
         if not h:
             raise RuntimeError(err.value.decode())
         return RefGraph(self, h)
@@ -343,6 +354,11 @@ class RefGraph:
         else:
             self.ref.L.gkr_graph_arrays(self.h, off.ctypes.data, nb.ctypes.data, None, None)
         return g
+
+    def write_sg(self, path: str, weight_seed: int = -1):
+        err = C.create_string_buffer(256)
+        if not self.ref.L.gkr_write_sg(self.h, str(path).encode(), weight_seed, err, 256):
+            raise RuntimeError(err.value.decode())
 
     def pick_sources(self, count: int, seed: int = 24601) -> np.ndarray:
         out = np.empty(max(count, 1), np.uint32)

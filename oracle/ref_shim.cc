@@ -252,6 +252,35 @@ int64_t gkr_bfs_schedule(void* hp, uint32_t src, int64_t alpha, int64_t beta, in
   return ns;
 }
 
+// WriteSerialized / ReadSerialized (io.hpp:364-456) for the .sg fixtures.
+int gkr_write_sg(void* hp, const char* path, int weighted_seed_or_minus1, char* err, int errlen) {
+  try {
+    const CsrGraph& g = static_cast<RefGraph*>(hp)->g;
+    if (weighted_seed_or_minus1 >= 0)
+      WriteSerialized(EnsureWeighted(g, static_cast<uint64_t>(weighted_seed_or_minus1)), path);
+    else
+      WriteSerialized(g, path);
+    return 1;
+  } catch (const std::exception& e) {
+    SetErr(err, errlen, e.what());
+    return 0;
+  }
+}
+
+void* gkr_read_sg(const char* path, char* err, int errlen) {
+  try {
+    auto* h = new RefGraph;
+    h->g = ReadSerialized(path);
+    h->directed = h->g.directed();
+    h->n = h->g.num_nodes();
+    h->sealed = true;
+    return h;
+  } catch (const std::exception& e) {
+    SetErr(err, errlen, e.what());
+    return nullptr;
+  }
+}
+
 void gkr_bfs_depths(void* hp, uint32_t src, int32_t* depth) {
   std::vector<int32_t> d = detail::BfsDepths(static_cast<RefGraph*>(hp)->g, src);
   std::memcpy(depth, d.data(), d.size() * 4);

@@ -21,7 +21,7 @@ import numpy as np
 from . import _lib
 from ._lib import BfsStats, CsrView, Step
 
-__all__ = ["Bfs", "BfsOptions", "BfsStrategy", "BfsResult", "ConfigError", "GapkitError",
+__all__ = ["Bfs", "BfsOptions", "BfsStrategy", "BfsResult", "ConfigError", "GapkitError", "LoadError",
            "DeviceGraph", "PinnedBuffer", "device_count"]
 
 kDefaultSeed = 24601  # types.hpp:33
@@ -33,6 +33,10 @@ class GapkitError(RuntimeError):
 
 class ConfigError(GapkitError):
     """gapkit::ConfigError (errors.hpp:30-32)."""
+
+
+class LoadError(GapkitError):
+    """gapkit::LoadError (errors.hpp:35-46): bad magic / version / truncated."""
 
 
 class BfsStrategy(enum.IntEnum):
@@ -75,6 +79,8 @@ def _check(status: int, what: str):
     msg = _lib.last_error()
     if status in (_lib.GK_ERR_SOURCE_RANGE, _lib.GK_ERR_BAD_PARAM, _lib.GK_ERR_NO_EDGES):
         raise ConfigError(msg)
+    if status == _lib.GK_ERR_LOAD:
+        raise LoadError(msg)
     raise GapkitError(f"{what}: {msg} (status {status})")
 
 
@@ -152,6 +158,17 @@ class DeviceGraph:
         _check(_lib.load().gk_graph_generate_grid(rows, cols, p_delete, p_diag, seed, device, C.byref(h)),
                "gk_graph_generate_grid")
         return cls(h.value)
+
+    @classmethod
+    def load_sg(cls, path: str, device: int = 0) -> "DeviceGraph":
+        """ReadSerialized (io.hpp:392-456) straight into HBM."""
+        h = C.c_void_p()
+        _check(_lib.load().gk_graph_load_sg(str(path).encode(), device, C.byref(h)), "gk_graph_load_sg")
+        return cls(h.value)
+
+    def save_sg(self, path: str):
+        """WriteSerialized (io.hpp:364-389) from HBM."""
+        _check(_lib.load().gk_graph_save_sg(self._h, str(path).encode()), "gk_graph_save_sg")
 
     def __del__(self):
         try:

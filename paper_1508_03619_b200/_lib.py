@@ -22,6 +22,7 @@ GK_ERR_NO_DEVICE = 6
 GK_ERR_INVALID = 7
 GK_ERR_TIMEOUT = 8
 GK_ERR_NO_EDGES = 9
+GK_ERR_LOAD = 10
 
 # Exported symbols declared in include/gk_bfs.h (checked by the CPU tests).
 EXPORTED = (
@@ -32,7 +33,7 @@ EXPORTED = (
     "gk_shard_last_error", "gk_shard_generate", "gk_shard_upload", "gk_shard_free", "gk_shard_info",
     "gk_shard_set_stream", "gk_shard_degree", "gk_shard_begin", "gk_shard_td_expand", "gk_shard_td_apply",
     "gk_shard_tail", "gk_shard_rescan", "gk_shard_q2b", "gk_shard_bu", "gk_shard_b2q", "gk_shard_result",
-    "gk_shard_launches", "gk_bfs_verify",
+    "gk_shard_launches", "gk_bfs_verify", "gk_graph_load_sg", "gk_graph_save_sg",
 )
 
 
@@ -72,6 +73,8 @@ def load() -> C.CDLL:
     L.gk_graph_upload.argtypes = [C.POINTER(CsrView), C.c_int, C.POINTER(vp)]
     L.gk_graph_generate.argtypes = [C.c_int, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.POINTER(vp)]
     L.gk_graph_generate_grid.argtypes = [i64, i64, C.c_double, C.c_double, u64, C.c_int, C.POINTER(vp)]
+    L.gk_graph_load_sg.argtypes = [C.c_char_p, C.c_int, C.POINTER(vp)]
+    L.gk_graph_save_sg.argtypes = [vp, C.c_char_p]
     L.gk_graph_free.argtypes = [vp]
     L.gk_graph_free.restype = None
     L.gk_graph_info.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)]

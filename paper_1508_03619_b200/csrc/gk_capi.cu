@@ -218,6 +218,41 @@ gk_status gk_graph_generate_grid(int64_t rows, int64_t cols, double p_delete, do
   return finish_graph(g, out);
 }
 
+gk_status gk_graph_load_sg(const char* path, int device, gk_graph** out) {
+  if (!path || !out) return fail(GK_ERR_INVALID, "gk_graph_load_sg: null argument");
+  gk_status st = need_device(device);
+  if (st != GK_OK) return st;
+  auto* g = new gk_graph;
+  g->device = device;
+  std::string err;
+  int64_t n = 0, m = 0;
+  int directed = 0;
+  const int code = gk::sg_load(path, &n, &m, &directed, &g->out_off, &g->out_nb, &g->in_off, &g->in_nb, &err);
+  if (code) {
+    delete g;
+    if (code == 7 || code == 8) return fail(GK_ERR_OOM, err);
+    if (code == 2) return fail(GK_ERR_INVALID, err);
+    return fail(GK_ERR_LOAD, err);
+  }
+  g->n = n;
+  g->m = m;
+  g->directed = directed;
+  if (!directed) {
+    g->in_off = g->out_off;
+    g->in_nb = g->out_nb;
+  }
+  return finish_graph(g, out);
+}
+
+gk_status gk_graph_save_sg(const gk_graph* g, const char* path) {
+  if (!g || !path) return fail(GK_ERR_INVALID, "gk_graph_save_sg: null argument");
+  CK(cudaSetDevice(g->device), "cudaSetDevice");
+  std::string err;
+  const int code = gk::sg_save(path, g->n, g->m, g->directed, g->out_off, g->out_nb, g->in_off, g->in_nb, &err);
+  if (code) return fail(code == 2 ? GK_ERR_INVALID : GK_ERR_LOAD, err);
+  return GK_OK;
+}
+
 void gk_graph_free(gk_graph* g) { free_graph(g); }
 
 gk_status gk_graph_info(const gk_graph* g, int64_t* n, int64_t* m, int32_t* directed) {

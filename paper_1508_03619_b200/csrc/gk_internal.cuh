@@ -119,6 +119,12 @@ struct DevCsr {
 };
 cudaError_t build_generated(int kind, int scale, int degree, uint64_t seed, int permute, int64_t klo,
                             int64_t khi, DevCsr* out, std::string* err);
+// Serialized-graph cache (gk_sg.cu); return 0 on success, else an error code
+// (2 open, 3 bad magic, 4 truncated/io, 5 version, 6 flags, 7-8 alloc, 9 data).
+int sg_load(const char* path, int64_t* n, int64_t* m, int* directed, int64_t** off, uint32_t** nb,
+            int64_t** in_off, uint32_t** in_nb, std::string* err);
+int sg_save(const char* path, int64_t n, int64_t m, int directed, const int64_t* off, const uint32_t* nb,
+            const int64_t* in_off, const uint32_t* in_nb, std::string* err);
 cudaError_t build_grid(int64_t rows, int64_t cols, double p_delete, double p_diag,
                        uint64_t seed, DevCsr* out, std::string* err);
 

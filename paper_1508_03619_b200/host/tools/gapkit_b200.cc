@@ -2,7 +2,7 @@
 // subcommand, tools/gapkit.cc:47-152, with a hand-rolled parser because
 // CLI11 is not vendored).
 //
-//   gapkit_b200 bfs (-g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS]
+//   gapkit_b200 bfs (-f FILE.sg | -g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS]
 //               [-r SOURCE] [-v] [--seed S] [--no-permute] [--host-build]
 //               [--threads T] [-o FILE.csv]
 //
@@ -23,6 +23,7 @@
 #include "gapkit_b200/builder.hpp"
 #include "gapkit_b200/generator.hpp"
 #include "gapkit_b200/harness.hpp"
+#include "gapkit_b200/io.hpp"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -32,7 +33,7 @@ namespace {
 
 int Usage(const char* argv0) {
   std::fprintf(stderr,
-               "usage: %s bfs (-g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS] [-r SOURCE]\n"
+               "usage: %s bfs (-f FILE.sg | -g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS] [-r SOURCE]\n"
                "          [-v] [--seed S] [--no-permute] [--host-build] [--threads T] [-o FILE.csv]\n",
                argv0);
   return 2;
@@ -52,7 +53,7 @@ int main(int argc, char** argv) {
   long long rows = 0, cols = 0;
   unsigned long long seed = gapkit::kDefaultSeed;
   bool verify = false, permute = true, host_build = false;
-  std::string output;
+  std::string output, file;
   for (int i = 2; i < argc; i++) {
     std::string a = argv[i];
     auto need = [&](long long* dst) {
@@ -74,7 +75,10 @@ int main(int argc, char** argv) {
     } else if (a == "-v") verify = true;
     else if (a == "--no-permute") permute = false;
     else if (a == "--host-build") host_build = true;
-    else if (a == "-o" || a == "--output") {
+    else if (a == "-f" || a == "--file") {
+      if (i + 1 >= argc) return Usage(argv[0]);
+      file = argv[++i];
+    } else if (a == "-o" || a == "--output") {
       if (i + 1 >= argc) return Usage(argv[0]);
       output = argv[++i];
     } else if (a == "--grid") {
@@ -91,11 +95,16 @@ int main(int argc, char** argv) {
   if (threads > 0) omp_set_num_threads(static_cast<int>(threads));
 #endif
   try {
-    const int sources = (kron >= 0) + (urand >= 0) + (rows > 0);
-    if (sources != 1) throw gapkit::ConfigError("exactly one graph source required (-g, -u, or --grid)");
+    const int sources = (kron >= 0) + (urand >= 0) + (rows > 0) + !file.empty();
+    if (sources != 1) throw gapkit::ConfigError("exactly one graph source required (-f, -g, -u, or --grid)");
     gapkit::CsrGraph g;
     std::string name;
-    if (rows > 0) {
+    if (!file.empty()) {  // gapkit.cc:85-88 (serialized formats; text formats are out of scope)
+      const auto slash = file.find_last_of('/');
+      name = file.substr(slash == std::string::npos ? 0 : slash + 1);
+      name = name.substr(0, name.find_last_of('.'));
+      g = gapkit::ReadSerializedOnDevice(file);
+    } else if (rows > 0) {
       name = "grid" + std::to_string(rows) + "x" + std::to_string(cols);
       g = host_build ? gapkit::BuildCsr(gapkit::GenerateGrid(rows, cols, 0.15, 0.02, seed), false, true)
                      : gapkit::GenerateGridOnDevice(rows, cols, 0.15, 0.02, seed);

@@ -94,6 +94,15 @@ def main():
     gold["kat"]["isolated_parent"] = [int(x) for x in g.bfs(0)]
     gold["kat"]["perm_scale16_first8"] = [O.permute(v, 16, SEED) for v in range(8)]
     gold["kat"]["perm_keys_s16"] = [f"{int(k):016x}" for k in O.perm_keys(SEED, 16)]
+    # .sg fixtures written by the reference's WriteSerialized (io.hpp:364-389)
+    gdir = os.path.dirname(os.path.abspath(__file__))
+    R.build(2, np.array([0, 1], np.uint32), directed=True, symmetrize=False).write_sg(
+        os.path.join(gdir, "directed_1edge.sg"))  # test_io.cc:174-203's golden graph
+    kg = R.build(1 << 10, R.gen("kron", 10, 16, SEED))
+    kg.write_sg(os.path.join(gdir, "kron10.sg"))
+    kg.write_sg(os.path.join(gdir, "kron10.wsg"), SEED)
+    R.build(1 << 9, R.gen("kron", 9, 8, 5), directed=True, symmetrize=False).write_sg(
+        os.path.join(gdir, "dkron9.sg"))
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:
         json.dump(gold, f, indent=1, sort_keys=True)

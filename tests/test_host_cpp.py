@@ -86,6 +86,18 @@ def test_cli_bfs_verified(tools, graph, tmp_path):
 
 
 @pytest.mark.gpu
+def test_cli_serialized_file(tools, tmp_path):
+    out = tmp_path / "bfs.csv"
+    r = run(tools[1], "bfs", "-f", os.path.join(ROOT, "tests", "golden", "kron10.sg"), "-n", "8", "-v", "-o", out)
+    assert r.returncode == 0, r.stderr
+    assert "kron10: n=1024" in r.stdout and "all verified" in r.stdout
+    bad = tmp_path / "bad.sg"
+    bad.write_bytes(b"nope")
+    r = run(tools[1], "bfs", "-f", bad, "-n", "1")
+    assert r.returncode == 1 and "bad magic" in r.stderr
+
+
+@pytest.mark.gpu
 def test_cli_fixed_source_and_host_build(tools, tmp_path):
     out = tmp_path / "bfs.csv"
     r = run(tools[1], "bfs", "-g", "12", "-n", "3", "-r", "1", "--host-build", "-v", "-o", out)
