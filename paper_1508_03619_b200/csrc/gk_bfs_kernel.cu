@@ -18,7 +18,7 @@
 //             bfs.hpp:83)
 //   TD light  frontier tiles of 512 vertices, CTA-wide scan of degrees,
 //             load-balanced edge gather (bfs.hpp:68-91); vertices of degree
-//             > kHeavy are cut into kChunk-edge chunks instead
+//             > chunk are cut into chunk-edge chunks (128..1024 by step size)
 //   TD heavy  chunks spread over all warps (hub expansion)
 //   q2b       QueueToBitmap (bfs.hpp:93-97)
 //   BU        one warp per 32-vertex bitmap word: visited-word skip, per-lane
@@ -36,8 +36,8 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kQBuf = 256;         // per-warp queue staging (QueueBuffer analogue)
-constexpr int64_t kHeavy = 1024;   // degree above which a vertex is chunked
-constexpr int kChunk = 1024;       // edges per heavy chunk
+constexpr int kChunkMax = 1024;    // edges per heavy chunk (large steps)
+constexpr int kChunkMin = 128;     // ... and for small steps, so every warp gets a chunk
 
 
 struct __align__(16) SmemT {
@@ -332,31 +332,31 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
 template <bool kBig>
 __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, unsigned long long qs,
                          unsigned long long qe, uint32_t* nextbm, int lvl, bool encode,
-                         long long& scout, int& qcnt) {
+                         long long& scout, int& qcnt, int tile_sz, int64_t chunk) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
   // First tile of each CTA is static (no atomic on the latency chain of
   // small levels); the rest are handed out dynamically.
   unsigned long long tile = blockIdx.x;
   for (;;) {
-    const unsigned long long start = qs + tile * (unsigned long long)kBlock;
+    const unsigned long long start = qs + tile * (unsigned long long)tile_sz;
     if (start >= qe) break;
     const unsigned long long i = start + threadIdx.x;
     uint32_t u = 0;
     int64_t b = 0, dl = 0;
-    if (i < qe) {
+    if ((int)threadIdx.x < tile_sz && i < qe) {
       u = __ldcg(P.queue + i);
       b = P.out_off[u];
       const int64_t d = P.out_off[u + 1] - b;
-      if (d > kHeavy) {
-        const int64_t nch = (d + kChunk - 1) / kChunk;
+      if (d > chunk) {
+        const int64_t nch = (d + chunk - 1) / chunk;
         const unsigned long long base = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
         if ((int64_t)(base + nch) <= P.chunk_cap) {
           for (int64_t c = 0; c < nch; c++) {
             Chunk ch;
             ch.u = u;
-            ch.start = b + c * kChunk;
-            ch.len = (uint32_t)((d - c * kChunk) < kChunk ? (d - c * kChunk) : kChunk);
+            ch.start = b + c * chunk;
+            ch.len = (uint32_t)((d - c * chunk) < chunk ? (d - c * chunk) : chunk);
             P.chunks[base + c] = ch;
           }
         } else {
@@ -394,9 +394,9 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       }
       claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
     }
-    if (threadIdx.x == 0 && start + kBlock < qe) s.bcast[1] = gridDim.x + atomicAdd(&cnt[kTile], 1ull);
+    if (threadIdx.x == 0 && start + tile_sz < qe) s.bcast[1] = gridDim.x + atomicAdd(&cnt[kTile], 1ull);
     __syncthreads();
-    if (start + kBlock >= qe) break;  // every later tile starts past qe too
+    if (start + tile_sz >= qe) break;  // every later tile starts past qe too
     tile = s.bcast[1];
     __syncthreads();
   }
@@ -408,7 +408,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
                          uint32_t* nextbm, int lvl, bool encode, long long& scout, int& qcnt) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   const unsigned lane = lane_id();
-  // Chunks are equal-sized (kChunk edges but the tails), so a static
+  // Chunks are equal-sized (chunk edges but the tails), so a static
   // round-robin over warps balances without a contended grab counter.
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
@@ -500,17 +500,21 @@ __device__ __forceinline__ bool front_bit(const uint32_t* front, uint32_t u) {
 
 template <bool kSmem>
 __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_t* front, uint32_t* next,
-                        int lvl, unsigned long long long_base, long long& awake) {
+                        int lvl, unsigned long long long_base, int tw_log, long long& awake) {
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   uint32_t* acc_n = s.bu_acc[warp][0];
   uint32_t* acc_d = s.bu_acc[warp][1];
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
-  const long long ntasks = (P.w32 + 31) >> 5;
+  // A task is 2^tw_log consecutive words (<= 32): small graphs use small
+  // tasks so every warp gets work.
+  const int tw = 1 << tw_log;
+  const long long ntasks = (P.w32 + tw - 1) >> tw_log;
   for (long long t = gw; t < ntasks; t += nw) {
-    const long long w = (t << 5) + lane;
+    const long long tbase = t << tw_log;
+    const long long w = tbase + lane;
     uint32_t vis = 0xffffffffu, pad = 0u;
-    if (w < P.w32) {
+    if ((int)lane < tw && w < P.w32) {
       vis = ld_bits(P.visited + w);
       const int64_t rem = P.n - w * 32;  // mask off ids >= n in the last word
       if (rem < 32) pad = 0xffffffffu << rem;
@@ -555,13 +559,13 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         const uint32_t m = __shfl_sync(kFull, pm, lo);
         const int ex = __shfl_sync(kFull, excl, lo);
         if (need && c < total) {
-          v[k] = (uint32_t)(((t << 5) + lo) * 32 + (int)__fns(m, 0, c - ex + 1));
+          v[k] = (uint32_t)((tbase + lo) * 32 + (int)__fns(m, 0, c - ex + 1));
           b[k] = ld_off(P.in_off + v[k]);
           d[k] = (uint32_t)(ld_off(P.in_off + v[k] + 1) - b[k]);
           rounds[k] = 0;
           st[k] = 1;
           if (d[k] == 0) {  // no in-edges: never reachable; skip it from now on
-            atomicOr(&acc_d[(v[k] >> 5) & 31u], 1u << (v[k] & 31u));
+            atomicOr(&acc_d[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
             st[k] = 0;
           }
         }
@@ -595,7 +599,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         if (hit) {
           P.parent[v[k]] = (int32_t)par;
           if (P.want_depth) P.depth[v[k]] = lvl + 1;
-          atomicOr(&acc_n[(v[k] >> 5) & 31u], 1u << (v[k] & 31u));
+          atomicOr(&acc_n[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
           st[k] = 0;
         } else {
           const uint32_t tk = d[k] < (uint32_t)kPerRound ? d[k] : (uint32_t)kPerRound;
@@ -611,7 +615,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
       }
     }
     __syncwarp();
-    if (w < P.w32) {
+    if ((int)lane < tw && w < P.w32) {
       const uint32_t nbits = acc_n[lane], dbits = acc_d[lane];
       next[w] = nbits;
       if (nbits | dbits) P.visited[w] = vis | nbits | dbits;
@@ -745,6 +749,9 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   uint32_t* frontg = P.bm0;
   uint32_t* nextg = P.bm1;
   uint32_t* sfront = reinterpret_cast<uint32_t*>(dyn_smem);
+  const long long nwarps = gthreads >> 5;
+  int bu_tw_log = 5;  // bottom-up task = 32 words unless that leaves warps idle
+  while (bu_tw_log > 0 && ((P.w32 + (1 << bu_tw_log) - 1) >> bu_tw_log) < nwarps) bu_tw_log--;
 
   while (qe > qs) {
     const bool go_bu = P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha;
@@ -783,8 +790,8 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         long long acc = 0;
         // long-list scratch: queue slots past the tail are unused during bottom-up
         const unsigned long long lbase = qe;
-        if (P.front_in_smem) bu_step<true>(P, s, ph, fr, nextg, lvl, lbase, acc);
-        else bu_step<false>(P, s, ph, fr, nextg, lvl, lbase, acc);
+        if (P.front_in_smem) bu_step<true>(P, s, ph, fr, nextg, lvl, lbase, bu_tw_log, acc);
+        else bu_step<false>(P, s, ph, fr, nextg, lvl, lbase, bu_tw_log, acc);
         unsigned set = ph & 3;
         block_add(acc, &P.ctrl->cnt[set][kSum], s);
         if (!grid_sync(P, s, ph, kTagBU)) return;
@@ -821,6 +828,12 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       // high-MLP pass; small ones keep everything inline, so a long chain of
       // tiny levels costs one grid barrier each.
       const bool big = scout > P.bitmap_td_min;
+      // Granularity from the step size the heuristic already knows: enough
+      // tiles / chunks for every CTA / warp (hardware-derived, not per graph).
+      int tile_sz = kBlock;
+      while (tile_sz > 32 && (long long)(qe - qs) < (long long)tile_sz * gridDim.x) tile_sz >>= 1;
+      int64_t chunk = kChunkMax;
+      while (chunk > kChunkMin && scout < chunk * nwarps) chunk >>= 1;
       long long sacc = 0;
       unsigned set;
       if (big) {
@@ -831,9 +844,9 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       {
         const QApp qa = qapp(P, ph, qtail);
         if (big) {
-          td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt);
+          td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk);
         } else {
-          td_light<false>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt);
+          td_light<false>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk);
           wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
         }
       }

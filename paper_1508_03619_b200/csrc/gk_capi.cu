@@ -81,7 +81,7 @@ gk_status alloc_workspace(gk_graph* g) {
   g->bm0 = g->bits + wbytes / 4;
   g->bm1 = g->bits + 2 * (wbytes / 4);
   CK(cudaMalloc(&g->queue, sizeof(uint32_t) * (n + 1)), "alloc queue");
-  g->chunk_cap = 2 * (g->m / 1024) + 64;
+  g->chunk_cap = 2 * (g->m / 1024) + 65536;  // >= 4 x warps when chunks shrink to 128 edges
   CK(cudaMalloc(&g->chunks, sizeof(gk::Chunk) * g->chunk_cap), "alloc chunks");
   CK(cudaMalloc(&g->ctrl, sizeof(gk::Ctrl)), "alloc ctrl");
   g->step_cap = std::min<int64_t>(n + 2, int64_t(1) << 20);
