@@ -27,6 +27,18 @@ __device__ __forceinline__ T block_sum(T x, T* sm) {
   return t;
 }
 
+// Bit v set when v has no in-edges (it can never be reached from another
+// vertex) or v >= n (padding of the last word).  The traversal seeds its
+// visited map with it so bottom-up sweeps never revisit such vertices.
+__global__ void k_dead(const int64_t* __restrict__ in_off, int64_t n, int64_t w32, uint32_t* __restrict__ dead) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;  // a multiple of 32
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < w32 * 32; v += stride) {
+    const bool d = v >= n || in_off[v + 1] == in_off[v];
+    const unsigned bits = __ballot_sync(0xffffffffu, d);
+    if ((threadIdx.x & 31) == 0) dead[v >> 5] = bits;
+  }
+}
+
 __global__ void k_count_reached(const int32_t* __restrict__ parent, const int64_t* __restrict__ off,
                                 int64_t n, unsigned long long* out) {
   __shared__ unsigned long long sm[kAuxBlock / 32];
@@ -189,6 +201,12 @@ int aux_grid(int64_t n) {
 }
 
 }  // namespace
+
+cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s) {
+  const int64_t w32 = (n + 31) / 32;
+  k_dead<<<aux_grid(w32 * 32), kAuxBlock, 0, s>>>(in_off, n, w32, dead);
+  return cudaGetLastError();
+}
 
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s) {

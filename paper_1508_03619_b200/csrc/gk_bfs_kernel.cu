@@ -289,21 +289,17 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
   uint32_t w[4];
   bool c[4];
   if (kBig) {
-    // Fire-and-forget claims: a target is taken when neither its visited
-    // bit nor its next-frontier bit is set; racing writers all store a valid
-    // parent (any frontier neighbour) and OR the same next bit.  visited is
-    // folded in afterwards by td_scout_bits.  No atomic round trip sits on
-    // the chain, and the next-bit pre-check filters repeat targets once the
-    // first RED lands.
+    // Fire-and-forget claims: the next-frontier bitmap starts as a copy of
+    // visited, so one pre-check covers both "already visited" and "already
+    // claimed this step"; racing writers all store a valid parent (any
+    // frontier neighbour) and OR the same bit.  td_scout_bits strips the
+    // visited bits afterwards.  No atomic round trip sits on the chain.
     uint32_t x[4];
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-      w[k] = ok[k] ? ld_bits_l1(P.visited + (v[k] >> 5)) : 0xffffffffu;
-      x[k] = ok[k] ? ld_bits(nextbm + (v[k] >> 5)) : 0xffffffffu;
-    }
+    for (int k = 0; k < 4; k++) x[k] = ok[k] ? ld_bits(nextbm + (v[k] >> 5)) : 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-      if (!(((w[k] | x[k]) >> (v[k] & 31u)) & 1u)) {
+      if (!((x[k] >> (v[k] & 31u)) & 1u)) {
         st_parent(P.parent + v[k], (int32_t)u[k]);
         atomicOr(nextbm + (v[k] >> 5), 1u << (v[k] & 31u));  // result unused -> RED
       }
@@ -432,45 +428,78 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
 // ---- degrees of the vertices a large top-down step claimed ----------------
 // scout = sum of -old over the claims (bfs.hpp:83) = sum of max(deg, 1)
 // with the degree encoding, or the claim count without it (bfs.hpp:129).
-// Walks the claim bitmap in vertex order, kSW words per warp iteration, so
-// the degree reads are coalesced offset runs instead of random gathers.
-constexpr int kSW = 4;
-__device__ void td_scout_bits(const BfsParams& P, const uint32_t* bm, int lvl, bool encode,
+// A warp walks 32 bitmap words (1024 vertices) per iteration in vertex
+// order: lane l owns word l (claims = next & ~visited become the next
+// frontier and are folded into visited), then the claimed vertices are
+// numbered by a warp prefix sum and spread over the lanes, four per lane in
+// flight, so the offset reads are sorted, mostly coalesced runs.  The next
+// iteration's words are loaded one iteration ahead.
+__device__ void td_scout_bits(const BfsParams& P, uint32_t* bm, int lvl, bool encode,
                               long long& scout, long long& count) {
   const unsigned lane = lane_id();
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
-  for (long long w0 = gw * kSW; w0 < P.w32; w0 += nw * kSW) {
-    uint32_t wd[kSW];
-    int64_t o0[kSW], o1[kSW];
-#pragma unroll
-    for (int k = 0; k < kSW; k++) wd[k] = (w0 + k < P.w32) ? ld_bits(bm + w0 + k) : 0u;
-    // fold the claims into visited (one owner per word)
-    if (lane < kSW && w0 + lane < P.w32) {
-      uint32_t mine = wd[0];
-#pragma unroll
-      for (int k = 1; k < kSW; k++)
-        if ((int)lane == k) mine = wd[k];
-      if (mine) P.visited[w0 + lane] |= mine;
+  auto load2 = [&](long long w0, uint32_t& nx, uint32_t& vis) {
+    const long long w = w0 + lane;
+    nx = vis = 0u;
+    if (w < P.w32) {
+      nx = ld_bits(bm + w);
+      vis = ld_bits(P.visited + w);
     }
+  };
+  long long w0 = gw * 32;
+  uint32_t nx, vis;
+  load2(w0, nx, vis);
+  for (; w0 < P.w32; w0 += nw * 32) {
+    uint32_t nx_n, vis_n;
+    load2(w0 + nw * 32, nx_n, vis_n);
+    const uint32_t cl = nx & ~vis;
+    if (w0 + lane < P.w32) {
+      if (cl != nx) bm[w0 + lane] = cl;
+      if (cl) P.visited[w0 + lane] = vis | cl;
+    }
+    const int cnt = __popc(cl);
+    count += cnt;
+    int incl = cnt;
 #pragma unroll
-    for (int k = 0; k < kSW; k++) {
-      o0[k] = o1[k] = 0;
-      if ((wd[k] >> lane) & 1u) {
-        const int64_t v = (w0 + k) * 32 + lane;
-        o0[k] = __ldg(P.out_off + v);
-        o1[k] = __ldg(P.out_off + v + 1);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(kFull, incl, 31);
+    for (int base = 0; base < total; base += 128) {
+      int64_t o0[4], o1[4];
+      int64_t v[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int c = base + k * 32 + (int)lane;
+        int lo = 0;  // word holding the c-th claim: last lane with excl <= c
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int e = __shfl_sync(kFull, excl, lo + step);
+          if (e <= c) lo += step;
+        }
+        const uint32_t m = __shfl_sync(kFull, cl, lo);
+        const int ex = __shfl_sync(kFull, excl, lo);
+        v[k] = -1;
+        o0[k] = o1[k] = 0;
+        if (c < total) {
+          v[k] = (w0 + lo) * 32 + (int)__fns(m, 0, c - ex + 1);
+          o0[k] = __ldg(P.out_off + v[k]);
+          o1[k] = __ldg(P.out_off + v[k] + 1);
+        }
       }
-    }
 #pragma unroll
-    for (int k = 0; k < kSW; k++) {
-      if ((wd[k] >> lane) & 1u) {
+      for (int k = 0; k < 4; k++) {
+        if (v[k] < 0) continue;
         const long long d = o1[k] - o0[k];
         scout += encode ? (d ? d : 1) : 1;
-        if (P.want_depth) P.depth[(w0 + k) * 32 + lane] = lvl + 1;
+        if (P.want_depth) P.depth[v[k]] = lvl + 1;
       }
-      if (lane == 0) count += __popc(wd[k]);
     }
+    nx = nx_n;
+    vis = vis_n;
   }
 }
 
@@ -718,20 +747,20 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       P.parent[i] = -1;
       if (P.want_depth) P.depth[i] = -1;
     }
+    // visited starts as the never-reachable set, so sweeps skip it
     const long long w4 = P.w32 >> 2;
-    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
     for (long long i = gtid; i < w4; i += gthreads) {
-      reinterpret_cast<uint4*>(P.visited)[i] = z4;
+      reinterpret_cast<uint4*>(P.visited)[i] = __ldg(reinterpret_cast<const uint4*>(P.dead) + i);
     }
     for (long long i = (w4 << 2) + gtid; i < P.w32; i += gthreads) {
-      P.visited[i] = 0u;
+      P.visited[i] = __ldg(P.dead + i);
     }
   }
   if (!grid_sync(P, s, ph, kTagInit)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // bfs.hpp:132-136
     P.parent[src] = (int32_t)src;
     if (P.want_depth) P.depth[src] = 0;
-    P.visited[src >> 5] = 1u << (src & 31u);
+    P.visited[src >> 5] |= 1u << (src & 31u);
     P.queue[0] = src;
   }
   if (!grid_sync(P, s, ph, kTagInit)) return;
@@ -836,8 +865,8 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       while (chunk > kChunkMin && scout < chunk * nwarps) chunk >>= 1;
       long long sacc = 0;
       unsigned set;
-      if (big) {
-        for (long long i = gtid; i < P.w32; i += gthreads) nextg[i] = 0u;
+      if (big) {  // next := visited (see claim4<true>)
+        for (long long i = gtid; i < P.w32; i += gthreads) nextg[i] = __ldcg(P.visited + i);
         if (!grid_sync(P, s, ph, kTagZero)) return;
       }
       set = ph & 3;

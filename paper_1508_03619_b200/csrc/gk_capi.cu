@@ -76,10 +76,11 @@ gk_status alloc_workspace(gk_graph* g) {
   CK(cudaMalloc(&g->parent, sizeof(int32_t) * std::max<int64_t>(n, 4) + 16), "alloc parent");
   // visited | front | next bitmaps in one block so one L2 access-policy
   // window can keep them resident while the graph streams past.
-  CK(cudaMalloc(&g->bits, 3 * wbytes + 64), "alloc bitmaps");
+  CK(cudaMalloc(&g->bits, 4 * wbytes + 64), "alloc bitmaps");
   g->visited = g->bits;
   g->bm0 = g->bits + wbytes / 4;
   g->bm1 = g->bits + 2 * (wbytes / 4);
+  g->dead = g->bits + 3 * (wbytes / 4);
   CK(cudaMalloc(&g->queue, sizeof(uint32_t) * (n + 1)), "alloc queue");
   g->chunk_cap = 2 * (g->m / 1024) + 65536;  // >= 4 x warps when chunks shrink to 128 edges
   CK(cudaMalloc(&g->chunks, sizeof(gk::Chunk) * g->chunk_cap), "alloc chunks");
@@ -91,6 +92,8 @@ gk_status alloc_workspace(gk_graph* g) {
   CK(cudaEventCreate(&g->ev0), "event");
   CK(cudaEventCreate(&g->ev1), "event");
   CK(gk::bfs_configure(g->device, &g->launch), "configure bfs kernel");
+  CK(gk::dead_bitmap(g->in_off, n, g->dead, g->stream), "dead-vertex bitmap");
+  CK(cudaStreamSynchronize(g->stream), "dead-vertex bitmap");
   const char* pers = getenv("GK_L2_PERSIST");
   if (!pers || atoi(pers) != 0) {
     int max_win = 0, max_pers = 0;
@@ -352,6 +355,7 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   p.parent = g->parent;
   p.depth = g->depth;
   p.visited = g->visited;
+  p.dead = g->dead;
   p.bm0 = g->bm0;
   p.bm1 = g->bm1;
   // Large top-down steps additionally clear and fill the n/8-byte next
@@ -368,6 +372,8 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
   p.stop_after = 0xffffffffu;
   if (const char* sa = getenv("GK_STOP_AFTER")) p.stop_after = (unsigned)strtoul(sa, nullptr, 10);
+  p.exp_flags = 0;
+  if (const char* ex = getenv("GK_EXP")) p.exp_flags = (unsigned)strtoul(ex, nullptr, 10);
 
   cudaStream_t s = g->stream;
   CK(cudaEventRecord(g->ev0, s), "event record");

@@ -76,6 +76,7 @@ struct BfsParams {
   uint32_t* visited;
   uint32_t* bm0;
   uint32_t* bm1;
+  const uint32_t* dead;  // in-degree-0 vertices (+ ids >= n): never reachable
   uint32_t* queue;
   Chunk* chunks;
   int64_t chunk_cap;
@@ -84,6 +85,7 @@ struct BfsParams {
   int64_t step_cap;
   unsigned long long timeout_ns;
   unsigned stop_after;  // leave after this many grid barriers (profiling only)
+  unsigned exp_flags;   // experiment switches (GK_EXP, profiling only)
 };
 
 constexpr int kBlock = 512;
@@ -100,6 +102,7 @@ cudaError_t bfs_configure(int device, BfsLaunch* cfg);
 cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t s);
 
 // Auxiliary (untimed) kernels.
+cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s);
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s);
 cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
@@ -142,10 +145,11 @@ struct gk_graph {
   // workspace
   int32_t* parent = nullptr;
   int32_t* depth = nullptr;
-  uint32_t* bits = nullptr;  // one block: visited | bm0 | bm1
+  uint32_t* bits = nullptr;  // one block: visited | bm0 | bm1 | dead
   uint32_t* visited = nullptr;
   uint32_t* bm0 = nullptr;
   uint32_t* bm1 = nullptr;
+  uint32_t* dead = nullptr;  // graph property, computed once by finish_graph
   uint32_t* queue = nullptr;
   gk::Chunk* chunks = nullptr;
   int64_t chunk_cap = 0;
