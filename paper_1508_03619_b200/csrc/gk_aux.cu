@@ -39,6 +39,19 @@ __global__ void k_dead(const int64_t* __restrict__ in_off, int64_t n, int64_t w3
   }
 }
 
+__global__ void k_head(const int64_t* __restrict__ in_off, const uint32_t* __restrict__ in_nb, int64_t n,
+                       uint4* __restrict__ head) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = in_off[v], d = in_off[v + 1] - b;
+    uint32_t h[kHead];
+#pragma unroll
+    for (int j = 0; j < kHead; j++) h[j] = j < d ? in_nb[b + j] : kNoVertex;
+#pragma unroll
+    for (int q = 0; q < kHead / 4; q++)
+      head[v * (kHead / 4) + q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+  }
+}
+
 __global__ void k_count_reached(const int32_t* __restrict__ parent, const int64_t* __restrict__ off,
                                 int64_t n, unsigned long long* out) {
   __shared__ unsigned long long sm[kAuxBlock / 32];
@@ -205,6 +218,11 @@ int aux_grid(int64_t n) {
 cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s) {
   const int64_t w32 = (n + 31) / 32;
   k_dead<<<aux_grid(w32 * 32), kAuxBlock, 0, s>>>(in_off, n, w32, dead);
+  return cudaGetLastError();
+}
+
+cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, uint4* head, cudaStream_t s) {
+  k_head<<<aux_grid(n), kAuxBlock, 0, s>>>(in_off, in_nb, n, head);
   return cudaGetLastError();
 }
 

@@ -509,16 +509,22 @@ __device__ void td_scout_bits(const BfsParams& P, uint32_t* bm, int lvl, bool en
 // prefix sum.  Every lane keeps kBuSlots vertices in flight and refills a slot
 // (select-the-c-th-pending-vertex: shuffle binary search + __fns) as soon as
 // its vertex resolves, so one slow list never idles the other lanes.  Per
-// round a slot tests the next kPerRound in-neighbours of its vertex; after
-// kLaneRounds rounds a still-unresolved vertex is deferred to the long list,
-// scanned after the sweep by whole warps with a ballot per 32 neighbours.
-// The chosen parent is the first in-neighbour (ascending) whose front bit is
-// set, as in bfs.hpp:55-60.  Results are OR-ed into per-warp shared-memory
-// words and written back once per task; vertices without in-edges are
-// marked visited ("dead") the first time they are seen.
+// round a slot tests the next kPerRound in-neighbours of its vertex: round 1
+// reads the vertex's head (its first kHead in-neighbours, a dense 16-byte
+// record per vertex, so the sweep streams it in vertex order instead of
+// paying one random in_nb sector per vertex), later rounds continue in
+// in_nb.  After kLaneRounds rounds a still-unresolved vertex is deferred to
+// the long list, scanned after the sweep by whole warps with a ballot per 32
+// neighbours.  The chosen parent is the first in-neighbour (ascending) whose
+// front bit is set, as in bfs.hpp:55-60.  Results are OR-ed into per-warp
+// shared-memory words and written back once per task.  Vertices without
+// in-edges never appear: visited starts as the graph's dead bitmap.
 constexpr int kBuSlots = 2;
 constexpr int kPerRound = 4;    // in-neighbours tested per slot per round
 constexpr int kLaneRounds = 8;  // rounds before a list is deferred to the long list
+static_assert(kPerRound == 4 && kHead % 4 == 0, "a head round tests one uint4 of neighbours");
+constexpr int kHeadParts = kHead / 4;  // head rounds: slot states 1..kHeadParts
+constexpr int kListState = kHeadParts + 1;
 
 // front is either the global bitmap or its shared-memory copy (small graphs).
 template <bool kSmem>
@@ -564,7 +570,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
     int next_c = 0;
     uint32_t v[kBuSlots], d[kBuSlots], rounds[kBuSlots];
     int64_t b[kBuSlots];
-    int st[kBuSlots];  // 0 empty, 1 scanning
+    int st[kBuSlots];  // 0 empty, 1..kHeadParts head rounds, kListState in_nb rounds
 #pragma unroll
     for (int k = 0; k < kBuSlots; k++) {
       st[k] = 0;
@@ -589,14 +595,8 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         const int ex = __shfl_sync(kFull, excl, lo);
         if (need && c < total) {
           v[k] = (uint32_t)((tbase + lo) * 32 + (int)__fns(m, 0, c - ex + 1));
-          b[k] = ld_off(P.in_off + v[k]);
-          d[k] = (uint32_t)(ld_off(P.in_off + v[k] + 1) - b[k]);
           rounds[k] = 0;
           st[k] = 1;
-          if (d[k] == 0) {  // no in-edges: never reachable; skip it from now on
-            atomicOr(&acc_d[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
-            st[k] = 0;
-          }
         }
       }
       bool active = false;
@@ -606,12 +606,22 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         if (next_c >= total) break;
         continue;
       }
+      // Round 1 of a vertex reads its head (dense, vertex order); later
+      // rounds continue in in_nb after the head.
       uint32_t u[kBuSlots][kPerRound];
 #pragma unroll
       for (int k = 0; k < kBuSlots; k++) {
+        if (st[k] >= 1 && st[k] <= kHeadParts) {
+          const uint4 h = __ldg(P.head + (size_t)v[k] * kHeadParts + (st[k] - 1));
+          u[k][0] = h.x;
+          u[k][1] = h.y;
+          u[k][2] = h.z;
+          u[k][3] = h.w;
+        } else {
 #pragma unroll
-        for (int j = 0; j < kPerRound; j++)
-          u[k][j] = (st[k] && d[k] > (uint32_t)j) ? ld_nb(P.in_nb + b[k] + j) : 0u;
+          for (int j = 0; j < kPerRound; j++)
+            u[k][j] = (st[k] && d[k] > (uint32_t)j) ? ld_nb(P.in_nb + b[k] + j) : kNoVertex;
+        }
       }
 #pragma unroll
       for (int k = 0; k < kBuSlots; k++) {
@@ -620,7 +630,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         uint32_t par = 0;
 #pragma unroll
         for (int j = 0; j < kPerRound; j++) {
-          if (!hit && d[k] > (uint32_t)j && front_bit<kSmem>(front, u[k][j])) {
+          if (!hit && u[k][j] != kNoVertex && front_bit<kSmem>(front, u[k][j])) {
             hit = true;
             par = u[k][j];
           }
@@ -630,6 +640,20 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
           if (P.want_depth) P.depth[v[k]] = lvl + 1;
           atomicOr(&acc_n[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
           st[k] = 0;
+        } else if (st[k] <= kHeadParts) {
+          if (st[k] == 1 && u[k][0] == kNoVertex) {  // no in-edges: never reachable; skip it from now on
+            atomicOr(&acc_d[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
+            st[k] = 0;
+          } else if (u[k][3] == kNoVertex) {
+            st[k] = 0;  // the list ended inside the head: not reached at this level
+          } else if (st[k] < kHeadParts) {
+            st[k]++;  // next part of the head
+          } else {
+            b[k] = ld_off(P.in_off + v[k]) + kHead;
+            d[k] = (uint32_t)(ld_off(P.in_off + v[k] + 1) - b[k]);
+            rounds[k] = kHeadParts;
+            st[k] = d[k] ? kListState : 0;
+          }
         } else {
           const uint32_t tk = d[k] < (uint32_t)kPerRound ? d[k] : (uint32_t)kPerRound;
           b[k] += tk;

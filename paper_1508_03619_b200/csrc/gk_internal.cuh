@@ -77,6 +77,7 @@ struct BfsParams {
   uint32_t* bm0;
   uint32_t* bm1;
   const uint32_t* dead;  // in-degree-0 vertices (+ ids >= n): never reachable
+  const uint4* head;     // first kHead in-neighbours of every vertex (kNoVertex-padded), kHead/4 uint4 each
   uint32_t* queue;
   Chunk* chunks;
   int64_t chunk_cap;
@@ -103,6 +104,12 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t s)
 
 // Auxiliary (untimed) kernels.
 cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s);
+// head[v] = the first kHead in-neighbours of v in CSR (ascending) order,
+// padded with kNoVertex: the bottom-up sweep's first round reads this dense
+// array (sequential in v) instead of one random sector of in_nb per vertex.
+constexpr int kHead = 4;  // one uint4 per vertex
+constexpr uint32_t kNoVertex = 0xffffffffu;
+cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, uint4* head, cudaStream_t s);
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s);
 cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
@@ -150,6 +157,7 @@ struct gk_graph {
   uint32_t* bm0 = nullptr;
   uint32_t* bm1 = nullptr;
   uint32_t* dead = nullptr;  // graph property, computed once by finish_graph
+  uint4* head = nullptr;     // ditto: the first kHead entries of every in-list
   uint32_t* queue = nullptr;
   gk::Chunk* chunks = nullptr;
   int64_t chunk_cap = 0;
