@@ -3,6 +3,8 @@
 // device BFS certificate (§8(f)-2).  None runs inside the timed traversal.
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "gk_internal.cuh"
 
 namespace gk {
@@ -39,16 +41,26 @@ __global__ void k_dead(const int64_t* __restrict__ in_off, int64_t n, int64_t w3
   }
 }
 
+__global__ void k_live_count(const uint32_t* __restrict__ dead, int64_t w32, uint32_t* __restrict__ cnt) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < w32; w += (int64_t)gridDim.x * blockDim.x)
+    cnt[w] = __popc(~dead[w]);
+}
+
+// Heads are stored only for live (not dead) vertices, in vertex order:
+// v's record is hbase[v/32] + (live vertices before v in its word).
 __global__ void k_head(const int64_t* __restrict__ in_off, const uint32_t* __restrict__ in_nb, int64_t n,
-                       uint4* __restrict__ head) {
+                       const uint32_t* __restrict__ dead, const uint32_t* __restrict__ hbase,
+                       HeadRec* __restrict__ head) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t live = ~dead[v >> 5];
+    const uint32_t bit = (uint32_t)(v & 31);
+    if (!((live >> bit) & 1u)) continue;
+    const int64_t idx = (int64_t)hbase[v >> 5] + __popc(live & ((1u << bit) - 1u));
     const int64_t b = in_off[v], d = in_off[v + 1] - b;
     uint32_t h[kHead];
 #pragma unroll
     for (int j = 0; j < kHead; j++) h[j] = j < d ? in_nb[b + j] : kNoVertex;
-#pragma unroll
-    for (int q = 0; q < kHead / 4; q++)
-      head[v * (kHead / 4) + q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+    head[idx] = head_pack(h, (HeadRec*)nullptr);
   }
 }
 
@@ -221,9 +233,32 @@ cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, uint4* head, cudaStream_t s) {
-  k_head<<<aux_grid(n), kAuxBlock, 0, s>>>(in_off, in_nb, n, head);
-  return cudaGetLastError();
+cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, const uint32_t* dead,
+                       uint32_t* hbase, HeadRec** head, cudaStream_t s) {
+  const int64_t w32 = (n + 31) / 32;
+  uint32_t* cnt = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  uint32_t last[2] = {0, 0};
+  cudaError_t e;
+  if ((e = cudaMalloc(&cnt, sizeof(uint32_t) * (w32 + 1)))) return e;
+  k_live_count<<<aux_grid(w32), kAuxBlock, 0, s>>>(dead, w32, cnt);
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, hbase, (int)w32, s))) goto out;
+  if ((e = cudaMalloc(&tmp, tb))) goto out;
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, hbase, (int)w32, s))) goto out;
+  if ((e = cudaMemcpyAsync(&last[0], hbase + w32 - 1, 4, cudaMemcpyDeviceToHost, s))) goto out;
+  if ((e = cudaMemcpyAsync(&last[1], cnt + w32 - 1, 4, cudaMemcpyDeviceToHost, s))) goto out;
+  if ((e = cudaStreamSynchronize(s))) goto out;
+  {
+    const int64_t live = (int64_t)last[0] + last[1];
+    if ((e = cudaMalloc(head, sizeof(HeadRec) * (live > 0 ? live : 1)))) goto out;
+    k_head<<<aux_grid(n), kAuxBlock, 0, s>>>(in_off, in_nb, n, dead, hbase, *head);
+    e = cudaGetLastError();
+  }
+out:
+  cudaFree(tmp);
+  cudaFree(cnt);
+  return e;
 }
 
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,

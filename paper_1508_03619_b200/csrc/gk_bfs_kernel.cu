@@ -408,6 +408,34 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
   // round-robin over warps balances without a contended grab counter.
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  if (kBig) {
+    // 8 edges per lane in flight and the next chunk descriptor prefetched:
+    // the hub step is bound by the nb -> bitmap-word dependent latency
+    constexpr int kE = 8;
+    Chunk ch = gw < (long long)nch ? P.chunks[gw] : Chunk{};
+    for (unsigned long long c = gw; c < nch; c += nw) {
+      const Chunk chn = c + nw < nch ? P.chunks[c + nw] : Chunk{};
+      for (uint32_t o = 0; o < ch.len; o += 32 * kE) {
+        uint32_t v[kE], x[kE];
+#pragma unroll
+        for (int k = 0; k < kE; k++) {
+          const uint32_t j = o + lane + 32u * k;
+          v[k] = j < ch.len ? ld_nb_once(P.out_nb + ch.start + j) : kNoVertex;
+        }
+#pragma unroll
+        for (int k = 0; k < kE; k++) x[k] = v[k] != kNoVertex ? ld_bits(nextbm + (v[k] >> 5)) : 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < kE; k++) {
+          if (!((x[k] >> (v[k] & 31u)) & 1u)) {  // see claim4<true>
+            st_parent(P.parent + v[k], (int32_t)ch.u);
+            atomicOr(nextbm + (v[k] >> 5), 1u << (v[k] & 31u));
+          }
+        }
+      }
+      ch = chn;
+    }
+    return;
+  }
   for (unsigned long long c = gw; c < nch; c += nw) {
     const Chunk ch = P.chunks[c];
     const uint32_t uu[4] = {ch.u, ch.u, ch.u, ch.u};
@@ -522,9 +550,7 @@ __device__ void td_scout_bits(const BfsParams& P, uint32_t* bm, int lvl, bool en
 constexpr int kBuSlots = 2;
 constexpr int kPerRound = 4;    // in-neighbours tested per slot per round
 constexpr int kLaneRounds = 8;  // rounds before a list is deferred to the long list
-static_assert(kPerRound == 4 && kHead % 4 == 0, "a head round tests one uint4 of neighbours");
-constexpr int kHeadParts = kHead / 4;  // head rounds: slot states 1..kHeadParts
-constexpr int kListState = kHeadParts + 1;
+static_assert(kHead <= kPerRound, "a head round tests one head record");
 
 // front is either the global bitmap or its shared-memory copy (small graphs).
 template <bool kSmem>
@@ -548,9 +574,11 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
   for (long long t = gw; t < ntasks; t += nw) {
     const long long tbase = t << tw_log;
     const long long w = tbase + lane;
-    uint32_t vis = 0xffffffffu, pad = 0u;
+    uint32_t vis = 0xffffffffu, pad = 0u, live = 0u, hb = 0u;
     if ((int)lane < tw && w < P.w32) {
       vis = ld_bits(P.visited + w);
+      live = ~__ldg(P.dead + w);
+      hb = __ldg(P.hbase + w);
       const int64_t rem = P.n - w * 32;  // mask off ids >= n in the last word
       if (rem < 32) pad = 0xffffffffu << rem;
     }
@@ -570,7 +598,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
     int next_c = 0;
     uint32_t v[kBuSlots], d[kBuSlots], rounds[kBuSlots];
     int64_t b[kBuSlots];
-    int st[kBuSlots];  // 0 empty, 1..kHeadParts head rounds, kListState in_nb rounds
+    int st[kBuSlots];  // 0 empty, 1 head round, 2 in_nb rounds
 #pragma unroll
     for (int k = 0; k < kBuSlots; k++) {
       st[k] = 0;
@@ -593,8 +621,12 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         }
         const uint32_t m = __shfl_sync(kFull, pm, lo);
         const int ex = __shfl_sync(kFull, excl, lo);
+        const uint32_t lv = __shfl_sync(kFull, live, lo);
+        const uint32_t hbl = __shfl_sync(kFull, hb, lo);
         if (need && c < total) {
-          v[k] = (uint32_t)((tbase + lo) * 32 + (int)__fns(m, 0, c - ex + 1));
+          const uint32_t bit = __fns(m, 0, c - ex + 1);
+          v[k] = (uint32_t)((tbase + lo) * 32 + (int)bit);
+          b[k] = (int64_t)hbl + __popc(lv & ((1u << bit) - 1u));  // head record (head rounds)
           rounds[k] = 0;
           st[k] = 1;
         }
@@ -611,12 +643,8 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
       uint32_t u[kBuSlots][kPerRound];
 #pragma unroll
       for (int k = 0; k < kBuSlots; k++) {
-        if (st[k] >= 1 && st[k] <= kHeadParts) {
-          const uint4 h = __ldg(P.head + (size_t)v[k] * kHeadParts + (st[k] - 1));
-          u[k][0] = h.x;
-          u[k][1] = h.y;
-          u[k][2] = h.z;
-          u[k][3] = h.w;
+        if (st[k] == 1) {
+          head_unpack(__ldg(P.head + b[k]), u[k]);
         } else {
 #pragma unroll
           for (int j = 0; j < kPerRound; j++)
@@ -640,19 +668,17 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
           if (P.want_depth) P.depth[v[k]] = lvl + 1;
           atomicOr(&acc_n[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
           st[k] = 0;
-        } else if (st[k] <= kHeadParts) {
-          if (st[k] == 1 && u[k][0] == kNoVertex) {  // no in-edges: never reachable; skip it from now on
+        } else if (st[k] == 1) {
+          if (u[k][0] == kNoVertex) {  // no in-edges: never reachable; skip it from now on
             atomicOr(&acc_d[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
             st[k] = 0;
-          } else if (u[k][3] == kNoVertex) {
+          } else if (u[k][kHead - 1] == kNoVertex) {
             st[k] = 0;  // the list ended inside the head: not reached at this level
-          } else if (st[k] < kHeadParts) {
-            st[k]++;  // next part of the head
           } else {
             b[k] = ld_off(P.in_off + v[k]) + kHead;
             d[k] = (uint32_t)(ld_off(P.in_off + v[k] + 1) - b[k]);
-            rounds[k] = kHeadParts;
-            st[k] = d[k] ? kListState : 0;
+            rounds[k] = 1;
+            st[k] = d[k] ? 2 : 0;
           }
         } else {
           const uint32_t tk = d[k] < (uint32_t)kPerRound ? d[k] : (uint32_t)kPerRound;
@@ -679,7 +705,8 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
 }
 
 // Long in-lists deferred by bu_step: one warp per vertex, ballot over 32
-// neighbours at a time, resuming after the kPerRound*kLaneRounds tested.
+// neighbours at a time, resuming after the head and the kLaneRounds-1
+// in_nb rounds bu_step tested.
 template <bool kSmem>
 __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* next,
                         unsigned long long base, unsigned long long count, int lvl, long long& awake) {
@@ -689,7 +716,7 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
   for (long long i = gw; i < (long long)count; i += nw) {
     const uint32_t v = __ldcg(P.queue + base + i);
     const int64_t le = P.in_off[v + 1];
-    for (int64_t j = P.in_off[v] + kPerRound * kLaneRounds; j < le; j += 32) {
+    for (int64_t j = P.in_off[v] + kHead + kPerRound * (kLaneRounds - 1); j < le; j += 32) {
       const int64_t jj = j + lane;
       bool h = false;
       uint32_t u = 0;

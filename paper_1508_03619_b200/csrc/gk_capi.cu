@@ -57,6 +57,7 @@ void free_graph(gk_graph* g) {
   cudaFree(g->depth);
   cudaFree(g->bits);
   cudaFree(g->head);
+  cudaFree(g->hbase);
   cudaFree(g->queue);
   cudaFree(g->chunks);
   cudaFree(g->ctrl);
@@ -94,8 +95,8 @@ gk_status alloc_workspace(gk_graph* g) {
   CK(cudaEventCreate(&g->ev1), "event");
   CK(gk::bfs_configure(g->device, &g->launch), "configure bfs kernel");
   CK(gk::dead_bitmap(g->in_off, n, g->dead, g->stream), "dead-vertex bitmap");
-  CK(cudaMalloc(&g->head, sizeof(uint4) * (gk::kHead / 4) * std::max<int64_t>(n, 1)), "alloc in-list heads");
-  CK(gk::build_head(g->in_off, g->in_nb, n, g->head, g->stream), "in-list heads");
+  CK(cudaMalloc(&g->hbase, sizeof(uint32_t) * std::max<int64_t>(w32, 1)), "alloc head index");
+  CK(gk::build_head(g->in_off, g->in_nb, n, g->dead, g->hbase, &g->head, g->stream), "in-list heads");
   CK(cudaStreamSynchronize(g->stream), "dead-vertex bitmap");
   const char* pers = getenv("GK_L2_PERSIST");
   if (!pers || atoi(pers) != 0) {
@@ -360,6 +361,7 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   p.visited = g->visited;
   p.dead = g->dead;
   p.head = g->head;
+  p.hbase = g->hbase;
   p.bm0 = g->bm0;
   p.bm1 = g->bm1;
   // Large top-down steps additionally clear and fill the n/8-byte next

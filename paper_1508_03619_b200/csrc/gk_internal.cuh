@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <mutex>
+#include <type_traits>
 #include <string>
 
 #include "../../include/gk_bfs.h"
@@ -56,6 +57,25 @@ struct Chunk {
   int64_t start;
 };
 
+// Head records: the first kHead in-neighbours of a vertex, kNoVertex-padded.
+constexpr int kHead = 4;
+constexpr uint32_t kNoVertex = 0xffffffffu;
+using HeadRec = std::conditional<kHead == 2, uint2, uint4>::type;
+static_assert(kHead == 2 || kHead == 4, "head records are uint2 or uint4");
+__host__ __device__ inline uint2 head_pack(const uint32_t* h, uint2*) { return make_uint2(h[0], h[1]); }
+__host__ __device__ inline uint4 head_pack(const uint32_t* h, uint4*) { return make_uint4(h[0], h[1], h[2], h[3]); }
+__host__ __device__ inline void head_unpack(const uint2& r, uint32_t* u) {
+  u[0] = r.x;
+  u[1] = r.y;
+  u[2] = u[3] = kNoVertex;
+}
+__host__ __device__ inline void head_unpack(const uint4& r, uint32_t* u) {
+  u[0] = r.x;
+  u[1] = r.y;
+  u[2] = r.z;
+  u[3] = r.w;
+}
+
 struct BfsParams {
   int64_t n;
   int64_t m;
@@ -77,7 +97,8 @@ struct BfsParams {
   uint32_t* bm0;
   uint32_t* bm1;
   const uint32_t* dead;  // in-degree-0 vertices (+ ids >= n): never reachable
-  const uint4* head;     // first kHead in-neighbours of every vertex (kNoVertex-padded), kHead/4 uint4 each
+  const HeadRec* head;   // first kHead in-neighbours of every live vertex (kNoVertex-padded)
+  const uint32_t* hbase; // per bitmap word: index of its first live vertex's head
   uint32_t* queue;
   Chunk* chunks;
   int64_t chunk_cap;
@@ -107,9 +128,10 @@ cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaSt
 // head[v] = the first kHead in-neighbours of v in CSR (ascending) order,
 // padded with kNoVertex: the bottom-up sweep's first round reads this dense
 // array (sequential in v) instead of one random sector of in_nb per vertex.
-constexpr int kHead = 4;  // one uint4 per vertex
-constexpr uint32_t kNoVertex = 0xffffffffu;
-cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, uint4* head, cudaStream_t s);
+// hbase[w] = live (non-dead) vertices in words < w; head is allocated here
+// with one record per live vertex.
+cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, const uint32_t* dead,
+                       uint32_t* hbase, HeadRec** head, cudaStream_t s);
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s);
 cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
@@ -157,7 +179,8 @@ struct gk_graph {
   uint32_t* bm0 = nullptr;
   uint32_t* bm1 = nullptr;
   uint32_t* dead = nullptr;  // graph property, computed once by finish_graph
-  uint4* head = nullptr;     // ditto: the first kHead entries of every in-list
+  gk::HeadRec* head = nullptr;  // ditto: the first kHead entries of every live in-list
+  uint32_t* hbase = nullptr; // ditto: head index of each word's first live vertex
   uint32_t* queue = nullptr;
   gk::Chunk* chunks = nullptr;
   int64_t chunk_cap = 0;
