@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libgk_bfs.so")
+LIB_PATH = os.environ.get("GK_LIB_PATH") or os.path.join(PKG_DIR, "lib", "libgk_bfs.so")  # override: A/B runs
 
 GK_OK = 0
 GK_ERR_SOURCE_RANGE = 1
