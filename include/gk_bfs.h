@@ -181,7 +181,7 @@ GK_API gk_status gk_bfs_keep_depth(gk_graph* g, int32_t keep);
  * bfs.hpp:139-169 and the exchanges between these calls (all-reduce of
  * counters, all-to-all of (v,u) claim pairs, all-gather of bitmap slices)
  * are run by the host orchestrator (paper_1508_03619_b200/dist.py).  All
- * kernels run on the stream set with gk_shard_set_stream. */
+ * kernels run on the stream set with gk_shard_set_stream.  1 <= P <= 64. */
 typedef struct gk_shard gk_shard;
 GK_API const char* gk_shard_last_error(void);
 /* This rank's rows of the device-generated graph (same graph as

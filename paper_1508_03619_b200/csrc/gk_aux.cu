@@ -236,6 +236,8 @@ cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaSt
 cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, const uint32_t* dead,
                        uint32_t* hbase, HeadRec** head, cudaStream_t s) {
   const int64_t w32 = (n + 31) / 32;
+  *head = nullptr;
+  if (w32 == 0) return cudaSuccess;
   uint32_t* cnt = nullptr;
   void* tmp = nullptr;
   size_t tb = 0;

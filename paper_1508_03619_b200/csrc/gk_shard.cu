@@ -32,7 +32,7 @@ constexpr int kShChunk = 1024;
 constexpr unsigned kFullMask = 0xffffffffu;
 
 // device counter slots
-enum : int { cTail = 0, cPairs = 1, cScout = 2, cClaims = 3, cAwake = 4, cChunks = 5, cDest = 8 };
+enum : int { cTail = 0, cPairs = 1, cScout = 2, cClaims = 3, cAwake = 4, cChunks = 5, cLong = 6, cDest = 8 };
 
 struct ShardParams {
   int64_t n, lo, hi, nloc, block;
@@ -53,6 +53,13 @@ struct ShardParams {
   int want_depth;
   int encode;
   int dedup;  // use (and set) the sent bitmap this level
+  int big;    // large top-down step: owned claims go to `next`, then k_sh_sweep
+  uint32_t* next;        // owned next bitmap (big top-down steps), starts as visited
+  const uint32_t* dead;  // owned never-reachable bitmap
+  const HeadRec* head;   // head records of the owned live vertices
+  const uint32_t* hbase; // head index of each owned word's first live vertex
+  uint32_t* longq;       // bottom-up long-list scratch (aliases pairs)
+  int64_t long_cap;
 };
 
 __device__ __forceinline__ unsigned lmask_lt() {
@@ -83,46 +90,126 @@ __device__ __forceinline__ long long local_degree(const ShardParams& P, uint32_t
   return P.off[r + 1] - P.off[r];
 }
 
-// Claim owned v for parent u; returns true if this thread won.
-__device__ __forceinline__ bool claim_local(const ShardParams& P, uint32_t v, uint32_t u, int lvl,
-                                            long long& scout) {
-  const uint32_t r = (uint32_t)((int64_t)v - P.lo);
-  const uint32_t bit = 1u << (r & 31u);
-  uint32_t* w = P.visited + (r >> 5);
-  if (__ldcg(w) & bit) return false;
-  if (atomicOr(w, bit) & bit) return false;
-  P.parent[r] = (int32_t)u;
-  if (P.want_depth) P.depth[r] = lvl + 1;
-  if (P.encode) {
-    const long long d = local_degree(P, v);
-    scout += d ? d : 1;  // -old of the degree-encoded slot (bfs.hpp:83)
-  } else {
-    scout += 1;
+// ---- per-warp append buffers (QueueBuffer analogue, sliding_queue.hpp:62-86)
+constexpr int kQB = 256;  // queue entries per warp buffer
+constexpr int kPB = 128;  // remote pairs per warp buffer
+
+__device__ __forceinline__ void flush_q(const ShardParams& P, uint32_t* buf, int& n, int* overflow) {
+  __syncwarp();
+  if (n == 0) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&P.ctr[cTail], (unsigned long long)n);
+  base = __shfl_sync(kFullMask, base, 0);
+  for (int i = lane; i < n; i += 32) {
+    if ((int64_t)(base + i) < P.nloc + 1) P.queue[base + i] = buf[i];
+    else *overflow = 1;
   }
-  return true;
+  __syncwarp();
+  n = 0;
+}
+__device__ __forceinline__ void push_q(const ShardParams& P, bool want, uint32_t v, uint32_t* buf, int& n,
+                                       int* overflow) {
+  const unsigned m = __ballot_sync(kFullMask, want);
+  if (!m) return;
+  if (want) buf[n + __popc(m & lmask_lt())] = v;
+  n += __popc(m);
+  if (n > kQB - 32) flush_q(P, buf, n, overflow);
+}
+__device__ __forceinline__ void flush_p(const ShardParams& P, uint64_t* buf, int& n, int* overflow) {
+  __syncwarp();
+  if (n == 0) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&P.ctr[cPairs], (unsigned long long)n);
+  base = __shfl_sync(kFullMask, base, 0);
+  for (int i = lane; i < n; i += 32) {
+    if ((int64_t)(base + i) < P.pair_cap) P.pairs[base + i] = buf[i];
+    else *overflow = 1;
+  }
+  __syncwarp();
+  n = 0;
+}
+__device__ __forceinline__ void push_p(const ShardParams& P, bool want, uint64_t pr, uint64_t* buf, int& n,
+                                       int* overflow) {
+  const unsigned m = __ballot_sync(kFullMask, want);
+  if (!m) return;
+  if (want) buf[n + __popc(m & lmask_lt())] = pr;
+  n += __popc(m);
+  if (n > kPB - 32) flush_p(P, buf, n, overflow);
 }
 
-// One edge (u -> v) of the owned frontier: claim in place or post a pair.
-__device__ __forceinline__ void td_edge(const ShardParams& P, bool ok, uint32_t u, uint32_t v, int lvl,
-                                        long long& scout, long long& claims, int* overflow) {
-  bool local = false, remote = false;
-  if (ok) {
-    const int owner = (int)((int64_t)v / P.block);
-    if (owner == P.rank) {
-      local = claim_local(P, v, u, lvl, scout);
-    } else {
-      if (P.dedup) {
-        const uint32_t bit = 1u << (v & 31u);
-        uint32_t* w = P.sent + (v >> 5);
-        remote = !(__ldcg(w) & bit) && !(atomicOr(w, bit) & bit);
-      } else {
-        remote = true;
-      }
+struct WarpBufs {
+  uint32_t* q;
+  uint64_t* p;
+  int qn, pn;
+};
+
+// N edges (u_k -> v_k) per thread, loads and atomics of all N issued
+// together.  Owned targets: small steps claim with a visited pre-check +
+// atomicOr (bfs.hpp:78-84) and append to the owned queue; big steps
+// (P.big) only store a parent and RED the bit into the owned next-bitmap
+// (which starts as a copy of visited), leaving degrees and the queue to
+// the claim sweep.  Remote targets become (v, u) pairs for their owner,
+// deduplicated per level through the sent-bitmap when P.dedup.
+template <int N>
+__device__ __forceinline__ void td_edges(const ShardParams& P, const uint32_t (&u)[N], const uint32_t (&v)[N],
+                                         int lvl, long long& scout, long long& claims, WarpBufs& wb,
+                                         int* overflow) {
+  bool loc[N], rem[N];
+  uint32_t w[N];
+#pragma unroll
+  for (int k = 0; k < N; k++) {
+    const bool ok = v[k] != kNoVertex;
+    loc[k] = ok && (int64_t)v[k] >= P.lo && (int64_t)v[k] < P.hi;
+    rem[k] = ok && !loc[k];
+    w[k] = 0xffffffffu;
+    if (loc[k]) {
+      const uint32_t r = (uint32_t)((int64_t)v[k] - P.lo);
+      w[k] = __ldcg((P.big ? P.next : P.visited) + (r >> 5));
+    } else if (rem[k] && P.dedup) {
+      w[k] = __ldcg(P.sent + (v[k] >> 5));
     }
   }
-  claims += local;
-  warp_append<uint32_t>(local, v, P.queue, &P.ctr[cTail], P.nloc + 1, overflow);
-  warp_append<uint64_t>(remote, ((uint64_t)v << 32) | u, P.pairs, &P.ctr[cPairs], P.pair_cap, overflow);
+#pragma unroll
+  for (int k = 0; k < N; k++) {
+    if (loc[k]) {
+      const uint32_t r = (uint32_t)((int64_t)v[k] - P.lo);
+      const uint32_t bit = 1u << (r & 31u);
+      if (P.big) {
+        if (!(w[k] & bit)) {
+          P.parent[r] = (int32_t)u[k];
+          atomicOr(P.next + (r >> 5), bit);  // result unused -> RED
+        }
+        loc[k] = false;
+      } else {
+        loc[k] = !(w[k] & bit) && !(atomicOr(P.visited + (r >> 5), bit) & bit);
+      }
+    } else if (rem[k] && P.dedup) {
+      const uint32_t bit = 1u << (v[k] & 31u);
+      rem[k] = !(w[k] & bit) && !(atomicOr(P.sent + (v[k] >> 5), bit) & bit);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < N; k++) {
+    if (loc[k]) {
+      const uint32_t r = (uint32_t)((int64_t)v[k] - P.lo);
+      P.parent[r] = (int32_t)u[k];
+      if (P.want_depth) P.depth[r] = lvl + 1;
+      if (P.encode) {
+        const long long d = local_degree(P, v[k]);
+        scout += d ? d : 1;  // -old of the degree-encoded slot (bfs.hpp:83)
+      } else {
+        scout += 1;
+      }
+      claims++;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < N; k++) {
+    push_q(P, loc[k], v[k], wb.q, wb.qn, overflow);
+    push_p(P, rem[k], ((uint64_t)v[k] << 32) | u[k], wb.p, wb.pn, overflow);
+  }
 }
 
 __device__ void block_sum2(long long a, long long b, unsigned long long* da, unsigned long long* db) {
@@ -147,6 +234,7 @@ __device__ void block_sum2(long long a, long long b, unsigned long long* da, uns
   }
 }
 
+// parent := -1, visited := the owned dead bitmap (never-reachable vertices)
 __global__ void k_sh_init(ShardParams P) {
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long gs = (long long)gridDim.x * blockDim.x;
@@ -154,7 +242,7 @@ __global__ void k_sh_init(ShardParams P) {
     P.parent[i] = -1;
     if (P.want_depth) P.depth[i] = -1;
   }
-  for (long long i = gt; i < (P.nloc + 31) / 32; i += gs) P.visited[i] = 0u;
+  for (long long i = gt; i < (P.nloc + 31) / 32; i += gs) P.visited[i] = __ldg(P.dead + i);
 }
 
 __global__ void k_sh_set_source(ShardParams P, uint32_t src) {
@@ -166,18 +254,29 @@ __global__ void k_sh_set_source(ShardParams P, uint32_t src) {
   P.ctr[cTail] = 1;
 }
 
+__global__ void k_sh_copy_words(const uint32_t* src, uint32_t* dst, long long words) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < words;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = __ldcg(src + i);
+}
+
 // Top-down expansion of queue[qs, qe): tiles of kSB frontier vertices, CTA
-// scan of degrees, load-balanced edge gather; vertices of degree > kShHeavy
-// become kShChunk-edge chunks handled by k_sh_td_heavy.
+// scan of degrees, load-balanced edge gather, 4 edges per thread in flight;
+// vertices of degree > kShHeavy become kShChunk-edge chunks for
+// k_sh_td_heavy.
 __global__ void __launch_bounds__(kSB) k_sh_td_light(ShardParams P, unsigned long long qs, unsigned long long qe,
                                                      int lvl) {
   __shared__ int64_t t_b[kSB];
   __shared__ int64_t t_pre[kSB + 1];
   __shared__ uint32_t t_u[kSB];
   __shared__ int64_t wsum[kSB / 32 + 1];
+  __shared__ uint32_t qbuf[kSB / 32][kQB];
+  __shared__ uint64_t pbuf[kSB / 32][kPB];
   __shared__ int overflow;
   if (threadIdx.x == 0) overflow = 0;
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpBufs wb{qbuf[warp], pbuf[warp], 0, 0};
   long long scout = 0, claims = 0;
   for (unsigned long long tile = blockIdx.x; qs + tile * kSB < qe; tile += gridDim.x) {
     const unsigned long long i = qs + tile * kSB + threadIdx.x;
@@ -206,9 +305,7 @@ __global__ void __launch_bounds__(kSB) k_sh_td_light(ShardParams P, unsigned lon
         dl = d;
       }
     }
-    // CTA exclusive scan of dl
     int64_t incl = dl;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int o = 1; o < 32; o <<= 1) {
       const int64_t y = __shfl_up_sync(kFullMask, incl, o);
       if (lane >= o) incl += y;
@@ -230,87 +327,217 @@ __global__ void __launch_bounds__(kSB) k_sh_td_light(ShardParams P, unsigned lon
     t_b[threadIdx.x] = b;
     const int64_t tot = wsum[kSB / 32];
     __syncthreads();
-    for (int64_t eb = 0; eb < tot; eb += kSB) {
-      const int64_t ei = eb + threadIdx.x;
-      bool ok = ei < tot;
-      uint32_t uu = 0, v = 0;
-      if (ok) {
-        int lo = 0, hi = kSB - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (t_pre[mid] <= ei) lo = mid;
-          else hi = mid - 1;
+    for (int64_t eb = 0; eb < tot; eb += 4 * kSB) {
+      uint32_t uu[4], v[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int64_t ei = eb + k * kSB + threadIdx.x;
+        uu[k] = 0;
+        v[k] = kNoVertex;
+        if (ei < tot) {
+          int lo = 0, hi = kSB - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (t_pre[mid] <= ei) lo = mid;
+            else hi = mid - 1;
+          }
+          uu[k] = t_u[lo];
+          v[k] = __ldg(P.nb + t_b[lo] + (ei - t_pre[lo]));
         }
-        uu = t_u[lo];
-        v = __ldg(P.nb + t_b[lo] + (ei - t_pre[lo]));
       }
-      td_edge(P, ok, uu, v, lvl, scout, claims, &overflow);
+      td_edges<4>(P, uu, v, lvl, scout, claims, wb, &overflow);
     }
     __syncthreads();
   }
+  flush_q(P, wb.q, wb.qn, &overflow);
+  flush_p(P, wb.p, wb.pn, &overflow);
   block_sum2(scout, claims, &P.ctr[cScout], &P.ctr[cClaims]);
   if (threadIdx.x == 0 && overflow) atomicExch((unsigned*)&P.ctr[7], 1u);
 }
 
+// Heavy chunks: static round-robin over warps, 8 edges per lane in flight.
 __global__ void __launch_bounds__(kSB) k_sh_td_heavy(ShardParams P, unsigned long long nch, int lvl) {
+  __shared__ uint32_t qbuf[kSB / 32][kQB];
+  __shared__ uint64_t pbuf[kSB / 32][kPB];
   __shared__ int overflow;
   if (threadIdx.x == 0) overflow = 0;
   __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpBufs wb{qbuf[warp], pbuf[warp], 0, 0};
   long long scout = 0, claims = 0;
-  const int lane = threadIdx.x & 31;
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   for (unsigned long long c = gw; c < nch; c += nw) {
     const Chunk ch = P.chunks[c];
-    for (uint32_t o = 0; o < ch.len; o += 32) {
-      const uint32_t j = o + lane;
-      const bool ok = j < ch.len;
-      const uint32_t v = ok ? __ldg(P.nb + ch.start + j) : 0u;
-      td_edge(P, ok, ch.u, v, lvl, scout, claims, &overflow);
+    uint32_t uu[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) uu[k] = ch.u;
+    for (uint32_t o = 0; o < ch.len; o += 256) {
+      uint32_t v[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const uint32_t j = o + lane + 32u * k;
+        v[k] = j < ch.len ? __ldg(P.nb + ch.start + j) : kNoVertex;
+      }
+      td_edges<8>(P, uu, v, lvl, scout, claims, wb, &overflow);
     }
   }
+  flush_q(P, wb.q, wb.qn, &overflow);
+  flush_p(P, wb.p, wb.pn, &overflow);
   block_sum2(scout, claims, &P.ctr[cScout], &P.ctr[cClaims]);
   if (threadIdx.x == 0 && overflow) atomicExch((unsigned*)&P.ctr[7], 1u);
 }
 
 // Bucket the outbox by owner rank: count, then scatter into pairs_out at
 // per-destination offsets (exclusive scan done on the host, P is small).
-__global__ void k_sh_count_dest(ShardParams P, unsigned long long npairs) {
+// Both passes aggregate per CTA in shared memory (one global atomic per
+// CTA and destination: per-pair atomics on P counters serialise).
+constexpr int kMaxRanksSmem = 64;
+__global__ void __launch_bounds__(kSB) k_sh_count_dest(ShardParams P, unsigned long long npairs) {
+  __shared__ unsigned hist[kMaxRanksSmem];
+  for (int i = threadIdx.x; i < P.nranks; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < npairs;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const uint32_t v = (uint32_t)(P.pairs[i] >> 32);
-    atomicAdd(&P.ctr[cDest + (int)((int64_t)v / P.block)], 1ull);
+    atomicAdd(&hist[(int)((int64_t)v / P.block)], 1u);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P.nranks; i += blockDim.x)
+    if (hist[i]) atomicAdd(&P.ctr[cDest + i], (unsigned long long)hist[i]);
 }
-__global__ void k_sh_scatter_dest(ShardParams P, unsigned long long npairs, unsigned long long* cursor) {
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < npairs;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(kSB) k_sh_scatter_dest(ShardParams P, unsigned long long npairs,
+                                                         unsigned long long* cursor) {
+  __shared__ unsigned hist[kMaxRanksSmem];
+  __shared__ unsigned long long base[kMaxRanksSmem];
+  // contiguous slice of the outbox per CTA
+  const unsigned long long per = (npairs + gridDim.x - 1) / gridDim.x;
+  const unsigned long long b0 = per * blockIdx.x, b1 = b0 + per < npairs ? b0 + per : npairs;
+  for (int i = threadIdx.x; i < P.nranks; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (unsigned long long i = b0 + threadIdx.x; i < b1; i += blockDim.x)
+    atomicAdd(&hist[(int)((int64_t)(P.pairs[i] >> 32) / P.block)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < P.nranks; i += blockDim.x) {
+    base[i] = hist[i] ? atomicAdd(&cursor[i], (unsigned long long)hist[i]) : 0ull;
+    hist[i] = 0;
+  }
+  __syncthreads();
+  for (unsigned long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
     const uint64_t pr = P.pairs[i];
     const int d = (int)((int64_t)(pr >> 32) / P.block);
-    P.pairs_out[atomicAdd(&cursor[d], 1ull)] = pr;
+    P.pairs_out[base[d] + atomicAdd(&hist[d], 1u)] = pr;
   }
 }
 
-// Received (v, u) pairs: claim owned v.
+// Received (v, u) pairs: claim owned v (same two modes as td_edges).
 __global__ void __launch_bounds__(kSB) k_sh_td_apply(ShardParams P, const uint64_t* in, unsigned long long npairs,
                                                      int lvl) {
+  __shared__ uint32_t qbuf[kSB / 32][kQB];
+  __shared__ uint64_t pbuf[kSB / 32][kPB];
   __shared__ int overflow;
   if (threadIdx.x == 0) overflow = 0;
   __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  WarpBufs wb{qbuf[warp], pbuf[warp], 0, 0};
   long long scout = 0, claims = 0;
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  const unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x;
+  const unsigned long long stride = 4ull * gridDim.x * blockDim.x;
+  const unsigned long long base = 4ull * blockIdx.x * blockDim.x;
   for (unsigned long long i0 = 0; i0 < npairs; i0 += stride) {
-    const unsigned long long i = i0 + base + threadIdx.x;
-    bool won = false;
-    uint32_t v = 0;
-    if (i < npairs) {
-      const uint64_t pr = in[i];
-      v = (uint32_t)(pr >> 32);
-      won = claim_local(P, v, (uint32_t)pr, lvl, scout);
+    uint32_t u[4], v[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const unsigned long long i = i0 + base + (unsigned long long)k * blockDim.x + threadIdx.x;
+      u[k] = 0;
+      v[k] = kNoVertex;
+      if (i < npairs) {
+        const uint64_t pr = in[i];
+        v[k] = (uint32_t)(pr >> 32);
+        u[k] = (uint32_t)pr;
+      }
     }
-    claims += won;
-    warp_append<uint32_t>(won, v, P.queue, &P.ctr[cTail], P.nloc + 1, &overflow);
+    td_edges<4>(P, u, v, lvl, scout, claims, wb, &overflow);
+  }
+  flush_q(P, wb.q, wb.qn, &overflow);
+  block_sum2(scout, claims, &P.ctr[cScout], &P.ctr[cClaims]);
+  if (threadIdx.x == 0 && overflow) atomicExch((unsigned*)&P.ctr[7], 1u);
+}
+
+// Claim sweep after a big top-down step (the owned analogue of the
+// persistent kernel's td_scout_bits): a warp takes 32 owned words; claims =
+// next & ~visited are folded into visited and appended to the queue in
+// vertex order (one fetch-add per warp), and their degrees are read as
+// sorted offset runs for scout.
+__global__ void __launch_bounds__(kSB) k_sh_sweep(ShardParams P, int lvl) {
+  __shared__ int overflow;
+  if (threadIdx.x == 0) overflow = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long w32 = (P.nloc + 31) / 32;
+  long long scout = 0, claims = 0;
+  for (long long w0 = gw * 32; w0 < w32; w0 += nw * 32) {
+    const long long w = w0 + lane;
+    uint32_t cl = 0;
+    if (w < w32) {
+      const uint32_t nx = __ldcg(P.next + w), vis = __ldcg(P.visited + w);
+      cl = nx & ~vis;
+      if (cl) P.visited[w] = vis | cl;
+    }
+    const int cnt = __popc(cl);
+    claims += cnt;
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFullMask, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(kFullMask, incl, 31);
+    if (total == 0) continue;
+    unsigned long long qb = 0;
+    if (lane == 0) qb = atomicAdd(&P.ctr[cTail], (unsigned long long)total);
+    qb = __shfl_sync(kFullMask, qb, 0);
+    {
+      uint32_t m = cl;
+      unsigned long long q = qb + excl;
+      while (m) {
+        const int bp = __ffs(m) - 1;
+        m &= m - 1;
+        if ((int64_t)q < P.nloc + 1) P.queue[q] = (uint32_t)(P.lo + w * 32 + bp);
+        else overflow = 1;
+        q++;
+      }
+    }
+    for (int base = 0; base < total; base += 128) {
+      int64_t o0[4], o1[4], r[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int c = base + k * 32 + lane;
+        int lo = 0;  // word holding the c-th claim: last lane with excl <= c
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int e = __shfl_sync(kFullMask, excl, lo + step);
+          if (e <= c) lo += step;
+        }
+        const uint32_t m = __shfl_sync(kFullMask, cl, lo);
+        const int ex = __shfl_sync(kFullMask, excl, lo);
+        r[k] = -1;
+        o0[k] = o1[k] = 0;
+        if (c < total) {
+          r[k] = (w0 + lo) * 32 + (int)__fns(m, 0, c - ex + 1);
+          o0[k] = __ldg(P.off + r[k]);
+          o1[k] = __ldg(P.off + r[k] + 1);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        if (r[k] < 0) continue;
+        const long long d = o1[k] - o0[k];
+        scout += P.encode ? (d ? d : 1) : 1;
+        if (P.want_depth) P.depth[r[k]] = lvl + 1;
+      }
+    }
   }
   block_sum2(scout, claims, &P.ctr[cScout], &P.ctr[cClaims]);
   if (threadIdx.x == 0 && overflow) atomicExch((unsigned*)&P.ctr[7], 1u);
@@ -326,86 +553,185 @@ __global__ void k_sh_q2b(ShardParams P, unsigned long long qs, unsigned long lon
 }
 
 // Bottom-up sweep of the owned vertices against the replicated front
-// (bfs.hpp:47-66): lane per vertex, 4 in-neighbours per round, then
-// warp-cooperative ballots; parent = first in-neighbour (ascending) with its
-// front bit, as the reference picks.
+// (bfs.hpp:47-66), the persistent kernel's bu_step on owned rows: a warp
+// task is 32 owned words; pending (not visited, not dead) vertices are
+// numbered by a warp prefix sum; 2 slots per lane refilled as they resolve;
+// round 1 reads the vertex's head record, later rounds 4 in-neighbours of
+// the list; after kLaneRounds rounds a vertex is deferred to k_sh_bu_long.
+// Parent = first in-neighbour (ascending) with its front bit, as the
+// reference picks.
+constexpr int kShSlots = 2;
+constexpr int kShRounds = 8;
 __global__ void __launch_bounds__(kSB) k_sh_bu(ShardParams P, const uint32_t* front, uint32_t* next_slice, int lvl) {
+  __shared__ uint32_t acc_all[kSB / 32][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* acc = acc_all[warp];
   long long awake = 0;
-  const int lane = threadIdx.x & 31;
   const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long w32 = (P.nloc + 31) / 32;
-  for (long long w = gw; w < w32; w += nw) {
-    const uint32_t vis = __ldcg(P.visited + w);
-    const int64_t r = w * 32 + lane;
-    bool pend = r < P.nloc && !((vis >> lane) & 1u);
-    if (__ballot_sync(kFullMask, pend) == 0) {
-      if (lane == 0) next_slice[w] = 0u;
-      continue;
+  int tw_log = 5;  // task = 2^tw_log words, smaller when that leaves warps idle
+  while (tw_log > 0 && ((w32 + (1 << tw_log) - 1) >> tw_log) < nw) tw_log--;
+  const int tw = 1 << tw_log;
+  const long long ntasks = (w32 + tw - 1) >> tw_log;
+  for (long long t = gw; t < ntasks; t += nw) {
+    const long long tbase = t << tw_log;
+    const long long w = tbase + lane;
+    uint32_t vis = 0xffffffffu, pad = 0u, live = 0u, hb = 0u;
+    if (lane < tw && w < w32) {
+      vis = __ldcg(P.visited + w);
+      live = ~__ldg(P.dead + w);
+      hb = __ldg(P.hbase + w);
+      const int64_t rem = P.nloc - w * 32;
+      if (rem < 32) pad = 0xffffffffu << rem;
     }
-    bool found = false, dead = false;
-    uint32_t par = 0;
-    int64_t b = 0, e = 0;
-    if (pend) {
-      b = P.off[r];
-      e = P.off[r + 1];
-      if (b == e) {
-        dead = true;
-        pend = false;
-      }
+    const uint32_t pm = ~(vis | pad);
+    const int cnt = __popc(pm);
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFullMask, incl, o);
+      if (lane >= o) incl += y;
     }
-    for (int round = 0; round < 4 && __ballot_sync(kFullMask, pend); round++) {
-      if (pend) {
-        uint32_t u[4];
+    const int excl = incl - cnt;
+    const int total = __shfl_sync(kFullMask, incl, 31);
+    acc[lane] = 0u;
+    __syncwarp();
+    int next_c = 0;
+    uint32_t r[kShSlots], d[kShSlots], rounds[kShSlots];
+    int64_t b[kShSlots];
+    int st[kShSlots];  // 0 empty, 1 head round, 2 list rounds
 #pragma unroll
-        for (int j = 0; j < 4; j++) u[j] = (b + j < e) ? __ldg(P.nb + b + j) : 0u;
+    for (int k = 0; k < kShSlots; k++) {
+      st[k] = 0;
+      r[k] = d[k] = rounds[k] = 0;
+      b[k] = 0;
+    }
+    for (;;) {
+#pragma unroll
+      for (int k = 0; k < kShSlots; k++) {
+        const bool need = st[k] == 0;
+        const unsigned nm = __ballot_sync(kFullMask, need);
+        const int c = next_c + __popc(nm & lmask_lt());
+        next_c += __popc(nm);
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int e = __shfl_sync(kFullMask, excl, lo + step);
+          if (e <= c) lo += step;
+        }
+        const uint32_t m = __shfl_sync(kFullMask, pm, lo);
+        const int ex = __shfl_sync(kFullMask, excl, lo);
+        const uint32_t lv = __shfl_sync(kFullMask, live, lo);
+        const uint32_t hbl = __shfl_sync(kFullMask, hb, lo);
+        if (need && c < total) {
+          const uint32_t bit = __fns(m, 0, c - ex + 1);
+          r[k] = (uint32_t)((tbase + lo) * 32 + (int)bit);
+          b[k] = (int64_t)hbl + __popc(lv & ((1u << bit) - 1u));
+          rounds[k] = 0;
+          st[k] = 1;
+        }
+      }
+      bool active = false;
+#pragma unroll
+      for (int k = 0; k < kShSlots; k++) active |= st[k] != 0;
+      if (__ballot_sync(kFullMask, active) == 0) {
+        if (next_c >= total) break;
+        continue;
+      }
+      uint32_t u[kShSlots][4];
+#pragma unroll
+      for (int k = 0; k < kShSlots; k++) {
+        if (st[k] == 1) {
+          head_unpack(__ldg(P.head + b[k]), u[k]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; j++) u[k][j] = (st[k] && d[k] > (uint32_t)j) ? __ldg(P.nb + b[k] + j) : kNoVertex;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kShSlots; k++) {
+        if (!st[k]) continue;
+        bool hit = false;
+        uint32_t par = 0;
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-          if (!found && b + j < e && ((front[u[j] >> 5] >> (u[j] & 31u)) & 1u)) {
-            found = true;
-            par = u[j];
+          if (!hit && u[k][j] != kNoVertex && ((__ldg(front + (u[k][j] >> 5)) >> (u[k][j] & 31u)) & 1u)) {
+            hit = true;
+            par = u[k][j];
           }
         }
-        if (found) pend = false;
-        else {
-          b += 4;
-          pend = b < e;
+        if (hit) {
+          P.parent[r[k]] = (int32_t)par;
+          if (P.want_depth) P.depth[r[k]] = lvl + 1;
+          atomicOr(&acc[(r[k] >> 5) - tbase], 1u << (r[k] & 31u));
+          st[k] = 0;
+        } else if (st[k] == 1) {
+          if (u[k][kHead - 1] == kNoVertex) {
+            st[k] = 0;  // the list ended inside the head
+          } else {
+            b[k] = P.off[r[k]] + kHead;
+            d[k] = (uint32_t)(P.off[r[k] + 1] - b[k]);
+            rounds[k] = 1;
+            st[k] = d[k] ? 2 : 0;
+          }
+        } else {
+          const uint32_t tk = d[k] < 4u ? d[k] : 4u;
+          b[k] += tk;
+          d[k] -= tk;
+          if (d[k] == 0) {
+            st[k] = 0;
+          } else if (++rounds[k] >= kShRounds) {
+            const unsigned long long q = atomicAdd(&P.ctr[cLong], 1ull);
+            if ((int64_t)q < P.long_cap) P.longq[q] = r[k];
+            else atomicExch((unsigned*)&P.ctr[7], 1u);
+            st[k] = 0;
+          }
         }
       }
     }
-    unsigned pm = __ballot_sync(kFullMask, pend);
-    while (pm) {
-      const int l = __ffs(pm) - 1;
-      pm &= pm - 1;
-      const int64_t lb = __shfl_sync(kFullMask, b, l), le = __shfl_sync(kFullMask, e, l);
-      for (int64_t j = lb; j < le; j += 32) {
-        const int64_t jj = j + lane;
-        uint32_t u = 0;
-        bool h = false;
-        if (jj < le) {
-          u = __ldg(P.nb + jj);
-          h = (front[u >> 5] >> (u & 31u)) & 1u;
-        }
-        const unsigned bal = __ballot_sync(kFullMask, h);
-        if (bal) {
-          const uint32_t hu = __shfl_sync(kFullMask, u, __ffs(bal) - 1);
-          if (lane == l) {
-            found = true;
-            par = hu;
-          }
-          break;
-        }
-      }
-    }
-    if (found) {
-      P.parent[r] = (int32_t)par;
-      if (P.want_depth) P.depth[r] = lvl + 1;
-    }
-    const unsigned nbits = __ballot_sync(kFullMask, found), dbits = __ballot_sync(kFullMask, dead);
-    if (lane == 0) {
+    __syncwarp();
+    if (lane < tw && w < w32) {
+      const uint32_t nbits = acc[lane];
       next_slice[w] = nbits;
-      if (nbits | dbits) P.visited[w] = vis | nbits | dbits;
+      if (nbits) P.visited[w] = vis | nbits;
       awake += __popc(nbits);
+    }
+    __syncwarp();
+  }
+  block_sum2(awake, 0, &P.ctr[cAwake], &P.ctr[cAwake]);
+}
+
+// Long in-lists deferred by k_sh_bu: one warp per vertex, ballot over 32
+// neighbours, resuming after the head and the kShRounds-1 list rounds.
+__global__ void __launch_bounds__(kSB) k_sh_bu_long(ShardParams P, const uint32_t* front, uint32_t* next_slice,
+                                                    unsigned long long count, int lvl) {
+  const int lane = threadIdx.x & 31;
+  long long awake = 0;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long i = gw; i < (long long)count; i += nw) {
+    const uint32_t r = P.longq[i];
+    const int64_t le = P.off[r + 1];
+    for (int64_t j = P.off[r] + kHead + 4 * (kShRounds - 1); j < le; j += 32) {
+      const int64_t jj = j + lane;
+      bool h = false;
+      uint32_t u = 0;
+      if (jj < le) {
+        u = __ldg(P.nb + jj);
+        h = (__ldg(front + (u >> 5)) >> (u & 31u)) & 1u;
+      }
+      const unsigned bal = __ballot_sync(kFullMask, h);
+      if (bal) {
+        const uint32_t hu = __shfl_sync(kFullMask, u, __ffs(bal) - 1);
+        if (lane == 0) {
+          P.parent[r] = (int32_t)hu;
+          if (P.want_depth) P.depth[r] = lvl + 1;
+          atomicOr(next_slice + (r >> 5), 1u << (r & 31u));
+          atomicOr(P.visited + (r >> 5), 1u << (r & 31u));
+          awake++;
+        }
+        break;
+      }
     }
   }
   block_sum2(awake, 0, &P.ctr[cAwake], &P.ctr[cAwake]);
@@ -476,6 +802,11 @@ struct gk_shard {
   cudaStream_t stream = nullptr;  // caller's stream (e.g. torch's current stream)
   int want_depth = 0;
   int encode = 1;
+  int big = 0;                  // the current top-down step is a large one
+  uint32_t* next = nullptr;     // owned next bitmap for large top-down steps
+  uint32_t* dead = nullptr;     // owned never-reachable bitmap (built once)
+  gk::HeadRec* head = nullptr;  // head records of owned live vertices (built once)
+  uint32_t* hbase = nullptr;
   long long launches = 0;  // kernels launched on this shard (telemetry)
 };
 
@@ -516,6 +847,13 @@ gk::ShardParams params(const gk_shard* s) {
   p.ctr = s->ctr;
   p.want_depth = s->want_depth;
   p.encode = s->encode;
+  p.big = s->big;
+  p.next = s->next;
+  p.dead = s->dead;
+  p.head = s->head;
+  p.hbase = s->hbase;
+  p.longq = reinterpret_cast<uint32_t*>(s->pairs);
+  p.long_cap = 2 * s->pair_cap;
   return p;
 }
 
@@ -532,6 +870,13 @@ gk_status shard_alloc(gk_shard* s) {
   SCK(cudaMalloc(&s->chunks, sizeof(gk::Chunk) * s->chunk_cap), "alloc chunks");
   SCK(cudaMalloc(&s->ctr, sizeof(unsigned long long) * (gk::cDest + s->nranks + 8)), "alloc counters");
   SCK(cudaMalloc(&s->acc, sizeof(unsigned long long) * 4), "alloc acc");
+  SCK(cudaMalloc(&s->next, sizeof(uint32_t) * wl), "alloc next");
+  SCK(cudaMalloc(&s->dead, sizeof(uint32_t) * wl), "alloc dead");
+  SCK(cudaMalloc(&s->hbase, sizeof(uint32_t) * wl), "alloc head index");
+  // graph-derived, once: never-reachable owned vertices, head records
+  SCK(gk::dead_bitmap(s->off, s->nloc, s->dead, nullptr), "dead bitmap");
+  SCK(gk::build_head(s->off, s->nb, s->nloc, s->dead, s->hbase, &s->head, nullptr), "head records");
+  SCK(cudaStreamSynchronize(nullptr), "shard derived data");
   return GK_OK;
 }
 
@@ -540,7 +885,8 @@ void shard_free(gk_shard* s) {
   cudaSetDevice(s->device);
   for (void* p : {(void*)s->off, (void*)s->nb, (void*)s->parent, (void*)s->depth, (void*)s->visited,
                   (void*)s->sent, (void*)s->queue, (void*)s->pairs, (void*)s->chunks,
-                  (void*)s->ctr, (void*)s->acc})
+                  (void*)s->ctr, (void*)s->acc, (void*)s->next, (void*)s->dead, (void*)s->head,
+                  (void*)s->hbase})
     cudaFree(p);
   delete s;
 }
@@ -564,7 +910,8 @@ GK_API const char* gk_shard_last_error(void) { return g_shard_err.c_str(); }
 
 GK_API gk_status gk_shard_generate(int kind, int scale, int degree, uint64_t seed, int permute, int rank,
                                    int nranks, int device, gk_shard** out) {
-  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return shard_fail(GK_ERR_INVALID, "bad shard spec");
+  if (!out || nranks < 1 || nranks > gk::kMaxRanksSmem || rank < 0 || rank >= nranks)
+    return shard_fail(GK_ERR_INVALID, "bad shard spec");
   if (kind != 0 && kind != 1) return shard_fail(GK_ERR_INVALID, "generator kind must be 0 or 1");
   if (scale < 5 || scale > 31) return shard_fail(GK_ERR_INVALID, "sharded generator scale must be in [5, 31]");
   int ndev = 0;
@@ -601,7 +948,7 @@ GK_API gk_status gk_shard_generate(int kind, int scale, int degree, uint64_t see
 
 GK_API gk_status gk_shard_upload(int64_t n, int rank, int nranks, const int64_t* local_offsets,
                                  const uint32_t* neighbors, int device, gk_shard** out) {
-  if (!out || !local_offsets || nranks < 1 || rank < 0 || rank >= nranks || n < 1)
+  if (!out || !local_offsets || nranks < 1 || nranks > gk::kMaxRanksSmem || rank < 0 || rank >= nranks || n < 1)
     return shard_fail(GK_ERR_INVALID, "bad shard spec");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -701,6 +1048,15 @@ GK_API gk_status gk_shard_td_expand(gk_shard* s, uint64_t qs, uint64_t qe, int32
   SCK(cudaMemsetAsync(s->ctr + gk::cChunks, 0, sizeof(unsigned long long), s->stream), "memset");
   SCK(cudaMemsetAsync(s->ctr + gk::cDest, 0, sizeof(unsigned long long) * P, s->stream), "memset");
   if (dedup) SCK(cudaMemsetAsync(s->sent, 0, sizeof(uint32_t) * ((s->n + 31) / 32), s->stream), "memset");
+  // large steps (the orchestrator's dedup threshold = the persistent
+  // kernel's "big" threshold): owned claims go to next := visited
+  s->big = dedup ? 1 : 0;
+  p.big = s->big;
+  if (s->big) {
+    s->launches++;
+    gk::k_sh_copy_words<<<gk::grid_of((s->nloc + 31) / 32), gk::kSB, 0, s->stream>>>(s->visited, s->next,
+                                                                                  (s->nloc + 31) / 32);
+  }
   s->launches++;
   gk::k_sh_td_light<<<gk::grid_of((int64_t)(qe - qs)), gk::kSB, 0, s->stream>>>(p, qs, qe, lvl);
   SCK(cudaGetLastError(), "td_light");
@@ -756,6 +1112,12 @@ GK_API gk_status gk_shard_td_apply(gk_shard* s, const uint64_t* pairs_in, int64_
     gk::k_sh_td_apply<<<gk::grid_of(npairs), gk::kSB, 0, s->stream>>>(p, pairs_in, (unsigned long long)npairs, lvl);
     SCK(cudaGetLastError(), "td_apply");
   }
+  if (s->big) {  // claim sweep: fold, queue, scout for the whole step
+    s->launches++;
+    gk::k_sh_sweep<<<gk::grid_of(s->nloc / 32), gk::kSB, 0, s->stream>>>(p, lvl);
+    SCK(cudaGetLastError(), "sweep");
+    s->big = 0;
+  }
   unsigned long long h[gk::cDest];
   gk_status st = read_ctr(s, h, gk::cDest);
   if (st != GK_OK) return st;
@@ -808,12 +1170,21 @@ GK_API gk_status gk_shard_bu(gk_shard* s, const uint32_t* front_dev, uint32_t* n
   gk::ShardParams p = params(s);
   SCK(cudaMemsetAsync(s->ctr + gk::cAwake, 0, sizeof(unsigned long long), s->stream), "memset");
   SCK(cudaMemsetAsync(next_slice_dev, 0, sizeof(uint32_t) * (s->block / 32), s->stream), "memset");
+  SCK(cudaMemsetAsync(s->ctr + gk::cLong, 0, sizeof(unsigned long long), s->stream), "memset");
   s->launches++;
   gk::k_sh_bu<<<gk::grid_of(s->nloc), gk::kSB, 0, s->stream>>>(p, front_dev, next_slice_dev, lvl);
   SCK(cudaGetLastError(), "bu");
   unsigned long long h[gk::cDest];
   gk_status st = read_ctr(s, h, gk::cDest);
   if (st != GK_OK) return st;
+  if (h[gk::cLong]) {
+    s->launches++;
+    gk::k_sh_bu_long<<<gk::grid_of((int64_t)h[gk::cLong] * 32), gk::kSB, 0, s->stream>>>(p, front_dev, next_slice_dev,
+                                                                                       h[gk::cLong], lvl);
+    SCK(cudaGetLastError(), "bu_long");
+    st = read_ctr(s, h, gk::cDest);
+    if (st != GK_OK) return st;
+  }
   *awake = (int64_t)h[gk::cAwake];
   return GK_OK;
 }
