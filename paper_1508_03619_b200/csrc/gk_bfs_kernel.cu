@@ -38,6 +38,8 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kQBuf = 256;         // per-warp queue staging (QueueBuffer analogue)
 constexpr int kChunkMax = 1024;    // edges per heavy chunk (large steps)
 constexpr int kChunkMin = 128;     // ... and for small steps, so every warp gets a chunk
+constexpr long long kTinyStep = 1 << 16;  // top-down steps up to this many edges are latency-first
+constexpr long long kTinyFrontier = 32768;  // ... and this many frontier vertices
 
 
 struct __align__(16) SmemT {
@@ -285,9 +287,40 @@ template <bool kBig>
 __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const uint32_t (&u)[4],
                                        const uint32_t (&v)[4], const bool (&ok)[4],
                                        uint32_t* nextbm, int lvl, bool encode, long long& scout,
-                                       uint32_t* buf, int& qcnt) {
+                                       uint32_t* buf, int& qcnt, bool tiny) {
   uint32_t w[4];
   bool c[4];
+  if (!kBig && tiny) {
+    // Tiny steps are latency chains (one grid barrier each on high-diameter
+    // graphs): no L2 pre-check, and the degree reads go out together with
+    // the claim atomics instead of after them.
+    int64_t o0[4], o1[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      o0[k] = o1[k] = 0;
+      if (ok[k] && encode) {
+        o0[k] = P.out_off[v[k]];
+        o1[k] = P.out_off[v[k] + 1];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const uint32_t bit = 1u << (v[k] & 31u);
+      c[k] = ok[k] && !(atomicOr(P.visited + (v[k] >> 5), bit) & bit);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      if (c[k]) {
+        P.parent[v[k]] = (int32_t)u[k];
+        if (P.want_depth) P.depth[v[k]] = lvl + 1;
+        const long long d = o1[k] - o0[k];
+        scout += encode ? (d ? d : 1) : 1;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) wq_push(P, qa, c[k], v[k], buf, qcnt);
+    return;
+  }
   if (kBig) {
     // Fire-and-forget claims: the next-frontier bitmap starts as a copy of
     // visited, so one pre-check covers both "already visited" and "already
@@ -328,7 +361,7 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
 template <bool kBig>
 __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, unsigned long long qs,
                          unsigned long long qe, uint32_t* nextbm, int lvl, bool encode,
-                         long long& scout, int& qcnt, int tile_sz, int64_t chunk) {
+                         long long& scout, int& qcnt, int tile_sz, int64_t chunk, bool tiny) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
   // First tile of each CTA is static (no atomic on the latency chain of
@@ -388,7 +421,7 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
           v[k] = ld_nb_once(P.out_nb + s.td.t_b[lo] + (ei - s.td.t_pre[lo]));
         }
       }
-      claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
+      claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt, tiny);
     }
     if (threadIdx.x == 0 && start + tile_sz < qe) s.bcast[1] = gridDim.x + atomicAdd(&cnt[kTile], 1ull);
     __syncthreads();
@@ -401,7 +434,7 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
 // ---- top-down, heavy chunks: one warp per chunk, 4 edges per lane in flight --
 template <bool kBig>
 __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, unsigned long long nch,
-                         uint32_t* nextbm, int lvl, bool encode, long long& scout, int& qcnt) {
+                         uint32_t* nextbm, int lvl, bool encode, long long& scout, int& qcnt, bool tiny) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   const unsigned lane = lane_id();
   // Chunks are equal-sized (chunk edges but the tails), so a static
@@ -448,7 +481,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
         ok[k] = j < ch.len;
         v[k] = ok[k] ? ld_nb_once(P.out_nb + ch.start + j) : 0u;
       }
-      claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt);
+      claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt, tiny);
     }
   }
 }
@@ -908,6 +941,9 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       // high-MLP pass; small ones keep everything inline, so a long chain of
       // tiny levels costs one grid barrier each.
       const bool big = scout > P.bitmap_td_min;
+      // (after a bottom-up phase scout is 1, bfs.hpp:156: the frontier size
+      // bounds the step then)
+      const bool tiny = scout <= kTinyStep && fsize <= kTinyFrontier;
       // Granularity from the step size the heuristic already knows: enough
       // tiles / chunks for every CTA / warp (hardware-derived, not per graph).
       int tile_sz = kBlock;
@@ -924,9 +960,9 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       {
         const QApp qa = qapp(P, ph, qtail);
         if (big) {
-          td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk);
+          td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk, false);
         } else {
-          td_light<false>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk);
+          td_light<false>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk, tiny);
           wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
         }
       }
@@ -940,9 +976,9 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         set = ph & 3;
         const QApp qa = qapp(P, ph, qtail);
         if (big) {
-          td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt);
+          td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, false);
         } else {
-          td_heavy<false>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt);
+          td_heavy<false>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, tiny);
           wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
         }
         block_add(sacc, &P.ctrl->cnt[set][kSum], s);
