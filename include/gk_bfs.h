@@ -174,6 +174,18 @@ GK_API gk_status gk_bfs_verify(gk_graph* g, uint32_t source, int64_t* errors);
 /* Keep depths on the device for subsequent gk_bfs calls (for the model). */
 GK_API gk_status gk_bfs_keep_depth(gk_graph* g, int32_t keep);
 
+/* ---- Brandes betweenness, SURVEY.md §8(f)-4 ----------------------------
+ * Replaces ScoreArray gapkit::Brandes(const CsrGraph&, span<const NodeId>)
+ * (proj/include/gapkit/kernels/betweenness.hpp:84-145).  scores_out (n
+ * floats, may be NULL) receives the max-normalised scores.  Errors, in the
+ * reference's order: no sources -> GK_ERR_BAD_PARAM "betweenness requires
+ * at least one source"; source >= n -> GK_ERR_SOURCE_RANGE "betweenness
+ * source out of range"; out-degree 0 -> GK_ERR_BAD_PARAM "betweenness source
+ * has zero out-degree".  *device_ms (may be NULL) = CUDA-event time of all
+ * sources plus the normalisation. */
+GK_API gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources,
+                            float* scores_out, double* device_ms);
+
 /* ---- Sharded (1D-partitioned) traversal, SURVEY.md §8(e) ----------------
  * Rank r of P owns vertices [r*block, min(n, (r+1)*block)), block =
  * ceil(n/P) rounded up to a multiple of 32.  A gk_shard holds the owned CSR

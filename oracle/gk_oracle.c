@@ -526,3 +526,88 @@ uint64_t gko_fnv1a(const void* data, int64_t len) {
   }
   return h;
 }
+
+
+/* ---- Brandes betweenness (betweenness.hpp:38-145), serial restatement ----
+ * Test infrastructure only.  Forward: level-synchronous BFS over out-edges
+ * counting shortest paths (sigma) and flagging successor edges (one flag per
+ * stored arc), betweenness.hpp:38-80 run serially.  Backward: levels deepest
+ * first, delta(u) = sum over flagged arcs (u,v), in arc order, of
+ * sigma(u)/sigma(v) * (1 + delta(v)); scores(u) += (float)delta(u) for u !=
+ * source (betweenness.hpp:104-122).  Then max normalisation (:129-143).
+ * Returns 0, or -1 for no sources, -2 out of range, -3 zero out-degree. */
+int gko_brandes(int64_t n, const int64_t* off, const uint32_t* nb, const uint32_t* sources,
+                int64_t count, float* scores) {
+  if (count <= 0) return -1;
+  for (int64_t i = 0; i < count; i++) {
+    if ((int64_t)sources[i] >= n) return -2;
+    if (off[sources[i] + 1] == off[sources[i]]) return -3;
+  }
+  const int64_t m = off[n];
+  double* sigma = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  double* delta = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  int32_t* depth = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  uint32_t* q = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(n > 0 ? n : 1));
+  int64_t* bounds = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 2));
+  uint8_t* succ = (uint8_t*)malloc((size_t)(m > 0 ? m : 1));
+  for (int64_t v = 0; v < n; v++) scores[v] = 0.0f;
+  for (int64_t si = 0; si < count; si++) {
+    const uint32_t src = sources[si];
+    for (int64_t v = 0; v < n; v++) {
+      sigma[v] = 0.0;
+      depth[v] = -1;
+    }
+    memset(succ, 0, (size_t)(m > 0 ? m : 1));
+    depth[src] = 0;
+    sigma[src] = 1.0;
+    int64_t tail = 0, nb_levels = 0;
+    q[tail++] = src;
+    bounds[nb_levels++] = 0;
+    int64_t qs = 0, qe = 1;
+    int32_t d = 0;
+    while (qs < qe) {
+      d++;
+      for (int64_t i = qs; i < qe; i++) {
+        const uint32_t u = q[i];
+        for (int64_t j = off[u]; j < off[u + 1]; j++) {
+          const uint32_t v = nb[j];
+          if (depth[v] == -1) {
+            depth[v] = d;
+            q[tail++] = v;
+          }
+          if (depth[v] == d) {
+            succ[j] = 1;
+            sigma[v] += sigma[u];
+          }
+        }
+      }
+      bounds[nb_levels++] = qe;
+      qs = qe;
+      qe = tail;
+    }
+    /* bounds[] = level starts, ending with the empty window */
+    for (int64_t v = 0; v < n; v++) delta[v] = 0.0;
+    for (int64_t l = nb_levels - 2; l >= 0; l--) {
+      for (int64_t i = bounds[l]; i < bounds[l + 1]; i++) {
+        const uint32_t u = q[i];
+        double du = 0.0;
+        for (int64_t j = off[u]; j < off[u + 1]; j++)
+          if (succ[j]) du += (sigma[u] / sigma[nb[j]]) * (1.0 + delta[nb[j]]);
+        delta[u] = du;
+        if (u != src) scores[u] += (float)du;
+      }
+    }
+  }
+  float mx = 0.0f;
+  for (int64_t v = 0; v < n; v++)
+    if (scores[v] > mx) mx = scores[v];
+  if (mx > 0.0f)
+    for (int64_t v = 0; v < n; v++) scores[v] /= mx;
+  free(sigma);
+  free(delta);
+  free(depth);
+  free(q);
+  free(bounds);
+  free(succ);
+  return 0;
+}

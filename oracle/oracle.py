@@ -61,6 +61,8 @@ def _load():
     lib.gko_component_edges.restype = C.c_int64
     lib.gko_fnv1a.argtypes = [C.c_void_p, C.c_int64]
     lib.gko_fnv1a.restype = C.c_uint64
+    lib.gko_brandes.argtypes = [C.c_int64, _I64P, _U32P, _U32P, C.c_int64, C.POINTER(C.c_float)]
+    lib.gko_brandes.restype = C.c_int
     return lib
 
 
@@ -166,6 +168,22 @@ def bfs_depths(g: Csr, src: int) -> np.ndarray:
     d = np.empty(g.n, np.int32)
     lib().gko_bfs_depths(g.n, g.off, _nbp(g.nb), src, d)
     return d
+
+
+_BC_ERRORS = {-1: "betweenness requires at least one source", -2: "betweenness source out of range",
+              -3: "betweenness source has zero out-degree"}
+
+
+def brandes(g: Csr, sources) -> np.ndarray:
+    """Serial Brandes restatement (gko_brandes, betweenness.hpp:38-145);
+    raises ValueError with the reference's ConfigError message."""
+    src = np.ascontiguousarray(np.asarray(sources, dtype=np.uint32))
+    out = np.empty(max(g.n, 1), np.float32)
+    rc = lib().gko_brandes(g.n, g.off, _nbp(g.nb), src if src.size else np.zeros(1, np.uint32), src.size,
+                           out.ctypes.data_as(C.POINTER(C.c_float)))
+    if rc:
+        raise ValueError(_BC_ERRORS[rc])
+    return out[: g.n]
 
 
 def verify_bfs(g: Csr, src: int, parent: np.ndarray) -> tuple[bool, str]:
@@ -287,6 +305,10 @@ class RefLib:
         L.gkr_read_sg.restype = vp
         L.gkr_verify_bfs.argtypes = [vp, C.c_uint32, _I32P, C.c_char_p, C.c_int]
         L.gkr_verify_bfs.restype = C.c_int
+        L.gkr_brandes.argtypes = [vp, _U32P, C.c_int64, C.POINTER(C.c_float), C.c_char_p, C.c_int]
+        L.gkr_brandes.restype = C.c_int
+        L.gkr_verify_bc.argtypes = [vp, _U32P, C.c_int64, C.POINTER(C.c_float), C.c_char_p, C.c_int]
+        L.gkr_verify_bc.restype = C.c_int
         self.L = L
 
     def gen(self, kind: str, scale: int, degree: int = 16, seed: int = 24601) -> np.ndarray:
@@ -401,6 +423,24 @@ class RefGraph:
     def verify(self, src: int, parent: np.ndarray) -> tuple[bool, str]:
         msg = C.create_string_buffer(512)
         ok = self.ref.L.gkr_verify_bfs(self.h, src, np.ascontiguousarray(parent, np.int32), msg, 512)
+        return bool(ok), msg.value.decode()
+
+    def brandes(self, sources) -> np.ndarray:
+        """The reference's Brandes; raises ValueError with its ConfigError text."""
+        src = np.ascontiguousarray(np.asarray(sources, dtype=np.uint32))
+        out = np.empty(max(self.n, 1), np.float32)
+        err = C.create_string_buffer(256)
+        if self.ref.L.gkr_brandes(self.h, src if src.size else np.zeros(1, np.uint32), src.size,
+                                  out.ctypes.data_as(C.POINTER(C.c_float)), err, 256):
+            raise ValueError(err.value.decode())
+        return out[: self.n]
+
+    def verify_bc(self, sources, scores: np.ndarray) -> tuple[bool, str]:
+        """The reference's VerifyBetweenness (verify.hpp:216-270)."""
+        src = np.ascontiguousarray(np.asarray(sources, dtype=np.uint32))
+        sc = np.ascontiguousarray(scores, np.float32)
+        msg = C.create_string_buffer(512)
+        ok = self.ref.L.gkr_verify_bc(self.h, src, src.size, sc.ctypes.data_as(C.POINTER(C.c_float)), msg, 512)
         return bool(ok), msg.value.decode()
 
 

@@ -295,4 +295,31 @@ int gkr_verify_bfs(void* hp, uint32_t src, const int32_t* parent, char* msg,
   return r.ok ? 1 : 0;
 }
 
+// Brandes (kernels/betweenness.hpp:84-145).  Returns 0, or 1 with the
+// ConfigError message in err.
+int gkr_brandes(void* hp, const uint32_t* sources, int64_t count, float* scores, char* err,
+                int errlen) {
+  const CsrGraph& g = static_cast<RefGraph*>(hp)->g;
+  std::vector<NodeId> s(sources, sources + count);
+  try {
+    ScoreArray sc = Brandes(g, s);
+    std::memcpy(scores, sc.data(), sc.size() * sizeof(float));
+    return 0;
+  } catch (const std::exception& e) {
+    SetErr(err, errlen, e.what());
+    return 1;
+  }
+}
+
+// VerifyBetweenness (verify.hpp:216-270), default tolerance 1e-4.
+int gkr_verify_bc(void* hp, const uint32_t* sources, int64_t count, const float* scores, char* msg,
+                  int msglen) {
+  const CsrGraph& g = static_cast<RefGraph*>(hp)->g;
+  std::vector<NodeId> s(sources, sources + count);
+  ScoreArray sc(scores, scores + g.num_nodes());
+  VerifyReport r = VerifyBetweenness(g, s, sc);
+  SetErr(msg, msglen, r.failure_detail);
+  return r.ok ? 1 : 0;
+}
+
 }  // extern "C"

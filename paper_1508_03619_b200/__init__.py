@@ -21,7 +21,7 @@ import numpy as np
 from . import _lib
 from ._lib import BfsStats, CsrView, Step
 
-__all__ = ["Bfs", "BfsOptions", "BfsStrategy", "BfsResult", "ConfigError", "GapkitError", "LoadError",
+__all__ = ["Bfs", "Brandes", "BfsOptions", "BfsStrategy", "BfsResult", "ConfigError", "GapkitError", "LoadError",
            "DeviceGraph", "PinnedBuffer", "device_count"]
 
 kDefaultSeed = 24601  # types.hpp:33
@@ -261,6 +261,26 @@ class DeviceGraph:
 
     def device_parent_ptr(self) -> int:
         return int(_lib.load().gk_bfs_device_parent(self._h) or 0)
+
+    def brandes(self, sources) -> tuple[np.ndarray, float]:
+        """Betweenness scores over `sources` (gk_brandes) and the device ms."""
+        src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64))
+        if src.size and (src.min() < 0 or src.max() > 0xFFFFFFFF):
+            raise ConfigError("betweenness source out of range")
+        s32 = src.astype(np.uint32)
+        out = np.empty(self.n, np.float32)
+        ms = C.c_double()
+        _check(_lib.load().gk_brandes(self._h, s32.ctypes.data if s32.size else None, int(s32.size),
+                                      out.ctypes.data, C.byref(ms)), "gk_brandes")
+        return out, ms.value
+
+
+def Brandes(g: DeviceGraph, sources) -> np.ndarray:
+    """gapkit::Brandes (betweenness.hpp:84-145): approximate betweenness over
+    `sources`, normalised so the maximum is 1 (float32 scores).  Raises
+    ConfigError like the reference (no sources, source out of range, source
+    with zero out-degree)."""
+    return g.brandes(sources)[0]
 
 
 def Bfs(g: DeviceGraph, source: int, opts: BfsOptions | None = None) -> np.ndarray:

@@ -33,7 +33,7 @@ EXPORTED = (
     "gk_shard_last_error", "gk_shard_generate", "gk_shard_upload", "gk_shard_free", "gk_shard_info",
     "gk_shard_set_stream", "gk_shard_degree", "gk_shard_begin", "gk_shard_td_expand", "gk_shard_td_apply",
     "gk_shard_tail", "gk_shard_rescan", "gk_shard_q2b", "gk_shard_bu", "gk_shard_b2q", "gk_shard_result",
-    "gk_shard_launches", "gk_bfs_verify", "gk_graph_load_sg", "gk_graph_save_sg",
+    "gk_shard_launches", "gk_bfs_verify", "gk_graph_load_sg", "gk_graph_save_sg", "gk_brandes",
 )
 
 
@@ -87,6 +87,7 @@ def load() -> C.CDLL:
     L.gk_bfs_keep_depth.argtypes = [vp, i32]
     L.gk_bfs_verify.argtypes = [vp, u32, vp]
     L.gk_bfs_trace.argtypes = [vp, C.POINTER(C.c_uint64), C.c_char_p, i32, C.POINTER(i32)]
+    L.gk_brandes.argtypes = [vp, vp, i64, vp, C.POINTER(C.c_double)]
     L.gk_shard_last_error.restype = C.c_char_p
     L.gk_shard_generate.argtypes = [C.c_int, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(vp)]

@@ -49,7 +49,10 @@ struct __align__(16) SmemT {
     int64_t t_pre[kBlock];
     uint32_t t_u[kBlock];
   } td;
-  uint32_t bu_acc[kWarps][2][32];  // bottom-up: per-warp next/dead bits of a task
+  union {
+    uint32_t bu_acc[kWarps][2][32];  // bottom-up: per-warp next/dead bits of a task
+    double bc_sig[kBlock];           // Brandes forward: sigma of the tile's frontier vertices
+  };
   long long red[kWarps + 2];
   unsigned long long bcast[4];
   int ok;
@@ -1031,6 +1034,337 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   // written -1 by init and never touched.
 }
 
+
+// ============================================================================
+// Brandes betweenness (betweenness.hpp:38-80, 84-145), one source per launch.
+//
+// Forward: level-synchronous top-down BFS that also counts shortest paths
+// (sigma, doubles; path counts are integers, so the order of the atomic
+// adds does not change them below 2^53) and flags each shortest-path
+// successor edge in an m-bit bitmap, exactly the reference's BrandesForward
+// (betweenness.hpp:38-80): a target first seen at depth -1 is claimed with a
+// CAS; every edge whose target ends up at the current depth sets its
+// successor bit and adds sigma[u] into sigma[v].  The queue keeps every
+// level in place; bc_bounds[d] marks where level d starts.
+// Backward (betweenness.hpp:104-122): levels deepest first; delta[u] = sum
+// over u's flagged edges of sigma[u]/sigma[v] * (1 + delta[v]).  Vertices of
+// degree <= 32 are summed by one lane in edge order (the reference's order);
+// up to kBcWarpDeg by a whole warp; larger ones are cut into chunks whose
+// partial sums are added atomically.  Finally scores[u] += (float)delta[u]
+// for every reached u != source.
+// ============================================================================
+constexpr int64_t kBcChunk = 1024;
+constexpr int64_t kBcWarpDeg = 8192;
+
+__device__ __forceinline__ void bc_edges4(const BfsParams& P, const QApp& qa, const double (&su)[4],
+                                          const uint32_t (&v)[4], const int64_t (&e)[4], const bool (&ok)[4],
+                                          int lvl, uint32_t* buf, int& qcnt) {
+  int dv[4];
+  bool cl[4];
+#pragma unroll
+  for (int k = 0; k < 4; k++) dv[k] = ok[k] ? __ldcg(P.depth + v[k]) : -2;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    cl[k] = false;
+    if (dv[k] == -1) {  // betweenness.hpp:62-65
+      const int old = atomicCAS(P.depth + v[k], -1, lvl);
+      cl[k] = old == -1;
+      dv[k] = cl[k] ? lvl : old;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    if (dv[k] == lvl) {  // betweenness.hpp:66-69
+      atomicOr(P.bc_succ + (e[k] >> 5), 1u << (e[k] & 31));
+      atomicAdd(P.bc_sigma + v[k], su[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; k++) wq_push(P, qa, cl[k], v[k], buf, qcnt);
+}
+
+// Forward expansion of queue[qs, qe): tiles of kBlock frontier vertices,
+// CTA scan of degrees, load-balanced edge gather; degree > kBcChunk vertices
+// become chunks for bc_forward_heavy.
+__device__ void bc_forward_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa,
+                                 unsigned long long qs, unsigned long long qe, int lvl, int& qcnt) {
+  uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
+  unsigned long long* cnt = P.ctrl->cnt[ph & 3];
+  for (unsigned long long tile = blockIdx.x;; tile += gridDim.x) {
+    const unsigned long long start = qs + tile * (unsigned long long)kBlock;
+    if (start >= qe) break;
+    const unsigned long long i = start + threadIdx.x;
+    uint32_t u = 0;
+    int64_t b = 0, dl = 0;
+    double su = 0.0;
+    if (i < qe) {
+      u = __ldcg(P.queue + i);
+      b = P.out_off[u];
+      su = __ldcg(P.bc_sigma + u);
+      const int64_t d = P.out_off[u + 1] - b;
+      if (d > kBcChunk) {
+        const int64_t nch = (d + kBcChunk - 1) / kBcChunk;
+        const unsigned long long base = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
+        if ((int64_t)(base + nch) <= P.chunk_cap) {
+          for (int64_t c = 0; c < nch; c++) {
+            Chunk ch;
+            ch.u = u;
+            ch.start = b + c * kBcChunk;
+            ch.len = (uint32_t)((d - c * kBcChunk) < kBcChunk ? (d - c * kBcChunk) : kBcChunk);
+            P.chunks[base + c] = ch;
+          }
+        } else {
+          atomicExch(&P.ctrl->error, 3);
+        }
+      } else {
+        dl = d;
+      }
+    }
+    s.td.t_u[threadIdx.x] = u;
+    s.td.t_b[threadIdx.x] = b;
+    s.bc_sig[threadIdx.x] = su;
+    int64_t tot;
+    const int64_t pre = block_exscan(dl, &tot, s);
+    s.td.t_pre[threadIdx.x] = pre;
+    __syncthreads();
+    for (int64_t eb = 0; eb < tot; eb += 4 * kBlock) {
+      uint32_t v[4];
+      int64_t e[4];
+      double sg[4];
+      bool ok[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int64_t ei = eb + k * kBlock + threadIdx.x;
+        ok[k] = ei < tot;
+        v[k] = 0;
+        e[k] = 0;
+        sg[k] = 0.0;
+        if (ok[k]) {
+          int lo = 0, hi = kBlock - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s.td.t_pre[mid] <= ei) lo = mid;
+            else hi = mid - 1;
+          }
+          e[k] = s.td.t_b[lo] + (ei - s.td.t_pre[lo]);
+          v[k] = __ldg(P.out_nb + e[k]);
+          sg[k] = s.bc_sig[lo];
+        }
+      }
+      bc_edges4(P, qa, sg, v, e, ok, lvl, buf, qcnt);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void bc_forward_heavy(const BfsParams& P, const QApp& qa, unsigned long long nch, int lvl, SmemT& s,
+                                 int& qcnt) {
+  uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
+  const unsigned lane = lane_id();
+  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  for (unsigned long long c = gw; c < nch; c += nw) {
+    const Chunk ch = P.chunks[c];
+    const double su = __ldcg(P.bc_sigma + ch.u);
+    const double sg[4] = {su, su, su, su};
+    for (uint32_t o = 0; o < ch.len; o += 128) {
+      uint32_t v[4];
+      int64_t e[4];
+      bool ok[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const uint32_t j = o + lane + 32u * k;
+        ok[k] = j < ch.len;
+        e[k] = ch.start + j;
+        v[k] = ok[k] ? __ldg(P.out_nb + e[k]) : 0u;
+      }
+      bc_edges4(P, qa, sg, v, e, ok, lvl, buf, qcnt);
+    }
+  }
+}
+
+// sigma[u]/sigma[v] * (1 + delta[v]) for a flagged edge (betweenness.hpp:115)
+__device__ __forceinline__ double bc_term(const BfsParams& P, double su, uint32_t v) {
+  return (su / __ldcg(P.bc_sigma + v)) * (1.0 + __ldcg(P.bc_delta + v));
+}
+
+// Backward pass A over one level's vertices.
+__device__ void bc_backward_level(const BfsParams& P, unsigned ph, unsigned long long b0, unsigned long long b1) {
+  const unsigned lane = lane_id();
+  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  unsigned long long* cnt = P.ctrl->cnt[ph & 3];
+  for (unsigned long long base = b0 + (unsigned long long)gw * 32; base < b1; base += (unsigned long long)nw * 32) {
+    const unsigned long long i = base + lane;
+    uint32_t u = 0;
+    int64_t eb = 0, d = 0;
+    double su = 0.0;
+    if (i < b1) {
+      u = __ldcg(P.queue + i);
+      eb = P.out_off[u];
+      d = P.out_off[u + 1] - eb;
+      su = __ldcg(P.bc_sigma + u);
+    }
+    if (i < b1 && d <= 32) {  // one lane, in edge order
+      double acc = 0.0;
+      if (d > 0) {
+        const uint32_t w0 = __ldcg(P.bc_succ + (eb >> 5));
+        const uint32_t w1 = __ldcg(P.bc_succ + ((eb + d - 1) >> 5));
+        for (int k = 0; k < (int)d; k++) {
+          const int64_t e = eb + k;
+          const uint32_t w = ((e >> 5) == (eb >> 5)) ? w0 : w1;
+          if ((w >> (e & 31)) & 1u) acc += bc_term(P, su, __ldg(P.out_nb + e));
+        }
+      }
+      P.bc_delta[u] = acc;
+    }
+    unsigned big = __ballot_sync(kFull, i < b1 && d > 32);
+    while (big) {
+      const int l = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t ul = __shfl_sync(kFull, u, l);
+      const int64_t ebl = __shfl_sync(kFull, eb, l);
+      const int64_t dl = __shfl_sync(kFull, d, l);
+      const double sul = __shfl_sync(kFull, su, l);
+      if (dl > kBcWarpDeg) {  // cut into chunks, summed in pass B
+        if (lane == 0) {
+          const int64_t nch = (dl + kBcChunk - 1) / kBcChunk;
+          const unsigned long long cb = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
+          if ((int64_t)(cb + nch) <= P.chunk_cap) {
+            for (int64_t c = 0; c < nch; c++) {
+              Chunk ch;
+              ch.u = ul;
+              ch.start = ebl + c * kBcChunk;
+              ch.len = (uint32_t)((dl - c * kBcChunk) < kBcChunk ? (dl - c * kBcChunk) : kBcChunk);
+              P.chunks[cb + c] = ch;
+            }
+          } else {
+            atomicExch(&P.ctrl->error, 3);
+          }
+          P.bc_delta[ul] = 0.0;
+        }
+        continue;
+      }
+      double acc = 0.0;
+      for (int64_t j = lane; j < dl; j += 32) {
+        const int64_t e = ebl + j;
+        if ((__ldcg(P.bc_succ + (e >> 5)) >> (e & 31)) & 1u) acc += bc_term(P, sul, __ldg(P.out_nb + e));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+      if (lane == 0) P.bc_delta[ul] = acc;
+    }
+  }
+}
+
+// Backward pass B: chunks of the level's high-degree vertices.
+__device__ void bc_backward_chunks(const BfsParams& P, unsigned long long nch) {
+  const unsigned lane = lane_id();
+  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  for (unsigned long long c = gw; c < nch; c += nw) {
+    const Chunk ch = P.chunks[c];
+    const double su = __ldcg(P.bc_sigma + ch.u);
+    double acc = 0.0;
+    for (uint32_t j = lane; j < ch.len; j += 32) {
+      const int64_t e = ch.start + j;
+      if ((__ldcg(P.bc_succ + (e >> 5)) >> (e & 31)) & 1u) acc += bc_term(P, su, __ldg(P.out_nb + e));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+    if (lane == 0 && acc != 0.0) atomicAdd(P.bc_delta + ch.u, acc);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
+  __shared__ SmemT s;
+  unsigned ph = 0;
+  const long long gtid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long gthreads = (long long)gridDim.x * kBlock;
+  const uint32_t src = P.src;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->ts[0] = globaltimer();
+  // init (betweenness.hpp:96-101)
+  for (long long i = gtid; i < P.n; i += gthreads) {
+    P.depth[i] = -1;
+    P.bc_sigma[i] = 0.0;
+    P.bc_delta[i] = 0.0;
+  }
+  const long long sw = (P.m + 31) >> 5;
+  for (long long i = gtid; i < sw; i += gthreads) P.bc_succ[i] = 0u;
+  if (!grid_sync(P, s, ph, kTagInit)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // betweenness.hpp:44-48
+    P.depth[src] = 0;
+    P.bc_sigma[src] = 1.0;
+    P.queue[0] = src;
+    P.bc_bounds[0] = 0;
+  }
+  if (!grid_sync(P, s, ph, kTagInit)) return;
+  unsigned long long qs = 0, qe = 1, qtail = 1;
+  int lvl = 0;
+  int qcnt = 0;
+  while (qe > qs) {  // forward levels
+    lvl++;
+    if (lvl + 1 >= P.bc_bounds_cap) {
+      if (threadIdx.x == 0) atomicExch(&P.ctrl->error, 4);
+      return;
+    }
+    unsigned set = ph & 3;
+    {
+      const QApp qa = qapp(P, ph, qtail);
+      bc_forward_light(P, s, ph, qa, qs, qe, lvl, qcnt);
+      wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+    }
+    if (!grid_sync(P, s, ph, kTagTD)) return;
+    qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
+    const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
+    if (nch) {
+      set = ph & 3;
+      const QApp qa = qapp(P, ph, qtail);
+      bc_forward_heavy(P, qa, nch, lvl, s, qcnt);
+      wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+      if (!grid_sync(P, s, ph, kTagHeavy)) return;
+      qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.bc_bounds[lvl] = (int64_t)qe;  // level lvl starts at qe
+    qs = qe;
+    qe = qtail;
+  }
+  // levels 0 .. lvl-1: level d = [bounds[d], bounds[d+1]), bounds[lvl] = qtail
+  for (int d = lvl - 1; d >= 0; d--) {
+    const unsigned long long b0 = d == 0 ? 0ull : (unsigned long long)__ldcg(P.bc_bounds + d);
+    const unsigned long long b1 = d + 1 == lvl ? qtail : (unsigned long long)__ldcg(P.bc_bounds + d + 1);
+    const unsigned set = ph & 3;
+    bc_backward_level(P, ph, b0, b1);
+    if (!grid_sync(P, s, ph, kTagBcBack)) return;
+    const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
+    if (nch) {
+      bc_backward_chunks(P, nch);
+      if (!grid_sync(P, s, ph, kTagBcChunk)) return;
+    }
+  }
+  // betweenness.hpp:118-119
+  for (unsigned long long i = gtid; i < qtail; i += gthreads) {
+    const uint32_t u = __ldcg(P.queue + i);
+    if (u != src) P.bc_scores[u] += static_cast<float>(__ldcg(P.bc_delta + u));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->num_steps = lvl;
+}
+
+__global__ void k_bc_max(const float* __restrict__ x, int64_t n, float* out) {
+  float m = 0.0f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, x[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+  // scores are >= 0, so the float bit pattern orders like an unsigned int
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned*>(out), __float_as_uint(m));
+}
+__global__ void k_bc_scale(float* __restrict__ x, int64_t n, const float* mx) {
+  const float m = *mx;
+  if (!(m > 0.0f)) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] /= m;
+}
+
 }  // namespace
 
 cudaError_t bfs_configure(int device, BfsLaunch* cfg) {
@@ -1073,6 +1407,29 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st
   void* args[] = {&local};
   return cudaLaunchCooperativeKernel((const void*)bfs_persistent, dim3(grid), dim3(cfg.block), args,
                                      dyn, st);
+}
+
+cudaError_t bc_launch(const BfsParams& p, int device, cudaStream_t st) {
+  cudaError_t e;
+  int sms = 0, occ = 0;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device))) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bc_persistent, kBlock, 0))) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  BfsParams local = p;
+  void* args[] = {&local};
+  return cudaLaunchCooperativeKernel((const void*)bc_persistent, dim3(sms * occ), dim3(kBlock), args, 0, st);
+}
+
+cudaError_t bc_normalize(float* scores, int64_t n, float* scratch_max, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(scratch_max, 0, sizeof(float), st))) return e;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+  k_bc_max<<<grid, 256, 0, st>>>(scores, n, scratch_max);
+  k_bc_scale<<<grid, 256, 0, st>>>(scores, n, scratch_max);
+  return cudaGetLastError();
 }
 
 }  // namespace gk

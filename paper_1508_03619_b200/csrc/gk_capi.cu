@@ -57,6 +57,11 @@ void free_graph(gk_graph* g) {
   cudaFree(g->depth);
   cudaFree(g->bits);
   cudaFree(g->head);
+  cudaFree(g->bc_sigma);
+  cudaFree(g->bc_delta);
+  cudaFree(g->bc_succ);
+  cudaFree(g->bc_scores);
+  cudaFree(g->bc_bounds);
   cudaFree(g->hbase);
   cudaFree(g->queue);
   cudaFree(g->chunks);
@@ -483,6 +488,85 @@ gk_status gk_bfs_verify(gk_graph* g, uint32_t source, int64_t* errors) {
   long long e8[8];
   CK(gk::verify_bfs(g->out_off, g->out_nb, g->parent, g->depth, g->n, source, e8, g->stream), "verify");
   for (int i = 0; i < 8; i++) errors[i] = e8[i];
+  return GK_OK;
+}
+
+// Brandes betweenness over the given sources (betweenness.hpp:84-145): one
+// cooperative launch per source accumulates into device scores, then one
+// max-normalisation.  Validation order and messages follow
+// betweenness.hpp:86-93.
+gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, float* scores_out,
+                     double* device_ms) {
+  if (!g) return fail(GK_ERR_INVALID, "null graph");
+  if (!sources || num_sources <= 0) return fail(GK_ERR_BAD_PARAM, "betweenness requires at least one source");
+  std::lock_guard<std::mutex> lock(g->mu);
+  CK(cudaSetDevice(g->device), "cudaSetDevice");
+  for (int64_t i = 0; i < num_sources; i++) {
+    if ((int64_t)sources[i] >= g->n) return fail(GK_ERR_SOURCE_RANGE, "betweenness source out of range");
+    int64_t o[2];
+    CK(cudaMemcpy(o, g->out_off + sources[i], sizeof(o), cudaMemcpyDeviceToHost), "read degree");
+    if (o[1] == o[0]) return fail(GK_ERR_BAD_PARAM, "betweenness source has zero out-degree");
+  }
+  const int64_t n = g->n;
+  if (!g->depth) CK(cudaMalloc(&g->depth, sizeof(int32_t) * std::max<int64_t>(n, 4) + 16), "alloc depth");
+  if (!g->bc_sigma) {
+    CK(cudaMalloc(&g->bc_sigma, sizeof(double) * std::max<int64_t>(n, 1)), "alloc sigma");
+    CK(cudaMalloc(&g->bc_delta, sizeof(double) * std::max<int64_t>(n, 1)), "alloc delta");
+    CK(cudaMalloc(&g->bc_succ, sizeof(uint32_t) * ((g->m + 31) / 32 + 1)), "alloc successor bitmap");
+    CK(cudaMalloc(&g->bc_scores, sizeof(float) * std::max<int64_t>(n, 1) + 16), "alloc scores");
+    g->bc_bounds_cap = n + 2;
+    CK(cudaMalloc(&g->bc_bounds, sizeof(int64_t) * g->bc_bounds_cap), "alloc level bounds");
+  }
+  g->last_valid = 0;  // depth/queue now hold Brandes state
+  g->depth_valid = 0;
+  gk::BfsParams p{};
+  p.n = n;
+  p.m = g->m;
+  p.w32 = (n + 31) / 32;
+  p.out_off = g->out_off;
+  p.out_nb = g->out_nb;
+  p.in_off = g->in_off;
+  p.in_nb = g->in_nb;
+  p.depth = g->depth;
+  p.queue = g->queue;
+  p.chunks = g->chunks;
+  p.chunk_cap = g->chunk_cap;
+  p.ctrl = g->ctrl;
+  p.steps = g->steps;
+  p.step_cap = g->step_cap;
+  p.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
+  p.stop_after = 0xffffffffu;
+  p.bc_sigma = g->bc_sigma;
+  p.bc_delta = g->bc_delta;
+  p.bc_succ = g->bc_succ;
+  p.bc_scores = g->bc_scores;
+  p.bc_bounds = g->bc_bounds;
+  p.bc_bounds_cap = g->bc_bounds_cap;
+  cudaStream_t s = g->stream;
+  CK(cudaMemsetAsync(g->bc_scores, 0, sizeof(float) * n, s), "clear scores");
+  CK(cudaEventRecord(g->ev0, s), "event record");
+  for (int64_t i = 0; i < num_sources; i++) {
+    p.src = sources[i];
+    CK(cudaMemsetAsync(g->ctrl, 0, sizeof(gk::Ctrl), s), "reset ctrl");
+    CK(gk::bc_launch(p, g->device, s), "launch brandes kernel");
+    int err = 0;
+    CK(cudaMemcpyAsync(&err, &g->ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s), "read status");
+    CK(cudaStreamSynchronize(s), "brandes kernel");
+    if (err == 2) return fail(GK_ERR_TIMEOUT, "brandes kernel watchdog fired (grid barrier timeout)");
+    if (err == 3) return fail(GK_ERR_CUDA, "brandes kernel: chunk buffer overflow");
+    if (err == 4) return fail(GK_ERR_CUDA, "brandes kernel: level bound buffer overflow");
+    if (err) return fail(GK_ERR_CUDA, "brandes kernel failed");
+  }
+  CK(gk::bc_normalize(g->bc_scores, n, g->bc_scores + n, s), "normalize scores");
+  CK(cudaEventRecord(g->ev1, s), "event record");
+  if (scores_out) CK(cudaMemcpyAsync(scores_out, g->bc_scores, sizeof(float) * n, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaStreamSynchronize(s), "brandes");
+  if (device_ms) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1), "event time");
+    *device_ms = ms;
+  }
   return GK_OK;
 }
 

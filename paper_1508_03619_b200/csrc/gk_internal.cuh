@@ -33,7 +33,8 @@ namespace gk {
 // appends).  kLongCount: bottom-up vertices deferred to the long list.
 constexpr int kTraceCap = 512;
 enum PhaseTag : unsigned char { kTagInit = 'I', kTagTD = 'T', kTagHeavy = 'H', kTagZero = 'Z', kTagQ2B = 'Q',
-                                kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S', kTagLong = 'L' };
+                                kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S', kTagLong = 'L',
+                                kTagBcBack = 'D', kTagBcChunk = 'E', kTagBcScore = 'F' };
 enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend = 4, kLongCount = 5, kCount = 6, kSlots = 8 };
 
 struct Ctrl {
@@ -108,6 +109,13 @@ struct BfsParams {
   unsigned long long timeout_ns;
   unsigned stop_after;  // leave after this many grid barriers (profiling only)
   unsigned exp_flags;   // experiment switches (GK_EXP, profiling only)
+  // Brandes (betweenness.hpp:38-80), bc_persistent only
+  double* bc_sigma;     // shortest-path counts
+  double* bc_delta;     // dependencies
+  uint32_t* bc_succ;    // one bit per stored arc: shortest-path successor edge
+  float* bc_scores;     // accumulated over sources
+  int64_t* bc_bounds;   // level d = queue[bounds[d], bounds[d+1])
+  int64_t bc_bounds_cap;
 };
 
 constexpr int kBlock = 512;
@@ -122,6 +130,10 @@ struct BfsLaunch {
 };
 cudaError_t bfs_configure(int device, BfsLaunch* cfg);
 cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t s);
+// One source of Brandes' forward + backward pass (cooperative launch).
+cudaError_t bc_launch(const BfsParams& p, int device, cudaStream_t s);
+// scores /= max(scores) when the max is > 0 (betweenness.hpp:136-143).
+cudaError_t bc_normalize(float* scores, int64_t n, float* scratch_max, cudaStream_t s);
 
 // Auxiliary (untimed) kernels.
 cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s);
@@ -181,6 +193,13 @@ struct gk_graph {
   uint32_t* dead = nullptr;  // graph property, computed once by finish_graph
   gk::HeadRec* head = nullptr;  // ditto: the first kHead entries of every live in-list
   uint32_t* hbase = nullptr; // ditto: head index of each word's first live vertex
+  // Brandes workspace, allocated on first use
+  double* bc_sigma = nullptr;
+  double* bc_delta = nullptr;
+  uint32_t* bc_succ = nullptr;
+  float* bc_scores = nullptr;
+  int64_t* bc_bounds = nullptr;
+  int64_t bc_bounds_cap = 0;
   uint32_t* queue = nullptr;
   gk::Chunk* chunks = nullptr;
   int64_t chunk_cap = 0;

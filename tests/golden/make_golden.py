@@ -94,6 +94,23 @@ def main():
     gold["kat"]["isolated_parent"] = [int(x) for x in g.bfs(0)]
     gold["kat"]["perm_scale16_first8"] = [O.permute(v, 16, SEED) for v in range(8)]
     gold["kat"]["perm_keys_s16"] = [f"{int(k):016x}" for k in O.perm_keys(SEED, 16)]
+    # Brandes betweenness (betweenness.hpp:84-145) from the reference; the
+    # graphs of test_kernels_source.cc:136-180 plus kron10/urand10
+    gold["bc"] = {}
+    bc_cases = {
+        "star5": (R.build(5, np.array([x for v in range(4) for x in (4, v)], np.uint32)), [0, 1, 2, 3, 4]),
+        "path2": (R.build(2, np.array([0, 1], np.uint32)), [0]),
+    }
+    for nm, kind, scale, seed, directed in (("kron10", "kron", 10, SEED, False), ("urand10", "urand", 10, SEED, False),
+                                            ("dkron9_s13", "kron", 9, 13, True)):
+        g = R.build(1 << scale, R.gen(kind, scale, 16, seed), directed=directed, symmetrize=not directed)
+        bc_cases[nm] = (g, [int(x) for x in g.pick_sources(4, SEED)])
+    for nm, (g, srcs) in bc_cases.items():
+        sc = g.brandes(srcs)
+        ok, msg = g.verify_bc(srcs, sc)
+        assert ok, (nm, msg)
+        gold["bc"][nm] = {"sources": [int(x) for x in srcs], "scores": [float(x) for x in sc],
+                          "directed": bool(g.directed)}
     # .sg fixtures written by the reference's WriteSerialized (io.hpp:364-389)
     gdir = os.path.dirname(os.path.abspath(__file__))
     R.build(2, np.array([0, 1], np.uint32), directed=True, symmetrize=False).write_sg(

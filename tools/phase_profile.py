@@ -16,11 +16,12 @@ def main():
     ap.add_argument("--config", default="kron27")
     ap.add_argument("--sources", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--src", type=int, nargs="*", help="explicit sources instead of the first picked ones")
     a = ap.parse_args()
     cfg = bench.parse_config(a.config)
     g, bs = bench.build_graph(cfg, 0)
     print(f"{a.config}: n={g.n} arcs={g.m} build {bs:.2f}s")
-    srcs = [int(s) for s in g.pick_sources(a.sources, bench.SEED)]
+    srcs = a.src or [int(s) for s in g.pick_sources(a.sources, bench.SEED)]
     for s in srcs[: a.warmup]:
         g.bfs(s, parent=False)
     tot = defaultdict(float)
