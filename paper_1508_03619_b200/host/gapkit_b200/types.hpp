@@ -18,6 +18,8 @@ namespace gapkit {
 using NodeId = uint32_t;           // types.hpp:15
 using ParentEntry = int32_t;       // types.hpp:19
 using ParentArray = std::vector<ParentEntry>;  // types.hpp:20
+using Score = float;                           // types.hpp:26
+using ScoreArray = std::vector<Score>;         // types.hpp:27
 inline constexpr uint64_t kDefaultSeed = 24601;  // types.hpp:33
 
 struct Error : std::runtime_error {  // errors.hpp:13-15

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "gapkit_b200/betweenness.hpp"
 #include "gapkit_b200/bfs.hpp"
 #include "gapkit_b200/builder.hpp"
 #include "gapkit_b200/generator.hpp"
@@ -111,6 +112,34 @@ int main(int argc, char** argv) {
     bad[2] = -1;
     CHECK(VerifyBfs(path, 0, bad).failure_detail.find("unreached") != std::string::npos);
     std::printf("errors ok\n");
+    return 0;
+  }
+  if (cmd == "bc") {  // test_kernels_source.cc:136-158 through the device
+    EdgeList star;
+    star.node_count = 5;
+    for (NodeId v = 0; v < 4; v++) star.Add(4, v);
+    CsrGraph sg = BuildCsr(star, false, true);
+    std::vector<NodeId> all = {0, 1, 2, 3, 4};
+    ScoreArray sc = Brandes(sg, all);
+    CHECK(sc[4] == 1.0f);
+    for (int leaf = 0; leaf < 4; leaf++) CHECK(sc[leaf] == 0.0f);
+    EdgeList p2;
+    p2.Add(0, 1);
+    std::vector<NodeId> zero = {0};
+    ScoreArray pz = Brandes(BuildCsr(p2, false, true), zero);
+    CHECK(pz[0] == 0.0f && pz[1] == 0.0f);
+    EdgeList e3;
+    e3.node_count = 3;
+    e3.Add(0, 1);
+    CsrGraph g3 = BuildCsr(e3, false, true);
+    std::vector<NodeId> none, iso = {2};
+    CHECK(Throws([&] { Brandes(g3, none); }, "betweenness requires at least one source"));
+    CHECK(Throws([&] { Brandes(g3, iso); }, "zero out-degree"));
+    CsrGraph k = Build("kron", 10, kDefaultSeed);
+    std::vector<NodeId> src = PickSources(k, 4);
+    ScoreArray ks = Brandes(k, src);
+    for (Score x : ks) CHECK(x >= 0.0f && x <= 1.0f);
+    std::printf("bc ok\n");
     return 0;
   }
   if (cmd == "gpu") {

@@ -74,6 +74,13 @@ def test_host_shim_bfs_on_gpu(tools):
 
 
 @pytest.mark.gpu
+def test_host_shim_brandes_on_gpu(tools):
+    r = run(tools[0], "bc")
+    assert r.returncode == 0, r.stderr
+    assert "bc ok" in r.stdout
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("graph", [("-g", "14"), ("-u", "13"), ("--grid", "120x90")])
 def test_cli_bfs_verified(tools, graph, tmp_path):
     out = tmp_path / "bfs.csv"
