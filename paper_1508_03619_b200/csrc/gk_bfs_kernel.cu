@@ -1047,14 +1047,15 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
 // successor bit and adds sigma[u] into sigma[v].  The queue keeps every
 // level in place; bc_bounds[d] marks where level d starts.
 // Backward (betweenness.hpp:104-122): levels deepest first; delta[u] = sum
-// over u's flagged edges of sigma[u]/sigma[v] * (1 + delta[v]).  Vertices of
-// degree <= 32 are summed by one lane in edge order (the reference's order);
-// up to kBcWarpDeg by a whole warp; larger ones are cut into chunks whose
-// partial sums are added atomically.  Finally scores[u] += (float)delta[u]
-// for every reached u != source.
+// over u's flagged edges of sigma[u]/sigma[v] * (1 + delta[v]), edge-balanced
+// over the level like the forward expansion (per-vertex sums in shared
+// memory, high-degree vertices in chunks whose partial sums are added
+// atomically).  The summation order differs from the reference's serial
+// per-vertex loop, so dependencies agree to rounding (path counts are
+// exact).  Finally scores[u] += (float)delta[u] for every reached u !=
+// source.
 // ============================================================================
 constexpr int64_t kBcChunk = 1024;
-constexpr int64_t kBcWarpDeg = 8192;
 
 __device__ __forceinline__ void bc_edges4(const BfsParams& P, const QApp& qa, const double (&su)[4],
                                           const uint32_t (&v)[4], const int64_t (&e)[4], const bool (&ok)[4],
@@ -1188,72 +1189,93 @@ __device__ __forceinline__ double bc_term(const BfsParams& P, double su, uint32_
   return (su / __ldcg(P.bc_sigma + v)) * (1.0 + __ldcg(P.bc_delta + v));
 }
 
-// Backward pass A over one level's vertices.
-__device__ void bc_backward_level(const BfsParams& P, unsigned ph, unsigned long long b0, unsigned long long b1) {
-  const unsigned lane = lane_id();
-  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+// Backward pass A over one level's vertices queue[b0, b1): tiles of kBlock
+// vertices, CTA scan of degrees, load-balanced over the tile's edges with 4
+// edges per thread in flight; each flagged edge's term is added into its
+// vertex's shared-memory accumulator, written to delta once per tile.
+// Vertices of degree > kBcChunk are cut into chunks for pass B (their delta
+// stays 0 here and collects the chunk partials).
+__device__ void bc_backward_level(const BfsParams& P, SmemT& s, unsigned ph, unsigned long long b0,
+                                  unsigned long long b1) {
+  double* acc = reinterpret_cast<double*>(&s.td.qbuf[0][0]);  // kBlock doubles (qbuf unused here)
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
-  for (unsigned long long base = b0 + (unsigned long long)gw * 32; base < b1; base += (unsigned long long)nw * 32) {
-    const unsigned long long i = base + lane;
+  for (unsigned long long tile = blockIdx.x;; tile += gridDim.x) {
+    const unsigned long long start = b0 + tile * (unsigned long long)kBlock;
+    if (start >= b1) break;
+    const unsigned long long i = start + threadIdx.x;
     uint32_t u = 0;
-    int64_t eb = 0, d = 0;
+    int64_t b = 0, dl = 0;
     double su = 0.0;
+    bool heavy = false;
     if (i < b1) {
       u = __ldcg(P.queue + i);
-      eb = P.out_off[u];
-      d = P.out_off[u + 1] - eb;
+      b = P.out_off[u];
       su = __ldcg(P.bc_sigma + u);
-    }
-    if (i < b1 && d <= 32) {  // one lane, in edge order
-      double acc = 0.0;
-      if (d > 0) {
-        const uint32_t w0 = __ldcg(P.bc_succ + (eb >> 5));
-        const uint32_t w1 = __ldcg(P.bc_succ + ((eb + d - 1) >> 5));
-        for (int k = 0; k < (int)d; k++) {
-          const int64_t e = eb + k;
-          const uint32_t w = ((e >> 5) == (eb >> 5)) ? w0 : w1;
-          if ((w >> (e & 31)) & 1u) acc += bc_term(P, su, __ldg(P.out_nb + e));
-        }
-      }
-      P.bc_delta[u] = acc;
-    }
-    unsigned big = __ballot_sync(kFull, i < b1 && d > 32);
-    while (big) {
-      const int l = __ffs(big) - 1;
-      big &= big - 1;
-      const uint32_t ul = __shfl_sync(kFull, u, l);
-      const int64_t ebl = __shfl_sync(kFull, eb, l);
-      const int64_t dl = __shfl_sync(kFull, d, l);
-      const double sul = __shfl_sync(kFull, su, l);
-      if (dl > kBcWarpDeg) {  // cut into chunks, summed in pass B
-        if (lane == 0) {
-          const int64_t nch = (dl + kBcChunk - 1) / kBcChunk;
-          const unsigned long long cb = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
-          if ((int64_t)(cb + nch) <= P.chunk_cap) {
-            for (int64_t c = 0; c < nch; c++) {
-              Chunk ch;
-              ch.u = ul;
-              ch.start = ebl + c * kBcChunk;
-              ch.len = (uint32_t)((dl - c * kBcChunk) < kBcChunk ? (dl - c * kBcChunk) : kBcChunk);
-              P.chunks[cb + c] = ch;
-            }
-          } else {
-            atomicExch(&P.ctrl->error, 3);
+      const int64_t d = P.out_off[u + 1] - b;
+      if (d > kBcChunk) {
+        heavy = true;
+        const int64_t nch = (d + kBcChunk - 1) / kBcChunk;
+        const unsigned long long base = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
+        if ((int64_t)(base + nch) <= P.chunk_cap) {
+          for (int64_t c = 0; c < nch; c++) {
+            Chunk ch;
+            ch.u = u;
+            ch.start = b + c * kBcChunk;
+            ch.len = (uint32_t)((d - c * kBcChunk) < kBcChunk ? (d - c * kBcChunk) : kBcChunk);
+            P.chunks[base + c] = ch;
           }
-          P.bc_delta[ul] = 0.0;
+        } else {
+          atomicExch(&P.ctrl->error, 3);
         }
-        continue;
+      } else {
+        dl = d;
       }
-      double acc = 0.0;
-      for (int64_t j = lane; j < dl; j += 32) {
-        const int64_t e = ebl + j;
-        if ((__ldcg(P.bc_succ + (e >> 5)) >> (e & 31)) & 1u) acc += bc_term(P, sul, __ldg(P.out_nb + e));
+    }
+    s.td.t_b[threadIdx.x] = b;
+    s.bc_sig[threadIdx.x] = su;
+    acc[threadIdx.x] = 0.0;
+    int64_t tot;
+    const int64_t pre = block_exscan(dl, &tot, s);
+    s.td.t_pre[threadIdx.x] = pre;
+    __syncthreads();
+    for (int64_t eb = 0; eb < tot; eb += 4 * kBlock) {
+      int64_t e[4];
+      int lo[4];
+      bool f[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int64_t ei = eb + k * kBlock + threadIdx.x;
+        f[k] = false;
+        lo[k] = 0;
+        e[k] = 0;
+        if (ei < tot) {
+          int l = 0, h = kBlock - 1;
+          while (l < h) {
+            const int mid = (l + h + 1) >> 1;
+            if (s.td.t_pre[mid] <= ei) l = mid;
+            else h = mid - 1;
+          }
+          lo[k] = l;
+          e[k] = s.td.t_b[l] + (ei - s.td.t_pre[l]);
+          f[k] = (__ldcg(P.bc_succ + (e[k] >> 5)) >> (e[k] & 31)) & 1u;
+        }
+      }
+      uint32_t v[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) v[k] = f[k] ? __ldg(P.out_nb + e[k]) : 0u;
+      double sv[4], dv[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        sv[k] = f[k] ? __ldcg(P.bc_sigma + v[k]) : 1.0;
+        dv[k] = f[k] ? __ldcg(P.bc_delta + v[k]) : 0.0;
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-      if (lane == 0) P.bc_delta[ul] = acc;
+      for (int k = 0; k < 4; k++)
+        if (f[k]) atomicAdd(acc + lo[k], (s.bc_sig[lo[k]] / sv[k]) * (1.0 + dv[k]));
     }
+    __syncthreads();
+    if (i < b1 && !heavy) P.bc_delta[u] = acc[threadIdx.x];
+    __syncthreads();
   }
 }
 
@@ -1334,7 +1356,7 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
     const unsigned long long b0 = d == 0 ? 0ull : (unsigned long long)__ldcg(P.bc_bounds + d);
     const unsigned long long b1 = d + 1 == lvl ? qtail : (unsigned long long)__ldcg(P.bc_bounds + d + 1);
     const unsigned set = ph & 3;
-    bc_backward_level(P, ph, b0, b1);
+    bc_backward_level(P, s, ph, b0, b1);
     if (!grid_sync(P, s, ph, kTagBcBack)) return;
     const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
     if (nch) {

@@ -550,9 +550,11 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
     p.src = sources[i];
     CK(cudaMemsetAsync(g->ctrl, 0, sizeof(gk::Ctrl), s), "reset ctrl");
     CK(gk::bc_launch(p, g->device, s), "launch brandes kernel");
-    int err = 0;
-    CK(cudaMemcpyAsync(&err, &g->ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s), "read status");
+    gk::Ctrl& ctrl = g->last_ctrl;  // kept for gk_bfs_trace (phase timings of the last source)
+    CK(cudaMemcpyAsync(&ctrl, g->ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
     CK(cudaStreamSynchronize(s), "brandes kernel");
+    g->last_valid = 1;
+    const int err = ctrl.error;
     if (err == 2) return fail(GK_ERR_TIMEOUT, "brandes kernel watchdog fired (grid barrier timeout)");
     if (err == 3) return fail(GK_ERR_CUDA, "brandes kernel: chunk buffer overflow");
     if (err == 4) return fail(GK_ERR_CUDA, "brandes kernel: level bound buffer overflow");
