@@ -9,7 +9,7 @@ A "step" is one BFS (gk_bfs, the C-ABI replacement of gapkit::Bfs,
 bfs.hpp:117) from the next of PickSources(g, K, seed) (source_picker.hpp:47).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config kron27|urand27|kron16|grid4900|kronS|urandS]
+                  [--config kron27|urand27|kron16|grid4900|kron30|kronS|urandS]
 
 value     : harmonic mean over the K steps of m_cc(s)/t_dev(s) (GTEPS), t_dev the
             CUDA-event time of the traversal kernel, graph resident in HBM.
@@ -47,6 +47,9 @@ CONFIGS = {
                              "symmetrized+deduplicated, CSR"),
     "kron16": dict(kind="kron", scale=16, degree=16, permute=True,
                    workload="BASELINE config 1: Kronecker 2^16 vertices, edge factor 16, permuted"),
+    "kron30": dict(kind="kron", scale=30, degree=16, permute=True,
+                   workload="BASELINE config 5's graph: Kronecker 2^30 vertices, edge factor 16, permuted, "
+                            "symmetrized+deduplicated (34.0 G arcs, 145 GB CSR) on ONE B200"),
     "grid4900": dict(kind="grid", rows=4900, cols=4900, p_delete=0.15, p_diag=0.02,
                      workload="BASELINE config 4: 4900x4900 4-neighbour grid, 15% edges deleted, "
                               "2% diagonal shortcuts"),

@@ -290,7 +290,8 @@ template <bool kBig>
 __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const uint32_t (&u)[4],
                                        const uint32_t (&v)[4], const bool (&ok)[4],
                                        uint32_t* nextbm, int lvl, bool encode, long long& scout,
-                                       uint32_t* buf, int& qcnt, bool tiny) {
+                                       uint32_t* buf, int& qcnt, bool tiny, uint32_t rlo = 0,
+                                       uint32_t rhi = 0xffffffffu) {
   uint32_t w[4];
   bool c[4];
   if (!kBig && tiny) {
@@ -332,7 +333,8 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
     // visited bits afterwards.  No atomic round trip sits on the chain.
     uint32_t x[4];
 #pragma unroll
-    for (int k = 0; k < 4; k++) x[k] = ok[k] ? ld_bits(nextbm + (v[k] >> 5)) : 0xffffffffu;
+    for (int k = 0; k < 4; k++)
+      x[k] = (ok[k] && v[k] >= rlo && v[k] < rhi) ? ld_bits(nextbm + (v[k] >> 5)) : 0xffffffffu;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       if (!((x[k] >> (v[k] & 31u)) & 1u)) {
@@ -364,7 +366,8 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
 template <bool kBig>
 __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, unsigned long long qs,
                          unsigned long long qe, uint32_t* nextbm, int lvl, bool encode,
-                         long long& scout, int& qcnt, int tile_sz, int64_t chunk, bool tiny) {
+                         long long& scout, int& qcnt, int tile_sz, int64_t chunk, bool tiny,
+                         bool reg = true, uint32_t rlo = 0, uint32_t rhi = 0xffffffffu) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
   // First tile of each CTA is static (no atomic on the latency chain of
@@ -381,18 +384,20 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       b = P.out_off[u];
       const int64_t d = P.out_off[u + 1] - b;
       if (d > chunk) {
-        const int64_t nch = (d + chunk - 1) / chunk;
-        const unsigned long long base = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
-        if ((int64_t)(base + nch) <= P.chunk_cap) {
-          for (int64_t c = 0; c < nch; c++) {
-            Chunk ch;
-            ch.u = u;
-            ch.start = b + c * chunk;
-            ch.len = (uint32_t)((d - c * chunk) < chunk ? (d - c * chunk) : chunk);
-            P.chunks[base + c] = ch;
+        if (reg) {  // range passes after the first reuse the chunk list
+          const int64_t nch = (d + chunk - 1) / chunk;
+          const unsigned long long base = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
+          if ((int64_t)(base + nch) <= P.chunk_cap) {
+            for (int64_t c = 0; c < nch; c++) {
+              Chunk ch;
+              ch.u = u;
+              ch.start = b + c * chunk;
+              ch.len = (uint32_t)((d - c * chunk) < chunk ? (d - c * chunk) : chunk);
+              P.chunks[base + c] = ch;
+            }
+          } else {
+            atomicExch(&P.ctrl->error, 3);
           }
-        } else {
-          atomicExch(&P.ctrl->error, 3);
         }
       } else {
         dl = d;
@@ -424,7 +429,7 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
           v[k] = ld_nb_once(P.out_nb + s.td.t_b[lo] + (ei - s.td.t_pre[lo]));
         }
       }
-      claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt, tiny);
+      claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt, tiny, rlo, rhi);
     }
     if (threadIdx.x == 0 && start + tile_sz < qe) s.bcast[1] = gridDim.x + atomicAdd(&cnt[kTile], 1ull);
     __syncthreads();
@@ -437,7 +442,8 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
 // ---- top-down, heavy chunks: one warp per chunk, 4 edges per lane in flight --
 template <bool kBig>
 __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, unsigned long long nch,
-                         uint32_t* nextbm, int lvl, bool encode, long long& scout, int& qcnt, bool tiny) {
+                         uint32_t* nextbm, int lvl, bool encode, long long& scout, int& qcnt, bool tiny,
+                         uint32_t rlo = 0, uint32_t rhi = 0xffffffffu) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   const unsigned lane = lane_id();
   // Chunks are equal-sized (chunk edges but the tails), so a static
@@ -459,7 +465,8 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
           v[k] = j < ch.len ? ld_nb_once(P.out_nb + ch.start + j) : kNoVertex;
         }
 #pragma unroll
-        for (int k = 0; k < kE; k++) x[k] = v[k] != kNoVertex ? ld_bits(nextbm + (v[k] >> 5)) : 0xffffffffu;
+        for (int k = 0; k < kE; k++)
+          x[k] = (v[k] != kNoVertex && v[k] >= rlo && v[k] < rhi) ? ld_bits(nextbm + (v[k] >> 5)) : 0xffffffffu;
 #pragma unroll
         for (int k = 0; k < kE; k++) {
           if (!((x[k] >> (v[k] & 31u)) & 1u)) {  // see claim4<true>
@@ -959,35 +966,53 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         for (long long i = gtid; i < P.w32; i += gthreads) nextg[i] = __ldcg(P.visited + i);
         if (!grid_sync(P, s, ph, kTagZero)) return;
       }
-      set = ph & 3;
-      {
-        const QApp qa = qapp(P, ph, qtail);
-        if (big) {
-          td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk, false);
-        } else {
+      if (big) {
+        // Claims only touch next (n/8 bytes).  When that bitmap is larger
+        // than L2 can hold, the step runs in P.td_passes passes over target
+        // vertex ranges of P.td_span ids, each pass's slice of next (and of
+        // parent) staying L2-resident; the frontier's lists are re-streamed
+        // per pass, which HBM does at full bandwidth.
+        unsigned long long nch = 0;
+        for (int r = 0; r < P.td_passes; r++) {
+          const uint32_t rlo = (uint32_t)((int64_t)r * P.td_span);
+          const uint32_t rhi = r + 1 == P.td_passes ? 0xffffffffu : (uint32_t)((int64_t)(r + 1) * P.td_span);
+          set = ph & 3;
+          {
+            const QApp qa = qapp(P, ph, qtail);
+            td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk, false, r == 0,
+                           rlo, rhi);
+          }
+          if (!grid_sync(P, s, ph, kTagTD)) return;
+          if (r == 0) nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
+          if (nch) {
+            const QApp qa = qapp(P, ph, qtail);
+            td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, false, rlo, rhi);
+            if (!grid_sync(P, s, ph, kTagHeavy)) return;
+          }
+        }
+      } else {
+        set = ph & 3;
+        {
+          const QApp qa = qapp(P, ph, qtail);
           td_light<false>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk, tiny);
           wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
         }
-      }
-      block_add(sacc, &P.ctrl->cnt[set][kSum], s);
-      if (!grid_sync(P, s, ph, kTagTD)) return;
-      scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
-      qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
-      const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
-      if (nch) {
-        sacc = 0;
-        set = ph & 3;
-        const QApp qa = qapp(P, ph, qtail);
-        if (big) {
-          td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, false);
-        } else {
+        block_add(sacc, &P.ctrl->cnt[set][kSum], s);
+        if (!grid_sync(P, s, ph, kTagTD)) return;
+        scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
+        const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
+        if (nch) {
+          sacc = 0;
+          set = ph & 3;
+          const QApp qa = qapp(P, ph, qtail);
           td_heavy<false>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, tiny);
           wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+          block_add(sacc, &P.ctrl->cnt[set][kSum], s);
+          if (!grid_sync(P, s, ph, kTagHeavy)) return;
+          scout += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+          qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
         }
-        block_add(sacc, &P.ctrl->cnt[set][kSum], s);
-        if (!grid_sync(P, s, ph, kTagHeavy)) return;
-        scout += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
-        qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
       }
       if (big) {
         long long cacc = 0;
