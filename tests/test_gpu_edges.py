@@ -1,0 +1,109 @@
+"""Edge cases of the device traversal's data-layout shortcuts against the
+oracle: the never-reachable (dead) seed of visited, the per-vertex head
+records of the bottom-up sweep, tiny-step claims, large-step bitmap claims
+and their target-range passes, ragged vertex counts around bitmap words.
+
+Bar as in test_gpu_bfs.py: depths bit-exact, parents valid (VerifyBfs
+semantics), schedule and per-step counters equal to the reference's replay,
+bottom-up parents equal to the reference's first-hit choice."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1508_03619_b200 import Brandes, BfsStrategy, DeviceGraph
+
+pytestmark = pytest.mark.gpu
+
+
+def check(g, dg, s, alpha=15, beta=18, strategy=0):
+    res = dg.bfs(int(s), alpha, beta, strategy, depth=True, counts=True)
+    assert (res.depth == O.bfs_depths(g, int(s))).all()
+    ok, msg = O.verify_bfs(g, int(s), res.parent)
+    assert ok, msg
+    rp = O.bfs_replay(g, int(s), alpha, beta, strategy)
+    assert res.schedule == rp.dirs
+    assert [x[2] for x in res.steps] == rp.result
+    for i, c in enumerate(res.schedule):
+        if c == "B":
+            sel = res.depth == i + 1
+            assert (res.parent[sel] == rp.parent[sel]).all(), ("bottom-up parent", i)
+    return res
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 63, 65, 1000, 1025])
+def test_ragged_vertex_counts(n):
+    rng = np.random.default_rng(n)
+    m = 3 * n
+    e = rng.integers(0, n, size=2 * m, dtype=np.uint64).astype(np.uint32)
+    g = O.build_csr(n, e)
+    dg = DeviceGraph.from_csr(g)
+    for s in {0, n - 1, n // 2}:
+        for st in BfsStrategy:
+            for a, b in ((15, 18), (1, 1)):
+                check(g, dg, s, a, b, int(st))
+
+
+def test_heavy_hub_small_graph():
+    # one vertex of degree 6000 (> the 1024-edge chunk), plus a sparse ring:
+    # heavy chunks, a large (bitmap) top-down step and head/list rounds
+    n = 6001
+    e = [x for v in range(1, n) for x in (0, v)] + [x for v in range(1, n - 1) for x in (v, v + 1)]
+    g = O.build_csr(n, np.array(e, np.uint32))
+    dg = DeviceGraph.from_csr(g)
+    for s in (0, 1, 3000, n - 1):
+        for a, b in ((15, 18), (1000, 1), (1, 1000)):
+            check(g, dg, s, a, b)
+
+
+def test_isolated_source_and_dead_vertices():
+    # vertices 5..9 have no edges at all; BFS from one of them reaches only it
+    e = np.array([0, 1, 1, 2, 2, 3, 3, 4], np.uint32)
+    g = O.build_csr(10, e)
+    dg = DeviceGraph.from_csr(g)
+    r = dg.bfs(7, depth=True)
+    assert r.parent.tolist() == [-1] * 7 + [7] + [-1] * 2
+    assert r.depth.tolist() == [-1] * 7 + [0] + [-1] * 2
+    check(g, dg, 0, 1, 1)
+
+
+def test_directed_source_without_in_edges():
+    # vertex 0 only has out-edges: it is "dead" for the bottom-up sweep but a
+    # valid source; vertex 4 has in-edges only
+    e = np.array([0, 1, 0, 2, 1, 3, 2, 3, 3, 4, 1, 4], np.uint32)
+    g = O.build_csr(5, e, symmetrize=False, directed=True)
+    dg = DeviceGraph.from_csr(g)
+    for a, b in ((1, 1), (15, 18)):
+        r = check(g, dg, 0, a, b)
+        assert r.parent[0] == 0
+    r = dg.bfs(4, depth=True)
+    assert r.parent.tolist() == [-1, -1, -1, -1, 4]
+
+
+@pytest.mark.parametrize("passes", ["2", "3", "7"])
+def test_large_step_range_passes(passes, monkeypatch):
+    # GK_TD_PASSES forces the target-range passes of large top-down steps
+    # that kick in by themselves only when the next bitmap exceeds 64 MB
+    monkeypatch.setenv("GK_TD_PASSES", passes)
+    g = O.make_graph("kron", 16, permute=True)
+    dg = DeviceGraph.from_csr(g)
+    for s in O.pick_sources(g, 6, 5):
+        check(g, dg, int(s))
+    gu = O.make_graph("urand", 15)
+    dgu = DeviceGraph.from_csr(gu)
+    for s in O.pick_sources(gu, 3, 5):
+        check(gu, dgu, int(s))
+
+
+def test_handle_state_across_kernels():
+    # BFS, Brandes, BFS again on one handle: per-call state is re-initialised
+    g = O.make_graph("kron", 12, permute=True)
+    dg = DeviceGraph.from_csr(g)
+    srcs = [int(s) for s in O.pick_sources(g, 3)]
+    first = [dg.bfs(s, depth=True).depth.copy() for s in srcs]
+    sc = Brandes(dg, srcs)
+    assert np.abs(sc - O.brandes(g, srcs)).max() <= 1e-5
+    for s, d in zip(srcs, first):
+        r = check(g, dg, s)
+        assert (r.depth == d).all()
