@@ -55,6 +55,7 @@ struct __align__(16) SmemT {
   };
   long long red[kWarps + 2];
   unsigned long long bcast[4];
+  unsigned long long snap[kSlots];  // counter set of the phase the last grid_sync ended
   int ok;
 };
 
@@ -165,6 +166,11 @@ __device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& ph, unsigned c
       }
     }
     s.ok = ok;
+    // One read of the ended phase's counters per CTA, shared through smem
+    // (every thread reading them from L2 made a hot spot on one line).
+    const volatile unsigned long long* cs = c->cnt[ph & 3];
+#pragma unroll
+    for (int i = 0; i < kSlots; i++) s.snap[i] = cs[i];
     if (blockIdx.x == 0) {  // recycle the counter set two phases ahead; trace
       unsigned long long* z = c->cnt[(ph + 3) & 3];
 #pragma unroll
@@ -882,7 +888,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       const unsigned bset = ph & 3;
       b2q(P, qapp(P, ph, qtail), frontg, s);
       if (!grid_sync(P, s, ph, kTagB2Q)) return;
-      qtail += ld_volatile(&P.ctrl->cnt[bset][kAppend]);
+      qtail += s.snap[kAppend];
       queue_stale = false;
     }
     if (go_bu) {
@@ -918,8 +924,8 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         unsigned set = ph & 3;
         block_add(acc, &P.ctrl->cnt[set][kSum], s);
         if (!grid_sync(P, s, ph, kTagBU)) return;
-        const unsigned long long nlong = ld_volatile(&P.ctrl->cnt[set][kLongCount]);
-        long long awake_bu = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        const unsigned long long nlong = s.snap[kLongCount];
+        long long awake_bu = (long long)s.snap[kSum];
         if (nlong) {
           acc = 0;
           if (P.front_in_smem) bu_long<true>(P, fr, nextg, lbase, nlong, lvl, acc);
@@ -927,7 +933,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
           set = ph & 3;
           block_add(acc, &P.ctrl->cnt[set][kSum], s);
           if (!grid_sync(P, s, ph, kTagLong)) return;
-          awake_bu += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+          awake_bu += (long long)s.snap[kSum];
         }
         awake = awake_bu;
         log_step(P, nsteps++, 'B', old_awake, awake, etc);
@@ -939,7 +945,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       const unsigned bset = ph & 3;
       b2q(P, qapp(P, ph, qtail), frontg, s);  // bfs.hpp:155
       if (!grid_sync(P, s, ph, kTagB2Q)) return;
-      qtail += ld_volatile(&P.ctrl->cnt[bset][kAppend]);
+      qtail += s.snap[kAppend];
       qe = qtail;
       scout = 1;  // bfs.hpp:156
       front_ready = true;
@@ -983,7 +989,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
                            rlo, rhi);
           }
           if (!grid_sync(P, s, ph, kTagTD)) return;
-          if (r == 0) nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
+          if (r == 0) nch = s.snap[kChunkCount];
           if (nch) {
             const QApp qa = qapp(P, ph, qtail);
             td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, false, rlo, rhi);
@@ -999,9 +1005,9 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         }
         block_add(sacc, &P.ctrl->cnt[set][kSum], s);
         if (!grid_sync(P, s, ph, kTagTD)) return;
-        scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
-        qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
-        const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
+        scout = (long long)s.snap[kSum];
+        qtail += s.snap[kAppend];
+        const unsigned long long nch = s.snap[kChunkCount];
         if (nch) {
           sacc = 0;
           set = ph & 3;
@@ -1010,8 +1016,8 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
           wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
           block_add(sacc, &P.ctrl->cnt[set][kSum], s);
           if (!grid_sync(P, s, ph, kTagHeavy)) return;
-          scout += (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
-          qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
+          scout += (long long)s.snap[kSum];
+          qtail += s.snap[kAppend];
         }
       }
       if (big) {
@@ -1022,8 +1028,8 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         block_add(sacc, &P.ctrl->cnt[set][kSum], s);
         block_add(cacc, &P.ctrl->cnt[set][kCount], s);
         if (!grid_sync(P, s, ph, kTagSweep)) return;
-        scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
-        const unsigned long long claimed = ld_volatile(&P.ctrl->cnt[set][kCount]);
+        scout = (long long)s.snap[kSum];
+        const unsigned long long claimed = s.snap[kCount];
         uint32_t* t = frontg;
         frontg = nextg;
         nextg = t;
@@ -1048,7 +1054,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         set = ph & 3;
         block_add(tot, &P.ctrl->cnt[set][kSum], s);
         if (!grid_sync(P, s, ph, kTagRescan)) return;
-        scout = (long long)ld_volatile(&P.ctrl->cnt[set][kSum]);
+        scout = (long long)s.snap[kSum];
       }
       log_step(P, nsteps++, 'T', fsize, scout, etc);
       lvl++;
@@ -1362,15 +1368,15 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
       wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
     }
     if (!grid_sync(P, s, ph, kTagTD)) return;
-    qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
-    const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
+    qtail += s.snap[kAppend];
+    const unsigned long long nch = s.snap[kChunkCount];
     if (nch) {
       set = ph & 3;
       const QApp qa = qapp(P, ph, qtail);
       bc_forward_heavy(P, qa, nch, lvl, s, qcnt);
       wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
       if (!grid_sync(P, s, ph, kTagHeavy)) return;
-      qtail += ld_volatile(&P.ctrl->cnt[set][kAppend]);
+      qtail += s.snap[kAppend];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) P.bc_bounds[lvl] = (int64_t)qe;  // level lvl starts at qe
     qs = qe;
@@ -1383,7 +1389,7 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
     const unsigned set = ph & 3;
     bc_backward_level(P, s, ph, b0, b1);
     if (!grid_sync(P, s, ph, kTagBcBack)) return;
-    const unsigned long long nch = ld_volatile(&P.ctrl->cnt[set][kChunkCount]);
+    const unsigned long long nch = s.snap[kChunkCount];
     if (nch) {
       bc_backward_chunks(P, nch);
       if (!grid_sync(P, s, ph, kTagBcChunk)) return;
