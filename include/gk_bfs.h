@@ -147,6 +147,16 @@ GK_API gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t bet
                  int32_t strategy, int32_t* parent_out, int32_t* depth_out,
                  gk_bfs_stats* stats);
 
+/* gk_bfs over count sources (same validation, results and errors) with
+ * parents_out[i] (host, ideally pinned; may repeat or be NULL) receiving
+ * traversal i's ParentArray.  The copy of result i overlaps traversal i+1
+ * (two device parent buffers, a second stream), as the reference harness's
+ * trial loop would if it could (benchmark.hpp:178-185).  device_ms[i]
+ * (may be NULL) = CUDA-event time of traversal i's kernel. */
+GK_API gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int64_t alpha,
+                              int64_t beta, int32_t strategy, int32_t* const* parents_out,
+                              float* device_ms);
+
 /* Device pointer to the parent array of the last gk_bfs on this handle
  * (valid until the next call / free). */
 GK_API const int32_t* gk_bfs_device_parent(const gk_graph* g);

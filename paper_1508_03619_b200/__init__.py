@@ -262,6 +262,31 @@ class DeviceGraph:
     def device_parent_ptr(self) -> int:
         return int(_lib.load().gk_bfs_device_parent(self._h) or 0)
 
+    def bfs_batch(self, sources, outs=None, alpha: int = 15, beta: int = 18, strategy: int = 0) -> np.ndarray:
+        """gk_bfs_batch: one traversal per source, parent array i copied into
+        outs[i] (host int32 arrays of length n, ideally PinnedBuffer views;
+        entries may repeat or be None) while traversal i+1 runs.  Returns the
+        per-source kernel times (ms)."""
+        src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64))
+        if src.size and (src.min() < 0 or src.max() >= self.n):
+            raise ConfigError("bfs source out of range")
+        s32 = src.astype(np.uint32)
+        k = int(s32.size)
+        ptrs = (C.c_void_p * max(k, 1))()
+        if outs is not None:
+            if len(outs) != k:
+                raise ValueError("outs must have one entry per source")
+            for i, o in enumerate(outs):
+                if o is None:
+                    continue
+                if o.dtype != np.int32 or o.size != self.n or not o.flags["C_CONTIGUOUS"]:
+                    raise ValueError("each output must be a contiguous int32 array of length n")
+                ptrs[i] = o.ctypes.data
+        ms = np.zeros(max(k, 1), np.float32)
+        _check(_lib.load().gk_bfs_batch(self._h, s32.ctypes.data if k else None, k, alpha, beta, strategy,
+                                        ptrs, ms.ctypes.data), "gk_bfs_batch")
+        return ms[:k]
+
     def brandes(self, sources) -> tuple[np.ndarray, float]:
         """Betweenness scores over `sources` (gk_brandes) and the device ms."""
         src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64))

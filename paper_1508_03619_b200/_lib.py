@@ -34,6 +34,7 @@ EXPORTED = (
     "gk_shard_set_stream", "gk_shard_degree", "gk_shard_begin", "gk_shard_td_expand", "gk_shard_td_apply",
     "gk_shard_tail", "gk_shard_rescan", "gk_shard_q2b", "gk_shard_bu", "gk_shard_b2q", "gk_shard_result",
     "gk_shard_launches", "gk_bfs_verify", "gk_graph_load_sg", "gk_graph_save_sg", "gk_brandes",
+    "gk_bfs_batch",
 )
 
 
@@ -88,6 +89,7 @@ def load() -> C.CDLL:
     L.gk_bfs_verify.argtypes = [vp, u32, vp]
     L.gk_bfs_trace.argtypes = [vp, C.POINTER(C.c_uint64), C.c_char_p, i32, C.POINTER(i32)]
     L.gk_brandes.argtypes = [vp, vp, i64, vp, C.POINTER(C.c_double)]
+    L.gk_bfs_batch.argtypes = [vp, vp, i32, i64, i64, i32, vp, vp]
     L.gk_shard_last_error.restype = C.c_char_p
     L.gk_shard_generate.argtypes = [C.c_int, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(vp)]

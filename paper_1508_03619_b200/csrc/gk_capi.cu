@@ -54,6 +54,7 @@ void free_graph(gk_graph* g) {
   cudaFree(g->out_off);
   cudaFree(g->out_nb);
   cudaFree(g->parent);
+  cudaFree(g->parent2);
   cudaFree(g->depth);
   cudaFree(g->bits);
   cudaFree(g->head);
@@ -71,6 +72,7 @@ void free_graph(gk_graph* g) {
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->stream) cudaStreamDestroy(g->stream);
+  if (g->cstream) cudaStreamDestroy(g->cstream);
   delete g;
 }
 
@@ -124,6 +126,62 @@ gk_status alloc_workspace(gk_graph* g) {
     }
   }
   return GK_OK;
+}
+
+// Kernel parameters of one traversal on g (tuning knobs read from the environment).
+gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int32_t strategy,
+                          int want_depth) {
+  gk::BfsParams p{};
+  p.n = g->n;
+  p.m = g->m;
+  p.w32 = (g->n + 31) / 32;
+  p.out_off = g->out_off;
+  p.out_nb = g->out_nb;
+  p.in_off = g->in_off;
+  p.in_nb = g->in_nb;
+  p.src = source;
+  p.strategy = strategy;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.want_depth = want_depth;
+  p.front_in_smem = ((size_t)p.w32 * 4 <= g->launch.smem_front_max) ? 1 : 0;
+  p.parent = g->parent;
+  p.depth = g->depth;
+  p.visited = g->visited;
+  p.dead = g->dead;
+  p.head = g->head;
+  p.hbase = g->hbase;
+  p.bm0 = g->bm0;
+  p.bm1 = g->bm1;
+  // Large top-down steps additionally clear and fill the n/8-byte next
+  // bitmap and sum degrees in a separate pass; worth it above ~n/16 edges.
+  p.bitmap_td_min = std::max<int64_t>(4096, g->n / 16);
+  // Range passes keep each pass's slice of the next bitmap within ~64 MB of
+  // L2 (126 MB total; the rest holds visited lines, parent lines and the
+  // stream).  Measured at kron30 (128 MB bitmap): 1 pass 27.8/34.8 ms,
+  // 2 passes 23.0/27.5, 4 passes 25.8/32.5, 8 passes 29.5/38.7.
+  {
+    const int64_t budget = int64_t(64) << 20;
+    int64_t passes = (p.w32 * 4 + budget - 1) / budget;
+    if (const char* tp = getenv("GK_TD_PASSES")) passes = std::max<int64_t>(1, strtoll(tp, nullptr, 10));
+    p.td_passes = (int32_t)std::max<int64_t>(1, passes);
+    p.td_span = ((g->n + p.td_passes - 1) / p.td_passes + 31) / 32 * 32;
+  }
+  if (const char* bt = getenv("GK_BITMAP_TD_MIN")) p.bitmap_td_min = strtoll(bt, nullptr, 10);
+  p.queue = g->queue;
+  p.chunks = g->chunks;
+  p.chunk_cap = g->chunk_cap;
+  p.ctrl = g->ctrl;
+  p.steps = g->steps;
+  p.step_cap = g->step_cap;
+  p.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
+  p.stop_after = 0xffffffffu;
+  if (const char* sa = getenv("GK_STOP_AFTER")) p.stop_after = (unsigned)strtoul(sa, nullptr, 10);
+  p.exp_flags = 0;
+  if (const char* ex = getenv("GK_EXP")) p.exp_flags = (unsigned)strtoul(ex, nullptr, 10);
+
+  return p;
 }
 
 gk_status finish_graph(gk_graph* g, gk_graph** out) {
@@ -347,55 +405,7 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   if (want_depth && !g->depth)
     CK(cudaMalloc(&g->depth, sizeof(int32_t) * std::max<int64_t>(g->n, 4) + 16), "alloc depth");
 
-  gk::BfsParams p{};
-  p.n = g->n;
-  p.m = g->m;
-  p.w32 = (g->n + 31) / 32;
-  p.out_off = g->out_off;
-  p.out_nb = g->out_nb;
-  p.in_off = g->in_off;
-  p.in_nb = g->in_nb;
-  p.src = source;
-  p.strategy = strategy;
-  p.alpha = alpha;
-  p.beta = beta;
-  p.want_depth = want_depth;
-  p.front_in_smem = ((size_t)p.w32 * 4 <= g->launch.smem_front_max) ? 1 : 0;
-  p.parent = g->parent;
-  p.depth = g->depth;
-  p.visited = g->visited;
-  p.dead = g->dead;
-  p.head = g->head;
-  p.hbase = g->hbase;
-  p.bm0 = g->bm0;
-  p.bm1 = g->bm1;
-  // Large top-down steps additionally clear and fill the n/8-byte next
-  // bitmap and sum degrees in a separate pass; worth it above ~n/16 edges.
-  p.bitmap_td_min = std::max<int64_t>(4096, g->n / 16);
-  // Range passes keep each pass's slice of the next bitmap within ~64 MB of
-  // L2 (126 MB total; the rest holds visited lines, parent lines and the
-  // stream).  Measured at kron30 (128 MB bitmap): 1 pass 27.8/34.8 ms,
-  // 2 passes 23.0/27.5, 4 passes 25.8/32.5, 8 passes 29.5/38.7.
-  {
-    const int64_t budget = int64_t(64) << 20;
-    int64_t passes = (p.w32 * 4 + budget - 1) / budget;
-    if (const char* tp = getenv("GK_TD_PASSES")) passes = std::max<int64_t>(1, strtoll(tp, nullptr, 10));
-    p.td_passes = (int32_t)std::max<int64_t>(1, passes);
-    p.td_span = ((g->n + p.td_passes - 1) / p.td_passes + 31) / 32 * 32;
-  }
-  if (const char* bt = getenv("GK_BITMAP_TD_MIN")) p.bitmap_td_min = strtoll(bt, nullptr, 10);
-  p.queue = g->queue;
-  p.chunks = g->chunks;
-  p.chunk_cap = g->chunk_cap;
-  p.ctrl = g->ctrl;
-  p.steps = g->steps;
-  p.step_cap = g->step_cap;
-  p.timeout_ns = 20ull * 1000 * 1000 * 1000;
-  if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
-  p.stop_after = 0xffffffffu;
-  if (const char* sa = getenv("GK_STOP_AFTER")) p.stop_after = (unsigned)strtoul(sa, nullptr, 10);
-  p.exp_flags = 0;
-  if (const char* ex = getenv("GK_EXP")) p.exp_flags = (unsigned)strtoul(ex, nullptr, 10);
+  gk::BfsParams p = make_params(g, source, alpha, beta, strategy, want_depth);
 
   cudaStream_t s = g->stream;
   CK(cudaEventRecord(g->ev0, s), "event record");
@@ -450,6 +460,84 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
     CK(cudaMemcpyAsync(depth_out, g->depth, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, s), "D2H depth");
   if (parent_out || depth_out) CK(cudaStreamSynchronize(s), "D2H");
   return GK_OK;
+}
+
+// Many traversals with their parent arrays returned to host memory: the
+// D2H copy of traversal i (on a second stream) overlaps traversal i+1 (two
+// device parent buffers), so a run is bound by max(kernel, copy) per
+// source instead of their sum.  Same validation and results as gk_bfs.
+gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int64_t alpha, int64_t beta,
+                       int32_t strategy, int32_t* const* parents_out, float* device_ms) {
+  if (!g) return fail(GK_ERR_INVALID, "null graph");
+  if (count < 0 || (count > 0 && !sources)) return fail(GK_ERR_INVALID, "null argument");
+  for (int32_t i = 0; i < count; i++)
+    if ((int64_t)sources[i] >= g->n) return fail(GK_ERR_SOURCE_RANGE, "bfs source out of range");
+  if (alpha <= 0 || beta <= 0) return fail(GK_ERR_BAD_PARAM, "bfs alpha and beta must be positive");
+  if (strategy < 0 || strategy > 2) return fail(GK_ERR_BAD_PARAM, "unknown bfs strategy");
+  if (count == 0) return GK_OK;
+  std::lock_guard<std::mutex> lock(g->mu);
+  CK(cudaSetDevice(g->device), "cudaSetDevice");
+  if (!g->parent2) CK(cudaMalloc(&g->parent2, sizeof(int32_t) * std::max<int64_t>(g->n, 4) + 16), "alloc parent");
+  if (!g->cstream) CK(cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking), "stream");
+  cudaStream_t s = g->stream, cs = g->cstream;
+  std::vector<cudaEvent_t> ev(2 * (size_t)count + 4, nullptr);
+  int* errs = nullptr;
+  gk_status st = GK_OK;
+  auto cleanup = [&]() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (errs) cudaFreeHost(errs);
+  };
+  for (auto& e : ev)
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      cleanup();
+      return fail(GK_ERR_CUDA, "event create");
+    }
+  if (cudaHostAlloc(&errs, sizeof(int) * count, cudaHostAllocDefault) != cudaSuccess) {
+    cleanup();
+    return fail(GK_ERR_CUDA, "cudaHostAlloc");
+  }
+  cudaEvent_t* kdone = &ev[2 * (size_t)count];  // [2] kernel of slot done
+  cudaEvent_t* cdone = kdone + 2;               // [2] copy of slot done
+  int32_t* buf[2] = {g->parent, g->parent2};
+  g->last_valid = 0;
+  g->depth_valid = 0;
+  cudaError_t e = cudaSuccess;
+  for (int32_t i = 0; i < count && e == cudaSuccess; i++) {
+    const int slot = i & 1;
+    gk::BfsParams p = make_params(g, sources[i], alpha, beta, strategy, 0);
+    p.parent = buf[slot];
+    if (i >= 2 && (e = cudaStreamWaitEvent(s, cdone[slot], 0))) break;  // copy of i-2 has left buf
+    if ((e = cudaEventRecord(ev[2 * i], s))) break;
+    if ((e = cudaMemsetAsync(g->ctrl, 0, sizeof(gk::Ctrl), s))) break;
+    if ((e = gk::bfs_launch(p, g->launch, s))) break;
+    if ((e = cudaEventRecord(ev[2 * i + 1], s))) break;
+    if ((e = cudaMemcpyAsync(errs + i, &g->ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;
+    if ((e = cudaEventRecord(kdone[slot], s))) break;
+    if ((e = cudaStreamWaitEvent(cs, kdone[slot], 0))) break;
+    if (parents_out && parents_out[i] &&
+        (e = cudaMemcpyAsync(parents_out[i], buf[slot], sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, cs)))
+      break;
+    if ((e = cudaEventRecord(cdone[slot], cs))) break;
+  }
+  cudaError_t e2 = cudaStreamSynchronize(s), e3 = cudaStreamSynchronize(cs);
+  if (e == cudaSuccess) e = e2 != cudaSuccess ? e2 : e3;
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(GK_ERR_CUDA, std::string("bfs batch: ") + cudaGetErrorString(e));
+  }
+  for (int32_t i = 0; i < count && st == GK_OK; i++) {
+    if (errs[i] == 2) st = fail(GK_ERR_TIMEOUT, "bfs kernel watchdog fired (grid barrier timeout)");
+    else if (errs[i]) st = fail(GK_ERR_CUDA, "bfs kernel: heavy-chunk buffer overflow");
+    if (device_ms && st == GK_OK) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]);
+      device_ms[i] = ms;
+    }
+  }
+  if ((count - 1) & 1) std::swap(g->parent, g->parent2);  // g->parent = the last result
+  cleanup();
+  return st;
 }
 
 const int32_t* gk_bfs_device_parent(const gk_graph* g) { return g ? g->parent : nullptr; }

@@ -212,6 +212,8 @@ struct gk_graph {
   int32_t keep_depth = 0;
   int32_t depth_valid = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t cstream = nullptr;  // D2H stream of gk_bfs_batch (created on first use)
+  int32_t* parent2 = nullptr;      // second parent buffer of gk_bfs_batch's 2-deep pipeline
   cudaEvent_t ev0 = nullptr;
   cudaEvent_t ev1 = nullptr;
   gk::BfsLaunch launch;

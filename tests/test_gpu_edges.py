@@ -107,3 +107,28 @@ def test_handle_state_across_kernels():
     for s, d in zip(srcs, first):
         r = check(g, dg, s)
         assert (r.depth == d).all()
+
+
+def test_batch_matches_single_calls():
+    # gk_bfs_batch: per-source results identical in depth, all parents valid,
+    # copies overlapped with the next traversal
+    from paper_1508_03619_b200 import ConfigError, PinnedBuffer
+    g = O.make_graph("kron", 14, permute=True)
+    dg = DeviceGraph.from_csr(g)
+    srcs = [int(s) for s in O.pick_sources(g, 7)]
+    outs = [np.empty(g.n, np.int32) for _ in srcs]
+    ms = dg.bfs_batch(srcs, outs)
+    assert ms.shape == (7,) and (ms > 0).all()
+    for s, p in zip(srcs, outs):
+        ok, msg = O.verify_bfs(g, s, p)
+        assert ok, msg
+    # repeated pinned buffers (the bench's use): the last result lands last
+    pins = [PinnedBuffer(g.n), PinnedBuffer(g.n)]
+    dg.bfs_batch(srcs, [pins[i & 1].array for i in range(len(srcs))])
+    assert O.verify_bfs(g, srcs[-1], pins[0].array)[0] and O.verify_bfs(g, srcs[-2], pins[1].array)[0]
+    # the handle's device parent is the last traversal's
+    r = dg.bfs(srcs[0])
+    assert O.verify_bfs(g, srcs[0], r.parent)[0]
+    with pytest.raises(ConfigError, match="bfs source out of range"):
+        dg.bfs_batch([0, g.n])
+    assert dg.bfs_batch([]).size == 0
