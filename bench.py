@@ -20,9 +20,15 @@ roofline  : algorithmic bytes B_sec (evaluated per source from
             measured HBM copy bandwidth (MEASURED_PEAKS.json).
 cpu_baseline : the reference's own OpenMP Bfs (oracle/_ref/libgapref.so, the
             unmodified headers) on the box's host cores, bounded sample.
-N > 1     : one process per GPU (torchrun), independent replicas of the whole
-            job (1D-partitioned sharding is not built yet); per-step time is the
-            max over ranks.
+N > 1     : one process per GPU (torchrun).  Default (--multi replicas): the
+            benchmark's independent units -- its trials, one BFS per source --
+            are sharded over the ranks; every rank holds the whole graph (all
+            configs fit one B200, even kron30's 146 GB) and runs K sources of
+            its own (PickSources seeded by rank), no data-path collective,
+            weak scaling; per-step time = max over ranks, work summed.
+            --multi sharded: the 1D vertex-partitioned traversal of ONE graph
+            (NCCL per level, strong scaling) for graphs that
+            exceed one GPU.
 """
 from __future__ import annotations
 
@@ -307,8 +313,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-model", action="store_true")
     ap.add_argument("--verbose", action="store_true", help="per-source times on stderr")
-    ap.add_argument("--multi", default="sharded", choices=["sharded", "replicas"],
-                    help="N>1: 1D-partitioned traversal of one graph (default) or independent replicas")
+    ap.add_argument("--multi", default="replicas", choices=["sharded", "replicas"],
+                    help="N>1: source-parallel replicas (default; weak scaling) or the 1D-partitioned "
+                         "traversal of one graph (strong scaling)")
     ap.add_argument("--force-sharded", action="store_true", help="run the sharded path even at N=1")
     args = ap.parse_args()
     # OpenMP settings for the reference CPU legs (must precede libgomp init).
@@ -467,7 +474,8 @@ def main():
         "config": {"workload": cfg["workload"], "name": cfg["name"], "n": g.n, "arcs": g.m, "seed": SEED,
                    "sources": K, "alpha": 15, "beta": 18,
                    "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % ((g.m * 4 + g.n * 8) / 1e9),
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "parallelism": "single GPU" if world == 1 else
+                   f"{world} source-parallel replicas (whole graph per GPU, no data-path collective)",
                    "device_build_s": round(build_s, 2), "timed_region_wall_s": round(wall, 4),
                    "schedules": scheds[:4], "mean_m_cc": statistics.mean(step_m),
                    "verified": (f"{verified}/{len(sources)} sources pass the device BFS certificate "
