@@ -738,22 +738,32 @@ __global__ void __launch_bounds__(kSB) k_sh_bu_long(ShardParams P, const uint32_
 }
 
 // Queue from the owned slice of the front (BitmapToQueue, bfs.hpp:99-113).
-__global__ void k_sh_b2q(ShardParams P, const uint32_t* slice) {
+__global__ void __launch_bounds__(kSB) k_sh_b2q(ShardParams P, const uint32_t* slice) {
+  // warp prefix sum of popcounts, one fetch-add per warp; entries in vertex order
   const long long w32 = (P.nloc + 31) / 32;
-  int overflow = 0;
-  for (long long w0 = (long long)blockIdx.x * blockDim.x; w0 < w32; w0 += (long long)gridDim.x * blockDim.x) {
-    const long long w = w0 + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  for (long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) & ~31ll; w0 < w32;
+       w0 += (long long)gridDim.x * blockDim.x) {
+    const long long w = w0 + lane;
     uint32_t word = w < w32 ? __ldcg(slice + w) : 0u;
-    // one warp-aggregated append per set bit round
-    while (__ballot_sync(kFullMask, word != 0)) {
-      const bool has = word != 0;
-      uint32_t v = 0;
-      if (has) {
-        const int bp = __ffs(word) - 1;
-        word &= word - 1;
-        v = (uint32_t)(P.lo + w * 32 + bp);
-      }
-      warp_append<uint32_t>(has, v, P.queue, &P.ctr[cTail], P.nloc + 1, &overflow);
+    const int cnt = __popc(word);
+    int incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFullMask, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(kFullMask, incl, 31);
+    if (total == 0) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&P.ctr[cTail], (unsigned long long)total);
+    base = __shfl_sync(kFullMask, base, 0);
+    unsigned long long q = base + incl - cnt;
+    while (word) {
+      const int bp = __ffs(word) - 1;
+      word &= word - 1;
+      if ((int64_t)q < P.nloc + 1) P.queue[q] = (uint32_t)(P.lo + w * 32 + bp);
+      else atomicExch((unsigned*)&P.ctr[7], 1u);
+      q++;
     }
   }
 }
@@ -1047,7 +1057,9 @@ GK_API gk_status gk_shard_td_expand(gk_shard* s, uint64_t qs, uint64_t qe, int32
   SCK(cudaMemsetAsync(s->ctr + gk::cScout, 0, sizeof(unsigned long long) * 2, s->stream), "memset");
   SCK(cudaMemsetAsync(s->ctr + gk::cChunks, 0, sizeof(unsigned long long), s->stream), "memset");
   SCK(cudaMemsetAsync(s->ctr + gk::cDest, 0, sizeof(unsigned long long) * P, s->stream), "memset");
-  if (dedup) SCK(cudaMemsetAsync(s->sent, 0, sizeof(uint32_t) * ((s->n + 31) / 32), s->stream), "memset");
+  // one rank has no remote targets: no sent-bitmap to clear or probe
+  p.dedup = (dedup && s->nranks > 1) ? 1 : 0;
+  if (p.dedup) SCK(cudaMemsetAsync(s->sent, 0, sizeof(uint32_t) * ((s->n + 31) / 32), s->stream), "memset");
   // large steps (the orchestrator's dedup threshold = the persistent
   // kernel's "big" threshold): owned claims go to next := visited
   s->big = dedup ? 1 : 0;
