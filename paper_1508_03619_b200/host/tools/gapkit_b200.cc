@@ -1,10 +1,13 @@
-// gapkit_b200 -- BFS benchmark CLI on the B200 (the reference's `gapkit bfs`
-// subcommand, tools/gapkit.cc:47-152, with a hand-rolled parser because
-// CLI11 is not vendored).
+// gapkit_b200 -- benchmark CLI on the B200 (the reference's `gapkit bfs` and
+// `gapkit bc` subcommands, tools/gapkit.cc:47-152, 232-260, with a
+// hand-rolled parser because CLI11 is not vendored).
 //
-//   gapkit_b200 bfs (-f FILE.sg | -g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS]
-//               [-r SOURCE] [-v] [--seed S] [--no-permute] [--host-build]
+//   gapkit_b200 bfs|bc (-f FILE.sg | -g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS]
+//               [-r SOURCE] [-i SOURCES_PER_TRIAL] [-v] [--seed S] [--no-permute] [--host-build]
 //               [--threads T] [-o FILE.csv]
+//
+// bc follows the reference's plan (benchmark.hpp:75): 16 trials x 4 sources
+// by default, -i sets the sources per trial.
 //
 // -g/-u generate a Kronecker / uniform graph (generator.hpp:56-112) and build
 // it symmetrized (gapkit.cc:89-96); Kronecker IDs are permuted (BASELINE
@@ -19,6 +22,7 @@
 #include <iostream>
 #include <string>
 
+#include "gapkit_b200/betweenness.hpp"
 #include "gapkit_b200/bfs.hpp"
 #include "gapkit_b200/builder.hpp"
 #include "gapkit_b200/generator.hpp"
@@ -33,8 +37,9 @@ namespace {
 
 int Usage(const char* argv0) {
   std::fprintf(stderr,
-               "usage: %s bfs (-f FILE.sg | -g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS] [-r SOURCE]\n"
-               "          [-v] [--seed S] [--no-permute] [--host-build] [--threads T] [-o FILE.csv]\n",
+               "usage: %s bfs|bc (-f FILE.sg | -g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS]\n"
+               "          [-r SOURCE] [-i SOURCES_PER_TRIAL] [-v] [--seed S] [--no-permute] [--host-build]\n"
+               "          [--threads T] [-o FILE.csv]\n",
                argv0);
   return 2;
 }
@@ -48,8 +53,9 @@ bool ParseInt(const char* s, long long* out) {
 }  // namespace
 
 int main(int argc, char** argv) {
-  if (argc < 2 || std::strcmp(argv[1], "bfs") != 0) return Usage(argv[0]);
-  long long kron = -1, urand = -1, degree = 16, trials = 64, fixed = -1, threads = 0;
+  if (argc < 2 || (std::strcmp(argv[1], "bfs") != 0 && std::strcmp(argv[1], "bc") != 0)) return Usage(argv[0]);
+  const bool bc = std::strcmp(argv[1], "bc") == 0;
+  long long kron = -1, urand = -1, degree = 16, trials = bc ? 16 : 64, fixed = -1, threads = 0, per_trial = 4;
   long long rows = 0, cols = 0;
   unsigned long long seed = gapkit::kDefaultSeed;
   bool verify = false, permute = true, host_build = false;
@@ -66,6 +72,7 @@ int main(int argc, char** argv) {
     else if (a == "-u" || a == "--urand") need(&urand);
     else if (a == "-k" || a == "--degree") need(&degree);
     else if (a == "-n") need(&trials);
+    else if (a == "-i") need(&per_trial);
     else if (a == "-r") need(&fixed);
     else if (a == "--threads") need(&threads);
     else if (a == "--seed") {
@@ -122,6 +129,30 @@ int main(int argc, char** argv) {
       } else {
         g = gapkit::GenerateOnDevice(spec, perm);
       }
+    }
+    if (bc) {  // gapkit.cc:99-121 with the bc row of the plan
+      if (trials < 1 || per_trial < 1) throw gapkit::ConfigError("bc needs at least one trial and one source");
+      std::string failure;
+      std::vector<gapkit::BcTrial> tr =
+          gapkit::RunBetweenness(g, static_cast<int>(trials), static_cast<int>(per_trial), seed, verify, &failure);
+      bool all_ok = true;
+      double dev = 0;
+      for (const auto& t : tr) {
+        all_ok &= !t.verified.has_value() || *t.verified;
+        dev += t.device_ms;
+      }
+      if (!output.empty()) {
+        std::ofstream out(output);
+        if (!out) throw gapkit::ConfigError("cannot open output file: " + output);
+        gapkit::WriteBcCsv(out, name, tr);
+      } else {
+        gapkit::WriteBcCsv(std::cout, name, tr);
+      }
+      std::printf("%s: n=%lld arcs=%lld bc trials=%zu x %lld sources, mean %.3f ms device per trial%s\n",
+                  name.c_str(), static_cast<long long>(g.num_nodes()), static_cast<long long>(g.num_edges()),
+                  tr.size(), per_trial, dev / tr.size(),
+                  verify ? (all_ok ? ", all verified" : (", VERIFY FAILED: " + failure).c_str()) : "");
+      return verify && !all_ok ? 1 : 0;
     }
     gapkit::BenchPlan plan;  // gapkit.cc:99-121
     plan.trials = static_cast<int>(trials);

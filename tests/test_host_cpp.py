@@ -113,3 +113,23 @@ def test_cli_fixed_source_and_host_build(tools, tmp_path):
         return
     assert r.returncode == 0, r.stderr
     assert all(l.split(",")[3] == "1" for l in out.read_text().strip().splitlines()[1:])
+
+
+@pytest.mark.gpu
+def test_cli_bc_verified(tools, tmp_path):
+    # the reference's bc row: trials x sources-per-trial, -v checks every trial
+    # with the serial predecessor-list Brandes (verify.hpp:216-270)
+    out = tmp_path / "bc.csv"
+    r = run(tools[1], "bc", "-g", "11", "-n", "3", "-i", "4", "-v", "-o", out)
+    assert r.returncode == 0, r.stderr
+    assert "all verified" in r.stdout
+    lines = out.read_text().strip().splitlines()
+    assert lines[0] == "kernel,graph,trial,source,elapsed_seconds,verified"
+    rows = [l.split(",") for l in lines[1:]]
+    assert len(rows) == 4 and rows[-1][2] == "summary"
+    assert all(row[0] == "bc" and len(row[3].split(";")) == 4 and row[5] == "1" for row in rows[:-1])
+
+
+def test_cli_bc_usage(tools):
+    assert run(tools[1], "bc").returncode == 2
+    assert run(tools[1], "bc", "-g", "8", "-i", "x").returncode == 2
