@@ -437,9 +437,12 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       }
       claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt, tiny, rlo, rhi);
     }
-    if (threadIdx.x == 0 && start + tile_sz < qe) s.bcast[1] = gridDim.x + atomicAdd(&cnt[kTile], 1ull);
+    // Dynamic tiles only exist past the first gridDim.x; when there are no
+    // more tiles than CTAs, nobody pays the fetch-add round trip.
+    const bool more = qs + (unsigned long long)gridDim.x * tile_sz < qe && start + tile_sz < qe;
+    if (threadIdx.x == 0 && more) s.bcast[1] = gridDim.x + atomicAdd(&cnt[kTile], 1ull);
     __syncthreads();
-    if (start + tile_sz >= qe) break;  // every later tile starts past qe too
+    if (!more) break;  // every later tile starts past qe too
     tile = s.bcast[1];
     __syncthreads();
   }
