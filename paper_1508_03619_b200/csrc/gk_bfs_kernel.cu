@@ -1111,7 +1111,7 @@ __device__ __forceinline__ void bc_edges4(const BfsParams& P, const QApp& qa, co
   for (int k = 0; k < 4; k++) {
     if (dv[k] == lvl) {  // betweenness.hpp:66-69
       atomicOr(P.bc_succ + (e[k] >> 5), 1u << (e[k] & 31));
-      atomicAdd(P.bc_sigma + v[k], su[k]);
+      atomicAdd(&P.bc_sd[v[k]].x, su[k]);
     }
   }
 #pragma unroll
@@ -1135,7 +1135,7 @@ __device__ void bc_forward_light(const BfsParams& P, SmemT& s, unsigned ph, cons
     if (i < qe) {
       u = __ldcg(P.queue + i);
       b = P.out_off[u];
-      su = __ldcg(P.bc_sigma + u);
+      su = __ldcg(&P.bc_sd[u].x);
       const int64_t d = P.out_off[u + 1] - b;
       if (d > kBcChunk) {
         const int64_t nch = (d + kBcChunk - 1) / kBcChunk;
@@ -1200,7 +1200,7 @@ __device__ void bc_forward_heavy(const BfsParams& P, const QApp& qa, unsigned lo
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
   for (unsigned long long c = gw; c < nch; c += nw) {
     const Chunk ch = P.chunks[c];
-    const double su = __ldcg(P.bc_sigma + ch.u);
+    const double su = __ldcg(&P.bc_sd[ch.u].x);
     const double sg[4] = {su, su, su, su};
     for (uint32_t o = 0; o < ch.len; o += 128) {
       uint32_t v[4];
@@ -1220,7 +1220,8 @@ __device__ void bc_forward_heavy(const BfsParams& P, const QApp& qa, unsigned lo
 
 // sigma[u]/sigma[v] * (1 + delta[v]) for a flagged edge (betweenness.hpp:115)
 __device__ __forceinline__ double bc_term(const BfsParams& P, double su, uint32_t v) {
-  return (su / __ldcg(P.bc_sigma + v)) * (1.0 + __ldcg(P.bc_delta + v));
+  const double2 sd = __ldcg(P.bc_sd + v);  // sigma and delta in one 16-byte access
+  return (su / sd.x) * (1.0 + sd.y);
 }
 
 // Backward pass A over one level's vertices queue[b0, b1): tiles of kBlock
@@ -1244,7 +1245,7 @@ __device__ void bc_backward_level(const BfsParams& P, SmemT& s, unsigned ph, uns
     if (i < b1) {
       u = __ldcg(P.queue + i);
       b = P.out_off[u];
-      su = __ldcg(P.bc_sigma + u);
+      su = __ldcg(&P.bc_sd[u].x);
       const int64_t d = P.out_off[u + 1] - b;
       if (d > kBcChunk) {
         heavy = true;
@@ -1300,15 +1301,16 @@ __device__ void bc_backward_level(const BfsParams& P, SmemT& s, unsigned ph, uns
       double sv[4], dv[4];
 #pragma unroll
       for (int k = 0; k < 4; k++) {
-        sv[k] = f[k] ? __ldcg(P.bc_sigma + v[k]) : 1.0;
-        dv[k] = f[k] ? __ldcg(P.bc_delta + v[k]) : 0.0;
+        const double2 sd = f[k] ? __ldcg(P.bc_sd + v[k]) : make_double2(1.0, 0.0);
+        sv[k] = sd.x;
+        dv[k] = sd.y;
       }
 #pragma unroll
       for (int k = 0; k < 4; k++)
         if (f[k]) atomicAdd(acc + lo[k], (s.bc_sig[lo[k]] / sv[k]) * (1.0 + dv[k]));
     }
     __syncthreads();
-    if (i < b1 && !heavy) P.bc_delta[u] = acc[threadIdx.x];
+    if (i < b1 && !heavy) P.bc_sd[u].y = acc[threadIdx.x];
     __syncthreads();
   }
 }
@@ -1320,7 +1322,7 @@ __device__ void bc_backward_chunks(const BfsParams& P, unsigned long long nch) {
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
   for (unsigned long long c = gw; c < nch; c += nw) {
     const Chunk ch = P.chunks[c];
-    const double su = __ldcg(P.bc_sigma + ch.u);
+    const double su = __ldcg(&P.bc_sd[ch.u].x);
     double acc = 0.0;
     for (uint32_t j = lane; j < ch.len; j += 32) {
       const int64_t e = ch.start + j;
@@ -1328,7 +1330,7 @@ __device__ void bc_backward_chunks(const BfsParams& P, unsigned long long nch) {
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
-    if (lane == 0 && acc != 0.0) atomicAdd(P.bc_delta + ch.u, acc);
+    if (lane == 0 && acc != 0.0) atomicAdd(&P.bc_sd[ch.u].y, acc);
   }
 }
 
@@ -1342,15 +1344,14 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
   // init (betweenness.hpp:96-101)
   for (long long i = gtid; i < P.n; i += gthreads) {
     P.depth[i] = -1;
-    P.bc_sigma[i] = 0.0;
-    P.bc_delta[i] = 0.0;
+    P.bc_sd[i] = make_double2(0.0, 0.0);
   }
   const long long sw = (P.m + 31) >> 5;
   for (long long i = gtid; i < sw; i += gthreads) P.bc_succ[i] = 0u;
   if (!grid_sync(P, s, ph, kTagInit)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // betweenness.hpp:44-48
     P.depth[src] = 0;
-    P.bc_sigma[src] = 1.0;
+    P.bc_sd[src].x = 1.0;
     P.queue[0] = src;
     P.bc_bounds[0] = 0;
   }
@@ -1401,7 +1402,7 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
   // betweenness.hpp:118-119
   for (unsigned long long i = gtid; i < qtail; i += gthreads) {
     const uint32_t u = __ldcg(P.queue + i);
-    if (u != src) P.bc_scores[u] += static_cast<float>(__ldcg(P.bc_delta + u));
+    if (u != src) P.bc_scores[u] += static_cast<float>(__ldcg(&P.bc_sd[u].y));
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->num_steps = lvl;
 }

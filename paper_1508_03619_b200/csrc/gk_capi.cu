@@ -58,8 +58,7 @@ void free_graph(gk_graph* g) {
   cudaFree(g->depth);
   cudaFree(g->bits);
   cudaFree(g->head);
-  cudaFree(g->bc_sigma);
-  cudaFree(g->bc_delta);
+  cudaFree(g->bc_sd);
   cudaFree(g->bc_succ);
   cudaFree(g->bc_scores);
   cudaFree(g->bc_bounds);
@@ -608,9 +607,8 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
   }
   const int64_t n = g->n;
   if (!g->depth) CK(cudaMalloc(&g->depth, sizeof(int32_t) * std::max<int64_t>(n, 4) + 16), "alloc depth");
-  if (!g->bc_sigma) {
-    CK(cudaMalloc(&g->bc_sigma, sizeof(double) * std::max<int64_t>(n, 1)), "alloc sigma");
-    CK(cudaMalloc(&g->bc_delta, sizeof(double) * std::max<int64_t>(n, 1)), "alloc delta");
+  if (!g->bc_sd) {
+    CK(cudaMalloc(&g->bc_sd, sizeof(double2) * std::max<int64_t>(n, 1)), "alloc sigma/delta");
     CK(cudaMalloc(&g->bc_succ, sizeof(uint32_t) * ((g->m + 31) / 32 + 1)), "alloc successor bitmap");
     CK(cudaMalloc(&g->bc_scores, sizeof(float) * std::max<int64_t>(n, 1) + 16), "alloc scores");
     g->bc_bounds_cap = n + 2;
@@ -636,8 +634,7 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
   p.timeout_ns = 20ull * 1000 * 1000 * 1000;
   if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
   p.stop_after = 0xffffffffu;
-  p.bc_sigma = g->bc_sigma;
-  p.bc_delta = g->bc_delta;
+  p.bc_sd = g->bc_sd;
   p.bc_succ = g->bc_succ;
   p.bc_scores = g->bc_scores;
   p.bc_bounds = g->bc_bounds;

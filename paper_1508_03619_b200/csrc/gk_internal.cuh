@@ -112,8 +112,7 @@ struct BfsParams {
   int32_t td_passes;    // large top-down steps: target-range passes (1 when next fits L2)
   int64_t td_span;      // ids per pass (multiple of 32)
   // Brandes (betweenness.hpp:38-80), bc_persistent only
-  double* bc_sigma;     // shortest-path counts
-  double* bc_delta;     // dependencies
+  double2* bc_sd;       // per vertex {shortest-path count sigma, dependency delta}
   uint32_t* bc_succ;    // one bit per stored arc: shortest-path successor edge
   float* bc_scores;     // accumulated over sources
   int64_t* bc_bounds;   // level d = queue[bounds[d], bounds[d+1])
@@ -196,8 +195,7 @@ struct gk_graph {
   gk::HeadRec* head = nullptr;  // ditto: the first kHead entries of every live in-list
   uint32_t* hbase = nullptr; // ditto: head index of each word's first live vertex
   // Brandes workspace, allocated on first use
-  double* bc_sigma = nullptr;
-  double* bc_delta = nullptr;
+  double2* bc_sd = nullptr;
   uint32_t* bc_succ = nullptr;
   float* bc_scores = nullptr;
   int64_t* bc_bounds = nullptr;
