@@ -1105,6 +1105,7 @@ __device__ __forceinline__ void bc_edges4(const BfsParams& P, const QApp& qa, co
       const int old = atomicCAS(P.depth + v[k], -1, lvl);
       cl[k] = old == -1;
       dv[k] = cl[k] ? lvl : old;
+      if (cl[k] && P.bc_lv) atomicOr(P.visited + (v[k] >> 5), 1u << (v[k] & 31u));  // for pull steps
     }
   }
 #pragma unroll
@@ -1231,7 +1232,7 @@ __device__ __forceinline__ double bc_term(const BfsParams& P, double su, uint32_
 // Vertices of degree > kBcChunk are cut into chunks for pass B (their delta
 // stays 0 here and collects the chunk partials).
 __device__ void bc_backward_level(const BfsParams& P, SmemT& s, unsigned ph, unsigned long long b0,
-                                  unsigned long long b1) {
+                                  unsigned long long b1, const uint32_t* lvb) {
   double* acc = reinterpret_cast<double*>(&s.td.qbuf[0][0]);  // kBlock doubles (qbuf unused here)
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
   for (unsigned long long tile = blockIdx.x;; tile += gridDim.x) {
@@ -1292,12 +1293,16 @@ __device__ void bc_backward_level(const BfsParams& P, SmemT& s, unsigned ph, uns
           }
           lo[k] = l;
           e[k] = s.td.t_b[l] + (ei - s.td.t_pre[l]);
-          f[k] = (__ldcg(P.bc_succ + (e[k] >> 5)) >> (e[k] & 31)) & 1u;
+          f[k] = lvb ? true : ((__ldcg(P.bc_succ + (e[k] >> 5)) >> (e[k] & 31)) & 1u);
         }
       }
       uint32_t v[4];
 #pragma unroll
       for (int k = 0; k < 4; k++) v[k] = f[k] ? __ldg(P.out_nb + e[k]) : 0u;
+      if (lvb) {  // level d+1 was found by a pull step: successor = member of its bitmap
+#pragma unroll
+        for (int k = 0; k < 4; k++) f[k] = f[k] && ((__ldcg(lvb + (v[k] >> 5)) >> (v[k] & 31u)) & 1u);
+      }
       double sv[4], dv[4];
 #pragma unroll
       for (int k = 0; k < 4; k++) {
@@ -1316,7 +1321,7 @@ __device__ void bc_backward_level(const BfsParams& P, SmemT& s, unsigned ph, uns
 }
 
 // Backward pass B: chunks of the level's high-degree vertices.
-__device__ void bc_backward_chunks(const BfsParams& P, unsigned long long nch) {
+__device__ void bc_backward_chunks(const BfsParams& P, unsigned long long nch, const uint32_t* lvb) {
   const unsigned lane = lane_id();
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
@@ -1326,11 +1331,100 @@ __device__ void bc_backward_chunks(const BfsParams& P, unsigned long long nch) {
     double acc = 0.0;
     for (uint32_t j = lane; j < ch.len; j += 32) {
       const int64_t e = ch.start + j;
-      if ((__ldcg(P.bc_succ + (e >> 5)) >> (e & 31)) & 1u) acc += bc_term(P, su, __ldg(P.out_nb + e));
+      if (lvb) {
+        const uint32_t v = __ldg(P.out_nb + e);
+        if ((__ldcg(lvb + (v >> 5)) >> (v & 31u)) & 1u) acc += bc_term(P, su, v);
+      } else if ((__ldcg(P.bc_succ + (e >> 5)) >> (e & 31)) & 1u) {
+        acc += bc_term(P, su, __ldg(P.out_nb + e));
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
     if (lane == 0 && acc != 0.0) atomicAdd(&P.bc_sd[ch.u].y, acc);
+  }
+}
+
+// Forward level found bottom-up (§8(f)-4's "TD/BU machinery" for Brandes):
+// every unvisited live vertex v sums sigma over ALL its in-neighbours in the
+// front (no early exit: sigma needs every shortest-path predecessor); v
+// joins the level when it has one.  Tiles of kBlock consecutive vertices,
+// CTA scan of the pending vertices' in-degrees, 4 in-edges per thread in
+// flight, per-vertex sums in shared memory.  The level's membership goes to
+// a bitmap (lv) that the backward pass uses as its successor test; sigma is
+// an integer count, so the summation order does not change it.
+__device__ void bc_pull_level(const BfsParams& P, SmemT& s, const QApp& qa, int lvl, const uint32_t* front,
+                              uint32_t* lv, int& qcnt, long long& found) {
+  uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
+  double* acc = s.bc_sig;
+  uint32_t* hit = s.td.t_u;
+  const long long ntiles = (P.n + kBlock - 1) / kBlock;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long v = tile * kBlock + threadIdx.x;
+    bool pend = false;
+    uint32_t vis = 0xffffffffu;
+    int64_t b = 0, dl = 0;
+    if (v < P.n) {
+      const long long w = v >> 5;
+      vis = __ldcg(P.visited + w) | __ldg(P.dead + w);
+      pend = !((vis >> (v & 31)) & 1u);
+      if (pend) {
+        b = P.in_off[v];
+        dl = P.in_off[v + 1] - b;
+      }
+    }
+    s.td.t_b[threadIdx.x] = b;
+    acc[threadIdx.x] = 0.0;
+    hit[threadIdx.x] = 0u;
+    int64_t tot;
+    const int64_t pre = block_exscan(dl, &tot, s);
+    s.td.t_pre[threadIdx.x] = pre;
+    __syncthreads();
+    for (int64_t eb = 0; eb < tot; eb += 4 * kBlock) {
+      uint32_t u[4];
+      int lo[4];
+      bool ok[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int64_t ei = eb + k * kBlock + threadIdx.x;
+        ok[k] = ei < tot;
+        lo[k] = 0;
+        u[k] = 0;
+        if (ok[k]) {
+          int l = 0, h = kBlock - 1;
+          while (l < h) {
+            const int mid = (l + h + 1) >> 1;
+            if (s.td.t_pre[mid] <= ei) l = mid;
+            else h = mid - 1;
+          }
+          lo[k] = l;
+          u[k] = ld_nb(P.in_nb + s.td.t_b[l] + (ei - s.td.t_pre[l]));
+        }
+      }
+      bool f[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) f[k] = ok[k] && ((ld_front(front + (u[k] >> 5)) >> (u[k] & 31u)) & 1u);
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        if (f[k]) {
+          atomicAdd(acc + lo[k], __ldcg(&P.bc_sd[u[k]].x));
+          hit[lo[k]] = 1u;
+        }
+      }
+    }
+    __syncthreads();
+    const bool got = pend && hit[threadIdx.x];
+    if (got) {
+      P.depth[v] = lvl;
+      P.bc_sd[v].x = acc[threadIdx.x];
+    }
+    const unsigned m = __ballot_sync(kFull, got);
+    if ((threadIdx.x & 31) == 0 && v < P.n) {  // tiles are word-aligned: one writer per word
+      lv[v >> 5] = m;
+      if (m) P.visited[v >> 5] = vis | m;
+      found += __popc(m);
+    }
+    wq_push(P, qa, got, (uint32_t)v, buf, qcnt);
+    __syncthreads();
   }
 }
 
@@ -1348,54 +1442,107 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
   }
   const long long sw = (P.m + 31) >> 5;
   for (long long i = gtid; i < sw; i += gthreads) P.bc_succ[i] = 0u;
+  if (P.bc_lv)
+    for (long long i = gtid; i < P.w32; i += gthreads) P.visited[i] = __ldg(P.dead + i);
   if (!grid_sync(P, s, ph, kTagInit)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // betweenness.hpp:44-48
     P.depth[src] = 0;
     P.bc_sd[src].x = 1.0;
     P.queue[0] = src;
     P.bc_bounds[0] = 0;
+    if (P.bc_lv) P.visited[src >> 5] |= 1u << (src & 31u);
   }
   if (!grid_sync(P, s, ph, kTagInit)) return;
   unsigned long long qs = 0, qe = 1, qtail = 1;
   int lvl = 0;
   int qcnt = 0;
+  int npull = 0;
+  const uint32_t* prev_lv = nullptr;  // bitmap of the previous level when it was pulled
+  long long nvis = 1;
+  constexpr long long kBcPullRatio = 15;  // pull when the frontier exceeds 1/15 of the unvisited ids
   while (qe > qs) {  // forward levels
     lvl++;
     if (lvl + 1 >= P.bc_bounds_cap) {
       if (threadIdx.x == 0) atomicExch(&P.ctrl->error, 4);
       return;
     }
-    unsigned set = ph & 3;
-    {
-      const QApp qa = qapp(P, ph, qtail);
-      bc_forward_light(P, s, ph, qa, qs, qe, lvl, qcnt);
-      wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+    const long long fsize = (long long)(qe - qs);
+    bool pull = P.bc_lv && npull < kBcMaxPull && fsize * kBcPullRatio > P.n - nvis;
+    if (P.bc_lv && npull < kBcMaxPull && !pull && fsize > kBlock) {
+      // a few high-degree vertices can hold most edges: decide by the
+      // frontier's degree sum against the arcs (BFS's alpha rule, bfs.hpp:144)
+      long long dsum = 0;
+      for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
+        const uint32_t u = __ldcg(P.queue + i);
+        dsum += P.out_off[u + 1] - P.out_off[u];
+      }
+      const unsigned set = ph & 3;
+      block_add(dsum, &P.ctrl->cnt[set][kSum], s);
+      if (!grid_sync(P, s, ph, kTagRescan)) return;
+      pull = (long long)s.snap[kSum] * kBcPullRatio > P.m;
     }
-    if (!grid_sync(P, s, ph, kTagTD)) return;
-    qtail += s.snap[kAppend];
-    const unsigned long long nch = s.snap[kChunkCount];
-    if (nch) {
-      set = ph & 3;
+    int64_t tag = 0;
+    if (pull) {
+      const uint32_t* front = prev_lv;
+      if (!front) {  // QueueToBitmap of the previous (top-down) level
+        for (long long i = gtid; i < P.w32; i += gthreads) P.bm0[i] = 0u;
+        if (!grid_sync(P, s, ph, kTagZero)) return;
+        for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
+          const uint32_t u = __ldcg(P.queue + i);
+          atomicOr(P.bm0 + (u >> 5), 1u << (u & 31u));
+        }
+        if (!grid_sync(P, s, ph, kTagQ2B)) return;
+        front = P.bm0;
+      }
+      uint32_t* lv = P.bc_lv + (int64_t)npull * P.bc_lvw;
       const QApp qa = qapp(P, ph, qtail);
-      bc_forward_heavy(P, qa, nch, lvl, s, qcnt);
+      long long found = 0;
+      bc_pull_level(P, s, qa, lvl, front, lv, qcnt, found);
       wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
-      if (!grid_sync(P, s, ph, kTagHeavy)) return;
+      if (!grid_sync(P, s, ph, kTagBU)) return;
       qtail += s.snap[kAppend];
+      tag = (int64_t)(npull + 1) << 56;
+      prev_lv = lv;
+      npull++;
+    } else {
+      unsigned set = ph & 3;
+      {
+        const QApp qa = qapp(P, ph, qtail);
+        bc_forward_light(P, s, ph, qa, qs, qe, lvl, qcnt);
+        wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+      }
+      if (!grid_sync(P, s, ph, kTagTD)) return;
+      qtail += s.snap[kAppend];
+      const unsigned long long nch = s.snap[kChunkCount];
+      if (nch) {
+        set = ph & 3;
+        const QApp qa = qapp(P, ph, qtail);
+        bc_forward_heavy(P, qa, nch, lvl, s, qcnt);
+        wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+        if (!grid_sync(P, s, ph, kTagHeavy)) return;
+        qtail += s.snap[kAppend];
+      }
+      prev_lv = nullptr;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.bc_bounds[lvl] = (int64_t)qe;  // level lvl starts at qe
+    // level lvl starts at qe
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.bc_bounds[lvl] = (int64_t)qe | tag;
+    nvis += (long long)(qtail - qe);
     qs = qe;
     qe = qtail;
   }
   // levels 0 .. lvl-1: level d = [bounds[d], bounds[d+1]), bounds[lvl] = qtail
+  constexpr int64_t kPosMask = (int64_t(1) << 56) - 1;
   for (int d = lvl - 1; d >= 0; d--) {
-    const unsigned long long b0 = d == 0 ? 0ull : (unsigned long long)__ldcg(P.bc_bounds + d);
-    const unsigned long long b1 = d + 1 == lvl ? qtail : (unsigned long long)__ldcg(P.bc_bounds + d + 1);
-    const unsigned set = ph & 3;
-    bc_backward_level(P, s, ph, b0, b1);
+    const int64_t bd = __ldcg(P.bc_bounds + d), bn = __ldcg(P.bc_bounds + d + 1);
+    const unsigned long long b0 = d == 0 ? 0ull : (unsigned long long)(bd & kPosMask);
+    const unsigned long long b1 = d + 1 == lvl ? qtail : (unsigned long long)(bn & kPosMask);
+    const int pk = (int)((unsigned long long)bn >> 56);  // level d+1 pulled: its bitmap is the successor test
+    const uint32_t* lvb = pk ? P.bc_lv + (int64_t)(pk - 1) * P.bc_lvw : nullptr;
+    bc_backward_level(P, s, ph, b0, b1, lvb);
     if (!grid_sync(P, s, ph, kTagBcBack)) return;
     const unsigned long long nch = s.snap[kChunkCount];
     if (nch) {
-      bc_backward_chunks(P, nch);
+      bc_backward_chunks(P, nch, lvb);
       if (!grid_sync(P, s, ph, kTagBcChunk)) return;
     }
   }

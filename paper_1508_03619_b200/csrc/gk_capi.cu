@@ -62,6 +62,7 @@ void free_graph(gk_graph* g) {
   cudaFree(g->bc_succ);
   cudaFree(g->bc_scores);
   cudaFree(g->bc_bounds);
+  cudaFree(g->bc_lv);
   cudaFree(g->hbase);
   cudaFree(g->queue);
   cudaFree(g->chunks);
@@ -613,6 +614,7 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
     CK(cudaMalloc(&g->bc_scores, sizeof(float) * std::max<int64_t>(n, 1) + 16), "alloc scores");
     g->bc_bounds_cap = n + 2;
     CK(cudaMalloc(&g->bc_bounds, sizeof(int64_t) * g->bc_bounds_cap), "alloc level bounds");
+    CK(cudaMalloc(&g->bc_lv, sizeof(uint32_t) * gk::kBcMaxPull * ((n + 31) / 32 + 4)), "alloc level bitmaps");
   }
   g->last_valid = 0;  // depth/queue now hold Brandes state
   g->depth_valid = 0;
@@ -639,6 +641,12 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
   p.bc_scores = g->bc_scores;
   p.bc_bounds = g->bc_bounds;
   p.bc_bounds_cap = g->bc_bounds_cap;
+  p.bc_lv = g->bc_lv;
+  p.bc_lvw = (n + 31) / 32 + 4;
+  p.visited = g->visited;
+  p.dead = g->dead;
+  p.bm0 = g->bm0;
+  if (getenv("GK_BC_NO_PULL")) p.bc_lv = nullptr;  // top-down only (the reference's forward)
   cudaStream_t s = g->stream;
   CK(cudaMemsetAsync(g->bc_scores, 0, sizeof(float) * n, s), "clear scores");
   CK(cudaEventRecord(g->ev0, s), "event record");

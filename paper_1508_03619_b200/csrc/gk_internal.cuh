@@ -115,11 +115,15 @@ struct BfsParams {
   double2* bc_sd;       // per vertex {shortest-path count sigma, dependency delta}
   uint32_t* bc_succ;    // one bit per stored arc: shortest-path successor edge
   float* bc_scores;     // accumulated over sources
-  int64_t* bc_bounds;   // level d = queue[bounds[d], bounds[d+1])
+  int64_t* bc_bounds;   // level d = queue[bounds[d], bounds[d+1]) (low 56 bits); bits 56..63 = 1 +
+                        // index of the level's bitmap in bc_lv when it was found by a pull step
+  uint32_t* bc_lv;      // kBcMaxPull level bitmaps of bc_lvw words (pull-found levels)
+  int64_t bc_lvw;
   int64_t bc_bounds_cap;
 };
 
 constexpr int kBlock = 512;
+constexpr int kBcMaxPull = 8;  // Brandes levels found by a pull (bottom-up) step, at most
 constexpr int kWarps = kBlock / 32;
 
 // Host-side launch of the persistent traversal kernel.
@@ -200,6 +204,7 @@ struct gk_graph {
   float* bc_scores = nullptr;
   int64_t* bc_bounds = nullptr;
   int64_t bc_bounds_cap = 0;
+  uint32_t* bc_lv = nullptr;
   uint32_t* queue = nullptr;
   gk::Chunk* chunks = nullptr;
   int64_t chunk_cap = 0;
