@@ -121,3 +121,18 @@ def test_device_high_diameter_and_directed():
     dgd = DeviceGraph.from_csr(gd)
     srcs = [int(s) for s in O.pick_sources(gd, 4)]
     assert np.abs(Brandes(dgd, srcs) - O.brandes(gd, srcs)).max() <= TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("no_pull", [False, True])
+def test_device_forward_directions(no_pull, monkeypatch):
+    # pulled (bottom-up) forward levels and the reference's top-down-only
+    # forward give the same scores
+    from paper_1508_03619_b200 import Brandes, DeviceGraph
+    if no_pull:
+        monkeypatch.setenv("GK_BC_NO_PULL", "1")
+    for kind, scale in (("kron", 15), ("urand", 14)):
+        dg = DeviceGraph.generate(kind, scale, 16, SEED, permute=kind == "kron")
+        g = O.make_graph(kind, scale, permute=kind == "kron")
+        srcs = [int(s) for s in dg.pick_sources(6, SEED)]
+        assert np.abs(Brandes(dg, srcs) - O.brandes(g, srcs)).max() <= TOL
