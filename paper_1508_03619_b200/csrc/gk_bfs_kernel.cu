@@ -1533,8 +1533,11 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
   // levels 0 .. lvl-1: level d = [bounds[d], bounds[d+1]), bounds[lvl] = qtail
   constexpr int64_t kPosMask = (int64_t(1) << 56) - 1;
   for (int d = lvl - 1; d >= 0; d--) {
-    const int64_t bd = __ldcg(P.bc_bounds + d), bn = __ldcg(P.bc_bounds + d + 1);
-    const unsigned long long b0 = d == 0 ? 0ull : (unsigned long long)(bd & kPosMask);
+    // bounds[lvl] (the empty last level) was written by CTA 0 after the last
+    // barrier: never read it -- level lvl has no vertices, so no successors
+    const int64_t bd = d == 0 ? 0 : __ldcg(P.bc_bounds + d);
+    const int64_t bn = d + 1 == lvl ? 0 : __ldcg(P.bc_bounds + d + 1);
+    const unsigned long long b0 = (unsigned long long)(bd & kPosMask);
     const unsigned long long b1 = d + 1 == lvl ? qtail : (unsigned long long)(bn & kPosMask);
     const int pk = (int)((unsigned long long)bn >> 56);  // level d+1 pulled: its bitmap is the successor test
     const uint32_t* lvb = pk ? P.bc_lv + (int64_t)(pk - 1) * P.bc_lvw : nullptr;
