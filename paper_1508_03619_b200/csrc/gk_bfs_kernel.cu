@@ -623,7 +623,14 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
   // tasks so every warp gets work.
   const int tw = 1 << tw_log;
   const long long ntasks = (P.w32 + tw - 1) >> tw_log;
-  for (long long t = gw; t < ntasks; t += nw) {
+  // First task static, later ones claimed dynamically (per-task work varies
+  // with the pending density and list lengths; a static stride left warps
+  // idle at the phase's barrier).  The next claim is issued when a task
+  // starts, so its round trip hides behind the task.
+  unsigned long long* tctr = &P.ctrl->cnt[ph & 3][kTile];
+  for (long long t = gw; t < ntasks;) {
+    long long tnext = 0;
+    if (lane == 0) tnext = nw + (long long)atomicAdd(tctr, 1ull);
     const long long tbase = t << tw_log;
     const long long w = tbase + lane;
     uint32_t vis = 0xffffffffu, pad = 0u, live = 0u, hb = 0u;
@@ -753,6 +760,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
       awake += __popc(nbits);
     }
     __syncwarp();
+    t = __shfl_sync(kFull, tnext, 0);
   }
 }
 
