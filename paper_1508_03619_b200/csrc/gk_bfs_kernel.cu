@@ -463,9 +463,15 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
     // 8 edges per lane in flight and the next chunk descriptor prefetched:
     // the hub step is bound by the nb -> bitmap-word dependent latency
     constexpr int kE = 8;
+    // first chunk static, later ones claimed dynamically; the next claim and
+    // its descriptor load are issued before the current chunk's edges
+    unsigned long long* cctr = &P.ctrl->cnt[ph & 3][kChunkNext];
     Chunk ch = gw < (long long)nch ? P.chunks[gw] : Chunk{};
-    for (unsigned long long c = gw; c < nch; c += nw) {
-      const Chunk chn = c + nw < nch ? P.chunks[c + nw] : Chunk{};
+    for (unsigned long long c = gw; c < nch;) {
+      unsigned long long cn = 0;
+      if (lane == 0) cn = nw + atomicAdd(cctr, 1ull);
+      cn = __shfl_sync(kFull, cn, 0);
+      const Chunk chn = cn < nch ? P.chunks[cn] : Chunk{};
       for (uint32_t o = 0; o < ch.len; o += 32 * kE) {
         uint32_t v[kE], x[kE];
 #pragma unroll
@@ -485,6 +491,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
         }
       }
       ch = chn;
+      c = cn;
     }
     return;
   }
