@@ -1368,7 +1368,7 @@ __device__ void bc_backward_chunks(const BfsParams& P, unsigned long long nch, c
 // a bitmap (lv) that the backward pass uses as its successor test; sigma is
 // an integer count, so the summation order does not change it.
 __device__ void bc_pull_level(const BfsParams& P, SmemT& s, const QApp& qa, int lvl, const uint32_t* front,
-                              uint32_t* lv, int& qcnt, long long& found) {
+                              uint32_t* lv, int& qcnt, long long& degsum) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   double* acc = s.bc_sig;
   uint32_t* hit = s.td.t_u;
@@ -1431,15 +1431,81 @@ __device__ void bc_pull_level(const BfsParams& P, SmemT& s, const QApp& qa, int 
     if (got) {
       P.depth[v] = lvl;
       P.bc_sd[v].x = acc[threadIdx.x];
+      degsum += dl;  // in-degree = the level's share of arcs a pushed backward pass scans
     }
     const unsigned m = __ballot_sync(kFull, got);
     if ((threadIdx.x & 31) == 0 && v < P.n) {  // tiles are word-aligned: one writer per word
       lv[v >> 5] = m;
       if (m) P.visited[v >> 5] = vis | m;
-      found += __popc(m);
     }
     wq_push(P, qa, got, (uint32_t)v, buf, qcnt);
     __syncthreads();
+  }
+}
+
+// Backward pass for level d pushed from level d+1 (used when d+1 was
+// pulled and its in-arcs are fewer than level d's out-arcs, e.g. the level
+// after a hub expansion): every v in level d+1 adds (1 + delta(v)) /
+// sigma(v) into delta(u) of each in-neighbour u in level d (membership
+// bitmap ld); bc_push_finish then scales delta(u) by sigma(u).  Same sum
+// as betweenness.hpp:115, sigma(u) factored out.
+__device__ void bc_push_level(const BfsParams& P, SmemT& s, unsigned long long b0, unsigned long long b1,
+                              const uint32_t* ld) {
+  double* tv = s.bc_sig;
+  for (unsigned long long tile = blockIdx.x;; tile += gridDim.x) {
+    const unsigned long long start = b0 + tile * (unsigned long long)kBlock;
+    if (start >= b1) break;
+    const unsigned long long i = start + threadIdx.x;
+    int64_t b = 0, dl = 0;
+    double t = 0.0;
+    if (i < b1) {
+      const uint32_t v = __ldcg(P.queue + i);
+      b = P.in_off[v];
+      dl = P.in_off[v + 1] - b;
+      const double2 sd = __ldcg(P.bc_sd + v);
+      t = (1.0 + sd.y) / sd.x;
+    }
+    s.td.t_b[threadIdx.x] = b;
+    tv[threadIdx.x] = t;
+    int64_t tot;
+    const int64_t pre = block_exscan(dl, &tot, s);
+    s.td.t_pre[threadIdx.x] = pre;
+    __syncthreads();
+    for (int64_t eb = 0; eb < tot; eb += 4 * kBlock) {
+      uint32_t u[4];
+      int lo[4];
+      bool ok[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int64_t ei = eb + k * kBlock + threadIdx.x;
+        ok[k] = ei < tot;
+        lo[k] = 0;
+        u[k] = 0;
+        if (ok[k]) {
+          int l = 0, h = kBlock - 1;
+          while (l < h) {
+            const int mid = (l + h + 1) >> 1;
+            if (s.td.t_pre[mid] <= ei) l = mid;
+            else h = mid - 1;
+          }
+          lo[k] = l;
+          u[k] = ld_nb(P.in_nb + s.td.t_b[l] + (ei - s.td.t_pre[l]));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++)
+        if (ok[k] && ((ld_front(ld + (u[k] >> 5)) >> (u[k] & 31u)) & 1u)) atomicAdd(&P.bc_sd[u[k]].y, tv[lo[k]]);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void bc_push_finish(const BfsParams& P, unsigned long long b0, unsigned long long b1) {
+  for (unsigned long long i = b0 + (unsigned long long)blockIdx.x * kBlock + threadIdx.x; i < b1;
+       i += (unsigned long long)gridDim.x * kBlock) {
+    const uint32_t u = __ldcg(P.queue + i);
+    const double2 sd = __ldcg(P.bc_sd + u);
+    P.bc_sd[u].y = sd.x * sd.y;
   }
 }
 
@@ -1511,11 +1577,14 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
       }
       uint32_t* lv = P.bc_lv + (int64_t)npull * P.bc_lvw;
       const QApp qa = qapp(P, ph, qtail);
-      long long found = 0;
-      bc_pull_level(P, s, qa, lvl, front, lv, qcnt, found);
+      long long degsum = 0;
+      const unsigned set = ph & 3;
+      bc_pull_level(P, s, qa, lvl, front, lv, qcnt, degsum);
       wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
+      block_add(degsum, &P.ctrl->cnt[set][kSum], s);
       if (!grid_sync(P, s, ph, kTagBU)) return;
       qtail += s.snap[kAppend];
+      if (blockIdx.x == 0 && threadIdx.x == 0) P.bc_lvdeg[npull] = (long long)s.snap[kSum];
       tag = (int64_t)(npull + 1) << 56;
       prev_lv = lv;
       npull++;
@@ -1556,6 +1625,43 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
     const unsigned long long b1 = d + 1 == lvl ? qtail : (unsigned long long)(bn & kPosMask);
     const int pk = (int)((unsigned long long)bn >> 56);  // level d+1 pulled: its bitmap is the successor test
     const uint32_t* lvb = pk ? P.bc_lv + (int64_t)(pk - 1) * P.bc_lvw : nullptr;
+    if (pk) {
+      // level d+1 was pulled: push from it when its in-arcs are fewer than
+      // level d's out-arcs
+      const unsigned long long b2 = d + 2 == lvl ? qtail : (unsigned long long)(__ldcg(P.bc_bounds + d + 2) & kPosMask);
+      const int pkd = (int)((unsigned long long)bd >> 56);
+      long long out_d;
+      if (pkd) {
+        out_d = __ldcg(P.bc_lvdeg + pkd - 1);
+      } else {  // degree sum of level d (top-down): one pass over its queue range
+        long long sum = 0;
+        for (unsigned long long i = b0 + gtid; i < b1; i += gthreads) {
+          const uint32_t u = __ldcg(P.queue + i);
+          sum += P.out_off[u + 1] - P.out_off[u];
+        }
+        const unsigned set = ph & 3;
+        block_add(sum, &P.ctrl->cnt[set][kSum], s);
+        if (!grid_sync(P, s, ph, kTagRescan)) return;
+        out_d = (long long)s.snap[kSum];
+      }
+      if (__ldcg(P.bc_lvdeg + pk - 1) < out_d) {
+        const uint32_t* ldm = pkd ? P.bc_lv + (int64_t)(pkd - 1) * P.bc_lvw : P.bm0;
+        if (!pkd) {  // membership bitmap of level d
+          for (long long i = gtid; i < P.w32; i += gthreads) P.bm0[i] = 0u;
+          if (!grid_sync(P, s, ph, kTagZero)) return;
+          for (unsigned long long i = b0 + gtid; i < b1; i += gthreads) {
+            const uint32_t u = __ldcg(P.queue + i);
+            atomicOr(P.bm0 + (u >> 5), 1u << (u & 31u));
+          }
+          if (!grid_sync(P, s, ph, kTagQ2B)) return;
+        }
+        bc_push_level(P, s, b1, b2, ldm);
+        if (!grid_sync(P, s, ph, kTagBcBack)) return;
+        bc_push_finish(P, b0, b1);
+        if (!grid_sync(P, s, ph, kTagBcChunk)) return;
+        continue;
+      }
+    }
     bc_backward_level(P, s, ph, b0, b1, lvb);
     if (!grid_sync(P, s, ph, kTagBcBack)) return;
     const unsigned long long nch = s.snap[kChunkCount];

@@ -63,6 +63,7 @@ void free_graph(gk_graph* g) {
   cudaFree(g->bc_scores);
   cudaFree(g->bc_bounds);
   cudaFree(g->bc_lv);
+  cudaFree(g->bc_lvdeg);
   cudaFree(g->hbase);
   cudaFree(g->queue);
   cudaFree(g->chunks);
@@ -615,6 +616,7 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
     g->bc_bounds_cap = n + 2;
     CK(cudaMalloc(&g->bc_bounds, sizeof(int64_t) * g->bc_bounds_cap), "alloc level bounds");
     CK(cudaMalloc(&g->bc_lv, sizeof(uint32_t) * gk::kBcMaxPull * ((n + 31) / 32 + 4)), "alloc level bitmaps");
+    CK(cudaMalloc(&g->bc_lvdeg, sizeof(long long) * gk::kBcMaxPull), "alloc level arc sums");
   }
   g->last_valid = 0;  // depth/queue now hold Brandes state
   g->depth_valid = 0;
@@ -643,6 +645,7 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
   p.bc_bounds_cap = g->bc_bounds_cap;
   p.bc_lv = g->bc_lv;
   p.bc_lvw = (n + 31) / 32 + 4;
+  p.bc_lvdeg = g->bc_lvdeg;
   p.visited = g->visited;
   p.dead = g->dead;
   p.bm0 = g->bm0;

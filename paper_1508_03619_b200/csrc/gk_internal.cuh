@@ -119,6 +119,7 @@ struct BfsParams {
                         // index of the level's bitmap in bc_lv when it was found by a pull step
   uint32_t* bc_lv;      // kBcMaxPull level bitmaps of bc_lvw words (pull-found levels)
   int64_t bc_lvw;
+  long long* bc_lvdeg;  // [kBcMaxPull] in-arc sum of each pull-found level
   int64_t bc_bounds_cap;
 };
 
@@ -205,6 +206,7 @@ struct gk_graph {
   int64_t* bc_bounds = nullptr;
   int64_t bc_bounds_cap = 0;
   uint32_t* bc_lv = nullptr;
+  long long* bc_lvdeg = nullptr;
   uint32_t* queue = nullptr;
   gk::Chunk* chunks = nullptr;
   int64_t chunk_cap = 0;
