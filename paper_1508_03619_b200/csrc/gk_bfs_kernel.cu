@@ -1367,13 +1367,17 @@ __device__ void bc_backward_chunks(const BfsParams& P, unsigned long long nch, c
 // flight, per-vertex sums in shared memory.  The level's membership goes to
 // a bitmap (lv) that the backward pass uses as its successor test; sigma is
 // an integer count, so the summation order does not change it.
-__device__ void bc_pull_level(const BfsParams& P, SmemT& s, const QApp& qa, int lvl, const uint32_t* front,
-                              uint32_t* lv, int& qcnt, long long& degsum) {
+__device__ void bc_pull_level(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, int lvl,
+                              const uint32_t* front, uint32_t* lv, int& qcnt, long long& degsum) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   double* acc = s.bc_sig;
   uint32_t* hit = s.td.t_u;
   const long long ntiles = (P.n + kBlock - 1) / kBlock;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // tiles after the first are claimed dynamically: a tile holding a hub's
+  // full in-list must not hold back the CTA's statically assigned others
+  unsigned long long* tctr = &P.ctrl->cnt[ph & 3][kTile];
+  for (long long tile = blockIdx.x; tile < ntiles;) {
+    if (threadIdx.x == 0) s.bcast[1] = gridDim.x + atomicAdd(tctr, 1ull);
     const long long v = tile * kBlock + threadIdx.x;
     bool pend = false;
     uint32_t vis = 0xffffffffu;
@@ -1439,6 +1443,8 @@ __device__ void bc_pull_level(const BfsParams& P, SmemT& s, const QApp& qa, int 
       if (m) P.visited[v >> 5] = vis | m;
     }
     wq_push(P, qa, got, (uint32_t)v, buf, qcnt);
+    __syncthreads();
+    tile = (long long)s.bcast[1];
     __syncthreads();
   }
 }
@@ -1579,7 +1585,7 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
       const QApp qa = qapp(P, ph, qtail);
       long long degsum = 0;
       const unsigned set = ph & 3;
-      bc_pull_level(P, s, qa, lvl, front, lv, qcnt, degsum);
+      bc_pull_level(P, s, ph, qa, lvl, front, lv, qcnt, degsum);
       wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);
       block_add(degsum, &P.ctrl->cnt[set][kSum], s);
       if (!grid_sync(P, s, ph, kTagBU)) return;
