@@ -179,8 +179,6 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
   if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
   p.stop_after = 0xffffffffu;
   if (const char* sa = getenv("GK_STOP_AFTER")) p.stop_after = (unsigned)strtoul(sa, nullptr, 10);
-  p.exp_flags = 0;
-  if (const char* ex = getenv("GK_EXP")) p.exp_flags = (unsigned)strtoul(ex, nullptr, 10);
 
   return p;
 }

@@ -108,7 +108,6 @@ struct BfsParams {
   int64_t step_cap;
   unsigned long long timeout_ns;
   unsigned stop_after;  // leave after this many grid barriers (profiling only)
-  unsigned exp_flags;   // experiment switches (GK_EXP, profiling only)
   int32_t td_passes;    // large top-down steps: target-range passes (1 when next fits L2)
   int64_t td_span;      // ids per pass (multiple of 32)
   // Brandes (betweenness.hpp:38-80), bc_persistent only
