@@ -184,6 +184,18 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
 }
 
 gk_status finish_graph(gk_graph* g, gk_graph** out) {
+  // every kernel indexes with these arrays: reject a malformed CSR up front
+  for (int pass = 0; pass < (g->directed ? 2 : 1); pass++) {
+    bool off_ok = true, ids_ok = true;
+    const cudaError_t e = gk::validate_csr(pass ? g->in_off : g->out_off, pass ? g->in_nb : g->out_nb, g->n, g->m,
+                                           &off_ok, &ids_ok, nullptr);
+    if (e != cudaSuccess || !off_ok || !ids_ok) {
+      free_graph(g);
+      if (e != cudaSuccess) return cuda_fail(e, "validate CSR");
+      return fail(GK_ERR_INVALID, !off_ok ? "invalid graph: offsets not monotone from 0 to m"
+                                          : "invalid graph: neighbour id out of range");
+    }
+  }
   gk_status st = alloc_workspace(g);
   if (st != GK_OK) {
     free_graph(g);
@@ -209,8 +221,8 @@ int gk_device_count(void) {
 gk_status gk_graph_upload(const gk_csr_view* csr, int device, gk_graph** out) {
   if (!csr || !out || !csr->out_offsets || csr->num_nodes < 0)
     return fail(GK_ERR_INVALID, "gk_graph_upload: null argument");
-  if (csr->num_nodes > (int64_t(1) << 32))
-    return fail(GK_ERR_INVALID, "gk_graph_upload: more than 2^32 vertices (NodeId is 32-bit)");
+  if (csr->num_nodes > (int64_t(1) << 31))
+    return fail(GK_ERR_INVALID, "gk_graph_upload: more than 2^31 vertices (parents are int32)");
   if (csr->directed && (!csr->in_offsets || (!csr->in_neighbors && csr->out_offsets[csr->num_nodes])))
     return fail(GK_ERR_INVALID, "gk_graph_upload: directed graph needs in_* arrays");
   gk_status st = need_device(device);

@@ -72,3 +72,14 @@ def test_null_arguments_are_errors_not_crashes(lib):
     assert lib.gk_graph_upload(None, 0, None) == 7  # GK_ERR_INVALID
     assert lib.gk_graph_info(None, None, None, None) == 7
     assert lib.gk_bfs(None, 0, 15, 18, 0, None, None, None) == 7
+
+
+def test_vertex_count_limit_checked_before_any_device_work(lib):
+    # parents are int32: more than 2^31 vertices is refused (no device needed)
+    import ctypes as C
+    from paper_1508_03619_b200._lib import CsrView
+    off = (C.c_int64 * 2)(0, 0)
+    v = CsrView((1 << 31) + 1, 0, 0, C.cast(off, C.c_void_p), None, None, None)
+    h = C.c_void_p()
+    assert lib.gk_graph_upload(C.byref(v), 0, C.byref(h)) == 7
+    assert b"2^31" in lib.gk_last_error()

@@ -132,3 +132,20 @@ def test_batch_matches_single_calls():
     with pytest.raises(ConfigError, match="bfs source out of range"):
         dg.bfs_batch([0, g.n])
     assert dg.bfs_batch([]).size == 0
+
+
+def test_malformed_csr_rejected():
+    # every kernel indexes with off/nb: a malformed CSR is refused at creation
+    from paper_1508_03619_b200 import GapkitError
+    with pytest.raises(GapkitError, match="neighbour id out of range"):
+        DeviceGraph.upload(3, np.array([0, 1, 2, 2], np.int64), np.array([1, 7], np.uint32))
+    with pytest.raises(GapkitError, match="offsets not monotone"):
+        DeviceGraph.upload(3, np.array([0, 2, 1, 2], np.int64), np.array([1, 0], np.uint32))
+    with pytest.raises(GapkitError, match="offsets not monotone"):
+        DeviceGraph.upload(2, np.array([1, 1, 2], np.int64), np.array([1, 0], np.uint32))
+    # directed: the in-CSR is checked too
+    with pytest.raises(GapkitError, match="neighbour id out of range"):
+        DeviceGraph.upload(2, np.array([0, 1, 1], np.int64), np.array([1], np.uint32), directed=True,
+                           in_offsets=np.array([0, 0, 1], np.int64), in_neighbors=np.array([5], np.uint32))
+    ok = DeviceGraph.upload(3, np.array([0, 1, 2, 2], np.int64), np.array([1, 0], np.uint32))
+    assert ok.bfs(0).parent.tolist() == [0, 0, -1]
