@@ -45,13 +45,13 @@ __global__ void k_dead(const int64_t* __restrict__ in_off, int64_t n, int64_t w3
 // CSR invariants every kernel relies on (graph.hpp:26-45): off[0] = 0,
 // non-decreasing, off[n] = m, every neighbour id < n.
 __global__ void k_validate_csr(const int64_t* __restrict__ off, const uint32_t* __restrict__ nb, int64_t n,
-                               int64_t m, unsigned long long* bad) {
+                               int64_t m, int64_t id_bound, unsigned long long* bad) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
     if (off[v] > off[v + 1] || off[v + 1] > m) atomicAdd(&bad[0], 1ull);
   if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n] != m)) atomicAdd(&bad[0], 1ull);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride)
-    if ((int64_t)nb[i] >= n) atomicAdd(&bad[1], 1ull);
+    if ((int64_t)nb[i] >= id_bound) atomicAdd(&bad[1], 1ull);
 }
 
 __global__ void k_live_count(const uint32_t* __restrict__ dead, int64_t w32, uint32_t* __restrict__ cnt) {
@@ -246,14 +246,14 @@ cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int64_t m, bool* offsets_ok,
-                         bool* ids_ok, cudaStream_t s) {
+cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int64_t m, int64_t id_bound,
+                         bool* offsets_ok, bool* ids_ok, cudaStream_t s) {
   unsigned long long* bad = nullptr;
   unsigned long long hb[2] = {0, 0};
   cudaError_t e;
   if ((e = cudaMalloc(&bad, sizeof(hb)))) return e;
   if (!(e = cudaMemsetAsync(bad, 0, sizeof(hb), s))) {
-    k_validate_csr<<<aux_grid(std::max<int64_t>(n, m)), kAuxBlock, 0, s>>>(off, nb, n, m, bad);
+    k_validate_csr<<<aux_grid(std::max<int64_t>(n, m)), kAuxBlock, 0, s>>>(off, nb, n, m, id_bound, bad);
     if (!(e = cudaGetLastError()) && !(e = cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s)))
       e = cudaStreamSynchronize(s);
   }

@@ -188,7 +188,7 @@ gk_status finish_graph(gk_graph* g, gk_graph** out) {
   for (int pass = 0; pass < (g->directed ? 2 : 1); pass++) {
     bool off_ok = true, ids_ok = true;
     const cudaError_t e = gk::validate_csr(pass ? g->in_off : g->out_off, pass ? g->in_nb : g->out_nb, g->n, g->m,
-                                           &off_ok, &ids_ok, nullptr);
+                                           g->n, &off_ok, &ids_ok, nullptr);
     if (e != cudaSuccess || !off_ok || !ids_ok) {
       free_graph(g);
       if (e != cudaSuccess) return cuda_fail(e, "validate CSR");

@@ -142,9 +142,9 @@ cudaError_t bc_normalize(float* scores, int64_t n, float* scratch_max, cudaStrea
 
 // Auxiliary (untimed) kernels.
 cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s);
-// CSR invariants (offsets monotone from 0 to m, neighbour ids < n).
-cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int64_t m, bool* offsets_ok,
-                         bool* ids_ok, cudaStream_t s);
+// CSR invariants: n rows with offsets monotone from 0 to m, neighbour ids < id_bound.
+cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int64_t m, int64_t id_bound,
+                         bool* offsets_ok, bool* ids_ok, cudaStream_t s);
 // head[v] = the first kHead in-neighbours of v in CSR (ascending) order,
 // padded with kNoVertex: the bottom-up sweep's first round reads this dense
 // array (sequential in v) instead of one random sector of in_nb per vertex.

@@ -868,6 +868,12 @@ gk::ShardParams params(const gk_shard* s) {
 }
 
 gk_status shard_alloc(gk_shard* s) {
+  {  // the owned rows must be a valid CSR over global neighbour ids
+    bool off_ok = true, ids_ok = true;
+    SCK(gk::validate_csr(s->off, s->nb, s->nloc, s->m, s->n, &off_ok, &ids_ok, nullptr), "validate shard CSR");
+    if (!off_ok) return shard_fail(GK_ERR_INVALID, "invalid shard: offsets not monotone from 0 to m");
+    if (!ids_ok) return shard_fail(GK_ERR_INVALID, "invalid shard: neighbour id out of range");
+  }
   const int64_t wl = (s->nloc + 31) / 32 + 4, wg = (s->n + 31) / 32 + 4;
   SCK(cudaMalloc(&s->parent, sizeof(int32_t) * std::max<int64_t>(s->nloc, 1)), "alloc parent");
   SCK(cudaMalloc(&s->depth, sizeof(int32_t) * std::max<int64_t>(s->nloc, 1)), "alloc depth");

@@ -128,3 +128,13 @@ def test_gpu_larger_shards():
     for src in full.pick_sources(2):
         res = sb.run(int(src), want_depth=True, gather=True)
         check(g, res, int(src))
+
+
+@pytest.mark.gpu
+def test_gpu_shard_rejects_malformed_rows():
+    from paper_1508_03619_b200 import GapkitError
+    from paper_1508_03619_b200.dist import GpuEngine
+    with pytest.raises(GapkitError, match="neighbour id out of range"):
+        GpuEngine.upload(64, 0, 2, np.array([0, 1] + [1] * 31, np.int64), np.array([64], np.uint32))
+    with pytest.raises(GapkitError, match="offsets not monotone"):
+        GpuEngine.upload(64, 0, 2, np.array([0, 2, 1] + [2] * 30, np.int64), np.array([1, 2], np.uint32))
