@@ -520,7 +520,6 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
       prev_lv = lv;
       npull++;
     } else {
-      unsigned set = ph & 3;
       {
         const QApp qa = qapp(P, ph, qtail);
         bc_forward_light(P, s, ph, qa, qs, qe, lvl, qcnt);
@@ -530,7 +529,6 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
       qtail += s.snap[kAppend];
       const unsigned long long nch = s.snap[kChunkCount];
       if (nch) {
-        set = ph & 3;
         const QApp qa = qapp(P, ph, qtail);
         bc_forward_heavy(P, qa, nch, lvl, s, qcnt);
         wq_flush(P, qa, s.td.qbuf[threadIdx.x >> 5], qcnt);

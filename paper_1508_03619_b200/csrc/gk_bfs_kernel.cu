@@ -32,15 +32,6 @@
 namespace gk {
 namespace {
 
-// Claim v for parent u (bfs.hpp:78-84).  The visited word is read from L2
-// first so already-visited targets cost no atomic.
-__device__ __forceinline__ bool try_claim(const BfsParams& P, uint32_t v) {
-  const uint32_t bit = 1u << (v & 31u);
-  uint32_t* w = P.visited + (v >> 5);
-  if (__ldcg(w) & bit) return false;
-  return (atomicOr(w, bit) & bit) == 0;
-}
-
 __device__ __forceinline__ void on_claim(const BfsParams& P, uint32_t u, uint32_t v, int lvl,
                                          bool encode, long long& scout) {
   P.parent[v] = (int32_t)u;
@@ -99,7 +90,7 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
     for (int k = 0; k < 4; k++) wq_push(P, qa, c[k], v[k], buf, qcnt);
     return;
   }
-  if (kBig) {
+  if constexpr (kBig) {
     // Fire-and-forget claims: the next-frontier bitmap starts as a copy of
     // visited, so one pre-check covers both "already visited" and "already
     // claimed this step"; racing writers all store a valid parent (any
@@ -117,7 +108,7 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
       }
     }
     return;
-  }
+  } else {
 #pragma unroll
   for (int k = 0; k < 4; k++) w[k] = ok[k] ? ld_bits_l1(P.visited + (v[k] >> 5)) : 0xffffffffu;
 #pragma unroll
@@ -134,6 +125,7 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
     if (c[k]) on_claim(P, u[k], v[k], lvl, encode, scout);
 #pragma unroll
   for (int k = 0; k < 4; k++) wq_push(P, qa, c[k], v[k], buf, qcnt);
+  }
 }
 
 // ---- top-down, light vertices + chunk registration ------------------------
@@ -227,7 +219,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
   // round-robin over warps balances without a contended grab counter.
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
-  if (kBig) {
+  if constexpr (kBig) {
     // 8 edges per lane in flight and the next chunk descriptor prefetched:
     // the hub step is bound by the nb -> bitmap-word dependent latency
     constexpr int kE = 8;
@@ -262,7 +254,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       c = cn;
     }
     return;
-  }
+  } else {
   for (unsigned long long c = gw; c < nch; c += nw) {
     const Chunk ch = P.chunks[c];
     const uint32_t uu[4] = {ch.u, ch.u, ch.u, ch.u};
@@ -277,6 +269,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       }
       claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt, tiny);
     }
+  }
   }
 }
 
@@ -376,7 +369,7 @@ __device__ void td_scout_bits(const BfsParams& P, uint32_t* bm, int lvl, bool en
 // in-edges never appear: visited starts as the graph's dead bitmap.
 constexpr int kBuSlots = 2;
 constexpr int kPerRound = 4;    // in-neighbours tested per slot per round
-constexpr int kLaneRounds = 8;  // rounds before a list is deferred to the long list
+constexpr int kLaneRounds = 12;  // rounds before a list is deferred to the long list (8-16 measured flat)
 static_assert(kHead <= kPerRound, "a head round tests one head record");
 
 // front is either the global bitmap or its shared-memory copy (small graphs).
@@ -671,7 +664,6 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   while (qe > qs) {
     const bool go_bu = P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha;
     if (!go_bu && queue_stale) {  // BitmapToQueue for the coming top-down step
-      const unsigned bset = ph & 3;
       b2q(P, qapp(P, ph, qtail), frontg, s);
       if (!grid_sync(P, s, ph, kTagB2Q)) return;
       qtail += s.snap[kAppend];
@@ -728,7 +720,6 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         frontg = nextg;
         nextg = t;
       } while (awake >= old_awake || awake > P.n / P.beta);
-      const unsigned bset = ph & 3;
       b2q(P, qapp(P, ph, qtail), frontg, s);  // bfs.hpp:155
       if (!grid_sync(P, s, ph, kTagB2Q)) return;
       qtail += s.snap[kAppend];
