@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
   const long long gthreads = (long long)gridDim.x * kBlock;
   const uint32_t src = P.src;
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->ts[0] = globaltimer();
+  zero_next_ctrl(P, gtid, gthreads);
   // init (betweenness.hpp:96-101)
   for (long long i = gtid; i < P.n; i += gthreads) {
     P.depth[i] = -1;

@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
 
   // ---- init (timed; replaces bfs.hpp:126-138) ----
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->ts[0] = globaltimer();
+  zero_next_ctrl(P, gtid, gthreads);
   {
     const long long n4 = P.n >> 2;
     int4* p4 = reinterpret_cast<int4*>(P.parent);

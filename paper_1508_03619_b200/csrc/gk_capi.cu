@@ -94,7 +94,8 @@ gk_status alloc_workspace(gk_graph* g) {
   CK(cudaMalloc(&g->queue, sizeof(uint32_t) * (n + 1)), "alloc queue");
   g->chunk_cap = 2 * (g->m / 1024) + 65536;  // >= 4 x warps when chunks shrink to 128 edges
   CK(cudaMalloc(&g->chunks, sizeof(gk::Chunk) * g->chunk_cap), "alloc chunks");
-  CK(cudaMalloc(&g->ctrl, sizeof(gk::Ctrl)), "alloc ctrl");
+  CK(cudaMalloc(&g->ctrl, 2 * sizeof(gk::Ctrl)), "alloc ctrl");
+  CK(cudaMemset(g->ctrl, 0, 2 * sizeof(gk::Ctrl)), "clear ctrl");
   g->step_cap = std::min<int64_t>(n + 2, int64_t(1) << 20);
   CK(cudaMalloc(&g->steps, sizeof(gk_step) * g->step_cap), "alloc step log");
   CK(cudaMalloc(&g->acc, sizeof(unsigned long long) * 8), "alloc acc");
@@ -181,6 +182,19 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
   if (const char* sa = getenv("GK_STOP_AFTER")) p.stop_after = (unsigned)strtoul(sa, nullptr, 10);
 
   return p;
+}
+
+// Control blocks alternate between launches: each launch zeroes the other
+// one during its init phase, so no memset sits between launches.  After a
+// failed launch both are cleared (the kernel may not have finished that).
+void use_ctrl(gk_graph* g, gk::BfsParams& p) {  // call launched() once the kernel is queued
+  p.ctrl = g->ctrl + (g->ctrl_epoch & 1);
+  p.ctrl_next = g->ctrl + ((g->ctrl_epoch + 1) & 1);
+}
+void launched(gk_graph* g) { g->ctrl_epoch++; }
+void reset_ctrl(gk_graph* g) {
+  cudaMemset(g->ctrl, 0, 2 * sizeof(gk::Ctrl));
+  g->ctrl_epoch = 0;
 }
 
 gk_status finish_graph(gk_graph* g, gk_graph** out) {
@@ -419,17 +433,19 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   gk::BfsParams p = make_params(g, source, alpha, beta, strategy, want_depth);
 
   cudaStream_t s = g->stream;
+  use_ctrl(g, p);
   CK(cudaEventRecord(g->ev0, s), "event record");
-  CK(cudaMemsetAsync(g->ctrl, 0, sizeof(gk::Ctrl), s), "reset ctrl");
   CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
+  launched(g);
   CK(cudaEventRecord(g->ev1, s), "event record");
   gk::Ctrl& ctrl = g->last_ctrl;
   g->last_valid = 0;
-  CK(cudaMemcpyAsync(&ctrl, g->ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
+  CK(cudaMemcpyAsync(&ctrl, p.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
   CK(cudaStreamSynchronize(s), "bfs kernel");
   g->last_valid = 1;
   g->depth_valid = want_depth;
   if (ctrl.error) {
+    reset_ctrl(g);
     if (ctrl.error == 2) {
       unsigned lo = ~0u, hi = 0;
       for (int i = 0; i < 2048; i++) {
@@ -518,12 +534,13 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     const int slot = i & 1;
     gk::BfsParams p = make_params(g, sources[i], alpha, beta, strategy, 0);
     p.parent = buf[slot];
+    use_ctrl(g, p);
     if (i >= 2 && (e = cudaStreamWaitEvent(s, cdone[slot], 0))) break;  // copy of i-2 has left buf
     if ((e = cudaEventRecord(ev[2 * i], s))) break;
-    if ((e = cudaMemsetAsync(g->ctrl, 0, sizeof(gk::Ctrl), s))) break;
     if ((e = gk::bfs_launch(p, g->launch, s))) break;
+    launched(g);
     if ((e = cudaEventRecord(ev[2 * i + 1], s))) break;
-    if ((e = cudaMemcpyAsync(errs + i, &g->ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;
+    if ((e = cudaMemcpyAsync(errs + i, &p.ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;
     if ((e = cudaEventRecord(kdone[slot], s))) break;
     if ((e = cudaStreamWaitEvent(cs, kdone[slot], 0))) break;
     if (parents_out && parents_out[i] &&
@@ -535,8 +552,14 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
   if (e == cudaSuccess) e = e2 != cudaSuccess ? e2 : e3;
   if (e != cudaSuccess) {
     cleanup();
+    reset_ctrl(g);
     return fail(GK_ERR_CUDA, std::string("bfs batch: ") + cudaGetErrorString(e));
   }
+  for (int32_t i = 0; i < count; i++)
+    if (errs[i]) {
+      reset_ctrl(g);
+      break;
+    }
   for (int32_t i = 0; i < count && st == GK_OK; i++) {
     if (errs[i] == 2) st = fail(GK_ERR_TIMEOUT, "bfs kernel watchdog fired (grid barrier timeout)");
     else if (errs[i]) st = fail(GK_ERR_CUDA, "bfs kernel: heavy-chunk buffer overflow");
@@ -665,13 +688,15 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
   CK(cudaEventRecord(g->ev0, s), "event record");
   for (int64_t i = 0; i < num_sources; i++) {
     p.src = sources[i];
-    CK(cudaMemsetAsync(g->ctrl, 0, sizeof(gk::Ctrl), s), "reset ctrl");
+    use_ctrl(g, p);
     CK(gk::bc_launch(p, g->device, s), "launch brandes kernel");
+    launched(g);
     gk::Ctrl& ctrl = g->last_ctrl;  // kept for gk_bfs_trace (phase timings of the last source)
-    CK(cudaMemcpyAsync(&ctrl, g->ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
+    CK(cudaMemcpyAsync(&ctrl, p.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
     CK(cudaStreamSynchronize(s), "brandes kernel");
     g->last_valid = 1;
     const int err = ctrl.error;
+    if (err) reset_ctrl(g);
     if (err == 2) return fail(GK_ERR_TIMEOUT, "brandes kernel watchdog fired (grid barrier timeout)");
     if (err == 3) return fail(GK_ERR_CUDA, "brandes kernel: chunk buffer overflow");
     if (err == 4) return fail(GK_ERR_CUDA, "brandes kernel: level bound buffer overflow");

@@ -52,6 +52,8 @@ struct Ctrl {
   unsigned char tag[kTraceCap];
 };
 
+static_assert(sizeof(Ctrl) % 16 == 0, "control blocks are cleared with 16-byte stores and laid out in pairs");
+
 struct Chunk {
   uint32_t u;
   uint32_t len;
@@ -104,6 +106,7 @@ struct BfsParams {
   Chunk* chunks;
   int64_t chunk_cap;
   Ctrl* ctrl;
+  Ctrl* ctrl_next;      // the other control block: zeroed by this launch for the next one
   gk_step* steps;
   int64_t step_cap;
   unsigned long long timeout_ns;
@@ -212,7 +215,8 @@ struct gk_graph {
   uint32_t* queue = nullptr;
   gk::Chunk* chunks = nullptr;
   int64_t chunk_cap = 0;
-  gk::Ctrl* ctrl = nullptr;
+  gk::Ctrl* ctrl = nullptr;   // two control blocks, used alternately (no per-launch memset)
+  int ctrl_epoch = 0;
   gk_step* steps = nullptr;
   int64_t step_cap = 0;
   unsigned long long* acc = nullptr;  // aux accumulators

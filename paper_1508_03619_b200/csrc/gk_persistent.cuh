@@ -166,6 +166,14 @@ __device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& ph, unsigned c
   return s.ok != 0 && ph < P.stop_after;
 }
 
+// The next launch's control block (launches alternate between two) is
+// cleared here, so no memset has to run between launches.
+__device__ __forceinline__ void zero_next_ctrl(const BfsParams& P, long long gtid, long long gthreads) {
+  if (!P.ctrl_next) return;
+  uint4* c = reinterpret_cast<uint4*>(P.ctrl_next);
+  for (long long i = gtid; i < (long long)(sizeof(Ctrl) / sizeof(uint4)); i += gthreads) c[i] = make_uint4(0, 0, 0, 0);
+}
+
 // Exclusive scan of one int64 per thread across the CTA; *total gets the sum.
 __device__ int64_t block_exscan(int64_t x, int64_t* total, SmemT& s) {
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
