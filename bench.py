@@ -404,7 +404,8 @@ def main():
     # copy of result i overlaps traversal i+1.  One-call-per-source timing
     # (gk_bfs, copy not overlapped) is reported beside it.
     pins = [PinnedBuffer(g.n), PinnedBuffer(g.n)]
-    g.bfs_batch(sources[:2], [p.array for p in pins])  # warm the copy stream
+    warm = sources[:2]
+    g.bfs_batch(warm, [pins[i].array for i in range(len(warm))])  # warm the copy stream
     t0 = time.perf_counter()
     g.bfs_batch(sources, [pins[i & 1].array for i in range(len(sources))])
     batch_s = time.perf_counter() - t0
