@@ -77,6 +77,54 @@ __global__ void k_head(const int64_t* __restrict__ in_off, const uint32_t* __res
   }
 }
 
+// Owned-range split rows (gk_internal.cuh OwnEnt).
+__global__ void k_hv_bits(const int64_t* __restrict__ off, int64_t n, int64_t w32, int64_t dmin,
+                          uint32_t* __restrict__ bits) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < w32 * 32;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const bool h = v < n && off[v + 1] - off[v] >= dmin;
+    const unsigned b = __ballot_sync(0xffffffffu, h);
+    if ((threadIdx.x & 31) == 0) bits[v >> 5] = b;
+  }
+}
+
+__global__ void k_popc(const uint32_t* __restrict__ bits, int64_t w32, uint32_t* __restrict__ cnt) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < w32; w += (int64_t)gridDim.x * blockDim.x)
+    cnt[w] = __popc(bits[w]);
+}
+
+__global__ void k_hv_list(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ base, int64_t w32,
+                          uint32_t* __restrict__ ids) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < w32; w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t b = bits[w], r = base[w];
+    while (b) {
+      ids[r++] = (uint32_t)(w * 32 + __ffs(b) - 1);
+      b &= b - 1;
+    }
+  }
+}
+
+// One CTA per row: check the list is ascending, then row[r] = lower_bound of
+// r*span in it for r = 0..nr.
+__global__ void k_split(const int64_t* __restrict__ off, const uint32_t* __restrict__ nb,
+                        const uint32_t* __restrict__ ids, int nr, int64_t span, uint32_t* __restrict__ split,
+                        unsigned long long* bad) {
+  const uint32_t u = ids[blockIdx.x];
+  const int64_t b = off[u], d = off[u + 1] - b;
+  for (int64_t i = threadIdx.x + 1; i < d; i += blockDim.x)
+    if (nb[b + i] < nb[b + i - 1]) atomicAdd(bad, 1ull);
+  for (int r = threadIdx.x; r <= nr; r += blockDim.x) {
+    const int64_t t = (int64_t)r * span;
+    int64_t lo = 0, hi = d;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)nb[b + mid] < t) lo = mid + 1;
+      else hi = mid;
+    }
+    split[(int64_t)blockIdx.x * (nr + 1) + r] = (uint32_t)lo;
+  }
+}
+
 __global__ void k_count_reached(const int32_t* __restrict__ parent, const int64_t* __restrict__ off,
                                 int64_t n, unsigned long long* out) {
   __shared__ unsigned long long sm[kAuxBlock / 32];
@@ -290,6 +338,59 @@ cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, 
 out:
   cudaFree(tmp);
   cudaFree(cnt);
+  return e;
+}
+
+cudaError_t build_own(const int64_t* out_off, const uint32_t* out_nb, int64_t n, int64_t dmin, int r,
+                      int64_t span_w, size_t max_bytes, uint32_t** hv_bits, uint32_t** hv_base,
+                      uint32_t** split, int64_t* nh, cudaStream_t s) {
+  const int64_t w32 = (n + 31) / 32;
+  *hv_bits = *hv_base = *split = nullptr;
+  *nh = 0;
+  if (w32 == 0 || r < 1) return cudaSuccess;
+  uint32_t* cnt = nullptr;
+  uint32_t* ids = nullptr;
+  unsigned long long* bad = nullptr;
+  unsigned long long hbad = 0;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  uint32_t last[2] = {0, 0};
+  int64_t rows = 0;
+  cudaError_t e;
+  if ((e = cudaMalloc(hv_bits, sizeof(uint32_t) * w32))) goto out;
+  if ((e = cudaMalloc(hv_base, sizeof(uint32_t) * w32))) goto out;
+  if ((e = cudaMalloc(&cnt, sizeof(uint32_t) * w32))) goto out;
+  k_hv_bits<<<aux_grid(w32 * 32), kAuxBlock, 0, s>>>(out_off, n, w32, dmin, *hv_bits);
+  k_popc<<<aux_grid(w32), kAuxBlock, 0, s>>>(*hv_bits, w32, cnt);
+  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, *hv_base, (int)w32, s))) goto out;
+  if ((e = cudaMalloc(&tmp, tb))) goto out;
+  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, *hv_base, (int)w32, s))) goto out;
+  if ((e = cudaMemcpyAsync(&last[0], *hv_base + w32 - 1, 4, cudaMemcpyDeviceToHost, s))) goto out;
+  if ((e = cudaMemcpyAsync(&last[1], cnt + w32 - 1, 4, cudaMemcpyDeviceToHost, s))) goto out;
+  if ((e = cudaStreamSynchronize(s))) goto out;
+  rows = (int64_t)last[0] + last[1];
+  if (rows == 0 || (size_t)rows * (r + 1) * 4 > max_bytes) goto out;
+  if ((e = cudaMalloc(&ids, sizeof(uint32_t) * rows))) goto out;
+  if ((e = cudaMalloc(split, sizeof(uint32_t) * rows * (r + 1)))) goto out;
+  if ((e = cudaMalloc(&bad, sizeof(unsigned long long)))) goto out;
+  if ((e = cudaMemsetAsync(bad, 0, sizeof(unsigned long long), s))) goto out;
+  k_hv_list<<<aux_grid(w32), kAuxBlock, 0, s>>>(*hv_bits, *hv_base, w32, ids);
+  k_split<<<(unsigned)rows, 512, 0, s>>>(out_off, out_nb, ids, r, span_w * 32, *split, bad);
+  if ((e = cudaGetLastError())) goto out;
+  if ((e = cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, s))) goto out;
+  if ((e = cudaStreamSynchronize(s))) goto out;
+  if (hbad == 0) *nh = rows;
+out:
+  cudaFree(tmp);
+  cudaFree(cnt);
+  cudaFree(ids);
+  cudaFree(bad);
+  if (*nh == 0) {  // off: nothing qualifies, a list is unsorted, too large, or an error
+    cudaFree(*hv_bits);
+    cudaFree(*hv_base);
+    cudaFree(*split);
+    *hv_bits = *hv_base = *split = nullptr;
+  }
   return e;
 }
 

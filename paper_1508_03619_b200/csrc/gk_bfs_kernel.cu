@@ -133,7 +133,7 @@ template <bool kBig>
 __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& qa, unsigned long long qs,
                          unsigned long long qe, uint32_t* nextbm, int lvl, bool encode,
                          long long& scout, int& qcnt, int tile_sz, int64_t chunk, bool tiny,
-                         bool reg = true, uint32_t rlo = 0, uint32_t rhi = 0xffffffffu) {
+                         bool reg = true, uint32_t rlo = 0, uint32_t rhi = 0xffffffffu, bool own = false) {
   uint32_t* buf = s.td.qbuf[threadIdx.x >> 5];
   unsigned long long* cnt = P.ctrl->cnt[ph & 3];
   // First tile of each CTA is static (no atomic on the latency chain of
@@ -149,7 +149,14 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       u = __ldcg(P.queue + i);
       b = P.out_off[u];
       const int64_t d = P.out_off[u + 1] - b;
-      if (d > chunk) {
+      if (own && d >= P.own_dmin) {  // expanded range by range in td_own
+        const uint32_t hw = __ldg(P.hv_bits + (u >> 5));
+        OwnEnt e;
+        e.u = u;
+        e.rank = __ldg(P.hv_base + (u >> 5)) + __popc(hw & ((1u << (u & 31u)) - 1u));
+        e.base = b;
+        P.own_list[atomicAdd(&cnt[kOwnCount], 1ull)] = e;
+      } else if (d > chunk) {
         if (reg) {  // range passes after the first reuse the chunk list
           const int64_t nch = (d + chunk - 1) / chunk;
           const unsigned long long base = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
@@ -270,6 +277,126 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       claim4<kBig>(P, qa, uu, v, ok, nextbm, lvl, encode, scout, buf, qcnt, tiny);
     }
   }
+  }
+}
+
+// ---- top-down, hubs by owned target range ---------------------------------
+// The large step's hubs (out-degree >= own_dmin, listed by td_light) are
+// expanded range by range: CTA r takes, of every listed hub, the run of its
+// ascending out-list whose targets fall in r's id range (the split row gives
+// the bounds) and claims them against its slice of the next bitmap held in
+// shared memory: a shared-memory test per arc instead of an L2 lookup, and
+// exactly one winner per vertex.  Winners are logged per window of
+// own_span_w ids; after the runs, each window's parents are gathered in
+// shared memory and stored in vertex order (coalesced) -- random 4-byte
+// parent stores cost a DRAM sector read-modify-write each (profiles/r01
+// random_store_order.txt: 23 vs ~100 G stores/s sorted).  The slice is OR-ed
+// back because chunk claims of other CTAs may land in it meanwhile.
+__device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, uint32_t* nextbm, uint32_t* sm) {
+  constexpr int kE = 8;
+  const int r = blockIdx.x;
+  const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  const int sw = P.own_span_w;  // words per range = ids per window
+  const long long w0 = (long long)r * sw;
+  const long long w1 = w0 + sw < P.w32 ? w0 + sw : P.w32;
+  const int nw = w1 > w0 ? (int)(w1 - w0) : 0;
+  uint2* stage = P.own_stage + (int64_t)r * kOwnWin * sw;
+  for (int i = threadIdx.x; i < nw; i += kBlock) sm[i] = ld_bits(nextbm + w0 + i);
+  if (threadIdx.x < kOwnWin) s.own_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (unsigned long long g0 = 0; g0 < nown; g0 += kBlock) {
+    // up to kBlock hubs: their runs in this range, concatenated
+    const unsigned long long i = g0 + threadIdx.x;
+    uint32_t u = 0;
+    int64_t b = 0, len = 0;
+    if (i < nown) {
+      const OwnEnt e = P.own_list[i];
+      const uint32_t* row = P.own_split + (int64_t)e.rank * (P.own_r + 1) + r;
+      const uint32_t s0 = __ldg(row), s1 = __ldg(row + 1);
+      u = e.u;
+      b = e.base + s0;
+      len = (int64_t)s1 - s0;
+    }
+    int64_t tot;
+    const int64_t pre = block_exscan(len, &tot, s);
+    s.td.t_u[threadIdx.x] = u;
+    s.td.t_b[threadIdx.x] = b - pre;  // arc of concatenated position e is t_b[o] + e
+    s.td.t_pre[threadIdx.x] = pre;
+    __syncthreads();
+    // Each warp takes a contiguous segment, lanes on consecutive positions
+    // (coalesced), and advances its run index as the positions cross run
+    // starts -- no per-arc search.
+    const int64_t seg = ((tot + kWarps - 1) / kWarps + 31) & ~int64_t(31);
+    const int64_t eb = (int64_t)warp * seg;
+    const int64_t ee = eb + seg < tot ? eb + seg : tot;
+    if (eb < ee) {
+      int lo = 0, hi = kBlock - 1;  // run holding position eb + lane (clamped)
+      const int64_t e0 = eb + lane < ee ? eb + lane : ee - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s.td.t_pre[mid] <= e0) lo = mid;
+        else hi = mid - 1;
+      }
+      int o = lo;
+      int64_t nxt = o + 1 < kBlock ? s.td.t_pre[o + 1] : tot;
+      int64_t ob = s.td.t_b[o];
+      uint32_t ou = s.td.t_u[o];
+      for (int64_t e = eb + lane; e - (int64_t)lane < ee; e += 32 * kE) {
+        uint32_t v[kE], uu[kE];
+#pragma unroll
+        for (int k = 0; k < kE; k++) {
+          const int64_t ek = e + 32 * k;
+          v[k] = kNoVertex;
+          uu[k] = 0;
+          if (ek < ee) {
+            while (ek >= nxt) {
+              o++;
+              nxt = o + 1 < kBlock ? s.td.t_pre[o + 1] : tot;
+              ob = s.td.t_b[o];
+              ou = s.td.t_u[o];
+            }
+            v[k] = ld_nb_once(P.out_nb + ob + ek);
+            uu[k] = ou;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kE; k++) {
+          if (v[k] == kNoVertex) continue;
+          const uint32_t vl = (uint32_t)((long long)v[k] - w0 * 32);  // id within the range
+          const uint32_t wl = vl >> 5, bit = 1u << (vl & 31u);
+          if (!(sm[wl] & bit) && !(atomicOr(&sm[wl], bit) & bit)) {
+            const uint32_t win = vl / (uint32_t)sw;
+            const uint32_t at = atomicAdd(&s.own_cnt[win], 1u);
+            stage[(int64_t)win * sw + at] = make_uint2(vl - win * sw, uu[k]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < nw; i += kBlock) atomicOr(nextbm + w0 + i, sm[i]);
+  __syncthreads();
+  // Parents, window by window: gather the window's logged claims into
+  // shared memory (the slice's space), then store them in vertex order.
+  int32_t* par = reinterpret_cast<int32_t*>(sm);
+  const long long id0 = w0 * 32;
+  for (int win = 0; win < kOwnWin; win++) {
+    const unsigned cnt = s.own_cnt[win];
+    if (cnt == 0) continue;  // uniform
+    const long long lo = id0 + (long long)win * sw;
+    for (int i = threadIdx.x; i < sw; i += kBlock) par[i] = -2;
+    __syncthreads();
+    const uint2* st = stage + (int64_t)win * sw;
+    for (unsigned j = threadIdx.x; j < cnt; j += kBlock) {
+      const uint2 c = __ldcg(st + j);
+      par[c.x] = (int32_t)c.y;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < sw; i += kBlock) {
+      const int32_t pv = par[i];
+      if (pv != -2) P.parent[lo + i] = pv;
+    }
+    __syncthreads();
   }
 }
 
@@ -756,7 +883,8 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         // vertex ranges of P.td_span ids, each pass's slice of next (and of
         // parent) staying L2-resident; the frontier's lists are re-streamed
         // per pass, which HBM does at full bandwidth.
-        unsigned long long nch = 0;
+        unsigned long long nch = 0, nown = 0;
+        const bool own = P.own_split != nullptr && P.td_passes == 1;
         for (int r = 0; r < P.td_passes; r++) {
           const uint32_t rlo = (uint32_t)((int64_t)r * P.td_span);
           const uint32_t rhi = r + 1 == P.td_passes ? 0xffffffffu : (uint32_t)((int64_t)(r + 1) * P.td_span);
@@ -764,14 +892,18 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
           {
             const QApp qa = qapp(P, ph, qtail);
             td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk, false, r == 0,
-                           rlo, rhi);
+                           rlo, rhi, own);
           }
           if (!grid_sync(P, s, ph, kTagTD)) return;
-          if (r == 0) nch = s.snap[kChunkCount];
-          if (nch) {
+          if (r == 0) {
+            nch = s.snap[kChunkCount];
+            nown = own ? s.snap[kOwnCount] : 0;
+          }
+          if (nch || nown) {
+            if (nown) td_own(P, s, nown, nextg, sfront);
             const QApp qa = qapp(P, ph, qtail);
-            td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, false, rlo, rhi);
-            if (!grid_sync(P, s, ph, kTagHeavy)) return;
+            if (nch) td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, false, rlo, rhi);
+            if (!grid_sync(P, s, ph, nown ? kTagOwn : kTagHeavy)) return;
           }
         }
       } else {
@@ -865,6 +997,9 @@ cudaError_t bfs_configure(int device, BfsLaunch* cfg) {
   if (occ < 1) return cudaErrorInvalidConfiguration;
   cfg->grid = sms * occ;
   cfg->block = kBlock;
+  size_t keep = 0;
+  if ((e = cudaOccupancyAvailableDynamicSMemPerBlock(&keep, bfs_persistent, occ, kBlock))) return e;
+  cfg->smem_keep_occ = keep & ~size_t(15);
   return cudaSuccess;
 }
 
@@ -880,6 +1015,9 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st
     if (e) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     grid = sms * occ;
+  } else if (p.own_split) {
+    dyn = (size_t)p.own_span_w * 4;
+    if (p.own_r != grid || dyn > cfg.smem_keep_occ) return cudaErrorInvalidConfiguration;
   }
   BfsParams local = p;
   void* args[] = {&local};

@@ -65,6 +65,11 @@ void free_graph(gk_graph* g) {
   cudaFree(g->bc_lv);
   cudaFree(g->bc_lvdeg);
   cudaFree(g->hbase);
+  cudaFree(g->hv_bits);
+  cudaFree(g->hv_base);
+  cudaFree(g->own_split);
+  cudaFree(g->own_list);
+  cudaFree(g->own_stage);
   cudaFree(g->queue);
   cudaFree(g->chunks);
   cudaFree(g->ctrl);
@@ -103,9 +108,34 @@ gk_status alloc_workspace(gk_graph* g) {
   CK(cudaEventCreate(&g->ev0), "event");
   CK(cudaEventCreate(&g->ev1), "event");
   CK(gk::bfs_configure(g->device, &g->launch), "configure bfs kernel");
+  if (getenv("GK_NO_FRONT_SMEM")) g->launch.smem_front_max = 0;  // tests: large-graph paths on small graphs
   CK(gk::dead_bitmap(g->in_off, n, g->dead, g->stream), "dead-vertex bitmap");
   CK(cudaMalloc(&g->hbase, sizeof(uint32_t) * std::max<int64_t>(w32, 1)), "alloc head index");
   CK(gk::build_head(g->in_off, g->in_nb, n, g->dead, g->hbase, &g->head, g->stream), "in-list heads");
+  // Owned-range hub expansion (gk_internal.cuh OwnEnt): one target range per
+  // CTA of the launch, its slice of the next bitmap in dynamic shared memory
+  // without lowering the occupancy; hubs (out-degree >= 4096) get split rows.
+  // Off when the slice does not fit (n > ~2^27 at 296 CTAs) or memory is short.
+  {
+    const int r = g->launch.grid;
+    const int64_t span_w = ((w32 + r - 1) / r + 3) & ~int64_t(3);
+    const bool fits = (size_t)span_w * 4 <= g->launch.smem_keep_occ && (size_t)w32 * 4 > g->launch.smem_front_max;
+    if (fits && !getenv("GK_NO_OWN")) {
+      int64_t nh = 0;
+      const char* dm = getenv("GK_OWN_DMIN");  // tests: hubs on small graphs
+      const int64_t dmin = dm ? std::max<int64_t>(1, strtoll(dm, nullptr, 10)) : 4096;
+      CK(gk::build_own(g->out_off, g->out_nb, n, dmin, r, span_w, size_t(1) << 30, &g->hv_bits, &g->hv_base,
+                       &g->own_split, &nh, g->stream),
+         "owned-range split rows");
+      if (nh > 0) {
+        CK(cudaMalloc(&g->own_list, sizeof(gk::OwnEnt) * nh), "alloc owned-range list");
+        CK(cudaMalloc(&g->own_stage, sizeof(uint2) * (size_t)r * gk::kOwnWin * span_w), "alloc owned-range log");
+        g->own_r = r;
+        g->own_span_w = span_w;
+        g->own_dmin = dmin;
+      }
+    }
+  }
   CK(cudaStreamSynchronize(g->stream), "dead-vertex bitmap");
   const char* pers = getenv("GK_L2_PERSIST");
   if (!pers || atoi(pers) != 0) {
@@ -153,6 +183,16 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
   p.dead = g->dead;
   p.head = g->head;
   p.hbase = g->hbase;
+  if (g->own_split && !p.front_in_smem && !getenv("GK_NO_OWN")) {
+    p.own_split = g->own_split;
+    p.hv_bits = g->hv_bits;
+    p.hv_base = g->hv_base;
+    p.own_list = g->own_list;
+    p.own_stage = g->own_stage;
+    p.own_r = g->own_r;
+    p.own_span_w = (int32_t)g->own_span_w;
+    p.own_dmin = g->own_dmin;
+  }
   p.bm0 = g->bm0;
   p.bm1 = g->bm1;
   // Large top-down steps additionally clear and fill the n/8-byte next

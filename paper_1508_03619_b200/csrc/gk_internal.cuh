@@ -34,8 +34,9 @@ namespace gk {
 constexpr int kTraceCap = 512;
 enum PhaseTag : unsigned char { kTagInit = 'I', kTagTD = 'T', kTagHeavy = 'H', kTagZero = 'Z', kTagQ2B = 'Q',
                                 kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S', kTagLong = 'L',
-                                kTagBcBack = 'D', kTagBcChunk = 'E', kTagBcScore = 'F' };
-enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend = 4, kLongCount = 5, kCount = 6, kSlots = 8 };
+                                kTagBcBack = 'D', kTagBcChunk = 'E', kTagBcScore = 'F', kTagOwn = 'O' };
+enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend = 4, kLongCount = 5, kCount = 6,
+                   kOwnCount = 7, kSlots = 8 };
 
 struct Ctrl {
   unsigned long long bar_count;  // monotonic grid-barrier arrivals
@@ -79,6 +80,20 @@ __host__ __device__ inline void head_unpack(const uint4& r, uint32_t* u) {
   u[3] = r.w;
 }
 
+// Owned-range hub expansion (large top-down steps): CTA r owns target ids
+// [r*span, (r+1)*span) (span = own_span_w*32) and stages that slice of the
+// next bitmap in shared memory; split[rank(u)*(R+1) + r] = first index in
+// u's (ascending) out-list whose target is >= r*span, for every vertex u of
+// out-degree >= own_dmin.  Claims are logged per window of own_span_w ids
+// (kOwnWin windows per range) in own_stage and their parents written window
+// by window in vertex order.
+constexpr int kOwnWin = 32;
+struct OwnEnt {
+  uint32_t u;
+  uint32_t rank;  // row of u in own_split
+  int64_t base;   // out_off[u]
+};
+
 struct BfsParams {
   int64_t n;
   int64_t m;
@@ -111,6 +126,14 @@ struct BfsParams {
   int64_t step_cap;
   unsigned long long timeout_ns;
   unsigned stop_after;  // leave after this many grid barriers (profiling only)
+  const uint32_t* own_split;  // null: owned-range expansion off
+  const uint32_t* hv_bits;    // vertices with a split row
+  const uint32_t* hv_base;    // per bitmap word: rank of its first split row
+  OwnEnt* own_list;           // the step's frontier vertices with split rows
+  uint2* own_stage;           // [R][kOwnWin][own_span_w] logged claims {id - window start, parent}
+  int32_t own_r;              // ranges = CTAs of the launch
+  int32_t own_span_w;         // bitmap words per range (multiple of 4) = ids per window
+  int64_t own_dmin;           // out-degree that gets a split row
   int32_t td_passes;    // large top-down steps: target-range passes (1 when next fits L2)
   int64_t td_span;      // ids per pass (multiple of 32)
   // Brandes (betweenness.hpp:38-80), bc_persistent only
@@ -135,6 +158,7 @@ struct BfsLaunch {
   int block = kBlock;
   size_t smem_static = 0;
   size_t smem_front_max = 0;  // largest front bitmap (bytes) staged in smem
+  size_t smem_keep_occ = 0;   // largest dynamic smem that keeps the occupancy of grid
 };
 cudaError_t bfs_configure(int device, BfsLaunch* cfg);
 cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t s);
@@ -145,6 +169,13 @@ cudaError_t bc_normalize(float* scores, int64_t n, float* scratch_max, cudaStrea
 
 // Auxiliary (untimed) kernels.
 cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s);
+// Owned-range split rows (see OwnEnt) for out-degree >= dmin, ranges of
+// span_w bitmap words.  *nh = rows built; 0 rows (and null arrays) when no
+// vertex qualifies, a qualifying out-list is not ascending, or the table
+// would exceed max_bytes.
+cudaError_t build_own(const int64_t* out_off, const uint32_t* out_nb, int64_t n, int64_t dmin, int r,
+                      int64_t span_w, size_t max_bytes, uint32_t** hv_bits, uint32_t** hv_base,
+                      uint32_t** split, int64_t* nh, cudaStream_t s);
 // CSR invariants: n rows with offsets monotone from 0 to m, neighbour ids < id_bound.
 cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int64_t m, int64_t id_bound,
                          bool* offsets_ok, bool* ids_ok, cudaStream_t s);
@@ -202,6 +233,13 @@ struct gk_graph {
   uint32_t* bm0 = nullptr;
   uint32_t* bm1 = nullptr;
   uint32_t* dead = nullptr;  // graph property, computed once by finish_graph
+  uint32_t* hv_bits = nullptr;   // owned-range hub expansion (see OwnEnt), null when off
+  uint32_t* hv_base = nullptr;
+  uint32_t* own_split = nullptr;
+  gk::OwnEnt* own_list = nullptr;
+  uint2* own_stage = nullptr;
+  int own_r = 0;
+  int64_t own_span_w = 0, own_dmin = 0;
   gk::HeadRec* head = nullptr;  // ditto: the first kHead entries of every live in-list
   uint32_t* hbase = nullptr; // ditto: head index of each word's first live vertex
   // Brandes workspace, allocated on first use

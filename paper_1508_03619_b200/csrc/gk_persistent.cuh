@@ -35,6 +35,7 @@ struct __align__(16) SmemT {
   long long red[kWarps + 2];
   unsigned long long bcast[4];
   unsigned long long snap[kSlots];  // counter set of the phase the last grid_sync ended
+  unsigned own_cnt[kOwnWin];        // td_own: claims logged per window
   int ok;
 };
 

@@ -149,3 +149,29 @@ def test_malformed_csr_rejected():
                            in_offsets=np.array([0, 0, 1], np.int64), in_neighbors=np.array([5], np.uint32))
     ok = DeviceGraph.upload(3, np.array([0, 1, 2, 2], np.int64), np.array([1, 0], np.uint32))
     assert ok.bfs(0).parent.tolist() == [0, 0, -1]
+
+
+@pytest.mark.parametrize("dmin", ["1", "40", "300"])
+def test_owned_range_hub_expansion(dmin, monkeypatch):
+    # GK_OWN_DMIN makes small graphs' hubs take the owned-range expansion of
+    # large top-down steps (td_own) that kron scale >= 21 uses by itself;
+    # GK_NO_FRONT_SMEM keeps the bitmaps in global memory as at that size
+    monkeypatch.setenv("GK_NO_FRONT_SMEM", "1")
+    monkeypatch.setenv("GK_OWN_DMIN", dmin)
+    seen = set()
+    for kind, scale in (("kron", 16), ("urand", 14)):
+        g = O.make_graph(kind, scale, permute=kind == "kron")
+        dg = DeviceGraph.from_csr(g)
+        for s in O.pick_sources(g, 6, 7):
+            for a, b in ((15, 18), (2, 2)):
+                check(g, dg, int(s), a, b)
+                seen |= {t[0] for t in dg.trace()}
+    assert "O" in seen  # the owned-range phase ran
+    for n in (33, 1000, 1025):
+        rng = np.random.default_rng(n)
+        e = rng.integers(0, n, size=6 * n, dtype=np.uint64).astype(np.uint32)
+        g = O.build_csr(n, e)
+        dg = DeviceGraph.from_csr(g)
+        for s in {0, n - 1}:
+            check(g, dg, s, 1, 1)
+            check(g, dg, s)
