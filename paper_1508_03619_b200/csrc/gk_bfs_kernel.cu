@@ -84,6 +84,8 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
         if (P.want_depth) P.depth[v[k]] = lvl + 1;
         const long long d = o1[k] - o0[k];
         scout += encode ? (d ? d : 1) : 1;
+        // the next level reads this list: start pulling it toward L2 now
+        if (encode && d) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.out_nb + o0[k]));
       }
     }
 #pragma unroll
