@@ -63,7 +63,7 @@ __global__ void k_live_count(const uint32_t* __restrict__ dead, int64_t w32, uin
 // v's record is hbase[v/32] + (live vertices before v in its word).
 __global__ void k_head(const int64_t* __restrict__ in_off, const uint32_t* __restrict__ in_nb, int64_t n,
                        const uint32_t* __restrict__ dead, const uint32_t* __restrict__ hbase,
-                       HeadRec* __restrict__ head) {
+                       HeadRec* __restrict__ head, HeadRec* __restrict__ head2) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t live = ~dead[v >> 5];
     const uint32_t bit = (uint32_t)(v & 31);
@@ -74,6 +74,11 @@ __global__ void k_head(const int64_t* __restrict__ in_off, const uint32_t* __res
 #pragma unroll
     for (int j = 0; j < kHead; j++) h[j] = j < d ? in_nb[b + j] : kNoVertex;
     head[idx] = head_pack(h, (HeadRec*)nullptr);
+    if (head2) {
+#pragma unroll
+      for (int j = 0; j < kHead; j++) h[j] = kHead + j < d ? in_nb[b + kHead + j] : kNoVertex;
+      head2[idx] = head_pack(h, (HeadRec*)nullptr);
+    }
   }
 }
 
@@ -312,9 +317,10 @@ cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int6
 }
 
 cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, const uint32_t* dead,
-                       uint32_t* hbase, HeadRec** head, cudaStream_t s) {
+                       uint32_t* hbase, HeadRec** head, HeadRec** head2, cudaStream_t s) {
   const int64_t w32 = (n + 31) / 32;
   *head = nullptr;
+  if (head2) *head2 = nullptr;
   if (w32 == 0) return cudaSuccess;
   uint32_t* cnt = nullptr;
   void* tmp = nullptr;
@@ -332,7 +338,11 @@ cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, 
   {
     const int64_t live = (int64_t)last[0] + last[1];
     if ((e = cudaMalloc(head, sizeof(HeadRec) * (live > 0 ? live : 1)))) goto out;
-    k_head<<<aux_grid(n), kAuxBlock, 0, s>>>(in_off, in_nb, n, dead, hbase, *head);
+    if (head2 && cudaMalloc(head2, sizeof(HeadRec) * (live > 0 ? live : 1)) != cudaSuccess) {
+      cudaGetLastError();  // optional: without it the second round reads in_off/in_nb
+      *head2 = nullptr;
+    }
+    k_head<<<aux_grid(n), kAuxBlock, 0, s>>>(in_off, in_nb, n, dead, hbase, *head, head2 ? *head2 : nullptr);
     e = cudaGetLastError();
   }
 out:

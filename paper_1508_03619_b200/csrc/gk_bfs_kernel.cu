@@ -554,7 +554,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
     int next_c = 0;
     uint32_t v[kBuSlots], d[kBuSlots], rounds[kBuSlots];
     int64_t b[kBuSlots];
-    int st[kBuSlots];  // 0 empty, 1 head round, 2 in_nb rounds
+    int st[kBuSlots];  // 0 empty, 1 head round, 3 second-head round, 2 in_nb rounds
 #pragma unroll
     for (int k = 0; k < kBuSlots; k++) {
       st[k] = 0;
@@ -567,6 +567,7 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
       for (int k = 0; k < kBuSlots; k++) {
         const bool need = st[k] == 0;
         const unsigned nm = __ballot_sync(kFull, need);
+        if (nm == 0 || next_c >= total) continue;  // uniform: nothing to hand out
         const int c = next_c + __popc(nm & lanemask_lt());
         next_c += __popc(nm);
         int lo = 0;  // word holding the c-th pending vertex: last lane with excl <= c
@@ -601,6 +602,8 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
       for (int k = 0; k < kBuSlots; k++) {
         if (st[k] == 1) {
           head_unpack(__ldg(P.head + b[k]), u[k]);
+        } else if (st[k] == 3) {
+          head_unpack(__ldg(P.head2 + b[k]), u[k]);
         } else {
 #pragma unroll
           for (int j = 0; j < kPerRound; j++)
@@ -630,10 +633,21 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
             st[k] = 0;
           } else if (u[k][kHead - 1] == kNoVertex) {
             st[k] = 0;  // the list ended inside the head: not reached at this level
+          } else if (P.head2) {
+            st[k] = 3;  // round 2: the next kHead in-neighbours, same record index
           } else {
             b[k] = ld_off(P.in_off + v[k]) + kHead;
             d[k] = (uint32_t)(ld_off(P.in_off + v[k] + 1) - b[k]);
             rounds[k] = 1;
+            st[k] = d[k] ? 2 : 0;
+          }
+        } else if (st[k] == 3) {
+          if (u[k][kHead - 1] == kNoVertex) {
+            st[k] = 0;  // the list ended inside the second head
+          } else {
+            b[k] = ld_off(P.in_off + v[k]) + 2 * kHead;
+            d[k] = (uint32_t)(ld_off(P.in_off + v[k] + 1) - b[k]);
+            rounds[k] = 2;
             st[k] = d[k] ? 2 : 0;
           }
         } else {

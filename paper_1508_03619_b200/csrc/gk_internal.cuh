@@ -116,6 +116,7 @@ struct BfsParams {
   uint32_t* bm1;
   const uint32_t* dead;  // in-degree-0 vertices (+ ids >= n): never reachable
   const HeadRec* head;   // first kHead in-neighbours of every live vertex (kNoVertex-padded)
+  const HeadRec* head2;  // the next kHead in-neighbours (same index), or null
   const uint32_t* hbase; // per bitmap word: index of its first live vertex's head
   uint32_t* queue;
   Chunk* chunks;
@@ -185,7 +186,7 @@ cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int6
 // hbase[w] = live (non-dead) vertices in words < w; head is allocated here
 // with one record per live vertex.
 cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, const uint32_t* dead,
-                       uint32_t* hbase, HeadRec** head, cudaStream_t s);
+                       uint32_t* hbase, HeadRec** head, HeadRec** head2, cudaStream_t s);
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s);
 cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
@@ -241,6 +242,7 @@ struct gk_graph {
   int own_r = 0;
   int64_t own_span_w = 0, own_dmin = 0;
   gk::HeadRec* head = nullptr;  // ditto: the first kHead entries of every live in-list
+  gk::HeadRec* head2 = nullptr; // ditto: entries kHead..2*kHead-1 (optional)
   uint32_t* hbase = nullptr; // ditto: head index of each word's first live vertex
   // Brandes workspace, allocated on first use
   double2* bc_sd = nullptr;
