@@ -175,3 +175,26 @@ def test_owned_range_hub_expansion(dmin, monkeypatch):
         for s in {0, n - 1}:
             check(g, dg, s, 1, 1)
             check(g, dg, s)
+
+
+@pytest.mark.parametrize("no_head2", ["0", "1"])
+def test_bottom_up_rounds_with_and_without_second_head(no_head2, monkeypatch):
+    # the second head record (in-neighbours 4..7) replaces the first in_nb
+    # round; without it (GK_NO_HEAD2) round 2 reads in_off/in_nb as before.
+    # Lists of every length around the 4/8 boundaries, bottom-up parents
+    # must equal the reference's first hit.
+    if no_head2 == "1":
+        monkeypatch.setenv("GK_NO_HEAD2", "1")
+    rng = np.random.default_rng(11)
+    n = 3000
+    deg = rng.integers(0, 14, size=n)
+    e = np.array([x for v in range(n) for w in rng.integers(0, n, size=deg[v]) for x in (v, w)], np.uint32)
+    g = O.build_csr(n, e)
+    dg = DeviceGraph.from_csr(g)
+    for s in O.pick_sources(g, 5, 3):
+        for a, b in ((1000, 1000), (15, 18), (1, 1)):
+            check(g, dg, int(s), a, b)
+    gu = O.make_graph("urand", 14)
+    dgu = DeviceGraph.from_csr(gu)
+    for s in O.pick_sources(gu, 3, 5):
+        check(gu, dgu, int(s))
