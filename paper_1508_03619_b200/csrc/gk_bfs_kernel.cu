@@ -615,12 +615,25 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         if (!st[k]) continue;
         bool hit = false;
         uint32_t par = 0;
+        // The first in-neighbour's front bit alone, then the rest of the
+        // round's at once: one lookup when the first hits, two latencies
+        // instead of up to kPerRound otherwise (measured against all-at-once
+        // and strictly sequential: +1.5-2% on kron27 and urand27).
+        uint32_t fw[kPerRound];
+        fw[0] = u[k][0] != kNoVertex ? (kSmem ? front[u[k][0] >> 5] : ld_front(front + (u[k][0] >> 5))) : 0u;
+        if ((fw[0] >> (u[k][0] & 31u)) & 1u) {
+          hit = true;
+          par = u[k][0];
+        } else {
 #pragma unroll
-        for (int j = 0; j < kPerRound; j++) {
-          if (!hit && u[k][j] != kNoVertex && front_bit<kSmem>(front, u[k][j])) {
-            hit = true;
-            par = u[k][j];
-          }
+          for (int j = 1; j < kPerRound; j++)
+            fw[j] = u[k][j] != kNoVertex ? (kSmem ? front[u[k][j] >> 5] : ld_front(front + (u[k][j] >> 5))) : 0u;
+#pragma unroll
+          for (int j = 1; j < kPerRound; j++)
+            if (!hit && ((fw[j] >> (u[k][j] & 31u)) & 1u)) {
+              hit = true;
+              par = u[k][j];
+            }
         }
         if (hit) {
           P.parent[v[k]] = (int32_t)par;
