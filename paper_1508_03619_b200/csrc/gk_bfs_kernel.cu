@@ -496,7 +496,10 @@ __device__ void td_scout_bits(const BfsParams& P, uint32_t* bm, int lvl, bool en
 // front bit is set, as in bfs.hpp:55-60.  Results are OR-ed into per-warp
 // shared-memory words and written back once per task.  Vertices without
 // in-edges never appear: visited starts as the graph's dead bitmap.
-constexpr int kBuSlots = 2;
+#ifndef GK_BU_SLOTS
+#define GK_BU_SLOTS 3  // 2: -0.9% on kron27; 4: spills, -7%
+#endif
+constexpr int kBuSlots = GK_BU_SLOTS;
 constexpr int kPerRound = 4;    // in-neighbours tested per slot per round
 constexpr int kLaneRounds = 12;  // rounds before a list is deferred to the long list (8-16 measured flat)
 static_assert(kHead <= kPerRound, "a head round tests one head record");
