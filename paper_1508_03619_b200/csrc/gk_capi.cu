@@ -5,6 +5,7 @@
 // CPU path: without a device, compute entry points fail with
 // GK_ERR_NO_DEVICE.
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -212,6 +213,9 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
     p.td_span = ((g->n + p.td_passes - 1) / p.td_passes + 31) / 32 * 32;
   }
   if (const char* bt = getenv("GK_BITMAP_TD_MIN")) p.bitmap_td_min = strtoll(bt, nullptr, 10);
+  // kTopDownRescan re-reads every new frontier's queue (bfs.hpp:161-167):
+  // its steps keep the queue path (large steps leave the frontier a bitmap)
+  if (strategy == GK_BFS_TOP_DOWN_RESCAN) p.bitmap_td_min = INT64_MAX;
   p.queue = g->queue;
   p.chunks = g->chunks;
   p.chunk_cap = g->chunk_cap;

@@ -198,3 +198,13 @@ def test_bottom_up_rounds_with_and_without_second_head(no_head2, monkeypatch):
     dgu = DeviceGraph.from_csr(gu)
     for s in O.pick_sources(gu, 3, 5):
         check(gu, dgu, int(s))
+
+
+def test_rescan_strategy_on_fresh_handle():
+    # kTopDownRescan re-reads each new frontier's queue (bfs.hpp:161-167):
+    # its large steps must write that queue even when no earlier traversal
+    # on the handle left the same entries behind
+    g = O.make_graph("kron", 16, permute=True)
+    for s in O.pick_sources(g, 3, 9):
+        dg = DeviceGraph.from_csr(g)
+        check(g, dg, int(s), strategy=int(BfsStrategy.kTopDownRescan))
