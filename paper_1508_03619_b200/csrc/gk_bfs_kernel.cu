@@ -298,11 +298,13 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
   constexpr int kE = 8;
   const int r = blockIdx.x;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-  const int sw = P.own_span_w;  // words per range = ids per window
+  const int sw = P.own_span_w;  // words per range
+  const int wlog = P.own_win_log;  // ids per window = 2^wlog <= sw (a shift, not a divide, per claim)
+  const int nwin = (32 * sw + (1 << wlog) - 1) >> wlog;  // <= kOwnWin
   const long long w0 = (long long)r * sw;
   const long long w1 = w0 + sw < P.w32 ? w0 + sw : P.w32;
   const int nw = w1 > w0 ? (int)(w1 - w0) : 0;
-  uint2* stage = P.own_stage + (int64_t)r * kOwnWin * sw;
+  uint2* stage = P.own_stage + (int64_t)r * ((int64_t)nwin << wlog);
   for (int i = threadIdx.x; i < nw; i += kBlock) sm[i] = ld_bits(nextbm + w0 + i);
   if (threadIdx.x < kOwnWin) s.own_cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -367,9 +369,9 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
           const uint32_t vl = (uint32_t)((long long)v[k] - w0 * 32);  // id within the range
           const uint32_t wl = vl >> 5, bit = 1u << (vl & 31u);
           if (!(sm[wl] & bit) && !(atomicOr(&sm[wl], bit) & bit)) {
-            const uint32_t win = vl / (uint32_t)sw;
+            const uint32_t win = vl >> wlog;
             const uint32_t at = atomicAdd(&s.own_cnt[win], 1u);
-            stage[(int64_t)win * sw + at] = make_uint2(vl - win * sw, uu[k]);
+            stage[((int64_t)win << wlog) + at] = make_uint2(vl & ((1u << wlog) - 1u), uu[k]);
           }
         }
       }
@@ -382,19 +384,20 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
   // shared memory (the slice's space), then store them in vertex order.
   int32_t* par = reinterpret_cast<int32_t*>(sm);
   const long long id0 = w0 * 32;
-  for (int win = 0; win < kOwnWin; win++) {
+  const int ws = 1 << wlog;
+  for (int win = 0; win < nwin; win++) {
     const unsigned cnt = s.own_cnt[win];
     if (cnt == 0) continue;  // uniform
-    const long long lo = id0 + (long long)win * sw;
-    for (int i = threadIdx.x; i < sw; i += kBlock) par[i] = -2;
+    const long long lo = id0 + ((long long)win << wlog);
+    for (int i = threadIdx.x; i < ws; i += kBlock) par[i] = -2;
     __syncthreads();
-    const uint2* st = stage + (int64_t)win * sw;
+    const uint2* st = stage + ((int64_t)win << wlog);
     for (unsigned j = threadIdx.x; j < cnt; j += kBlock) {
       const uint2 c = __ldcg(st + j);
       par[c.x] = (int32_t)c.y;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < sw; i += kBlock) {
+    for (int i = threadIdx.x; i < ws; i += kBlock) {
       const int32_t pv = par[i];
       if (pv != -2) P.parent[lo + i] = pv;
     }

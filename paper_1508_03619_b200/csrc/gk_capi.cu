@@ -131,7 +131,11 @@ gk_status alloc_workspace(gk_graph* g) {
          "owned-range split rows");
       if (nh > 0) {
         CK(cudaMalloc(&g->own_list, sizeof(gk::OwnEnt) * nh), "alloc owned-range list");
-        CK(cudaMalloc(&g->own_stage, sizeof(uint2) * (size_t)r * gk::kOwnWin * span_w), "alloc owned-range log");
+        int wl = 0;
+        while ((int64_t(2) << wl) <= span_w) wl++;
+        const int64_t nwin = (32 * span_w + (int64_t(1) << wl) - 1) >> wl;  // <= kOwnWin
+        CK(cudaMalloc(&g->own_stage, sizeof(uint2) * (size_t)r * (size_t)(nwin << wl)), "alloc owned-range log");
+        g->own_win_log = wl;
         g->own_r = r;
         g->own_span_w = span_w;
         g->own_dmin = dmin;
@@ -194,6 +198,7 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
     p.own_stage = g->own_stage;
     p.own_r = g->own_r;
     p.own_span_w = (int32_t)g->own_span_w;
+    p.own_win_log = g->own_win_log;
     p.own_dmin = g->own_dmin;
   }
   p.bm0 = g->bm0;

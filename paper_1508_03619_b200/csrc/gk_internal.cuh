@@ -87,7 +87,7 @@ __host__ __device__ inline void head_unpack(const uint4& r, uint32_t* u) {
 // out-degree >= own_dmin.  Claims are logged per window of own_span_w ids
 // (kOwnWin windows per range) in own_stage and their parents written window
 // by window in vertex order.
-constexpr int kOwnWin = 32;
+constexpr int kOwnWin = 64;  // windows per owned range, at most
 struct OwnEnt {
   uint32_t u;
   uint32_t rank;  // row of u in own_split
@@ -131,9 +131,10 @@ struct BfsParams {
   const uint32_t* hv_bits;    // vertices with a split row
   const uint32_t* hv_base;    // per bitmap word: rank of its first split row
   OwnEnt* own_list;           // the step's frontier vertices with split rows
-  uint2* own_stage;           // [R][kOwnWin][own_span_w] logged claims {id - window start, parent}
+  uint2* own_stage;           // [R][windows][2^own_win_log] logged claims {id - window start, parent}
   int32_t own_r;              // ranges = CTAs of the launch
-  int32_t own_span_w;         // bitmap words per range (multiple of 4) = ids per window
+  int32_t own_span_w;         // bitmap words per range (multiple of 4)
+  int32_t own_win_log;        // ids per claim-log window = 2^own_win_log <= own_span_w
   int64_t own_dmin;           // out-degree that gets a split row
   int32_t td_passes;    // large top-down steps: target-range passes (1 when next fits L2)
   int64_t td_span;      // ids per pass (multiple of 32)
@@ -241,6 +242,7 @@ struct gk_graph {
   uint2* own_stage = nullptr;
   int own_r = 0;
   int64_t own_span_w = 0, own_dmin = 0;
+  int own_win_log = 0;
   gk::HeadRec* head = nullptr;  // ditto: the first kHead entries of every live in-list
   gk::HeadRec* head2 = nullptr; // ditto: entries kHead..2*kHead-1 (optional)
   uint32_t* hbase = nullptr; // ditto: head index of each word's first live vertex
