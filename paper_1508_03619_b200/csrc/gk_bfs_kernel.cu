@@ -503,6 +503,8 @@ __device__ void td_scout_bits(const BfsParams& P, uint32_t* bm, int lvl, bool en
 #define GK_BU_SLOTS 3  // 2: -0.9% on kron27; 4: spills, -7%
 #endif
 constexpr int kBuSlots = GK_BU_SLOTS;
+constexpr int kBuListWords = 512 + 64;  // per warp: 1024 uint16 pending ids + 32 head bases + 32 live words
+constexpr size_t kBuListBytes = (size_t)kWarps * kBuListWords * 4;
 constexpr int kPerRound = 4;    // in-neighbours tested per slot per round
 constexpr int kLaneRounds = 12;  // rounds before a list is deferred to the long list (8-16 measured flat)
 static_assert(kHead <= kPerRound, "a head round tests one head record");
@@ -516,8 +518,21 @@ __device__ __forceinline__ bool front_bit(const uint32_t* front, uint32_t u) {
 
 template <bool kSmem>
 __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_t* front, uint32_t* next,
-                        int lvl, unsigned long long long_base, int tw_log, long long& awake) {
+                        int lvl, unsigned long long long_base, int tw_log, long long& awake, uint32_t* wsm) {
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+  // kList (front read from global memory, so the dynamic shared memory is
+  // free): the task's pending vertices are listed once in shared memory and
+  // a refill is one list read instead of a shuffle binary search.
+  constexpr bool kList = !kSmem;
+  uint16_t* lst = nullptr;
+  uint32_t* s_hb = nullptr;
+  uint32_t* s_lv = nullptr;
+  if constexpr (kList) {
+    uint32_t* base = wsm + warp * (kBuListWords);
+    lst = reinterpret_cast<uint16_t*>(base);
+    s_hb = base + 512;
+    s_lv = base + 544;
+  }
   uint32_t* acc_n = s.bu_acc[warp][0];
   uint32_t* acc_d = s.bu_acc[warp][1];
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
@@ -554,6 +569,17 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
     }
     const int excl = incl - cnt;
     const int total = __shfl_sync(kFull, incl, 31);
+    if constexpr (kList) {
+      s_hb[lane] = hb;
+      s_lv[lane] = live;
+      uint32_t m = pm;
+      int pos = excl;
+      while (m) {
+        const int bt = __ffs(m) - 1;
+        m &= m - 1;
+        lst[pos++] = (uint16_t)((lane << 5) | bt);
+      }
+    }
     acc_n[lane] = 0u;
     acc_d[lane] = 0u;
     __syncwarp();
@@ -576,6 +602,17 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         if (nm == 0 || next_c >= total) continue;  // uniform: nothing to hand out
         const int c = next_c + __popc(nm & lanemask_lt());
         next_c += __popc(nm);
+        if constexpr (kList) {
+          if (need && c < total) {
+            const uint32_t e = lst[c];
+            const uint32_t wd = e >> 5, bit = e & 31u;
+            v[k] = (uint32_t)((tbase + wd) * 32 + bit);
+            b[k] = (int64_t)s_hb[wd] + __popc(s_lv[wd] & ((1u << bit) - 1u));  // head record
+            rounds[k] = 0;
+            st[k] = 1;
+          }
+          continue;
+        }
         int lo = 0;  // word holding the c-th pending vertex: last lane with excl <= c
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1) {
@@ -860,8 +897,8 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         long long acc = 0;
         // long-list scratch: queue slots past the tail are unused during bottom-up
         const unsigned long long lbase = qe;
-        if (P.front_in_smem) bu_step<true>(P, s, ph, fr, nextg, lvl, lbase, bu_tw_log, acc);
-        else bu_step<false>(P, s, ph, fr, nextg, lvl, lbase, bu_tw_log, acc);
+        if (P.front_in_smem) bu_step<true>(P, s, ph, fr, nextg, lvl, lbase, bu_tw_log, acc, nullptr);
+        else bu_step<false>(P, s, ph, fr, nextg, lvl, lbase, bu_tw_log, acc, sfront);
         unsigned set = ph & 3;
         block_add(acc, &P.ctrl->cnt[set][kSum], s);
         if (!grid_sync(P, s, ph, kTagBU)) return;
@@ -1050,9 +1087,14 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st
     if (e) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     grid = sms * occ;
-  } else if (p.own_split) {
-    dyn = (size_t)p.own_span_w * 4;
-    if (p.own_r != grid || dyn > cfg.smem_keep_occ) return cudaErrorInvalidConfiguration;
+  } else {
+    // bottom-up pending lists; the owned-range slice when hub expansion is on
+    dyn = kBuListBytes;
+    if (p.own_split) {
+      if (p.own_r != grid) return cudaErrorInvalidConfiguration;
+      dyn = std::max(dyn, (size_t)p.own_span_w * 4);
+    }
+    if (dyn > cfg.smem_keep_occ) return cudaErrorInvalidConfiguration;
   }
   BfsParams local = p;
   void* args[] = {&local};
