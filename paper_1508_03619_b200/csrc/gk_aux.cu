@@ -317,9 +317,10 @@ cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int6
 }
 
 cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, const uint32_t* dead,
-                       uint32_t* hbase, HeadRec** head, HeadRec** head2, cudaStream_t s) {
+                       uint32_t* hbase, HeadRec** head, HeadRec** head2, int64_t* nlive, cudaStream_t s) {
   const int64_t w32 = (n + 31) / 32;
   *head = nullptr;
+  *nlive = 0;
   if (head2) *head2 = nullptr;
   if (w32 == 0) return cudaSuccess;
   uint32_t* cnt = nullptr;
@@ -337,6 +338,7 @@ cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, 
   if ((e = cudaStreamSynchronize(s))) goto out;
   {
     const int64_t live = (int64_t)last[0] + last[1];
+    *nlive = live;
     if ((e = cudaMalloc(head, sizeof(HeadRec) * (live > 0 ? live : 1)))) goto out;
     if (head2 && cudaMalloc(head2, sizeof(HeadRec) * (live > 0 ? live : 1)) != cudaSuccess) {
       cudaGetLastError();  // optional: without it the second round reads in_off/in_nb

@@ -734,14 +734,14 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
 // Long in-lists deferred by bu_step: one warp per vertex, ballot over 32
 // neighbours at a time, resuming after the head and the kLaneRounds-1
 // in_nb rounds bu_step tested.
-template <bool kSmem>
-__device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* next,
-                        unsigned long long base, unsigned long long count, int lvl, long long& awake) {
+template <bool kSmem, bool kPull = false>
+__device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* next, const uint32_t* lst,
+                        unsigned long long count, int lvl, long long& awake, long long& scout) {
   const unsigned lane = lane_id();
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
   for (long long i = gw; i < (long long)count; i += nw) {
-    const uint32_t v = __ldcg(P.queue + base + i);
+    const uint32_t v = __ldcg(lst + i);
     const int64_t le = P.in_off[v + 1];
     for (int64_t j = P.in_off[v] + kHead + kPerRound * (kLaneRounds - 1); j < le; j += 32) {
       const int64_t jj = j + lane;
@@ -760,6 +760,10 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
           atomicOr(next + (v >> 5), 1u << (v & 31u));
           atomicOr(P.visited + (v >> 5), 1u << (v & 31u));
           awake++;
+          if constexpr (kPull) {  // top-down result of the claim (bfs.hpp:83)
+            const int64_t dg = P.out_off[v + 1] - P.out_off[v];
+            scout += dg ? dg : 1;
+          }
         }
         break;
       }
@@ -767,24 +771,206 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
   }
 }
 
-// ---- BitmapToQueue (bfs.hpp:99-113) ----------------------------------------
-__device__ void b2q(const BfsParams& P, const QApp& qa, const uint32_t* front, SmemT& s) {
-  for (long long base = (long long)blockIdx.x * kBlock; base < P.w32;
-       base += (long long)gridDim.x * kBlock) {
-    const long long w = base + threadIdx.x;
-    uint32_t word = w < P.w32 ? __ldcg(front + w) : 0u;
-    int64_t tot;
-    const int64_t pre = block_exscan(__popc(word), &tot, s);
-    if (tot == 0) continue;
-    if (threadIdx.x == 0) s.bcast[0] = qa.base + atomicAdd(qa.ctr, (unsigned long long)tot);
-    __syncthreads();
-    unsigned long long q = s.bcast[0] + pre;
-    while (word) {
-      const int bp = __ffs(word) - 1;
-      word &= word - 1;
-      P.queue[q++] = (uint32_t)(w * 32 + bp);
+// ---- sparse sweeps: few vertices left unreached ----------------------------
+// Once the unreached (pending) vertices are few, a bottom-up step -- or a
+// top-down step of the reference's schedule whose frontier is larger than
+// the pending set, executed as a pull (same claimed set: unvisited vertices
+// with an in-neighbour in the frontier; parents are any frontier
+// in-neighbour, as top-down's racy claims also are) -- costs one list pass:
+// sp_list writes the pending vertices to a list (and clears next),
+// sp_scan gives each one a thread that scans its in-list in ascending order
+// (first hit = parent, as bfs.hpp:55-60) for up to kSparseScan entries and
+// defers longer lists to bu_long.  A full bu_step sweep costs ~0.1 ms at
+// scale 27 even when nothing is pending (one dependent chain per task).
+constexpr int kSparseScan = kHead + kPerRound * (kLaneRounds - 1);  // where bu_long resumes
+
+__device__ void sp_list(const BfsParams& P, unsigned long long* ctr, uint32_t* lst, uint32_t* next) {
+  const unsigned lane = lane_id();
+  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  for (long long seg = gw * 256; seg < P.w32; seg += nw * 256) {
+    const long long w0 = seg + lane * 8;
+    uint32_t wd[8];
+    if (w0 + 8 <= P.w32 && (w0 + 8) * 32 <= P.n) {  // two 16-byte loads and stores
+      const uint4 x = __ldcg(reinterpret_cast<const uint4*>(P.visited + w0));
+      const uint4 y = __ldcg(reinterpret_cast<const uint4*>(P.visited + w0 + 4));
+      wd[0] = ~x.x; wd[1] = ~x.y; wd[2] = ~x.z; wd[3] = ~x.w;
+      wd[4] = ~y.x; wd[5] = ~y.y; wd[6] = ~y.z; wd[7] = ~y.w;
+      reinterpret_cast<uint4*>(next + w0)[0] = make_uint4(0u, 0u, 0u, 0u);
+      reinterpret_cast<uint4*>(next + w0)[1] = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const long long w = w0 + j;
+        wd[j] = 0u;
+        if (w < P.w32) {
+          const int64_t rem = P.n - w * 32;
+          const uint32_t pad = rem < 32 ? 0xffffffffu << rem : 0u;
+          wd[j] = ~(ld_bits(P.visited + w) | pad);  // visited includes the dead set
+          next[w] = 0u;
+        }
+      }
     }
-    __syncthreads();
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) cnt += __popc(wd[j]);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    if (total == 0) continue;  // uniform
+    unsigned long long q = 0;
+    if (lane == 0) q = atomicAdd(ctr, (unsigned long long)total);
+    q = __shfl_sync(kFull, q, 0) + (incl - cnt);
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      for (uint32_t m = wd[j]; m; m &= m - 1) lst[q++] = (uint32_t)((w0 + j) * 32 + (__ffs(m) - 1));
+    }
+  }
+}
+
+template <bool kPull>
+__device__ void sp_scan(const BfsParams& P, unsigned ph, const uint32_t* front, uint32_t* next, const uint32_t* lst,
+                        unsigned long long cnt, uint32_t* lng, int lvl, long long& found, long long& scout) {
+  // two list entries per thread in flight, their in-list rounds interleaved
+  constexpr int kS = 2;
+  const long long gtid = (long long)blockIdx.x * kBlock + threadIdx.x;
+  const long long gthreads = (long long)gridDim.x * kBlock;
+  for (long long i0 = gtid; i0 < (long long)cnt; i0 += kS * gthreads) {
+    uint32_t v[kS], par[kS];
+    int64_t o0[kS], o1[kS], j[kS], lim[kS];
+    bool act[kS], hit[kS];
+#pragma unroll
+    for (int k = 0; k < kS; k++) {
+      const long long i = i0 + k * gthreads;
+      act[k] = i < (long long)cnt;
+      hit[k] = false;
+      par[k] = 0;
+      v[k] = act[k] ? __ldcg(lst + i) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kS; k++) {
+      o0[k] = act[k] ? ld_off(P.in_off + v[k]) : 0;
+      o1[k] = act[k] ? ld_off(P.in_off + v[k] + 1) : 0;
+      lim[k] = o1[k] - o0[k] > kSparseScan ? o0[k] + kSparseScan : o1[k];
+      j[k] = o0[k];
+      act[k] = act[k] && j[k] < lim[k];
+    }
+    while (act[0] || act[1]) {
+      uint32_t u[kS][kPerRound], fw[kS][kPerRound];
+#pragma unroll
+      for (int k = 0; k < kS; k++)
+#pragma unroll
+        for (int q = 0; q < kPerRound; q++) u[k][q] = act[k] && j[k] + q < lim[k] ? ld_nb(P.in_nb + j[k] + q) : kNoVertex;
+#pragma unroll
+      for (int k = 0; k < kS; k++)
+#pragma unroll
+        for (int q = 0; q < kPerRound; q++) fw[k][q] = u[k][q] != kNoVertex ? ld_front(front + (u[k][q] >> 5)) : 0u;
+#pragma unroll
+      for (int k = 0; k < kS; k++) {
+#pragma unroll
+        for (int q = 0; q < kPerRound; q++)
+          if (!hit[k] && ((fw[k][q] >> (u[k][q] & 31u)) & 1u)) {
+            hit[k] = true;
+            par[k] = u[k][q];
+          }
+        j[k] += kPerRound;
+        act[k] = act[k] && !hit[k] && j[k] < lim[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kS; k++) {
+      if (hit[k]) {
+        const uint32_t vv = v[k];
+        P.parent[vv] = (int32_t)par[k];
+        if (P.want_depth) P.depth[vv] = lvl + 1;
+        atomicOr(next + (vv >> 5), 1u << (vv & 31u));
+        atomicOr(P.visited + (vv >> 5), 1u << (vv & 31u));
+        found++;
+        if constexpr (kPull) {
+          const int64_t dg = P.out_off[vv + 1] - P.out_off[vv];
+          scout += dg ? dg : 1;
+        }
+      } else if (i0 + k * gthreads < (long long)cnt && o1[k] - o0[k] > kSparseScan) {
+        lng[atomicAdd(&P.ctrl->cnt[ph & 3][kLongCount], 1ull)] = v[k];
+      }
+    }
+  }
+}
+
+// One sparse step: list, scan, long lists.  found / scout (kPull) are the
+// grid totals (uniform) when it returns true.
+template <bool kPull>
+__device__ bool sparse_step(const BfsParams& P, SmemT& s, unsigned& ph, const uint32_t* front, uint32_t* next,
+                            int lvl, long long& found, long long& scout) {
+  uint32_t* lst = reinterpret_cast<uint32_t*>(P.chunks);  // free outside top-down steps
+  sp_list(P, &P.ctrl->cnt[ph & 3][kAppend], lst, next);
+  if (!grid_sync(P, s, ph, kTagZero)) return false;
+  const unsigned long long cnt = s.snap[kAppend];
+  long long f = 0, sc = 0;
+  sp_scan<kPull>(P, ph, front, next, lst, cnt, lst + cnt, lvl, f, sc);
+  unsigned set = ph & 3;
+  block_add(f, &P.ctrl->cnt[set][kSum], s);
+  if (kPull) block_add(sc, &P.ctrl->cnt[set][kCount], s);
+  if (!grid_sync(P, s, ph, kPull ? kTagPull : kTagBU)) return false;
+  found = (long long)s.snap[kSum];
+  scout = kPull ? (long long)s.snap[kCount] : 0;
+  const unsigned long long nlong = s.snap[kLongCount];
+  if (nlong) {
+    f = sc = 0;
+    bu_long<false, kPull>(P, front, next, lst + cnt, nlong, lvl, f, sc);
+    set = ph & 3;
+    block_add(f, &P.ctrl->cnt[set][kSum], s);
+    if (kPull) block_add(sc, &P.ctrl->cnt[set][kCount], s);
+    if (!grid_sync(P, s, ph, kTagLong)) return false;
+    found += (long long)s.snap[kSum];
+    if (kPull) scout += (long long)s.snap[kCount];
+  }
+  return true;
+}
+
+// ---- BitmapToQueue (bfs.hpp:99-113) ----------------------------------------
+__device__ void b2q(const BfsParams& P, const QApp& qa, const uint32_t* front) {
+  // A warp takes 256 words (lane l: 8 consecutive words, two 16-byte
+  // loads), numbers their vertices with a warp scan and appends them with
+  // one fetch-add: no CTA barriers, and few enough counter atomics that a
+  // sparse front costs about one pass over the bitmap.
+  const unsigned lane = lane_id();
+  const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * kBlock) >> 5;
+  for (long long seg = gw * 256; seg < P.w32; seg += nw * 256) {
+    const long long w0 = seg + lane * 8;
+    uint32_t wd[8];
+    if (w0 + 8 <= P.w32) {
+      const uint4 x = __ldcg(reinterpret_cast<const uint4*>(front + w0));
+      const uint4 y = __ldcg(reinterpret_cast<const uint4*>(front + w0 + 4));
+      wd[0] = x.x; wd[1] = x.y; wd[2] = x.z; wd[3] = x.w;
+      wd[4] = y.x; wd[5] = y.y; wd[6] = y.z; wd[7] = y.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; j++) wd[j] = w0 + j < P.w32 ? __ldcg(front + w0 + j) : 0u;
+    }
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) cnt += __popc(wd[j]);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if ((int)lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    if (total == 0) continue;  // uniform
+    unsigned long long q = 0;
+    if (lane == 0) q = qa.base + atomicAdd(qa.ctr, (unsigned long long)total);
+    q = __shfl_sync(kFull, q, 0) + (incl - cnt);
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      for (uint32_t m = wd[j]; m; m &= m - 1) P.queue[q++] = (uint32_t)((w0 + j) * 32 + (__ffs(m) - 1));
+    }
   }
 }
 
@@ -801,6 +987,9 @@ __device__ void log_step(const BfsParams& P, long long idx, int dir, long long f
   }
 }
 
+#ifndef GK_SPARSE
+#define GK_SPARSE 1
+#endif
 __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   extern __shared__ uint4 dyn_smem[];
   __shared__ SmemT s;
@@ -850,6 +1039,10 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   long long etc = P.m;                                  // bfs.hpp:139
   long long scout = P.out_off[src + 1] - P.out_off[src];  // bfs.hpp:140
   long long nsteps = 0;
+  long long reached = 1;  // vertices claimed so far (source included)
+  long long dummy = 0;
+  // sparse sweeps while few vertices are pending (and the list scratch holds them twice)
+  auto sparse_ok = [&](long long pend) { return !P.front_in_smem && GK_SPARSE && pend <= P.w32 && 2 * pend <= 4 * P.chunk_cap; };
   int lvl = 0;
   int qcnt = 0;
   bool front_ready = false;  // frontg holds exactly the current frontier
@@ -863,8 +1056,12 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
 
   while (qe > qs) {
     const bool go_bu = P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha;
-    if (!go_bu && queue_stale) {  // BitmapToQueue for the coming top-down step
-      b2q(P, qapp(P, ph, qtail), frontg, s);
+    // a top-down step whose (bitmap) frontier outnumbers the pending
+    // vertices is executed as a sparse pull (see sparse_step)
+    const bool pull = !go_bu && P.strategy == GK_BFS_DIRECTION_OPTIMIZING && front_ready &&
+                      P.live - reached <= (long long)(qe - qs) && sparse_ok(P.live - reached);
+    if (!go_bu && !pull && queue_stale) {  // BitmapToQueue for the coming top-down step
+      b2q(P, qapp(P, ph, qtail), frontg);
       if (!grid_sync(P, s, ph, kTagB2Q)) return;
       qtail += s.snap[kAppend];
       queue_stale = false;
@@ -895,6 +1092,18 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
           fr = sfront;
         }
         long long acc = 0;
+        if (sparse_ok(P.live - reached)) {
+          long long found = 0;
+          if (!sparse_step<false>(P, s, ph, frontg, nextg, lvl, found, dummy)) return;
+          awake = found;
+          reached += awake;
+          log_step(P, nsteps++, 'B', old_awake, awake, etc);
+          lvl++;
+          uint32_t* t = frontg;
+          frontg = nextg;
+          nextg = t;
+          continue;
+        }
         // long-list scratch: queue slots past the tail are unused during bottom-up
         const unsigned long long lbase = qe;
         if (P.front_in_smem) bu_step<true>(P, s, ph, fr, nextg, lvl, lbase, bu_tw_log, acc, nullptr);
@@ -906,29 +1115,54 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         long long awake_bu = (long long)s.snap[kSum];
         if (nlong) {
           acc = 0;
-          if (P.front_in_smem) bu_long<true>(P, fr, nextg, lbase, nlong, lvl, acc);
-          else bu_long<false>(P, fr, nextg, lbase, nlong, lvl, acc);
+          if (P.front_in_smem) bu_long<true>(P, fr, nextg, P.queue + lbase, nlong, lvl, acc, dummy);
+          else bu_long<false>(P, fr, nextg, P.queue + lbase, nlong, lvl, acc, dummy);
           set = ph & 3;
           block_add(acc, &P.ctrl->cnt[set][kSum], s);
           if (!grid_sync(P, s, ph, kTagLong)) return;
           awake_bu += (long long)s.snap[kSum];
         }
         awake = awake_bu;
+        reached += awake;
         log_step(P, nsteps++, 'B', old_awake, awake, etc);
         lvl++;
         uint32_t* t = frontg;
         frontg = nextg;
         nextg = t;
       } while (awake >= old_awake || awake > P.n / P.beta);
-      b2q(P, qapp(P, ph, qtail), frontg, s);  // bfs.hpp:155
-      if (!grid_sync(P, s, ph, kTagB2Q)) return;
-      qtail += s.snap[kAppend];
-      qe = qtail;
+      if (P.live - reached <= awake && sparse_ok(P.live - reached)) {
+        // the coming top-down step is pulled (see above): no queue needed
+        qs = qtail;
+        qe = qtail + awake;
+        queue_stale = true;
+      } else {
+        b2q(P, qapp(P, ph, qtail), frontg);  // bfs.hpp:155
+        if (!grid_sync(P, s, ph, kTagB2Q)) return;
+        qtail += s.snap[kAppend];
+        qe = qtail;
+      }
       scout = 1;  // bfs.hpp:156
       front_ready = true;
     } else {
       etc -= scout;  // bfs.hpp:158
       const long long fsize = (long long)(qe - qs);
+      if (pull) {
+        long long claimed = 0, sc = 0;
+        if (!sparse_step<true>(P, s, ph, frontg, nextg, lvl, claimed, sc)) return;
+        scout = sc;
+        reached += claimed;
+        uint32_t* t = frontg;
+        frontg = nextg;
+        nextg = t;
+        front_ready = true;
+        qs = qtail;  // bitmap-only frontier, as after a large top-down step
+        qe = qtail + claimed;
+        queue_stale = true;
+        log_step(P, nsteps++, 'T', fsize, scout, etc);
+        lvl++;
+        continue;
+      }
+      const unsigned long long qt0 = qtail;
       // Large frontiers (by the degree total the heuristic already holds)
       // also build the next-frontier bitmap and sum degrees in a separate
       // high-MLP pass; small ones keep everything inline, so a long chain of
@@ -1012,6 +1246,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         if (!grid_sync(P, s, ph, kTagSweep)) return;
         scout = (long long)s.snap[kSum];
         const unsigned long long claimed = s.snap[kCount];
+        reached += (long long)claimed;
         uint32_t* t = frontg;
         frontg = nextg;
         nextg = t;
@@ -1024,6 +1259,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         queue_stale = true;
       } else {
         front_ready = false;
+        reached += (long long)(qtail - qt0);
         qs = qe;  // SlideWindow (bfs.hpp:160)
         qe = qtail;
       }

@@ -113,7 +113,7 @@ gk_status alloc_workspace(gk_graph* g) {
   if (getenv("GK_NO_FRONT_SMEM")) g->launch.smem_front_max = 0;  // tests: large-graph paths on small graphs
   CK(gk::dead_bitmap(g->in_off, n, g->dead, g->stream), "dead-vertex bitmap");
   CK(cudaMalloc(&g->hbase, sizeof(uint32_t) * std::max<int64_t>(w32, 1)), "alloc head index");
-  CK(gk::build_head(g->in_off, g->in_nb, n, g->dead, g->hbase, &g->head, &g->head2, g->stream), "in-list heads");
+  CK(gk::build_head(g->in_off, g->in_nb, n, g->dead, g->hbase, &g->head, &g->head2, &g->live, g->stream), "in-list heads");
   // Owned-range hub expansion (gk_internal.cuh OwnEnt): one target range per
   // CTA of the launch, its slice of the next bitmap in dynamic shared memory
   // without lowering the occupancy; hubs (out-degree >= 4096) get split rows.
@@ -190,6 +190,7 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
   p.head = g->head;
   p.head2 = getenv("GK_NO_HEAD2") ? nullptr : g->head2;
   p.hbase = g->hbase;
+  p.live = g->live;
   if (g->own_split && !p.front_in_smem && !getenv("GK_NO_OWN")) {
     p.own_split = g->own_split;
     p.hv_bits = g->hv_bits;

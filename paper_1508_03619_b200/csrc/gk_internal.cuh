@@ -34,7 +34,7 @@ namespace gk {
 constexpr int kTraceCap = 512;
 enum PhaseTag : unsigned char { kTagInit = 'I', kTagTD = 'T', kTagHeavy = 'H', kTagZero = 'Z', kTagQ2B = 'Q',
                                 kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S', kTagLong = 'L',
-                                kTagBcBack = 'D', kTagBcChunk = 'E', kTagBcScore = 'F', kTagOwn = 'O' };
+                                kTagBcBack = 'D', kTagBcChunk = 'E', kTagBcScore = 'F', kTagOwn = 'O', kTagPull = 'P' };
 enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend = 4, kLongCount = 5, kCount = 6,
                    kOwnCount = 7, kSlots = 8 };
 
@@ -118,6 +118,7 @@ struct BfsParams {
   const HeadRec* head;   // first kHead in-neighbours of every live vertex (kNoVertex-padded)
   const HeadRec* head2;  // the next kHead in-neighbours (same index), or null
   const uint32_t* hbase; // per bitmap word: index of its first live vertex's head
+  int64_t live;          // vertices with in-edges (not dead)
   uint32_t* queue;
   Chunk* chunks;
   int64_t chunk_cap;
@@ -187,7 +188,7 @@ cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int6
 // hbase[w] = live (non-dead) vertices in words < w; head is allocated here
 // with one record per live vertex.
 cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, const uint32_t* dead,
-                       uint32_t* hbase, HeadRec** head, HeadRec** head2, cudaStream_t s);
+                       uint32_t* hbase, HeadRec** head, HeadRec** head2, int64_t* nlive, cudaStream_t s);
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s);
 cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
@@ -243,6 +244,7 @@ struct gk_graph {
   int own_r = 0;
   int64_t own_span_w = 0, own_dmin = 0;
   int own_win_log = 0;
+  int64_t live = 0;  // vertices with in-edges
   gk::HeadRec* head = nullptr;  // ditto: the first kHead entries of every live in-list
   gk::HeadRec* head2 = nullptr; // ditto: entries kHead..2*kHead-1 (optional)
   uint32_t* hbase = nullptr; // ditto: head index of each word's first live vertex

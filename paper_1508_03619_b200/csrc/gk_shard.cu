@@ -891,7 +891,8 @@ gk_status shard_alloc(gk_shard* s) {
   SCK(cudaMalloc(&s->hbase, sizeof(uint32_t) * wl), "alloc head index");
   // graph-derived, once: never-reachable owned vertices, head records
   SCK(gk::dead_bitmap(s->off, s->nloc, s->dead, nullptr), "dead bitmap");
-  SCK(gk::build_head(s->off, s->nb, s->nloc, s->dead, s->hbase, &s->head, nullptr, nullptr), "head records");
+  int64_t nlive = 0;
+  SCK(gk::build_head(s->off, s->nb, s->nloc, s->dead, s->hbase, &s->head, nullptr, &nlive, nullptr), "head records");
   SCK(cudaStreamSynchronize(nullptr), "shard derived data");
   return GK_OK;
 }
