@@ -291,7 +291,26 @@ int aux_grid(int64_t n) {
   return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
+// Out-degree per vertex clamped to 65535 (= "read the offsets"), zero past
+// n up to a whole bitmap word: the large top-down step's claim sweep sums
+// the claimed vertices' degrees from these 2n bytes instead of from the
+// 8n-byte offsets.
+__global__ void k_deg16(const int64_t* off, int64_t n, int64_t nw, uint16_t* deg16) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nw; v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t d = 0;
+    if (v < n) d = off[v + 1] - off[v];
+    deg16[v] = (uint16_t)(d < 65535 ? d : 65535);
+  }
+}
+
 }  // namespace
+
+cudaError_t build_deg16(const int64_t* off, int64_t n, uint16_t* deg16, cudaStream_t s) {
+  const int64_t nw = (n + 31) / 32 * 32;
+  if (nw == 0) return cudaSuccess;
+  k_deg16<<<aux_grid(nw), kAuxBlock, 0, s>>>(off, n, nw, deg16);
+  return cudaGetLastError();
+}
 
 cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s) {
   const int64_t w32 = (n + 31) / 32;

@@ -438,45 +438,40 @@ __device__ void td_scout_bits(const BfsParams& P, uint32_t* bm, int lvl, bool en
       if (cl != nx) bm[w0 + lane] = cl;
       if (cl) P.visited[w0 + lane] = vis | cl;
     }
-    const int cnt = __popc(cl);
-    count += cnt;
-    int incl = cnt;
+    count += __popc(cl);
+    if (cl) {
+      // degrees of the word's 32 vertices: 64 bytes of deg16, summed under
+      // the claim mask two at a time (halfword SIMD); 0 counts 1
+      // (bfs.hpp:130's encoding), 65535 means "read the offsets"
+      const uint4* dp = reinterpret_cast<const uint4*>(P.deg16 + (w0 + lane) * 32);
+      uint32_t dw[16];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(kFull, incl, o);
-      if ((int)lane >= o) incl += y;
-    }
-    const int excl = incl - cnt;
-    const int total = __shfl_sync(kFull, incl, 31);
-    for (int base = 0; base < total; base += 128) {
-      int64_t o0[4], o1[4];
-      int64_t v[4];
+      for (int q = 0; q < 4; q++) {
+        const uint4 t = __ldg(dp + q);
+        dw[4 * q] = t.x;
+        dw[4 * q + 1] = t.y;
+        dw[4 * q + 2] = t.z;
+        dw[4 * q + 3] = t.w;
+      }
+      if (!encode) {
+        scout += __popc(cl);
+      } else {
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const int c = base + k * 32 + (int)lane;
-        int lo = 0;  // word holding the c-th claim: last lane with excl <= c
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int e = __shfl_sync(kFull, excl, lo + step);
-          if (e <= c) lo += step;
-        }
-        const uint32_t m = __shfl_sync(kFull, cl, lo);
-        const int ex = __shfl_sync(kFull, excl, lo);
-        v[k] = -1;
-        o0[k] = o1[k] = 0;
-        if (c < total) {
-          v[k] = (w0 + lo) * 32 + (int)__fns(m, 0, c - ex + 1);
-          o0[k] = __ldg(P.out_off + v[k]);
-          o1[k] = __ldg(P.out_off + v[k] + 1);
+        for (int j = 0; j < 16; j++) {
+          const uint32_t pr = (cl >> (2 * j)) & 3u;
+          const uint32_t msk = (pr & 1u ? 0x0000FFFFu : 0u) | (pr & 2u ? 0xFFFF0000u : 0u);
+          scout += __vsadu2(dw[j] & msk, 0u) + __popc(__vcmpeq2(dw[j], 0u) & msk) / 16;
+          uint32_t big = __vcmpeq2(dw[j], 0xFFFFFFFFu) & msk;
+          while (big) {  // out-degree >= 65535: the exact value from the offsets
+            const int bt = (__ffs(big) - 1) >> 4;
+            big &= ~(0xFFFFu << (16 * bt));
+            const int64_t v = (w0 + lane) * 32 + 2 * j + bt;
+            scout += (P.out_off[v + 1] - P.out_off[v]) - 65535;
+          }
         }
       }
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        if (v[k] < 0) continue;
-        const long long d = o1[k] - o0[k];
-        scout += encode ? (d ? d : 1) : 1;
-        if (P.want_depth) P.depth[v[k]] = lvl + 1;
-      }
+      if (P.want_depth)
+        for (uint32_t m = cl; m; m &= m - 1) P.depth[(w0 + lane) * 32 + (__ffs(m) - 1)] = lvl + 1;
     }
     nx = nx_n;
     vis = vis_n;

@@ -67,6 +67,7 @@ void free_graph(gk_graph* g) {
   cudaFree(g->bc_lv);
   cudaFree(g->bc_lvdeg);
   cudaFree(g->hbase);
+  cudaFree(g->deg16);
   cudaFree(g->hv_bits);
   cudaFree(g->hv_base);
   cudaFree(g->own_split);
@@ -114,6 +115,8 @@ gk_status alloc_workspace(gk_graph* g) {
   CK(gk::dead_bitmap(g->in_off, n, g->dead, g->stream), "dead-vertex bitmap");
   CK(cudaMalloc(&g->hbase, sizeof(uint32_t) * std::max<int64_t>(w32, 1)), "alloc head index");
   CK(gk::build_head(g->in_off, g->in_nb, n, g->dead, g->hbase, &g->head, &g->head2, &g->live, g->stream), "in-list heads");
+  CK(cudaMalloc(&g->deg16, std::max<int64_t>(w32, 1) * 64), "alloc degree array");
+  CK(gk::build_deg16(g->out_off, n, g->deg16, g->stream), "degree array");
   // Owned-range hub expansion (gk_internal.cuh OwnEnt): one target range per
   // CTA of the launch, its slice of the next bitmap in dynamic shared memory
   // without lowering the occupancy; hubs (out-degree >= 4096) get split rows.
@@ -191,6 +194,7 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
   p.head2 = getenv("GK_NO_HEAD2") ? nullptr : g->head2;
   p.hbase = g->hbase;
   p.live = g->live;
+  p.deg16 = g->deg16;
   if (g->own_split && !p.front_in_smem && !getenv("GK_NO_OWN")) {
     p.own_split = g->own_split;
     p.hv_bits = g->hv_bits;

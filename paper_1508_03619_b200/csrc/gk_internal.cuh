@@ -119,6 +119,7 @@ struct BfsParams {
   const HeadRec* head2;  // the next kHead in-neighbours (same index), or null
   const uint32_t* hbase; // per bitmap word: index of its first live vertex's head
   int64_t live;          // vertices with in-edges (not dead)
+  const uint16_t* deg16; // out-degree clamped to 65535 (65535: read out_off), padded to whole words
   uint32_t* queue;
   Chunk* chunks;
   int64_t chunk_cap;
@@ -172,6 +173,7 @@ cudaError_t bc_normalize(float* scores, int64_t n, float* scratch_max, cudaStrea
 
 // Auxiliary (untimed) kernels.
 cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s);
+cudaError_t build_deg16(const int64_t* off, int64_t n, uint16_t* deg16, cudaStream_t s);
 // Owned-range split rows (see OwnEnt) for out-degree >= dmin, ranges of
 // span_w bitmap words.  *nh = rows built; 0 rows (and null arrays) when no
 // vertex qualifies, a qualifying out-list is not ascending, or the table
@@ -245,6 +247,7 @@ struct gk_graph {
   int64_t own_span_w = 0, own_dmin = 0;
   int own_win_log = 0;
   int64_t live = 0;  // vertices with in-edges
+  uint16_t* deg16 = nullptr;  // out-degree clamped to 65535, for the claim sweep
   gk::HeadRec* head = nullptr;  // ditto: the first kHead entries of every live in-list
   gk::HeadRec* head2 = nullptr; // ditto: entries kHead..2*kHead-1 (optional)
   uint32_t* hbase = nullptr; // ditto: head index of each word's first live vertex

@@ -208,3 +208,25 @@ def test_rescan_strategy_on_fresh_handle():
     for s in O.pick_sources(g, 3, 9):
         dg = DeviceGraph.from_csr(g)
         check(g, dg, int(s), strategy=int(BfsStrategy.kTopDownRescan))
+
+
+def test_sparse_sweeps_and_pulled_top_down(monkeypatch):
+    # Once few vertices are unreached, bottom-up steps scan a list of them
+    # and a top-down step whose frontier outnumbers them runs as a pull
+    # ('P' in the trace): same claimed set and counters as the reference's
+    # top-down step (schedule and results equal the replay), bottom-up
+    # parents still the reference's first hit.  Directed graphs pull over
+    # in-edges and sum out-degrees.
+    monkeypatch.setenv("GK_NO_FRONT_SMEM", "1")
+    seen = set()
+    graphs = [O.make_graph("kron", 16, permute=True), O.make_graph("urand", 15)]
+    n = 4000
+    rng = np.random.default_rng(5)
+    e = rng.integers(0, n, size=2 * 8 * n, dtype=np.uint64).astype(np.uint32)
+    graphs.append(O.build_csr(n, e, symmetrize=False, directed=True))
+    for g in graphs:
+        dg = DeviceGraph.from_csr(g)
+        for s in O.pick_sources(g, 6, 13):
+            check(g, dg, int(s))
+            seen |= {t[0] for t in dg.trace()}
+    assert "P" in seen
