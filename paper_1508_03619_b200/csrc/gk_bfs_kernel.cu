@@ -9,7 +9,8 @@
 // per level instead of a launch + sync.
 //
 // Phases (each ends at a grid barrier):
-//   init      parent[:] = -1, visited[:] = 0, parent[src] = src, queue = [src]
+//   init      parent[:] = -1 (a memset just ahead of the kernel, see bfs_launch),
+//             visited := dead set, parent[src] = src, queue = [src]
 //             (replaces the degree-encoding init bfs.hpp:126-132: the
 //             claim test uses a 1-bit visited map in L2 instead of the
 //             parent sign, and the claimed vertex's degree -- what the
@@ -1001,14 +1002,14 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
     int4* p4 = reinterpret_cast<int4*>(P.parent);
     int4* d4 = reinterpret_cast<int4*>(P.depth);
     const int4 m1 = make_int4(-1, -1, -1, -1);
+    if (!P.parent_preset) {
 #pragma unroll 4
-    for (long long i = gtid; i < n4; i += gthreads) {
-      p4[i] = m1;
-      if (P.want_depth) d4[i] = m1;
+      for (long long i = gtid; i < n4; i += gthreads) p4[i] = m1;
+      for (long long i = (n4 << 2) + gtid; i < P.n; i += gthreads) P.parent[i] = -1;
     }
-    for (long long i = (n4 << 2) + gtid; i < P.n; i += gthreads) {
-      P.parent[i] = -1;
-      if (P.want_depth) P.depth[i] = -1;
+    if (P.want_depth) {
+      for (long long i = gtid; i < n4; i += gthreads) d4[i] = m1;
+      for (long long i = (n4 << 2) + gtid; i < P.n; i += gthreads) P.depth[i] = -1;
     }
     // visited starts as the never-reachable set, so sweeps skip it
     const long long w4 = P.w32 >> 2;
@@ -1328,6 +1329,14 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st
     if (dyn > cfg.smem_keep_occ) return cudaErrorInvalidConfiguration;
   }
   BfsParams local = p;
+  // parent := -1 by a memset on the launch stream, inside the caller's timed
+  // region: measured 1% faster per BFS at scale 27 than the same stores in
+  // the kernel's init phase (GK_KERNEL_INIT=1 keeps them there)
+  if (!getenv("GK_KERNEL_INIT")) {
+    cudaError_t e = cudaMemsetAsync(p.parent, 0xFF, sizeof(int32_t) * (size_t)p.n, st);
+    if (e) return e;
+    local.parent_preset = 1;
+  }
   void* args[] = {&local};
   return cudaLaunchCooperativeKernel((const void*)bfs_persistent, dim3(grid), dim3(cfg.block), args,
                                      dyn, st);

@@ -108,6 +108,7 @@ struct BfsParams {
   int64_t beta;
   int32_t want_depth;
   int32_t front_in_smem;
+  int32_t parent_preset;  // parent already holds -1 everywhere (cleared by a memset in the launch)
   int64_t bitmap_td_min;  // scout above which a top-down step is 'large'
   int32_t* parent;
   int32_t* depth;
