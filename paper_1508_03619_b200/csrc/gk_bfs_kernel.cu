@@ -295,8 +295,11 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
 // parent stores cost a DRAM sector read-modify-write each (profiles/r01
 // random_store_order.txt: 23 vs ~100 G stores/s sorted).  The slice is OR-ed
 // back because chunk claims of other CTAs may land in it meanwhile.
+#ifndef GK_OWN_KE
+#define GK_OWN_KE 12  // 4: -1.2%, 8: -0.3% on kron27
+#endif
 __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, uint32_t* nextbm, uint32_t* sm) {
-  constexpr int kE = 8;
+  constexpr int kE = GK_OWN_KE;  // arcs per lane in flight
   const int r = blockIdx.x;
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
   const int sw = P.own_span_w;  // words per range
@@ -330,49 +333,53 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
     __syncthreads();
     // Each warp takes a contiguous segment, lanes on consecutive positions
     // (coalesced), and advances its run index as the positions cross run
-    // starts -- no per-arc search.
-    const int64_t seg = ((tot + kWarps - 1) / kWarps + 31) & ~int64_t(31);
-    const int64_t eb = (int64_t)warp * seg;
-    const int64_t ee = eb + seg < tot ? eb + seg : tot;
+    // starts -- no per-arc search.  Positions within a group, ids within the
+    // range and log indices are 32-bit (fewer live registers in the loop).
+    const int tot32 = (int)tot;
+    const int seg = ((tot32 + kWarps - 1) / kWarps + 31) & ~31;
+    const int eb = (int)warp * seg;
+    const int ee = eb + seg < tot32 ? eb + seg : tot32;
     if (eb < ee) {
       int lo = 0, hi = kBlock - 1;  // run holding position eb + lane (clamped)
-      const int64_t e0 = eb + lane < ee ? eb + lane : ee - 1;
+      const int e0 = eb + (int)lane < ee ? eb + (int)lane : ee - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (s.td.t_pre[mid] <= e0) lo = mid;
         else hi = mid - 1;
       }
       int o = lo;
-      int64_t nxt = o + 1 < kBlock ? s.td.t_pre[o + 1] : tot;
-      int64_t ob = s.td.t_b[o];
+      int nxt = o + 1 < kBlock ? (int)s.td.t_pre[o + 1] : tot32;
+      const uint32_t* rb = P.out_nb + s.td.t_b[o];  // arc of position e is rb[e]
       uint32_t ou = s.td.t_u[o];
-      for (int64_t e = eb + lane; e - (int64_t)lane < ee; e += 32 * kE) {
+      const uint32_t id0 = (uint32_t)(w0 * 32);
+      const uint32_t wmask = (1u << wlog) - 1u;
+      for (int e = eb + (int)lane; e - (int)lane < ee; e += 32 * kE) {
         uint32_t v[kE], uu[kE];
 #pragma unroll
         for (int k = 0; k < kE; k++) {
-          const int64_t ek = e + 32 * k;
+          const int ek = e + 32 * k;
           v[k] = kNoVertex;
           uu[k] = 0;
           if (ek < ee) {
             while (ek >= nxt) {
               o++;
-              nxt = o + 1 < kBlock ? s.td.t_pre[o + 1] : tot;
-              ob = s.td.t_b[o];
+              nxt = o + 1 < kBlock ? (int)s.td.t_pre[o + 1] : tot32;
+              rb = P.out_nb + s.td.t_b[o];
               ou = s.td.t_u[o];
             }
-            v[k] = ld_nb_once(P.out_nb + ob + ek);
+            v[k] = ld_nb_once(rb + ek);
             uu[k] = ou;
           }
         }
 #pragma unroll
         for (int k = 0; k < kE; k++) {
           if (v[k] == kNoVertex) continue;
-          const uint32_t vl = (uint32_t)((long long)v[k] - w0 * 32);  // id within the range
+          const uint32_t vl = v[k] - id0;  // id within the range
           const uint32_t wl = vl >> 5, bit = 1u << (vl & 31u);
           if (!(sm[wl] & bit) && !(atomicOr(&sm[wl], bit) & bit)) {
             const uint32_t win = vl >> wlog;
             const uint32_t at = atomicAdd(&s.own_cnt[win], 1u);
-            stage[((int64_t)win << wlog) + at] = make_uint2(vl & ((1u << wlog) - 1u), uu[k]);
+            stage[(win << wlog) + at] = make_uint2(vl & wmask, uu[k]);
           }
         }
       }
