@@ -59,7 +59,7 @@ class BfsResult:
     parent: np.ndarray | None
     depth: np.ndarray | None
     device_ms: float
-    steps: list = field(default_factory=list)  # (dir, frontier, result, edges_to_check)
+    steps: list = field(default_factory=list)  # (dir, frontier, result, edges_to_check, executed-as)
     num_steps: int = 0
     reached: int = -1
     component_edges: int = -1
@@ -227,7 +227,10 @@ class DeviceGraph:
         _check(L.gk_bfs(self._h, int(source), int(alpha), int(beta), int(strategy), pp, dp, C.byref(st)),
                "gk_bfs")
         k = min(st.num_steps, max_steps)
-        sl = [(chr(steps[i].dir), steps[i].frontier, steps[i].result, steps[i].edges_to_check) for i in range(k)]
+        # (direction, frontier, result, edges_to_check, executed-as: '' or 'P' pushed
+        # bottom-up / 'U' pulled top-down -- same claimed set and counters)
+        sl = [(chr(steps[i].dir), steps[i].frontier, steps[i].result, steps[i].edges_to_check,
+               chr(steps[i].pad) if steps[i].pad else "") for i in range(k)]
         return BfsResult(pa[: self.n] if pa is not None else None, da[: self.n] if da is not None else None,
                          st.device_ms, sl, st.num_steps, st.reached, st.component_edges)
 

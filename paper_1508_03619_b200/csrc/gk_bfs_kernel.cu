@@ -977,12 +977,14 @@ __device__ void b2q(const BfsParams& P, const QApp& qa, const uint32_t* front) {
   }
 }
 
+// exec: how the step ran when not as its direction names (0; 'P' a
+// bottom-up step executed as a push, 'U' a top-down step executed as a pull)
 __device__ void log_step(const BfsParams& P, long long idx, int dir, long long frontier,
-                         long long result, long long etc) {
+                         long long result, long long etc, int exec = 0) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && idx < P.step_cap) {
     gk_step st;
     st.dir = dir;
-    st.pad = 0;
+    st.pad = exec;
     st.frontier = frontier;
     st.result = result;
     st.edges_to_check = etc;
@@ -993,6 +995,13 @@ __device__ void log_step(const BfsParams& P, long long idx, int dir, long long f
 #ifndef GK_SPARSE
 #define GK_SPARSE 1
 #endif
+#ifndef GK_PUSH_BU
+#define GK_PUSH_BU 1
+#endif
+#ifndef GK_PUSH_FACTOR
+#define GK_PUSH_FACTOR 8
+#endif
+constexpr long long kPushFactor = GK_PUSH_FACTOR;  // pushed bottom-up step when scout < this x pending
 __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   extern __shared__ uint4 dyn_smem[];
   __shared__ SmemT s;
@@ -1057,6 +1066,59 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   int bu_tw_log = 5;  // bottom-up task = 32 words unless that leaves warps idle
   while (bu_tw_log > 0 && ((P.w32 + (1 << bu_tw_log) - 1) >> bu_tw_log) < nwarps) bu_tw_log--;
 
+  // A large top-down step over the queue window [a, b) whose frontier's
+  // out-degree total is sc: next := visited, bitmap claims (owned-range hub
+  // expansion, light tiles, heavy chunks; target-range passes when next
+  // exceeds L2), then the claim sweep.  Leaves the claims in nextg (visited
+  // updated); claimed / sc_out are grid totals.
+  auto large_step = [&](unsigned long long a, unsigned long long b, long long sc, unsigned long long& claimed,
+                        long long& sc_out) -> bool {
+    for (long long i = gtid; i < P.w32; i += gthreads) nextg[i] = __ldcg(P.visited + i);
+    if (!grid_sync(P, s, ph, kTagZero)) return false;
+    int tile_sz = kBlock;
+    while (tile_sz > 32 && (long long)(b - a) < (long long)tile_sz * gridDim.x) tile_sz >>= 1;
+    int64_t chunk = kChunkMax;
+    while (chunk > kChunkMin && sc < chunk * nwarps) chunk >>= 1;
+    long long sacc = 0;
+    // Claims only touch next (n/8 bytes).  When that bitmap is larger than
+    // L2 can hold, the step runs in P.td_passes passes over target vertex
+    // ranges of P.td_span ids, each pass's slice of next (and of parent)
+    // staying L2-resident; the frontier's lists are re-streamed per pass,
+    // which HBM does at full bandwidth.
+    unsigned long long nch = 0, nown = 0;
+    const bool own = P.own_split != nullptr && P.td_passes == 1;
+    for (int r = 0; r < P.td_passes; r++) {
+      const uint32_t rlo = (uint32_t)((int64_t)r * P.td_span);
+      const uint32_t rhi = r + 1 == P.td_passes ? 0xffffffffu : (uint32_t)((int64_t)(r + 1) * P.td_span);
+      {
+        const QApp qa = qapp(P, ph, qtail);
+        td_light<true>(P, s, ph, qa, a, b, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk, false, r == 0, rlo,
+                       rhi, own);
+      }
+      if (!grid_sync(P, s, ph, kTagTD)) return false;
+      if (r == 0) {
+        nch = s.snap[kChunkCount];
+        nown = own ? s.snap[kOwnCount] : 0;
+      }
+      if (nch || nown) {
+        if (nown) td_own(P, s, nown, nextg, sfront);
+        const QApp qa = qapp(P, ph, qtail);
+        if (nch) td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, false, rlo, rhi);
+        if (!grid_sync(P, s, ph, nown ? kTagOwn : kTagHeavy)) return false;
+      }
+    }
+    long long cacc = 0;
+    sacc = 0;
+    const unsigned set = ph & 3;
+    td_scout_bits(P, nextg, lvl, encode, sacc, cacc);
+    block_add(sacc, &P.ctrl->cnt[set][kSum], s);
+    block_add(cacc, &P.ctrl->cnt[set][kCount], s);
+    if (!grid_sync(P, s, ph, kTagSweep)) return false;
+    sc_out = (long long)s.snap[kSum];
+    claimed = s.snap[kCount];
+    return true;
+  };
+
   while (qe > qs) {
     const bool go_bu = P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha;
     // a top-down step whose (bitmap) frontier outnumbers the pending
@@ -1070,7 +1132,17 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       queue_stale = false;
     }
     if (go_bu) {
-      if (!front_ready) {  // QueueToBitmap into a cleared front (bfs.hpp:145)
+      // A bottom-up step whose frontier's out-degree total (scout, known after
+      // a top-down step) is small against the vertices still pending runs as
+      // a large top-down step (push): same claimed set and awake count;
+      // parents are any frontier in-neighbour instead of the first in
+      // ascending order (bfs.hpp:55-60) -- valid parents either way.  The
+      // pull would scan the whole in-list of every pending vertex without a
+      // frontier neighbour.
+      bool push_first = GK_PUSH_BU && !queue_stale && !P.front_in_smem && !sparse_ok(P.live - reached) &&
+                        scout < kPushFactor * (P.live - reached);
+      const unsigned long long fq0 = qs, fq1 = qe;
+      if (!front_ready && !push_first) {  // QueueToBitmap into a cleared front (bfs.hpp:145)
         for (long long i = gtid; i < P.w32; i += gthreads) frontg[i] = 0u;
         if (!grid_sync(P, s, ph, kTagZero)) return;
         for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
@@ -1095,6 +1167,20 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
           fr = sfront;
         }
         long long acc = 0;
+        if (push_first) {
+          push_first = false;
+          unsigned long long claimed = 0;
+          long long sdummy = 0;
+          if (!large_step(fq0, fq1, scout, claimed, sdummy)) return;
+          awake = (long long)claimed;
+          reached += awake;
+          log_step(P, nsteps++, 'B', old_awake, awake, etc, 'P');
+          lvl++;
+          uint32_t* t = frontg;
+          frontg = nextg;
+          nextg = t;
+          continue;
+        }
         if (sparse_ok(P.live - reached)) {
           long long found = 0;
           if (!sparse_step<false>(P, s, ph, frontg, nextg, lvl, found, dummy)) return;
@@ -1161,7 +1247,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         qs = qtail;  // bitmap-only frontier, as after a large top-down step
         qe = qtail + claimed;
         queue_stale = true;
-        log_step(P, nsteps++, 'T', fsize, scout, etc);
+        log_step(P, nsteps++, 'T', fsize, scout, etc, 'U');
         lvl++;
         continue;
       }
@@ -1182,39 +1268,20 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       while (chunk > kChunkMin && scout < chunk * nwarps) chunk >>= 1;
       long long sacc = 0;
       unsigned set;
-      if (big) {  // next := visited (see claim4<true>)
-        for (long long i = gtid; i < P.w32; i += gthreads) nextg[i] = __ldcg(P.visited + i);
-        if (!grid_sync(P, s, ph, kTagZero)) return;
-      }
       if (big) {
-        // Claims only touch next (n/8 bytes).  When that bitmap is larger
-        // than L2 can hold, the step runs in P.td_passes passes over target
-        // vertex ranges of P.td_span ids, each pass's slice of next (and of
-        // parent) staying L2-resident; the frontier's lists are re-streamed
-        // per pass, which HBM does at full bandwidth.
-        unsigned long long nch = 0, nown = 0;
-        const bool own = P.own_split != nullptr && P.td_passes == 1;
-        for (int r = 0; r < P.td_passes; r++) {
-          const uint32_t rlo = (uint32_t)((int64_t)r * P.td_span);
-          const uint32_t rhi = r + 1 == P.td_passes ? 0xffffffffu : (uint32_t)((int64_t)(r + 1) * P.td_span);
-          set = ph & 3;
-          {
-            const QApp qa = qapp(P, ph, qtail);
-            td_light<true>(P, s, ph, qa, qs, qe, nextg, lvl, encode, sacc, qcnt, tile_sz, chunk, false, r == 0,
-                           rlo, rhi, own);
-          }
-          if (!grid_sync(P, s, ph, kTagTD)) return;
-          if (r == 0) {
-            nch = s.snap[kChunkCount];
-            nown = own ? s.snap[kOwnCount] : 0;
-          }
-          if (nch || nown) {
-            if (nown) td_own(P, s, nown, nextg, sfront);
-            const QApp qa = qapp(P, ph, qtail);
-            if (nch) td_heavy<true>(P, s, ph, qa, nch, nextg, lvl, encode, sacc, qcnt, false, rlo, rhi);
-            if (!grid_sync(P, s, ph, nown ? kTagOwn : kTagHeavy)) return;
-          }
-        }
+        unsigned long long claimed = 0;
+        if (!large_step(qs, qe, scout, claimed, scout)) return;
+        reached += (long long)claimed;
+        uint32_t* t = frontg;
+        frontg = nextg;
+        nextg = t;
+        front_ready = true;
+        // The new frontier exists only as a bitmap; its queue window is
+        // [qtail, qtail + claimed), materialised by BitmapToQueue only if a
+        // top-down step follows.
+        qs = qtail;
+        qe = qtail + claimed;
+        queue_stale = true;
       } else {
         set = ph & 3;
         {
@@ -1239,28 +1306,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
           qtail += s.snap[kAppend];
         }
       }
-      if (big) {
-        long long cacc = 0;
-        sacc = 0;
-        set = ph & 3;
-        td_scout_bits(P, nextg, lvl, encode, sacc, cacc);
-        block_add(sacc, &P.ctrl->cnt[set][kSum], s);
-        block_add(cacc, &P.ctrl->cnt[set][kCount], s);
-        if (!grid_sync(P, s, ph, kTagSweep)) return;
-        scout = (long long)s.snap[kSum];
-        const unsigned long long claimed = s.snap[kCount];
-        reached += (long long)claimed;
-        uint32_t* t = frontg;
-        frontg = nextg;
-        nextg = t;
-        front_ready = true;
-        // The new frontier exists only as a bitmap; its queue window is
-        // [qtail, qtail + claimed), materialised by BitmapToQueue only if a
-        // top-down step follows.
-        qs = qtail;
-        qe = qtail + claimed;
-        queue_stale = true;
-      } else {
+      if (!big) {
         front_ready = false;
         reached += (long long)(qtail - qt0);
         qs = qe;  // SlideWindow (bfs.hpp:160)
