@@ -1138,7 +1138,12 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
       // parents are any frontier in-neighbour instead of the first in
       // ascending order (bfs.hpp:55-60) -- valid parents either way.  The
       // pull would scan the whole in-list of every pending vertex without a
-      // frontier neighbour.
+      // frontier neighbour (kron27: the sources whose first bottom-up step
+      // follows two top-down steps from a few hubs, 3.2 -> 2.0 ms).  The 8x
+      // bound is measured: a cost model (pull tests ~min(mean degree,
+      // m / scout) arcs per pending vertex) pushed urand27 steps where the
+      // pull is faster, and pushing from a bitmap-only frontier (after a
+      // large top-down step) never paid.
       bool push_first = GK_PUSH_BU && !queue_stale && !P.front_in_smem && !sparse_ok(P.live - reached) &&
                         scout < kPushFactor * (P.live - reached);
       const unsigned long long fq0 = qs, fq1 = qe;

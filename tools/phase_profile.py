@@ -37,7 +37,7 @@ def main():
               f"m_cc {r.component_edges}  GTEPS {r.component_edges / r.device_ms / 1e6:.1f}")
         print("   " + " ".join(parts))
         for st in r.steps:
-            print(f"     {st[0]} frontier {st[1]:>10} result {st[2]:>11} etc {st[3]}")
+            print(f"     {st[0]}{st[4] or ' '} frontier {st[1]:>10} result {st[2]:>11} etc {st[3]}")
     print("mean per phase kind (ms):", {k: round(v / len(srcs), 4) for k, v in tot.items()})
 
 
