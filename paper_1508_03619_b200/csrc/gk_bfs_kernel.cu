@@ -1404,9 +1404,10 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st
   // caller's timed region.  GK_INIT_MODE: 1 (default) cudaMemsetAsync,
   // measured 1% faster per BFS at scale 27 than 0 (the same stores in the
   // kernel's init phase) or 2 (a fill kernel); gk_bfs_batch's overlapped
-  // parent copies run at the same rate with all three.
+  // parent copies run at the same rate with all three.  Below 2^22 vertices
+  // the init phase clears parent (kron16: the memset launch cost 7 %).
   static const int init_mode = getenv("GK_INIT_MODE") ? atoi(getenv("GK_INIT_MODE")) : GK_INIT_MODE_DEF;
-  if (init_mode == 1) {
+  if (init_mode == 1 && p.n >= (int64_t(1) << 22)) {  // small graphs: the extra launch costs more than it saves
     cudaError_t e = cudaMemsetAsync(p.parent, 0xFF, sizeof(int32_t) * (size_t)p.n, st);
     if (e) return e;
     local.parent_preset = 1;
