@@ -30,6 +30,10 @@
 //   rescan    kTopDownRescan's extra degree pass (bfs.hpp:161-167)
 #include "gk_persistent.cuh"
 
+#ifndef GK_HEAVY_KE
+#define GK_HEAVY_KE 8  // heavy-chunk edges per lane in flight (large steps)
+#endif
+
 namespace gk {
 namespace {
 
@@ -232,7 +236,7 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
   if constexpr (kBig) {
     // 8 edges per lane in flight and the next chunk descriptor prefetched:
     // the hub step is bound by the nb -> bitmap-word dependent latency
-    constexpr int kE = 8;
+    constexpr int kE = GK_HEAVY_KE;
     // first chunk static, later ones claimed dynamically; the next claim and
     // its descriptor load are issued before the current chunk's edges
     unsigned long long* cctr = &P.ctrl->cnt[ph & 3][kChunkNext];
