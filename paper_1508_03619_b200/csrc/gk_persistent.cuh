@@ -14,6 +14,15 @@ namespace gk {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef GK_BITMAP_HINTS
+#define GK_BITMAP_HINTS 1  // evict_last on bitmap loads
+#endif
+#ifndef GK_PARENT_HINTS
+#define GK_PARENT_HINTS 1  // evict_first on random parent stores
+#endif
+#ifndef GK_STREAM_HINTS
+#define GK_STREAM_HINTS 1  // evict_first on top-down adjacency loads
+#endif
 constexpr int kQBuf = 256;         // per-warp queue staging (QueueBuffer analogue)
 constexpr int kChunkMax = 1024;    // edges per heavy chunk (large steps)
 constexpr int kChunkMin = 128;     // ... and for small steps, so every warp gets a chunk
@@ -69,7 +78,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 // Bitmap word, bypassing L1 (other SMs update bitmaps within a phase), kept in L2.
 __device__ __forceinline__ uint32_t ld_bits(const uint32_t* p) {
   uint32_t v;
+#if GK_BITMAP_HINTS
   asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+#else
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+#endif
   return v;
 }
 // Visited word for a claim pre-check: may be served stale from L1 (bits
@@ -82,7 +95,11 @@ __device__ __forceinline__ uint32_t ld_bits_l1(const uint32_t* p) {
 // Read-only front bitmap word within a bottom-up phase: L1-cacheable, kept in L2.
 __device__ __forceinline__ uint32_t ld_front(const uint32_t* p) {
   uint32_t v;
+#if GK_BITMAP_HINTS
   asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+#else
+  asm("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+#endif
   return v;
 }
 // Graph data: read-only path, default L2 policy (an evict-first hint made
@@ -96,12 +113,20 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 // Top-down edge lists are read exactly once per step: stream them.
 __device__ __forceinline__ uint32_t ld_nb_once(const uint32_t* p) {
   uint32_t v;
+#if GK_STREAM_HINTS
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_first()));
+#else
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+#endif
   return v;
 }
 // Random parent writes: do not let them displace the bitmaps in L2.
 __device__ __forceinline__ void st_parent(int32_t* p, int32_t v) {
+#if GK_PARENT_HINTS
   asm volatile("st.global.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(policy_evict_first()) : "memory");
+#else
+  *p = v;
+#endif
 }
 __device__ __forceinline__ int64_t ld_off(const int64_t* p) { return __ldg(p); }
 
