@@ -54,81 +54,32 @@ __global__ void k_validate_csr(const int64_t* __restrict__ off, const uint32_t* 
     if ((int64_t)nb[i] >= id_bound) atomicAdd(&bad[1], 1ull);
 }
 
-__global__ void k_live_count(const uint32_t* __restrict__ dead, int64_t w32, uint32_t* __restrict__ cnt) {
+// Vertices with in-edges per CTA (popcount of ~dead), summed into *live.
+__global__ void k_count_live(const uint32_t* __restrict__ dead, int64_t w32, unsigned long long* live) {
+  __shared__ unsigned long long sm[kAuxBlock / 32];
+  unsigned long long c = 0;
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < w32; w += (int64_t)gridDim.x * blockDim.x)
-    cnt[w] = __popc(~dead[w]);
+    c += __popc(~dead[w]);
+  c = block_sum(c, sm);
+  if (threadIdx.x == 0 && c) atomicAdd(live, c);
 }
 
-// Heads are stored only for live (not dead) vertices, in vertex order:
-// v's record is hbase[v/32] + (live vertices before v in its word).
-__global__ void k_head(const int64_t* __restrict__ in_off, const uint32_t* __restrict__ in_nb, int64_t n,
-                       const uint32_t* __restrict__ dead, const uint32_t* __restrict__ hbase,
-                       HeadRec* __restrict__ head, HeadRec* __restrict__ head2) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t live = ~dead[v >> 5];
-    const uint32_t bit = (uint32_t)(v & 31);
-    if (!((live >> bit) & 1u)) continue;
-    const int64_t idx = (int64_t)hbase[v >> 5] + __popc(live & ((1u << bit) - 1u));
-    const int64_t b = in_off[v], d = in_off[v + 1] - b;
-    uint32_t h[kHead];
-#pragma unroll
-    for (int j = 0; j < kHead; j++) h[j] = j < d ? in_nb[b + j] : kNoVertex;
-    head[idx] = head_pack(h, (HeadRec*)nullptr);
-    if (head2) {
-#pragma unroll
-      for (int j = 0; j < kHead; j++) h[j] = kHead + j < d ? in_nb[b + kHead + j] : kNoVertex;
-      head2[idx] = head_pack(h, (HeadRec*)nullptr);
-    }
+// Neighbour lists strictly ascending (graph.hpp:25: sorted, no duplicates):
+// a warp per vertex compares each arc with its predecessor.
+__global__ void k_check_sorted(const int64_t* __restrict__ off, const uint32_t* __restrict__ nb, int64_t n,
+                               unsigned long long* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long c = 0;
+  for (int64_t v = gw; v < n; v += nw) {
+    const int64_t b = off[v], e = off[v + 1];
+    for (int64_t j = b + 1 + lane; j < e; j += 32)
+      if (nb[j] <= nb[j - 1]) c++;
   }
+  if (c) atomicAdd(bad, c);
 }
 
-// Owned-range split rows (gk_internal.cuh OwnEnt).
-__global__ void k_hv_bits(const int64_t* __restrict__ off, int64_t n, int64_t w32, int64_t dmin,
-                          uint32_t* __restrict__ bits) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < w32 * 32;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const bool h = v < n && off[v + 1] - off[v] >= dmin;
-    const unsigned b = __ballot_sync(0xffffffffu, h);
-    if ((threadIdx.x & 31) == 0) bits[v >> 5] = b;
-  }
-}
-
-__global__ void k_popc(const uint32_t* __restrict__ bits, int64_t w32, uint32_t* __restrict__ cnt) {
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < w32; w += (int64_t)gridDim.x * blockDim.x)
-    cnt[w] = __popc(bits[w]);
-}
-
-__global__ void k_hv_list(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ base, int64_t w32,
-                          uint32_t* __restrict__ ids) {
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < w32; w += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t b = bits[w], r = base[w];
-    while (b) {
-      ids[r++] = (uint32_t)(w * 32 + __ffs(b) - 1);
-      b &= b - 1;
-    }
-  }
-}
-
-// One CTA per row: check the list is ascending, then row[r] = lower_bound of
-// r*span in it for r = 0..nr.
-__global__ void k_split(const int64_t* __restrict__ off, const uint32_t* __restrict__ nb,
-                        const uint32_t* __restrict__ ids, int nr, int64_t span, uint32_t* __restrict__ split,
-                        unsigned long long* bad) {
-  const uint32_t u = ids[blockIdx.x];
-  const int64_t b = off[u], d = off[u + 1] - b;
-  for (int64_t i = threadIdx.x + 1; i < d; i += blockDim.x)
-    if (nb[b + i] < nb[b + i - 1]) atomicAdd(bad, 1ull);
-  for (int r = threadIdx.x; r <= nr; r += blockDim.x) {
-    const int64_t t = (int64_t)r * span;
-    int64_t lo = 0, hi = d;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if ((int64_t)nb[b + mid] < t) lo = mid + 1;
-      else hi = mid;
-    }
-    split[(int64_t)blockIdx.x * (nr + 1) + r] = (uint32_t)lo;
-  }
-}
 
 __global__ void k_count_reached(const int32_t* __restrict__ parent, const int64_t* __restrict__ off,
                                 int64_t n, unsigned long long* out) {
@@ -233,7 +184,11 @@ __global__ void k_verify_vertices(const int64_t* __restrict__ off, const uint32_
       if (p != -1) bad = 1;
     } else if (p < 0 || (int64_t)p >= n) {
       bad = 2;
-    } else if (depth[p] != d - 1) {
+    } else if (d < 1 || depth[p] != d - 1) {
+      // d >= 1: only the source sits at depth 0, so every parent chain
+      // descends to it (a depth-0 vertex whose parent is unreached, depth -1,
+      // would otherwise pass d-1 == depth[p] and take a fake subtree with it
+      // on a directed graph, where no reverse arc exposes it)
       bad = 3;
     } else {
       int64_t lo = off[p], hi = off[p + 1];
@@ -291,137 +246,50 @@ int aux_grid(int64_t n) {
   return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
-// Out-degree per vertex clamped to 65535 (= "read the offsets"), zero past
-// n up to a whole bitmap word: the large top-down step's claim sweep sums
-// the claimed vertices' degrees from these 2n bytes instead of from the
-// 8n-byte offsets.
-__global__ void k_deg16(const int64_t* off, int64_t n, int64_t nw, uint16_t* deg16) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nw; v += (int64_t)gridDim.x * blockDim.x) {
-    int64_t d = 0;
-    if (v < n) d = off[v + 1] - off[v];
-    deg16[v] = (uint16_t)(d < 65535 ? d : 65535);
-  }
-}
-
 }  // namespace
 
-cudaError_t build_deg16(const int64_t* off, int64_t n, uint16_t* deg16, cudaStream_t s) {
-  const int64_t nw = (n + 31) / 32 * 32;
-  if (nw == 0) return cudaSuccess;
-  k_deg16<<<aux_grid(nw), kAuxBlock, 0, s>>>(off, n, nw, deg16);
-  return cudaGetLastError();
-}
-
-cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s) {
+cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, int64_t* live, cudaStream_t s) {
   const int64_t w32 = (n + 31) / 32;
+  *live = 0;
+  if (w32 == 0) return cudaSuccess;
   k_dead<<<aux_grid(w32 * 32), kAuxBlock, 0, s>>>(in_off, n, w32, dead);
-  return cudaGetLastError();
+  unsigned long long* d = nullptr;
+  unsigned long long h = 0;
+  cudaError_t e = cudaMallocAsync(&d, sizeof(h), s);
+  if (e) return e;
+  if (!(e = cudaMemsetAsync(d, 0, sizeof(h), s))) {
+    k_count_live<<<aux_grid(w32), kAuxBlock, 0, s>>>(dead, w32, d);
+    if (!(e = cudaGetLastError()) && !(e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s)))
+      e = cudaStreamSynchronize(s);
+  }
+  cudaFreeAsync(d, s);
+  *live = (int64_t)h;
+  return e;
 }
 
 cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int64_t m, int64_t id_bound,
-                         bool* offsets_ok, bool* ids_ok, cudaStream_t s) {
+                         bool* offsets_ok, bool* ids_ok, bool* sorted, cudaStream_t s) {
   unsigned long long* bad = nullptr;
-  unsigned long long hb[2] = {0, 0};
+  unsigned long long hb[3] = {0, 0, 0};
   cudaError_t e;
   if ((e = cudaMalloc(&bad, sizeof(hb)))) return e;
   if (!(e = cudaMemsetAsync(bad, 0, sizeof(hb), s))) {
     k_validate_csr<<<aux_grid(std::max<int64_t>(n, m)), kAuxBlock, 0, s>>>(off, nb, n, m, id_bound, bad);
-    if (!(e = cudaGetLastError()) && !(e = cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s)))
-      e = cudaStreamSynchronize(s);
+    e = cudaGetLastError();
+    if (!e && sorted) {
+      e = cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s);
+      if (!e) e = cudaStreamSynchronize(s);
+      if (!e && hb[0] == 0) {  // list bounds are trustworthy
+        k_check_sorted<<<aux_grid(32 * n), kAuxBlock, 0, s>>>(off, nb, n, bad + 2);
+        e = cudaGetLastError();
+      }
+    }
+    if (!e && !(e = cudaMemcpyAsync(hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s))) e = cudaStreamSynchronize(s);
   }
   cudaFree(bad);
   *offsets_ok = hb[0] == 0;
   *ids_ok = hb[1] == 0;
-  return e;
-}
-
-cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, const uint32_t* dead,
-                       uint32_t* hbase, HeadRec** head, HeadRec** head2, int64_t* nlive, cudaStream_t s) {
-  const int64_t w32 = (n + 31) / 32;
-  *head = nullptr;
-  *nlive = 0;
-  if (head2) *head2 = nullptr;
-  if (w32 == 0) return cudaSuccess;
-  uint32_t* cnt = nullptr;
-  void* tmp = nullptr;
-  size_t tb = 0;
-  uint32_t last[2] = {0, 0};
-  cudaError_t e;
-  if ((e = cudaMalloc(&cnt, sizeof(uint32_t) * (w32 + 1)))) return e;
-  k_live_count<<<aux_grid(w32), kAuxBlock, 0, s>>>(dead, w32, cnt);
-  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, hbase, (int)w32, s))) goto out;
-  if ((e = cudaMalloc(&tmp, tb))) goto out;
-  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, hbase, (int)w32, s))) goto out;
-  if ((e = cudaMemcpyAsync(&last[0], hbase + w32 - 1, 4, cudaMemcpyDeviceToHost, s))) goto out;
-  if ((e = cudaMemcpyAsync(&last[1], cnt + w32 - 1, 4, cudaMemcpyDeviceToHost, s))) goto out;
-  if ((e = cudaStreamSynchronize(s))) goto out;
-  {
-    const int64_t live = (int64_t)last[0] + last[1];
-    *nlive = live;
-    if ((e = cudaMalloc(head, sizeof(HeadRec) * (live > 0 ? live : 1)))) goto out;
-    if (head2 && cudaMalloc(head2, sizeof(HeadRec) * (live > 0 ? live : 1)) != cudaSuccess) {
-      cudaGetLastError();  // optional: without it the second round reads in_off/in_nb
-      *head2 = nullptr;
-    }
-    k_head<<<aux_grid(n), kAuxBlock, 0, s>>>(in_off, in_nb, n, dead, hbase, *head, head2 ? *head2 : nullptr);
-    e = cudaGetLastError();
-  }
-out:
-  cudaFree(tmp);
-  cudaFree(cnt);
-  return e;
-}
-
-cudaError_t build_own(const int64_t* out_off, const uint32_t* out_nb, int64_t n, int64_t dmin, int r,
-                      int64_t span_w, size_t max_bytes, uint32_t** hv_bits, uint32_t** hv_base,
-                      uint32_t** split, int64_t* nh, cudaStream_t s) {
-  const int64_t w32 = (n + 31) / 32;
-  *hv_bits = *hv_base = *split = nullptr;
-  *nh = 0;
-  if (w32 == 0 || r < 1) return cudaSuccess;
-  uint32_t* cnt = nullptr;
-  uint32_t* ids = nullptr;
-  unsigned long long* bad = nullptr;
-  unsigned long long hbad = 0;
-  void* tmp = nullptr;
-  size_t tb = 0;
-  uint32_t last[2] = {0, 0};
-  int64_t rows = 0;
-  cudaError_t e;
-  if ((e = cudaMalloc(hv_bits, sizeof(uint32_t) * w32))) goto out;
-  if ((e = cudaMalloc(hv_base, sizeof(uint32_t) * w32))) goto out;
-  if ((e = cudaMalloc(&cnt, sizeof(uint32_t) * w32))) goto out;
-  k_hv_bits<<<aux_grid(w32 * 32), kAuxBlock, 0, s>>>(out_off, n, w32, dmin, *hv_bits);
-  k_popc<<<aux_grid(w32), kAuxBlock, 0, s>>>(*hv_bits, w32, cnt);
-  if ((e = cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, *hv_base, (int)w32, s))) goto out;
-  if ((e = cudaMalloc(&tmp, tb))) goto out;
-  if ((e = cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, *hv_base, (int)w32, s))) goto out;
-  if ((e = cudaMemcpyAsync(&last[0], *hv_base + w32 - 1, 4, cudaMemcpyDeviceToHost, s))) goto out;
-  if ((e = cudaMemcpyAsync(&last[1], cnt + w32 - 1, 4, cudaMemcpyDeviceToHost, s))) goto out;
-  if ((e = cudaStreamSynchronize(s))) goto out;
-  rows = (int64_t)last[0] + last[1];
-  if (rows == 0 || (size_t)rows * (r + 1) * 4 > max_bytes) goto out;
-  if ((e = cudaMalloc(&ids, sizeof(uint32_t) * rows))) goto out;
-  if ((e = cudaMalloc(split, sizeof(uint32_t) * rows * (r + 1)))) goto out;
-  if ((e = cudaMalloc(&bad, sizeof(unsigned long long)))) goto out;
-  if ((e = cudaMemsetAsync(bad, 0, sizeof(unsigned long long), s))) goto out;
-  k_hv_list<<<aux_grid(w32), kAuxBlock, 0, s>>>(*hv_bits, *hv_base, w32, ids);
-  k_split<<<(unsigned)rows, 512, 0, s>>>(out_off, out_nb, ids, r, span_w * 32, *split, bad);
-  if ((e = cudaGetLastError())) goto out;
-  if ((e = cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, s))) goto out;
-  if ((e = cudaStreamSynchronize(s))) goto out;
-  if (hbad == 0) *nh = rows;
-out:
-  cudaFree(tmp);
-  cudaFree(cnt);
-  cudaFree(ids);
-  cudaFree(bad);
-  if (*nh == 0) {  // off: nothing qualifies, a list is unsorted, too large, or an error
-    cudaFree(*hv_bits);
-    cudaFree(*hv_base);
-    cudaFree(*split);
-    *hv_bits = *hv_base = *split = nullptr;
-  }
+  if (sorted) *sorted = hb[0] == 0 && hb[2] == 0;
   return e;
 }
 

@@ -447,7 +447,6 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
   const long long gthreads = (long long)gridDim.x * kBlock;
   const uint32_t src = P.src;
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->ts[0] = globaltimer();
-  zero_next_ctrl(P, gtid, gthreads);
   // init (betweenness.hpp:96-101)
   for (long long i = gtid; i < P.n; i += gthreads) {
     P.depth[i] = -1;
@@ -631,6 +630,7 @@ cudaError_t bc_launch(const BfsParams& p, int device, cudaStream_t st) {
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device))) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bc_persistent, kBlock, 0))) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
+  if ((e = cudaMemsetAsync(p.ctrl, 0, kCtrlClear, st))) return e;
   BfsParams local = p;
   void* args[] = {&local};
   return cudaLaunchCooperativeKernel((const void*)bc_persistent, dim3(sms * occ), dim3(kBlock), args, 0, st);

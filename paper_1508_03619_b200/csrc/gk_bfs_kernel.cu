@@ -157,12 +157,13 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
       b = P.out_off[u];
       const int64_t d = P.out_off[u + 1] - b;
       if (own && d >= P.own_dmin) {  // expanded range by range in td_own
-        const uint32_t hw = __ldg(P.hv_bits + (u >> 5));
         OwnEnt e;
         e.u = u;
-        e.rank = __ldg(P.hv_base + (u >> 5)) + __popc(hw & ((1u << (u & 31u)) - 1u));
+        e.deg = (uint32_t)d;
         e.base = b;
-        P.own_list[atomicAdd(&cnt[kOwnCount], 1ull)] = e;
+        const unsigned long long at = atomicAdd(&cnt[kOwnCount], 1ull);
+        if ((int64_t)at < P.own_cap) P.own_list[at] = e;
+        else atomicExch(&P.ctrl->error, 3);  // cannot happen: own_cap >= m / own_dmin
       } else if (d > chunk) {
         if (reg) {  // range passes after the first reuse the chunk list
           const int64_t nch = (d + chunk - 1) / chunk;
@@ -302,6 +303,98 @@ __device__ void td_heavy(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
 #ifndef GK_OWN_KE
 #define GK_OWN_KE 12  // 4: -1.2%, 8: -0.3% on kron27
 #endif
+
+// Lower bounds of key0 < key1 in the strictly ascending list a[0..d) of ids
+// in [0, n): *r0 / *r1 = first index whose id is >= key0 / key1.  A
+// bracket (lo, hi) with a[lo] < key <= a[hi] (virtual ends -1 and d)
+// shrinks by rounds of three concurrent probes around the interpolated
+// position (g - m, g, g + m; m = 2 + 2 sqrt(width)): ids of a permuted graph
+// are uniform, so the bracket holds the answer and the width drops to about
+// 2 sqrt(width) per round -- 2-3 rounds from a 10^6-arc list to a binary
+// search inside one or two cache lines.  Both searches advance together
+// (their loads overlap).  Any id distribution terminates with the exact
+// answer: a round only ever narrows a valid bracket.
+struct SplitSearch {
+  int64_t lo, hi;    // a[lo] < key <= a[hi]
+  uint32_t vlo, vhi; // ids strictly inside the bracket lie in [vlo, vhi)
+  uint32_t key;
+};
+__device__ __forceinline__ void split_init(SplitSearch& q, uint32_t d, uint32_t key, uint32_t n) {
+  q.key = key;
+  q.lo = -1;
+  q.hi = d;
+  q.vlo = 0;
+  q.vhi = n;
+  if (key == 0) q.hi = 0;        // answer 0
+  else if (key >= n) q.lo = (int64_t)d - 1;  // answer d
+}
+__device__ __forceinline__ int64_t split_width(const SplitSearch& q) { return q.hi - q.lo - 1; }
+__device__ __forceinline__ void split_probe_pos(const SplitSearch& q, int64_t& p0, int64_t& p1, int64_t& p2) {
+  const int64_t w = split_width(q);
+  // interpolated position; float is exact enough (the bracket absorbs it)
+  const float f = (float)(q.key - q.vlo) / (float)(q.vhi > q.vlo ? q.vhi - q.vlo : 1u);
+  int64_t g = q.lo + 1 + (int64_t)(f * (float)w);
+  if (g > q.hi - 1) g = q.hi - 1;
+  if (g < q.lo + 1) g = q.lo + 1;
+  const int64_t m = 2 + 2 * (int64_t)sqrtf((float)w);
+  p0 = g - m > q.lo + 1 ? g - m : q.lo + 1;
+  p1 = g;
+  p2 = g + m < q.hi - 1 ? g + m : q.hi - 1;
+}
+__device__ __forceinline__ void split_update(SplitSearch& q, int64_t p0, int64_t p1, int64_t p2, uint32_t x0,
+                                             uint32_t x1, uint32_t x2) {
+  if (x2 < q.key) {
+    q.lo = p2;
+    q.vlo = x2 + 1;
+  } else if (x1 < q.key) {
+    q.lo = p1;
+    q.vlo = x1 + 1;
+    q.hi = p2;
+    q.vhi = x2;
+  } else if (x0 < q.key) {
+    q.lo = p0;
+    q.vlo = x0 + 1;
+    q.hi = p1;
+    q.vhi = x1;
+  } else {
+    q.hi = p0;
+    q.vhi = x0;
+  }
+}
+__device__ __forceinline__ void split_run(const uint32_t* a, uint32_t d, uint32_t key0, uint32_t key1, uint32_t n,
+                                          uint32_t& r0, uint32_t& r1) {
+  SplitSearch q[2];
+  split_init(q[0], d, key0, n);
+  split_init(q[1], d, key1, n);
+  constexpr int64_t kBin = 32;  // bracket width finished by binary search (1-2 cache lines)
+#pragma unroll 1
+  for (int round = 0; round < 4; round++) {
+    const bool a0 = split_width(q[0]) > kBin, a1 = split_width(q[1]) > kBin;
+    if (!a0 && !a1) break;
+    int64_t p[2][3];
+    uint32_t x[2][3];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      if (k ? a1 : a0) split_probe_pos(q[k], p[k][0], p[k][1], p[k][2]);
+#pragma unroll
+      for (int j = 0; j < 3; j++) x[k][j] = (k ? a1 : a0) ? __ldg(a + p[k][j]) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++)
+      if (k ? a1 : a0) split_update(q[k], p[k][0], p[k][1], p[k][2], x[k][0], x[k][1], x[k][2]);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    int64_t lo = q[k].lo, hi = q[k].hi;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(a + mid) < q[k].key) lo = mid;
+      else hi = mid;
+    }
+    (k ? r1 : r0) = (uint32_t)hi;
+  }
+}
+
 __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, uint32_t* nextbm, uint32_t* sm) {
   constexpr int kE = GK_OWN_KE;  // arcs per lane in flight
   const int r = blockIdx.x;
@@ -313,6 +406,8 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
   const long long w1 = w0 + sw < P.w32 ? w0 + sw : P.w32;
   const int nw = w1 > w0 ? (int)(w1 - w0) : 0;
   uint2* stage = P.own_stage + (int64_t)r * ((int64_t)nwin << wlog);
+  const uint32_t key0 = (uint32_t)(w0 * 32);
+  const uint32_t key1 = (uint32_t)(w1 * 32 < P.n ? w1 * 32 : P.n);
   for (int i = threadIdx.x; i < nw; i += kBlock) sm[i] = ld_bits(nextbm + w0 + i);
   if (threadIdx.x < kOwnWin) s.own_cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -323,8 +418,8 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
     int64_t b = 0, len = 0;
     if (i < nown) {
       const OwnEnt e = P.own_list[i];
-      const uint32_t* row = P.own_split + (int64_t)e.rank * (P.own_r + 1) + r;
-      const uint32_t s0 = __ldg(row), s1 = __ldg(row + 1);
+      uint32_t s0, s1;  // this range's run of the hub's ascending list
+      split_run(P.out_nb + e.base, e.deg, key0, key1, (uint32_t)P.n, s0, s1);
       u = e.u;
       b = e.base + s0;
       len = (int64_t)s1 - s0;
@@ -393,7 +488,8 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
   for (int i = threadIdx.x; i < nw; i += kBlock) atomicOr(nextbm + w0 + i, sm[i]);
   __syncthreads();
   // Parents, window by window: gather the window's logged claims into
-  // shared memory (the slice's space), then store them in vertex order.
+  // shared memory (the slice's space), then store them in vertex order
+  // (coalesced: measured faster than storing the log entries directly).
   int32_t* par = reinterpret_cast<int32_t*>(sm);
   const long long id0 = w0 * 32;
   const int ws = 1 << wlog;
@@ -451,37 +547,49 @@ __device__ void td_scout_bits(const BfsParams& P, uint32_t* bm, int lvl, bool en
       if (cl) P.visited[w0 + lane] = vis | cl;
     }
     count += __popc(cl);
-    if (cl) {
-      // degrees of the word's 32 vertices: 64 bytes of deg16, summed under
-      // the claim mask two at a time (halfword SIMD); 0 counts 1
-      // (bfs.hpp:130's encoding), 65535 means "read the offsets"
-      const uint4* dp = reinterpret_cast<const uint4*>(P.deg16 + (w0 + lane) * 32);
-      uint32_t dw[16];
+    if (!encode) {
+      scout += __popc(cl);
+    } else if (__ballot_sync(kFull, cl != 0u)) {
+      // degrees of the iteration's claims from the offsets: the claims are
+      // numbered by a warp scan and spread over the lanes, 4 per lane in
+      // flight; claim c's word is found by a shuffle search of the scan
+      const int cnt = __popc(cl);
+      int incl = cnt;
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const uint4 t = __ldg(dp + q);
-        dw[4 * q] = t.x;
-        dw[4 * q + 1] = t.y;
-        dw[4 * q + 2] = t.z;
-        dw[4 * q + 3] = t.w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if ((int)lane >= o) incl += y;
       }
-      if (!encode) {
-        scout += __popc(cl);
-      } else {
+      const int excl = incl - cnt;
+      const int total = __shfl_sync(kFull, incl, 31);
+      for (int c0 = 0; c0 < total; c0 += 128) {
+        int64_t o0[4], o1[4];
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-          const uint32_t pr = (cl >> (2 * j)) & 3u;
-          const uint32_t msk = (pr & 1u ? 0x0000FFFFu : 0u) | (pr & 2u ? 0xFFFF0000u : 0u);
-          scout += __vsadu2(dw[j] & msk, 0u) + __popc(__vcmpeq2(dw[j], 0u) & msk) / 16;
-          uint32_t big = __vcmpeq2(dw[j], 0xFFFFFFFFu) & msk;
-          while (big) {  // out-degree >= 65535: the exact value from the offsets
-            const int bt = (__ffs(big) - 1) >> 4;
-            big &= ~(0xFFFFu << (16 * bt));
-            const int64_t v = (w0 + lane) * 32 + 2 * j + bt;
-            scout += (P.out_off[v + 1] - P.out_off[v]) - 65535;
+        for (int k = 0; k < 4; k++) {
+          const int c = c0 + 32 * k + (int)lane;
+          int lo = 0;  // last lane whose first claim is <= c
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int e = __shfl_sync(kFull, excl, lo + step);
+            if (e <= c) lo += step;
+          }
+          const uint32_t m = __shfl_sync(kFull, cl, lo);
+          const int ex = __shfl_sync(kFull, excl, lo);
+          o0[k] = o1[k] = -1;
+          if (c < total) {
+            const int64_t v = (w0 + lo) * 32 + (int64_t)__fns(m, 0, c - ex + 1);
+            o0[k] = ld_off(P.out_off + v);
+            o1[k] = ld_off(P.out_off + v + 1);
           }
         }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int64_t d = o1[k] - o0[k];
+          if (o0[k] >= 0) scout += d ? d : 1;  // -old of bfs.hpp:83 with bfs.hpp:130's encoding
+        }
       }
+    }
+    if (cl) {
       if (P.want_depth)
         for (uint32_t m = cl; m; m &= m - 1) P.depth[(w0 + lane) * 32 + (__ffs(m) - 1)] = lvl + 1;
     }
@@ -492,31 +600,36 @@ __device__ void td_scout_bits(const BfsParams& P, uint32_t* bm, int lvl, bool en
 
 // ---- bottom-up sweep (bfs.hpp:47-66) ---------------------------------------
 // A warp takes a task of 32 consecutive bitmap words (1024 vertices): lane l
-// loads word l and the task's unvisited vertices are numbered by a warp
-// prefix sum.  Every lane keeps kBuSlots vertices in flight and refills a slot
-// (select-the-c-th-pending-vertex: shuffle binary search + __fns) as soon as
-// its vertex resolves, so one slow list never idles the other lanes.  Per
-// round a slot tests the next kPerRound in-neighbours of its vertex: round 1
-// reads the vertex's head (its first kHead in-neighbours, a dense 16-byte
-// record per vertex, so the sweep streams it in vertex order instead of
-// paying one random in_nb sector per vertex), later rounds continue in
-// in_nb.  After kLaneRounds rounds a still-unresolved vertex is deferred to
-// the long list, scanned after the sweep by whole warps with a ballot per 32
-// neighbours.  The chosen parent is the first in-neighbour (ascending) whose
-// front bit is set, as in bfs.hpp:55-60.  Results are OR-ed into per-warp
-// shared-memory words and written back once per task.  Vertices without
-// in-edges never appear: visited starts as the graph's dead bitmap.
+// loads word l and the task's pending vertices (not visited; visited starts
+// as the graph's dead set, so vertices without in-edges never appear) are
+// numbered by a warp prefix sum and listed once in shared memory.  Every
+// lane keeps kBuSlots vertices in flight.  A slot is refilled with the next
+// pending vertex as soon as its vertex resolves: the refill issues the loads
+// of the vertex's two in-offsets and the slot starts its rounds in the next
+// loop iteration, so that latency overlaps the other slots' rounds.  Per
+// round a slot tests the next kPerRound in-neighbours (the first alone, then
+// the rest together).  After kLaneRounds rounds a still-unresolved vertex is
+// deferred to the long list, scanned after the sweep by whole warps with a
+// ballot per 32 neighbours.  The chosen parent is the first in-neighbour
+// (ascending) whose front bit is set, as in bfs.hpp:55-60.  Results are
+// OR-ed into per-warp shared-memory words and written back once per task.
 #ifndef GK_BU_SLOTS
-#define GK_BU_SLOTS 3  // 2: -0.9% on kron27; 4: spills, -7%
+#define GK_BU_SLOTS 3  // 2: -0.5%, 4: spills (-8%) on kron27
 #endif
 constexpr int kBuSlots = GK_BU_SLOTS;
-constexpr int kBuListWords = 512 + 64;  // per warp: 1024 uint16 pending ids + 32 head bases + 32 live words
+#ifndef GK_BU_PREFETCH_OFF
+#define GK_BU_PREFETCH_OFF 0
+#endif
+constexpr int kBuListWords = 512;  // per warp: 1024 uint16 pending ids
 constexpr size_t kBuListBytes = (size_t)kWarps * kBuListWords * 4;
-constexpr int kPerRound = 4;    // in-neighbours tested per slot per round
-constexpr int kLaneRounds = 12;  // rounds before a list is deferred to the long list (8-16 measured flat)
-static_assert(kHead <= kPerRound, "a head round tests one head record");
+constexpr int kPerRound = 4;     // in-neighbours tested per slot per round
+constexpr int kLaneRounds = 12;  // rounds before a list is deferred to the long list
+constexpr int kLaneScan = kPerRound * kLaneRounds;  // in-neighbours a lane tests (4-entry rounds)
+constexpr int kSparseScan = kLaneScan;  // entries sp_scan tests before deferring a list to bu_long
 
-// front is either the global bitmap or its shared-memory copy (small graphs).
+// Where bu_long resumes a list bu_step deferred.
+__device__ __forceinline__ int64_t bu_resume(int64_t o) { return o + kLaneScan; }
+
 template <bool kSmem>
 __device__ __forceinline__ bool front_bit(const uint32_t* front, uint32_t u) {
   const uint32_t w = kSmem ? front[u >> 5] : ld_front(front + (u >> 5));
@@ -532,16 +645,8 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
   // a refill is one list read instead of a shuffle binary search.
   constexpr bool kList = !kSmem;
   uint16_t* lst = nullptr;
-  uint32_t* s_hb = nullptr;
-  uint32_t* s_lv = nullptr;
-  if constexpr (kList) {
-    uint32_t* base = wsm + warp * (kBuListWords);
-    lst = reinterpret_cast<uint16_t*>(base);
-    s_hb = base + 512;
-    s_lv = base + 544;
-  }
-  uint32_t* acc_n = s.bu_acc[warp][0];
-  uint32_t* acc_d = s.bu_acc[warp][1];
+  if constexpr (kList) lst = reinterpret_cast<uint16_t*>(wsm + warp * kBuListWords);
+  uint32_t* acc_n = s.bu_acc[warp];
   const long long gw = ((long long)blockIdx.x * kBlock + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * kBlock) >> 5;
   // A task is 2^tw_log consecutive words (<= 32): small graphs use small
@@ -549,20 +654,17 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
   const int tw = 1 << tw_log;
   const long long ntasks = (P.w32 + tw - 1) >> tw_log;
   // First task static, later ones claimed dynamically (per-task work varies
-  // with the pending density and list lengths; a static stride left warps
-  // idle at the phase's barrier).  The next claim is issued when a task
-  // starts, so its round trip hides behind the task.
+  // with the pending density and list lengths); the next claim is issued
+  // when a task starts, so its round trip hides behind the task.
   unsigned long long* tctr = &P.ctrl->cnt[ph & 3][kTile];
   for (long long t = gw; t < ntasks;) {
     long long tnext = 0;
     if (lane == 0) tnext = nw + (long long)atomicAdd(tctr, 1ull);
     const long long tbase = t << tw_log;
     const long long w = tbase + lane;
-    uint32_t vis = 0xffffffffu, pad = 0u, live = 0u, hb = 0u;
+    uint32_t vis = 0xffffffffu, pad = 0u;
     if ((int)lane < tw && w < P.w32) {
       vis = ld_bits(P.visited + w);
-      live = ~__ldg(P.dead + w);
-      hb = __ldg(P.hbase + w);
       const int64_t rem = P.n - w * 32;  // mask off ids >= n in the last word
       if (rem < 32) pad = 0xffffffffu << rem;
     }
@@ -577,28 +679,35 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
     const int excl = incl - cnt;
     const int total = __shfl_sync(kFull, incl, 31);
     if constexpr (kList) {
-      s_hb[lane] = hb;
-      s_lv[lane] = live;
       uint32_t m = pm;
       int pos = excl;
+#if GK_BU_PREFETCH_OFF
+      uint32_t last_sec = 0xffffffffu;
+#endif
       while (m) {
         const int bt = __ffs(m) - 1;
         m &= m - 1;
         lst[pos++] = (uint16_t)((lane << 5) | bt);
+#if GK_BU_PREFETCH_OFF
+        const uint32_t sec = (uint32_t)bt >> 2;  // 4 offsets per 32-byte sector
+        if (sec != last_sec) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(P.in_off + w * 32 + bt));
+          last_sec = sec;
+        }
+#endif
       }
     }
     acc_n[lane] = 0u;
-    acc_d[lane] = 0u;
     __syncwarp();
     int next_c = 0;
     uint32_t v[kBuSlots], d[kBuSlots], rounds[kBuSlots];
-    int64_t b[kBuSlots];
-    int st[kBuSlots];  // 0 empty, 1 head round, 3 second-head round, 2 in_nb rounds
+    int64_t b[kBuSlots], e[kBuSlots];
+    int st[kBuSlots];  // 0 empty, 1 offsets in flight, 2 in-list rounds
 #pragma unroll
     for (int k = 0; k < kBuSlots; k++) {
       st[k] = 0;
       v[k] = d[k] = rounds[k] = 0;
-      b[k] = 0;
+      b[k] = e[k] = 0;
     }
     for (;;) {
       // refill empty slots with the next pending vertices of the task
@@ -611,11 +720,10 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         next_c += __popc(nm);
         if constexpr (kList) {
           if (need && c < total) {
-            const uint32_t e = lst[c];
-            const uint32_t wd = e >> 5, bit = e & 31u;
-            v[k] = (uint32_t)((tbase + wd) * 32 + bit);
-            b[k] = (int64_t)s_hb[wd] + __popc(s_lv[wd] & ((1u << bit) - 1u));  // head record
-            rounds[k] = 0;
+            const uint32_t en = lst[c];
+            v[k] = (uint32_t)((tbase + (en >> 5)) * 32 + (en & 31u));
+            b[k] = ld_off(P.in_off + v[k]);
+            e[k] = ld_off(P.in_off + v[k] + 1);
             st[k] = 1;
           }
           continue;
@@ -623,18 +731,15 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         int lo = 0;  // word holding the c-th pending vertex: last lane with excl <= c
 #pragma unroll
         for (int step = 16; step > 0; step >>= 1) {
-          const int e = __shfl_sync(kFull, excl, lo + step);
-          if (e <= c) lo += step;
+          const int ex = __shfl_sync(kFull, excl, lo + step);
+          if (ex <= c) lo += step;
         }
         const uint32_t m = __shfl_sync(kFull, pm, lo);
         const int ex = __shfl_sync(kFull, excl, lo);
-        const uint32_t lv = __shfl_sync(kFull, live, lo);
-        const uint32_t hbl = __shfl_sync(kFull, hb, lo);
         if (need && c < total) {
-          const uint32_t bit = __fns(m, 0, c - ex + 1);
-          v[k] = (uint32_t)((tbase + lo) * 32 + (int)bit);
-          b[k] = (int64_t)hbl + __popc(lv & ((1u << bit) - 1u));  // head record (head rounds)
-          rounds[k] = 0;
+          v[k] = (uint32_t)((tbase + lo) * 32 + (int)__fns(m, 0, c - ex + 1));
+          b[k] = ld_off(P.in_off + v[k]);
+          e[k] = ld_off(P.in_off + v[k] + 1);
           st[k] = 1;
         }
       }
@@ -645,30 +750,20 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         if (next_c >= total) break;
         continue;
       }
-      // Round 1 of a vertex reads its head (dense, vertex order); later
-      // rounds continue in in_nb after the head.
       uint32_t u[kBuSlots][kPerRound];
 #pragma unroll
-      for (int k = 0; k < kBuSlots; k++) {
-        if (st[k] == 1) {
-          head_unpack(__ldg(P.head + b[k]), u[k]);
-        } else if (st[k] == 3) {
-          head_unpack(__ldg(P.head2 + b[k]), u[k]);
-        } else {
+      for (int k = 0; k < kBuSlots; k++)
 #pragma unroll
-          for (int j = 0; j < kPerRound; j++)
-            u[k][j] = (st[k] && d[k] > (uint32_t)j) ? ld_nb(P.in_nb + b[k] + j) : kNoVertex;
-        }
-      }
+        for (int j = 0; j < kPerRound; j++)
+          u[k][j] = (st[k] == 2 && d[k] > (uint32_t)j) ? ld_nb(P.in_nb + b[k] + j) : kNoVertex;
 #pragma unroll
       for (int k = 0; k < kBuSlots; k++) {
-        if (!st[k]) continue;
+        if (st[k] != 2) continue;
         bool hit = false;
         uint32_t par = 0;
         // The first in-neighbour's front bit alone, then the rest of the
         // round's at once: one lookup when the first hits, two latencies
-        // instead of up to kPerRound otherwise (measured against all-at-once
-        // and strictly sequential: +1.5-2% on kron27 and urand27).
+        // instead of up to kPerRound otherwise.
         uint32_t fw[kPerRound];
         fw[0] = u[k][0] != kNoVertex ? (kSmem ? front[u[k][0] >> 5] : ld_front(front + (u[k][0] >> 5))) : 0u;
         if ((fw[0] >> (u[k][0] & 31u)) & 1u) {
@@ -690,29 +785,6 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
           if (P.want_depth) P.depth[v[k]] = lvl + 1;
           atomicOr(&acc_n[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
           st[k] = 0;
-        } else if (st[k] == 1) {
-          if (u[k][0] == kNoVertex) {  // no in-edges: never reachable; skip it from now on
-            atomicOr(&acc_d[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
-            st[k] = 0;
-          } else if (u[k][kHead - 1] == kNoVertex) {
-            st[k] = 0;  // the list ended inside the head: not reached at this level
-          } else if (P.head2) {
-            st[k] = 3;  // round 2: the next kHead in-neighbours, same record index
-          } else {
-            b[k] = ld_off(P.in_off + v[k]) + kHead;
-            d[k] = (uint32_t)(ld_off(P.in_off + v[k] + 1) - b[k]);
-            rounds[k] = 1;
-            st[k] = d[k] ? 2 : 0;
-          }
-        } else if (st[k] == 3) {
-          if (u[k][kHead - 1] == kNoVertex) {
-            st[k] = 0;  // the list ended inside the second head
-          } else {
-            b[k] = ld_off(P.in_off + v[k]) + 2 * kHead;
-            d[k] = (uint32_t)(ld_off(P.in_off + v[k] + 1) - b[k]);
-            rounds[k] = 2;
-            st[k] = d[k] ? 2 : 0;
-          }
         } else {
           const uint32_t tk = d[k] < (uint32_t)kPerRound ? d[k] : (uint32_t)kPerRound;
           b[k] += tk;
@@ -725,12 +797,21 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
           }
         }
       }
+      // slots refilled this iteration start their rounds in the next one
+#pragma unroll
+      for (int k = 0; k < kBuSlots; k++) {
+        if (st[k] == 1) {
+          d[k] = (uint32_t)(e[k] - b[k]);  // < 2^32 (in-degree of one vertex)
+          rounds[k] = 0;
+          st[k] = d[k] ? 2 : 0;
+        }
+      }
     }
     __syncwarp();
     if ((int)lane < tw && w < P.w32) {
-      const uint32_t nbits = acc_n[lane], dbits = acc_d[lane];
+      const uint32_t nbits = acc_n[lane];
       next[w] = nbits;
-      if (nbits | dbits) P.visited[w] = vis | nbits | dbits;
+      if (nbits) P.visited[w] = vis | nbits;
       awake += __popc(nbits);
     }
     __syncwarp();
@@ -739,9 +820,9 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
 }
 
 // Long in-lists deferred by bu_step: one warp per vertex, ballot over 32
-// neighbours at a time, resuming after the head and the kLaneRounds-1
-// in_nb rounds bu_step tested.
-template <bool kSmem, bool kPull = false>
+// neighbours at a time, resuming after the kLaneScan in-neighbours bu_step
+// tested.
+template <bool kSmem, bool kPull = false, bool kSparse = false>
 __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* next, const uint32_t* lst,
                         unsigned long long count, int lvl, long long& awake, long long& scout) {
   const unsigned lane = lane_id();
@@ -750,7 +831,7 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
   for (long long i = gw; i < (long long)count; i += nw) {
     const uint32_t v = __ldcg(lst + i);
     const int64_t le = P.in_off[v + 1];
-    for (int64_t j = P.in_off[v] + kHead + kPerRound * (kLaneRounds - 1); j < le; j += 32) {
+    for (int64_t j = kSparse ? P.in_off[v] + kSparseScan : bu_resume(P.in_off[v]); j < le; j += 32) {
       const int64_t jj = j + lane;
       bool h = false;
       uint32_t u = 0;
@@ -789,7 +870,6 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
 // (first hit = parent, as bfs.hpp:55-60) for up to kSparseScan entries and
 // defers longer lists to bu_long.  A full bu_step sweep costs ~0.1 ms at
 // scale 27 even when nothing is pending (one dependent chain per task).
-constexpr int kSparseScan = kHead + kPerRound * (kLaneRounds - 1);  // where bu_long resumes
 
 __device__ void sp_list(const BfsParams& P, unsigned long long* ctr, uint32_t* lst, uint32_t* next) {
   const unsigned lane = lane_id();
@@ -928,7 +1008,7 @@ __device__ bool sparse_step(const BfsParams& P, SmemT& s, unsigned& ph, const ui
   const unsigned long long nlong = s.snap[kLongCount];
   if (nlong) {
     f = sc = 0;
-    bu_long<false, kPull>(P, front, next, lst + cnt, nlong, lvl, f, sc);
+    bu_long<false, kPull, true>(P, front, next, lst + cnt, nlong, lvl, f, sc);
     set = ph & 3;
     block_add(f, &P.ctrl->cnt[set][kSum], s);
     if (kPull) block_add(sc, &P.ctrl->cnt[set][kCount], s);
@@ -1019,7 +1099,6 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
 
   // ---- init (timed; replaces bfs.hpp:126-138) ----
   if (blockIdx.x == 0 && threadIdx.x == 0) P.ctrl->ts[0] = globaltimer();
-  zero_next_ctrl(P, gtid, gthreads);
   {
     const long long n4 = P.n >> 2;
     int4* p4 = reinterpret_cast<int4*>(P.parent);
@@ -1070,7 +1149,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   uint32_t* nextg = P.bm1;
   uint32_t* sfront = reinterpret_cast<uint32_t*>(dyn_smem);
   const long long nwarps = gthreads >> 5;
-  int bu_tw_log = 5;  // bottom-up task = 32 words unless that leaves warps idle
+  int bu_tw_log = P.bu_tw_log_max;  // bottom-up task = 32 words unless that leaves warps idle
   while (bu_tw_log > 0 && ((P.w32 + (1 << bu_tw_log) - 1) >> bu_tw_log) < nwarps) bu_tw_log--;
 
   // A large top-down step over the queue window [a, b) whose frontier's
@@ -1093,7 +1172,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
     // staying L2-resident; the frontier's lists are re-streamed per pass,
     // which HBM does at full bandwidth.
     unsigned long long nch = 0, nown = 0;
-    const bool own = P.own_split != nullptr && P.td_passes == 1;
+    const bool own = P.own_list != nullptr && P.td_passes == 1;
     for (int r = 0; r < P.td_passes; r++) {
       const uint32_t rlo = (uint32_t)((int64_t)r * P.td_span);
       const uint32_t rhi = r + 1 == P.td_passes ? 0xffffffffu : (uint32_t)((int64_t)(r + 1) * P.td_span);
@@ -1397,13 +1476,15 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st
   } else {
     // bottom-up pending lists; the owned-range slice when hub expansion is on
     dyn = kBuListBytes;
-    if (p.own_split) {
+    if (p.own_list) {
       if (p.own_r != grid) return cudaErrorInvalidConfiguration;
       dyn = std::max(dyn, (size_t)p.own_span_w * 4);
     }
     if (dyn > cfg.smem_keep_occ) return cudaErrorInvalidConfiguration;
   }
   BfsParams local = p;
+  // barrier counter, counter ring, step count, trace tags := 0
+  if (cudaError_t e = cudaMemsetAsync(p.ctrl, 0, kCtrlClear, st)) return e;
   // parent := -1 ahead of the kernel on the launch stream, inside the
   // caller's timed region.  GK_INIT_MODE: 1 (default) cudaMemsetAsync,
   // measured 1% faster per BFS at scale 27 than 0 (the same stores in the

@@ -50,34 +50,20 @@ gk_status need_device(int device) {
 void free_graph(gk_graph* g) {
   if (!g) return;
   cudaSetDevice(g->device);
+  if (g->stream) {
+    if (g->parent) cudaFreeAsync(g->parent, g->stream);
+    cudaStreamSynchronize(g->stream);
+  }
   if (g->in_off && g->in_off != g->out_off) cudaFree(g->in_off);
   if (g->in_nb && g->in_nb != g->out_nb) cudaFree(g->in_nb);
   cudaFree(g->out_off);
   cudaFree(g->out_nb);
-  cudaFree(g->parent);
-  cudaFree(g->parent2);
+  cudaFree(g->dead);
   cudaFree(g->depth);
-  cudaFree(g->bits);
-  cudaFree(g->head);
-  cudaFree(g->head2);
-  cudaFree(g->bc_sd);
-  cudaFree(g->bc_succ);
-  cudaFree(g->bc_scores);
-  cudaFree(g->bc_bounds);
-  cudaFree(g->bc_lv);
-  cudaFree(g->bc_lvdeg);
-  cudaFree(g->hbase);
-  cudaFree(g->deg16);
-  cudaFree(g->hv_bits);
-  cudaFree(g->hv_base);
-  cudaFree(g->own_split);
-  cudaFree(g->own_list);
-  cudaFree(g->own_stage);
-  cudaFree(g->queue);
-  cudaFree(g->chunks);
-  cudaFree(g->ctrl);
-  cudaFree(g->steps);
   cudaFree(g->acc);
+  if (g->pool) cudaMemPoolDestroy(g->pool);
+  if (g->batch_err) cudaFreeHost(g->batch_err);
+  for (cudaEvent_t e : g->batch_ev) cudaEventDestroy(e);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->stream) cudaStreamDestroy(g->stream);
@@ -85,99 +71,96 @@ void free_graph(gk_graph* g) {
   delete g;
 }
 
-// Workspace sized for n vertices / m arcs; reused across trials and
-// re-initialised inside the timed kernel.
-gk_status alloc_workspace(gk_graph* g) {
+constexpr size_t kAlign = 256;
+size_t up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+size_t bitmap_bytes(int64_t n) { return up((size_t)((n + 31) / 32) * 4 + 64); }
+
+// Graph-lifetime state: the dead-vertex layout (shared by BFS and Brandes),
+// the launch geometry, streams/events and the per-trial memory pool.  No
+// traversal-specific structure is derived from the graph here: every
+// traversal builds its own scratch inside its timed region.
+gk_status setup_graph(gk_graph* g, bool sorted) {
   const int64_t n = g->n;
   const int64_t w32 = (n + 31) / 32;
-  const size_t wbytes = ((size_t)w32 * 4 + 15) & ~size_t(15);
-  CK(cudaMalloc(&g->parent, sizeof(int32_t) * std::max<int64_t>(n, 4) + 16), "alloc parent");
-  // visited | front | next bitmaps in one block so one L2 access-policy
-  // window can keep them resident while the graph streams past.
-  CK(cudaMalloc(&g->bits, 4 * wbytes + 64), "alloc bitmaps");
-  g->visited = g->bits;
-  g->bm0 = g->bits + wbytes / 4;
-  g->bm1 = g->bits + 2 * (wbytes / 4);
-  g->dead = g->bits + 3 * (wbytes / 4);
-  CK(cudaMalloc(&g->queue, sizeof(uint32_t) * (n + 1)), "alloc queue");
-  g->chunk_cap = 2 * (g->m / 1024) + 65536;  // >= 4 x warps when chunks shrink to 128 edges
-  CK(cudaMalloc(&g->chunks, sizeof(gk::Chunk) * g->chunk_cap), "alloc chunks");
-  CK(cudaMalloc(&g->ctrl, 2 * sizeof(gk::Ctrl)), "alloc ctrl");
-  CK(cudaMemset(g->ctrl, 0, 2 * sizeof(gk::Ctrl)), "clear ctrl");
-  g->step_cap = std::min<int64_t>(n + 2, int64_t(1) << 20);
-  CK(cudaMalloc(&g->steps, sizeof(gk_step) * g->step_cap), "alloc step log");
-  CK(cudaMalloc(&g->acc, sizeof(unsigned long long) * 8), "alloc acc");
   CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking), "stream");
   CK(cudaEventCreate(&g->ev0), "event");
   CK(cudaEventCreate(&g->ev1), "event");
+  CK(cudaMalloc(&g->acc, sizeof(unsigned long long) * 8), "alloc acc");
   CK(gk::bfs_configure(g->device, &g->launch), "configure bfs kernel");
   if (getenv("GK_NO_FRONT_SMEM")) g->launch.smem_front_max = 0;  // tests: large-graph paths on small graphs
-  CK(gk::dead_bitmap(g->in_off, n, g->dead, g->stream), "dead-vertex bitmap");
-  CK(cudaMalloc(&g->hbase, sizeof(uint32_t) * std::max<int64_t>(w32, 1)), "alloc head index");
-  CK(gk::build_head(g->in_off, g->in_nb, n, g->dead, g->hbase, &g->head, &g->head2, &g->live, g->stream), "in-list heads");
-  CK(cudaMalloc(&g->deg16, std::max<int64_t>(w32, 1) * 64), "alloc degree array");
-  CK(gk::build_deg16(g->out_off, n, g->deg16, g->stream), "degree array");
+  CK(cudaMalloc(&g->dead, bitmap_bytes(n)), "alloc dead-vertex bitmap");
+  CK(gk::dead_bitmap(g->in_off, n, g->dead, &g->live, g->stream), "dead-vertex bitmap");
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = g->device;
+  CK(cudaMemPoolCreate(&g->pool, &props), "memory pool");
+  uint64_t keep = UINT64_MAX;  // keep freed blocks for the next trial
+  CK(cudaMemPoolSetAttribute(g->pool, cudaMemPoolAttrReleaseThreshold, &keep), "memory pool");
+  g->chunk_cap = 2 * (g->m / 1024) + 65536;  // >= 4 x warps when chunks shrink to 128 edges
+  g->step_cap = std::min<int64_t>(n + 2, int64_t(1) << 20);
   // Owned-range hub expansion (gk_internal.cuh OwnEnt): one target range per
   // CTA of the launch, its slice of the next bitmap in dynamic shared memory
-  // without lowering the occupancy; hubs (out-degree >= 8192; 4096 and 16384
-  // measured within 0.4% on kron27) get split rows.
-  // Off when the slice does not fit (n > ~2^27 at 296 CTAs) or memory is short.
+  // without lowering the occupancy; hubs = out-degree >= 32768 (with the
+  // in-trial run search: 8192 -1%, 65536 same, 262144 -5% on kron27).  Off when the slice does not fit
+  // (n > ~2^27 at 296 CTAs) or a list is not ascending (the per-range runs
+  // are found by search).
   {
     const int r = g->launch.grid;
     const int64_t span_w = ((w32 + r - 1) / r + 3) & ~int64_t(3);
     const bool fits = (size_t)span_w * 4 <= g->launch.smem_keep_occ && (size_t)w32 * 4 > g->launch.smem_front_max;
-    if (fits && !getenv("GK_NO_OWN")) {
-      int64_t nh = 0;
+    if (fits && sorted && !getenv("GK_NO_OWN")) {
       const char* dm = getenv("GK_OWN_DMIN");  // tests: hubs on small graphs
-      const int64_t dmin = dm ? std::max<int64_t>(1, strtoll(dm, nullptr, 10)) : 8192;
-      CK(gk::build_own(g->out_off, g->out_nb, n, dmin, r, span_w, size_t(1) << 30, &g->hv_bits, &g->hv_base,
-                       &g->own_split, &nh, g->stream),
-         "owned-range split rows");
-      if (nh > 0) {
-        CK(cudaMalloc(&g->own_list, sizeof(gk::OwnEnt) * nh), "alloc owned-range list");
-        int wl = 0;
-        while ((int64_t(2) << wl) <= span_w) wl++;
-        const int64_t nwin = (32 * span_w + (int64_t(1) << wl) - 1) >> wl;  // <= kOwnWin
-        CK(cudaMalloc(&g->own_stage, sizeof(uint2) * (size_t)r * (size_t)(nwin << wl)), "alloc owned-range log");
-        g->own_win_log = wl;
-        g->own_r = r;
-        g->own_span_w = span_w;
-        g->own_dmin = dmin;
-      }
+      g->own_dmin = dm ? std::max<int64_t>(1, strtoll(dm, nullptr, 10)) : 32768;
+      int wl = 0;
+      while ((int64_t(2) << wl) <= span_w) wl++;
+      const int64_t nwin = (32 * span_w + (int64_t(1) << wl) - 1) >> wl;  // <= kOwnWin
+      g->own_win_log = wl;
+      g->own_r = r;
+      g->own_span_w = span_w;
+      g->own_cap = g->m / g->own_dmin + 1;  // hubs of one frontier, at most
+      g->own_stage_bytes = sizeof(uint2) * (size_t)r * (size_t)(nwin << wl);
     }
   }
-  CK(cudaStreamSynchronize(g->stream), "dead-vertex bitmap");
-  // L2 persisting window over the bitmaps: off by default since the
-  // pending-list / sparse / pushed-step kernels (kron27 +2.6 %, urand27
-  // +1.4 % without it; a 1-bitmap window measured the same as none); the
-  // bitmap loads keep their evict_last hints.  GK_L2_PERSIST=1 restores it.
-  const char* pers = getenv("GK_L2_PERSIST");
-  if (pers && atoi(pers) != 0) {
-    int max_win = 0, max_pers = 0;
-    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
-    cudaDeviceGetAttribute(&max_pers, cudaDevAttrMaxPersistingL2CacheSize, g->device);
-    const char* nbm = getenv("GK_L2_BITMAPS");  // A-B: bitmaps in the window (visited, bm0, bm1, dead)
-    const size_t want = std::min<size_t>({(nbm ? (size_t)atoi(nbm) : 3) * wbytes, (size_t)max_win, (size_t)max_pers});
-    if (want > 0) {
-      size_t cur = 0;
-      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-      if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-      cudaStreamAttrValue a{};
-      a.accessPolicyWindow.base_ptr = g->bits;
-      a.accessPolicyWindow.num_bytes = want;
-      a.accessPolicyWindow.hitRatio = 1.0f;
-      a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      cudaStreamSetAttribute(g->stream, cudaStreamAttributeAccessPolicyWindow, &a);
-      cudaGetLastError();  // best effort: persistence is an optimisation only
-    }
-  }
+  CK(cudaStreamSynchronize(g->stream), "graph setup");
   return GK_OK;
 }
 
+// Per-trial scratch: one pool block for the traversal state (freed when the
+// kernel is done), one for the bookkeeping read back afterwards (control
+// block, step log), and the parent array (the result, kept until the next
+// trial on this handle replaces it).
+struct TrialBlocks {
+  void* work = nullptr;
+  void* book = nullptr;
+};
+cudaError_t trial_alloc(gk_graph* g, gk_trial* t, TrialBlocks* tb, cudaStream_t s, bool own) {
+  const size_t wb = bitmap_bytes(g->n);
+  const size_t sz_bits = 3 * wb, sz_q = up(sizeof(uint32_t) * (g->n + 1)),
+               sz_ch = up(sizeof(gk::Chunk) * g->chunk_cap),
+               sz_ol = own ? up(sizeof(gk::OwnEnt) * g->own_cap) : 0, sz_os = own ? up(g->own_stage_bytes) : 0;
+  const size_t sz_ctrl = up(sizeof(gk::Ctrl)), sz_steps = up(sizeof(gk_step) * g->step_cap);
+  cudaError_t e;
+  if ((e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&t->parent),
+                                   up(sizeof(int32_t) * std::max<int64_t>(g->n, 4) + 16), g->pool, s)))
+    return e;
+  if ((e = cudaMallocFromPoolAsync(&tb->work, sz_bits + sz_q + sz_ch + sz_ol + sz_os, g->pool, s))) return e;
+  if ((e = cudaMallocFromPoolAsync(&tb->book, sz_ctrl + sz_steps, g->pool, s))) return e;
+  char* w = static_cast<char*>(tb->work);
+  t->bits = reinterpret_cast<uint32_t*>(w);
+  t->queue = reinterpret_cast<uint32_t*>(w + sz_bits);
+  t->chunks = reinterpret_cast<gk::Chunk*>(w + sz_bits + sz_q);
+  t->own_list = own ? reinterpret_cast<gk::OwnEnt*>(w + sz_bits + sz_q + sz_ch) : nullptr;
+  t->own_stage = own ? reinterpret_cast<uint2*>(w + sz_bits + sz_q + sz_ch + sz_ol) : nullptr;
+  char* b = static_cast<char*>(tb->book);
+  t->ctrl = reinterpret_cast<gk::Ctrl*>(b);
+  t->steps = reinterpret_cast<gk_step*>(b + sz_ctrl);
+  return cudaSuccess;
+}
+
 // Kernel parameters of one traversal on g (tuning knobs read from the environment).
-gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int32_t strategy,
-                          int want_depth) {
+gk::BfsParams make_params(gk_graph* g, const gk_trial& t, uint32_t source, int64_t alpha, int64_t beta,
+                          int32_t strategy, int want_depth) {
   gk::BfsParams p{};
   p.n = g->n;
   p.m = g->m;
@@ -192,28 +175,23 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
   p.beta = beta;
   p.want_depth = want_depth;
   p.front_in_smem = ((size_t)p.w32 * 4 <= g->launch.smem_front_max) ? 1 : 0;
-  p.parent = g->parent;
+  p.parent = t.parent;
   p.depth = g->depth;
-  p.visited = g->visited;
+  const size_t ww = bitmap_bytes(g->n) / 4;
+  p.visited = t.bits;
+  p.bm0 = t.bits + ww;
+  p.bm1 = t.bits + 2 * ww;
   p.dead = g->dead;
-  p.head = g->head;
-  p.head2 = getenv("GK_NO_HEAD2") ? nullptr : g->head2;
-  p.hbase = g->hbase;
   p.live = g->live;
-  p.deg16 = g->deg16;
-  if (g->own_split && !p.front_in_smem && !getenv("GK_NO_OWN")) {
-    p.own_split = g->own_split;
-    p.hv_bits = g->hv_bits;
-    p.hv_base = g->hv_base;
-    p.own_list = g->own_list;
-    p.own_stage = g->own_stage;
+  if (t.own_list && !p.front_in_smem) {
+    p.own_list = t.own_list;
+    p.own_cap = g->own_cap;
+    p.own_stage = t.own_stage;
     p.own_r = g->own_r;
     p.own_span_w = (int32_t)g->own_span_w;
     p.own_win_log = g->own_win_log;
     p.own_dmin = g->own_dmin;
   }
-  p.bm0 = g->bm0;
-  p.bm1 = g->bm1;
   // Large top-down steps additionally clear and fill the n/8-byte next
   // bitmap and sum degrees in a separate pass; worth it above ~n/16 edges.
   p.bitmap_td_min = std::max<int64_t>(4096, g->n / 16);
@@ -229,50 +207,61 @@ gk::BfsParams make_params(gk_graph* g, uint32_t source, int64_t alpha, int64_t b
     p.td_span = ((g->n + p.td_passes - 1) / p.td_passes + 31) / 32 * 32;
   }
   if (const char* bt = getenv("GK_BITMAP_TD_MIN")) p.bitmap_td_min = strtoll(bt, nullptr, 10);
+  p.bu_tw_log_max = 5;
+  if (const char* tw = getenv("GK_BU_TASK_LOG")) p.bu_tw_log_max = std::max(0, std::min(5, atoi(tw)));
   // kTopDownRescan re-reads every new frontier's queue (bfs.hpp:161-167):
   // its steps keep the queue path (large steps leave the frontier a bitmap)
   if (strategy == GK_BFS_TOP_DOWN_RESCAN) p.bitmap_td_min = INT64_MAX;
-  p.queue = g->queue;
-  p.chunks = g->chunks;
+  p.queue = t.queue;
+  p.chunks = t.chunks;
   p.chunk_cap = g->chunk_cap;
-  p.ctrl = g->ctrl;
-  p.steps = g->steps;
+  p.ctrl = t.ctrl;
+  p.steps = t.steps;
   p.step_cap = g->step_cap;
   p.timeout_ns = 20ull * 1000 * 1000 * 1000;
   if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
   p.stop_after = 0xffffffffu;
   if (const char* sa = getenv("GK_STOP_AFTER")) p.stop_after = (unsigned)strtoul(sa, nullptr, 10);
-
   return p;
 }
 
-// Control blocks alternate between launches: each launch zeroes the other
-// one during its init phase, so no memset sits between launches.  After a
-// failed launch both are cleared (the kernel may not have finished that).
-void use_ctrl(gk_graph* g, gk::BfsParams& p) {  // call launched() once the kernel is queued
-  p.ctrl = g->ctrl + (g->ctrl_epoch & 1);
-  p.ctrl_next = g->ctrl + ((g->ctrl_epoch + 1) & 1);
+bool use_own(const gk_graph* g) {
+  return g->own_r > 0 && (size_t)((g->n + 31) / 32) * 4 > g->launch.smem_front_max;
 }
-void launched(gk_graph* g) { g->ctrl_epoch++; }
-void reset_ctrl(gk_graph* g) {
-  cudaMemset(g->ctrl, 0, 2 * sizeof(gk::Ctrl));
-  g->ctrl_epoch = 0;
+
+gk_status kernel_error(const gk::Ctrl& ctrl, const char* what) {
+  if (ctrl.error == 2) {
+    unsigned lo = ~0u, hi = 0;
+    for (int i = 0; i < 2048; i++) {
+      if (ctrl.cta_ph[i] == 0) continue;
+      lo = std::min(lo, ctrl.cta_ph[i]);
+      hi = std::max(hi, ctrl.cta_ph[i]);
+    }
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "%s kernel watchdog fired (grid barrier timeout): CTA barrier counts min %u max %u, arrivals %llu",
+             what, lo, hi, (unsigned long long)ctrl.bar_count);
+    return fail(GK_ERR_TIMEOUT, buf);
+  }
+  return fail(GK_ERR_CUDA, std::string(what) + " kernel: scratch buffer overflow");
 }
 
 gk_status finish_graph(gk_graph* g, gk_graph** out) {
   // every kernel indexes with these arrays: reject a malformed CSR up front
+  bool sorted = true;
   for (int pass = 0; pass < (g->directed ? 2 : 1); pass++) {
-    bool off_ok = true, ids_ok = true;
+    bool off_ok = true, ids_ok = true, srt = true;
     const cudaError_t e = gk::validate_csr(pass ? g->in_off : g->out_off, pass ? g->in_nb : g->out_nb, g->n, g->m,
-                                           g->n, &off_ok, &ids_ok, nullptr);
+                                           g->n, &off_ok, &ids_ok, pass ? nullptr : &srt, nullptr);
     if (e != cudaSuccess || !off_ok || !ids_ok) {
       free_graph(g);
       if (e != cudaSuccess) return cuda_fail(e, "validate CSR");
       return fail(GK_ERR_INVALID, !off_ok ? "invalid graph: offsets not monotone from 0 to m"
                                           : "invalid graph: neighbour id out of range");
     }
+    if (!pass) sorted = srt;
   }
-  gk_status st = alloc_workspace(g);
+  gk_status st = setup_graph(g, sorted);
   if (st != GK_OK) {
     free_graph(g);
     return st;
@@ -310,7 +299,7 @@ gk_status gk_graph_upload(const gk_csr_view* csr, int device, gk_graph** out) {
   g->directed = csr->directed ? 1 : 0;
   const size_t ob = sizeof(int64_t) * (g->n + 1), nbb = sizeof(uint32_t) * std::max<int64_t>(g->m, 1);
   cudaError_t e;
-  if ((e = cudaMalloc(&g->out_off, ob + 16)) || (e = cudaMalloc(&g->out_nb, nbb)) ||
+  if ((e = cudaMalloc(&g->out_off, ob + 16)) || (e = cudaMalloc(&g->out_nb, nbb + gk::kNbPad)) ||
       (e = cudaMemcpy(g->out_off, csr->out_offsets, ob, cudaMemcpyHostToDevice)) ||
       (g->m && (e = cudaMemcpy(g->out_nb, csr->out_neighbors, sizeof(uint32_t) * g->m,
                                cudaMemcpyHostToDevice)))) {
@@ -318,7 +307,7 @@ gk_status gk_graph_upload(const gk_csr_view* csr, int device, gk_graph** out) {
     return cuda_fail(e, "upload CSR");
   }
   if (g->directed) {
-    if ((e = cudaMalloc(&g->in_off, ob + 16)) || (e = cudaMalloc(&g->in_nb, nbb)) ||
+    if ((e = cudaMalloc(&g->in_off, ob + 16)) || (e = cudaMalloc(&g->in_nb, nbb + gk::kNbPad)) ||
         (e = cudaMemcpy(g->in_off, csr->in_offsets, ob, cudaMemcpyHostToDevice)) ||
         (g->m && (e = cudaMemcpy(g->in_nb, csr->in_neighbors, sizeof(uint32_t) * g->m,
                                  cudaMemcpyHostToDevice)))) {
@@ -491,39 +480,33 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   const int want_depth = (depth_out != nullptr) || g->keep_depth;
   if (want_depth && !g->depth)
     CK(cudaMalloc(&g->depth, sizeof(int32_t) * std::max<int64_t>(g->n, 4) + 16), "alloc depth");
-
-  gk::BfsParams p = make_params(g, source, alpha, beta, strategy, want_depth);
-
   cudaStream_t s = g->stream;
-  use_ctrl(g, p);
+  g->last_valid = 0;
+  if (g->parent) {  // the previous result goes back to the pool
+    CK(cudaFreeAsync(g->parent, s), "free previous result");
+    g->parent = nullptr;
+  }
+  // Timed trial: allocation of the result and every scratch buffer, their
+  // initialisation, the traversal, the release of the scratch.
+  gk_trial t;
+  TrialBlocks tb;
   CK(cudaEventRecord(g->ev0, s), "event record");
+  CK(trial_alloc(g, &t, &tb, s, use_own(g)), "allocate trial scratch");
+  g->parent = t.parent;
+  gk::BfsParams p = make_params(g, t, source, alpha, beta, strategy, want_depth);
   CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
-  launched(g);
+  CK(cudaFreeAsync(tb.work, s), "free trial scratch");
   CK(cudaEventRecord(g->ev1, s), "event record");
   gk::Ctrl& ctrl = g->last_ctrl;
-  g->last_valid = 0;
-  CK(cudaMemcpyAsync(&ctrl, p.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
+  CK(cudaMemcpyAsync(&ctrl, t.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
   CK(cudaStreamSynchronize(s), "bfs kernel");
+  if (ctrl.error) {
+    cudaFreeAsync(tb.book, s);
+    return kernel_error(ctrl, "bfs");
+  }
   g->last_valid = 1;
   g->depth_valid = want_depth;
-  if (ctrl.error) {
-    reset_ctrl(g);
-    if (ctrl.error == 2) {
-      unsigned lo = ~0u, hi = 0;
-      for (int i = 0; i < 2048; i++) {
-        if (ctrl.cta_ph[i] == 0) continue;
-        lo = std::min(lo, ctrl.cta_ph[i]);
-        hi = std::max(hi, ctrl.cta_ph[i]);
-      }
-      char buf[256];
-      snprintf(buf, sizeof(buf),
-               "bfs kernel watchdog fired (grid barrier timeout): CTA barrier counts min %u max %u, "
-               "arrivals %llu",
-               lo, hi, (unsigned long long)ctrl.bar_count);
-      return fail(GK_ERR_TIMEOUT, buf);
-    }
-    return fail(GK_ERR_CUDA, "bfs kernel: heavy-chunk buffer overflow");
-  }
+  gk_status st = GK_OK;
   if (stats) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1), "event time");
@@ -532,7 +515,7 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
     if (stats->steps && stats->max_steps > 0) {
       int64_t k = std::min<int64_t>({(int64_t)stats->max_steps, ctrl.num_steps, g->step_cap});
       if (k > 0)
-        CK(cudaMemcpy(stats->steps, g->steps, sizeof(gk_step) * k, cudaMemcpyDeviceToHost), "read steps");
+        CK(cudaMemcpyAsync(stats->steps, t.steps, sizeof(gk_step) * k, cudaMemcpyDeviceToHost, s), "read steps");
     }
     if (stats->want_counts) {
       CK(gk::count_reached(g->parent, g->out_off, g->n, g->acc, s), "count reached");
@@ -543,18 +526,21 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
       stats->component_edges = (int64_t)(g->directed ? two[1] : two[1] / 2);
     }
   }
+  CK(cudaFreeAsync(tb.book, s), "free trial bookkeeping");
   if (parent_out && g->n)
     CK(cudaMemcpyAsync(parent_out, g->parent, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, s), "D2H parent");
   if (depth_out && g->n)
     CK(cudaMemcpyAsync(depth_out, g->depth, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, s), "D2H depth");
-  if (parent_out || depth_out) CK(cudaStreamSynchronize(s), "D2H");
-  return GK_OK;
+  CK(cudaStreamSynchronize(s), "D2H");
+  return st;
 }
 
 // Many traversals with their parent arrays returned to host memory: the
-// D2H copy of traversal i (on a second stream) overlaps traversal i+1 (two
-// device parent buffers), so a run is bound by max(kernel, copy) per
-// source instead of their sum.  Same validation and results as gk_bfs.
+// D2H copy of traversal i (on a second stream) overlaps traversal i+1, so a
+// run is bound by max(kernel, copy) per source instead of their sum.  Every
+// trial allocates its result and scratch from the pool inside its own
+// timed region; a result returns to the pool once its copy has finished.
+// Same validation and results as gk_bfs.
 gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int64_t alpha, int64_t beta,
                        int32_t strategy, int32_t* const* parents_out, float* device_ms) {
   if (!g) return fail(GK_ERR_INVALID, "null graph");
@@ -566,74 +552,68 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
   if (count == 0) return GK_OK;
   std::lock_guard<std::mutex> lock(g->mu);
   CK(cudaSetDevice(g->device), "cudaSetDevice");
-  if (!g->parent2) CK(cudaMalloc(&g->parent2, sizeof(int32_t) * std::max<int64_t>(g->n, 4) + 16), "alloc parent");
   if (!g->cstream) CK(cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking), "stream");
-  cudaStream_t s = g->stream, cs = g->cstream;
-  std::vector<cudaEvent_t> ev(2 * (size_t)count + 4, nullptr);
-  int* errs = nullptr;
-  gk_status st = GK_OK;
-  auto cleanup = [&]() {
-    for (cudaEvent_t e : ev)
-      if (e) cudaEventDestroy(e);
-    if (errs) cudaFreeHost(errs);
-  };
-  for (auto& e : ev)
-    if (cudaEventCreate(&e) != cudaSuccess) {
-      cleanup();
-      return fail(GK_ERR_CUDA, "event create");
-    }
-  if (cudaHostAlloc(&errs, sizeof(int) * count, cudaHostAllocDefault) != cudaSuccess) {
-    cleanup();
-    return fail(GK_ERR_CUDA, "cudaHostAlloc");
+  const size_t nev = 3 * (size_t)count;  // per trial: start, end, copy done
+  while (g->batch_ev.size() < nev) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e), "event create");
+    g->batch_ev.push_back(e);
   }
-  cudaEvent_t* kdone = &ev[2 * (size_t)count];  // [2] kernel of slot done
-  cudaEvent_t* cdone = kdone + 2;               // [2] copy of slot done
-  int32_t* buf[2] = {g->parent, g->parent2};
+  if (g->batch_err_cap < count) {
+    if (g->batch_err) cudaFreeHost(g->batch_err);
+    g->batch_err = nullptr;
+    g->batch_err_cap = 0;
+    CK(cudaHostAlloc(&g->batch_err, sizeof(int) * count, cudaHostAllocDefault), "cudaHostAlloc");
+    g->batch_err_cap = count;
+  }
+  cudaStream_t s = g->stream, cs = g->cstream;
+  cudaEvent_t* ev = g->batch_ev.data();
+  int* errs = g->batch_err;
   g->last_valid = 0;
   g->depth_valid = 0;
+  if (g->parent) {
+    CK(cudaFreeAsync(g->parent, s), "free previous result");
+    g->parent = nullptr;
+  }
+  const bool own = use_own(g);
   cudaError_t e = cudaSuccess;
   for (int32_t i = 0; i < count && e == cudaSuccess; i++) {
-    const int slot = i & 1;
-    gk::BfsParams p = make_params(g, sources[i], alpha, beta, strategy, 0);
-    p.parent = buf[slot];
-    use_ctrl(g, p);
-    if (i >= 2 && (e = cudaStreamWaitEvent(s, cdone[slot], 0))) break;  // copy of i-2 has left buf
-    if ((e = cudaEventRecord(ev[2 * i], s))) break;
+    gk_trial t;
+    TrialBlocks tb;
+    // the copy of trial i-2 has returned its result to the pool
+    if (i >= 2 && (e = cudaStreamWaitEvent(s, ev[3 * (i - 2) + 2], 0))) break;
+    if ((e = cudaEventRecord(ev[3 * i], s))) break;
+    if ((e = trial_alloc(g, &t, &tb, s, own))) break;
+    gk::BfsParams p = make_params(g, t, sources[i], alpha, beta, strategy, 0);
     if ((e = gk::bfs_launch(p, g->launch, s))) break;
-    launched(g);
-    if ((e = cudaEventRecord(ev[2 * i + 1], s))) break;
-    if ((e = cudaMemcpyAsync(errs + i, &p.ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;
-    if ((e = cudaEventRecord(kdone[slot], s))) break;
-    if ((e = cudaStreamWaitEvent(cs, kdone[slot], 0))) break;
+    if ((e = cudaFreeAsync(tb.work, s))) break;
+    if ((e = cudaEventRecord(ev[3 * i + 1], s))) break;
+    if ((e = cudaMemcpyAsync(errs + i, &t.ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;
+    if ((e = cudaFreeAsync(tb.book, s))) break;
+    if ((e = cudaStreamWaitEvent(cs, ev[3 * i + 1], 0))) break;
     if (parents_out && parents_out[i] &&
-        (e = cudaMemcpyAsync(parents_out[i], buf[slot], sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, cs)))
+        (e = cudaMemcpyAsync(parents_out[i], t.parent, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, cs)))
       break;
-    if ((e = cudaEventRecord(cdone[slot], cs))) break;
+    if (i + 1 < count) {
+      if ((e = cudaFreeAsync(t.parent, cs))) break;
+    } else {
+      g->parent = t.parent;  // the last result stays for gk_bfs_device_parent
+    }
+    if ((e = cudaEventRecord(ev[3 * i + 2], cs))) break;
   }
   cudaError_t e2 = cudaStreamSynchronize(s), e3 = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = e2 != cudaSuccess ? e2 : e3;
-  if (e != cudaSuccess) {
-    cleanup();
-    reset_ctrl(g);
-    return fail(GK_ERR_CUDA, std::string("bfs batch: ") + cudaGetErrorString(e));
-  }
-  for (int32_t i = 0; i < count; i++)
-    if (errs[i]) {
-      reset_ctrl(g);
-      break;
-    }
-  for (int32_t i = 0; i < count && st == GK_OK; i++) {
-    if (errs[i] == 2) st = fail(GK_ERR_TIMEOUT, "bfs kernel watchdog fired (grid barrier timeout)");
-    else if (errs[i]) st = fail(GK_ERR_CUDA, "bfs kernel: heavy-chunk buffer overflow");
-    if (device_ms && st == GK_OK) {
+  if (e != cudaSuccess) return fail(GK_ERR_CUDA, std::string("bfs batch: ") + cudaGetErrorString(e));
+  for (int32_t i = 0; i < count; i++) {
+    if (errs[i] == 2) return fail(GK_ERR_TIMEOUT, "bfs kernel watchdog fired (grid barrier timeout)");
+    if (errs[i]) return fail(GK_ERR_CUDA, "bfs kernel: scratch buffer overflow");
+    if (device_ms) {
       float ms = 0;
-      cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]);
+      cudaEventElapsedTime(&ms, ev[3 * i], ev[3 * i + 1]);
       device_ms[i] = ms;
     }
   }
-  if ((count - 1) & 1) std::swap(g->parent, g->parent2);  // g->parent = the last result
-  cleanup();
-  return st;
+  return GK_OK;
 }
 
 const int32_t* gk_bfs_device_parent(const gk_graph* g) { return g ? g->parent : nullptr; }
@@ -689,7 +669,9 @@ gk_status gk_bfs_verify(gk_graph* g, uint32_t source, int64_t* errors) {
 // Brandes betweenness over the given sources (betweenness.hpp:84-145): one
 // cooperative launch per source accumulates into device scores, then one
 // max-normalisation.  Validation order and messages follow
-// betweenness.hpp:86-93.
+// betweenness.hpp:86-93.  The whole call is one trial: its workspace
+// (sigma/delta, successor bits, level data, traversal scratch) is taken from
+// the pool inside the timed region and returned at its end.
 gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, float* scores_out,
                      double* device_ms) {
   if (!g) return fail(GK_ERR_INVALID, "null graph");
@@ -703,71 +685,83 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
     if (o[1] == o[0]) return fail(GK_ERR_BAD_PARAM, "betweenness source has zero out-degree");
   }
   const int64_t n = g->n;
-  if (!g->depth) CK(cudaMalloc(&g->depth, sizeof(int32_t) * std::max<int64_t>(n, 4) + 16), "alloc depth");
-  if (!g->bc_sd) {
-    CK(cudaMalloc(&g->bc_sd, sizeof(double2) * std::max<int64_t>(n, 1)), "alloc sigma/delta");
-    CK(cudaMalloc(&g->bc_succ, sizeof(uint32_t) * ((g->m + 31) / 32 + 1)), "alloc successor bitmap");
-    CK(cudaMalloc(&g->bc_scores, sizeof(float) * std::max<int64_t>(n, 1) + 16), "alloc scores");
-    g->bc_bounds_cap = n + 2;
-    CK(cudaMalloc(&g->bc_bounds, sizeof(int64_t) * g->bc_bounds_cap), "alloc level bounds");
-    CK(cudaMalloc(&g->bc_lv, sizeof(uint32_t) * gk::kBcMaxPull * ((n + 31) / 32 + 4)), "alloc level bitmaps");
-    CK(cudaMalloc(&g->bc_lvdeg, sizeof(long long) * gk::kBcMaxPull), "alloc level arc sums");
-  }
-  g->last_valid = 0;  // depth/queue now hold Brandes state
+  const int64_t w32 = (n + 31) / 32;
+  g->last_valid = 0;  // the trace now describes Brandes
   g->depth_valid = 0;
+  cudaStream_t s = g->stream;
+  const size_t sz_sd = up(sizeof(double2) * std::max<int64_t>(n, 1)),
+               sz_succ = up(sizeof(uint32_t) * ((g->m + 31) / 32 + 1)),
+               sz_sc = up(sizeof(float) * std::max<int64_t>(n, 1) + 16), sz_dep = up(sizeof(int32_t) * (n + 4)),
+               sz_bd = up(sizeof(int64_t) * (n + 2)), sz_lv = up(sizeof(uint32_t) * gk::kBcMaxPull * (w32 + 4)),
+               sz_lvd = up(sizeof(long long) * gk::kBcMaxPull), sz_bits = 2 * bitmap_bytes(n),
+               sz_q = up(sizeof(uint32_t) * (n + 1)), sz_ch = up(sizeof(gk::Chunk) * g->chunk_cap),
+               sz_ctrl = up(sizeof(gk::Ctrl)), sz_st = up(sizeof(gk_step) * g->step_cap);
+  const size_t total = sz_sd + sz_succ + sz_sc + sz_dep + sz_bd + sz_lv + sz_lvd + sz_bits + sz_q + sz_ch + sz_ctrl +
+                       sz_st;
+  CK(cudaEventRecord(g->ev0, s), "event record");
+  char* w = nullptr;
+  CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&w), total, g->pool, s), "allocate brandes workspace");
   gk::BfsParams p{};
+  size_t at = 0;
+  auto carve = [&](size_t sz) {
+    char* r = w + at;
+    at += sz;
+    return r;
+  };
+  p.bc_sd = reinterpret_cast<double2*>(carve(sz_sd));
+  p.bc_succ = reinterpret_cast<uint32_t*>(carve(sz_succ));
+  p.bc_scores = reinterpret_cast<float*>(carve(sz_sc));
+  p.depth = reinterpret_cast<int32_t*>(carve(sz_dep));
+  p.bc_bounds = reinterpret_cast<int64_t*>(carve(sz_bd));
+  p.bc_bounds_cap = n + 2;
+  p.bc_lv = reinterpret_cast<uint32_t*>(carve(sz_lv));
+  p.bc_lvw = w32 + 4;
+  p.bc_lvdeg = reinterpret_cast<long long*>(carve(sz_lvd));
+  p.visited = reinterpret_cast<uint32_t*>(carve(sz_bits));
+  p.bm0 = p.visited + bitmap_bytes(n) / 4;
+  p.queue = reinterpret_cast<uint32_t*>(carve(sz_q));
+  p.chunks = reinterpret_cast<gk::Chunk*>(carve(sz_ch));
+  p.ctrl = reinterpret_cast<gk::Ctrl*>(carve(sz_ctrl));
+  p.steps = reinterpret_cast<gk_step*>(carve(sz_st));
   p.n = n;
   p.m = g->m;
-  p.w32 = (n + 31) / 32;
+  p.w32 = w32;
   p.out_off = g->out_off;
   p.out_nb = g->out_nb;
   p.in_off = g->in_off;
   p.in_nb = g->in_nb;
-  p.depth = g->depth;
-  p.queue = g->queue;
-  p.chunks = g->chunks;
   p.chunk_cap = g->chunk_cap;
-  p.ctrl = g->ctrl;
-  p.steps = g->steps;
   p.step_cap = g->step_cap;
   p.timeout_ns = 20ull * 1000 * 1000 * 1000;
-  if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
+  if (const char* wd = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(wd, nullptr, 10) * 1000000ull;
   p.stop_after = 0xffffffffu;
-  p.bc_sd = g->bc_sd;
-  p.bc_succ = g->bc_succ;
-  p.bc_scores = g->bc_scores;
-  p.bc_bounds = g->bc_bounds;
-  p.bc_bounds_cap = g->bc_bounds_cap;
-  p.bc_lv = g->bc_lv;
-  p.bc_lvw = (n + 31) / 32 + 4;
-  p.bc_lvdeg = g->bc_lvdeg;
-  p.visited = g->visited;
   p.dead = g->dead;
-  p.bm0 = g->bm0;
+  p.live = g->live;
   if (getenv("GK_BC_NO_PULL")) p.bc_lv = nullptr;  // top-down only (the reference's forward)
-  cudaStream_t s = g->stream;
-  CK(cudaMemsetAsync(g->bc_scores, 0, sizeof(float) * n, s), "clear scores");
-  CK(cudaEventRecord(g->ev0, s), "event record");
-  for (int64_t i = 0; i < num_sources; i++) {
+  gk_status st = GK_OK;
+  cudaError_t e = cudaMemsetAsync(p.bc_scores, 0, sizeof(float) * n, s);
+  for (int64_t i = 0; i < num_sources && !e && st == GK_OK; i++) {
     p.src = sources[i];
-    use_ctrl(g, p);
-    CK(gk::bc_launch(p, g->device, s), "launch brandes kernel");
-    launched(g);
+    if ((e = gk::bc_launch(p, g->device, s))) break;
     gk::Ctrl& ctrl = g->last_ctrl;  // kept for gk_bfs_trace (phase timings of the last source)
-    CK(cudaMemcpyAsync(&ctrl, p.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
-    CK(cudaStreamSynchronize(s), "brandes kernel");
+    if ((e = cudaMemcpyAsync(&ctrl, p.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s))) break;
+    if ((e = cudaStreamSynchronize(s))) break;
     g->last_valid = 1;
     const int err = ctrl.error;
-    if (err) reset_ctrl(g);
-    if (err == 2) return fail(GK_ERR_TIMEOUT, "brandes kernel watchdog fired (grid barrier timeout)");
-    if (err == 3) return fail(GK_ERR_CUDA, "brandes kernel: chunk buffer overflow");
-    if (err == 4) return fail(GK_ERR_CUDA, "brandes kernel: level bound buffer overflow");
-    if (err) return fail(GK_ERR_CUDA, "brandes kernel failed");
+    if (err == 2) st = fail(GK_ERR_TIMEOUT, "brandes kernel watchdog fired (grid barrier timeout)");
+    else if (err == 3) st = fail(GK_ERR_CUDA, "brandes kernel: chunk buffer overflow");
+    else if (err == 4) st = fail(GK_ERR_CUDA, "brandes kernel: level bound buffer overflow");
+    else if (err) st = fail(GK_ERR_CUDA, "brandes kernel failed");
   }
-  CK(gk::bc_normalize(g->bc_scores, n, g->bc_scores + n, s), "normalize scores");
-  CK(cudaEventRecord(g->ev1, s), "event record");
-  if (scores_out) CK(cudaMemcpyAsync(scores_out, g->bc_scores, sizeof(float) * n, cudaMemcpyDeviceToHost, s), "D2H");
-  CK(cudaStreamSynchronize(s), "brandes");
+  if (!e && st == GK_OK) e = gk::bc_normalize(p.bc_scores, n, p.bc_scores + n, s);
+  if (!e && st == GK_OK) e = cudaEventRecord(g->ev1, s);
+  if (!e && st == GK_OK && scores_out)
+    e = cudaMemcpyAsync(scores_out, p.bc_scores, sizeof(float) * n, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(w, s);
+  const cudaError_t es = cudaStreamSynchronize(s);
+  if (!e) e = es;
+  if (e) return cuda_fail(e, "brandes");
+  if (st != GK_OK) return st;
   if (device_ms) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1), "event time");

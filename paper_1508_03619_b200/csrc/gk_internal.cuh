@@ -2,24 +2,31 @@
 //
 // Layout in HBM (one gk_graph per device):
 //   graph     : out_off int64[n+1], out_nb uint32[m]; in_* alias out_* when
-//               undirected (graph.hpp:64-67), separate arrays when directed.
+//               undirected (graph.hpp:64-67), separate arrays when directed;
+//               dead uint32[ceil(n/32)] + live: the in-degree-0 vertices, a
+//               graph property read by every traversal kernel (BFS and
+//               Brandes seed their visited maps with it).
 //   per-trial : parent int32[n]           -- the result (ParentArray)
 //   scratch     visited/bm0/bm1 uint32[ceil(n/32)] -- 1 bit per vertex
 //               queue uint32[n+1]        -- sliding frontier queue
 //                                           (sliding_queue.hpp:24-57)
 //               chunks                   -- heavy-vertex edge chunks
-//               ctrl                     -- grid barrier + counter ring
-//   Scratch is re-initialised inside the timed kernel each trial
-//   (GAP rule: only the graph is reused between trials).
+//               own_list / own_stage     -- owned-range hub expansion
+//               ctrl, step log           -- grid barrier, counter ring, trace
+//   Everything per-trial is allocated from the graph's stream-ordered pool
+//   and initialised inside the timed region of each trial, and freed at its
+//   end (GAP rule: only the graph is reused between trials).
 #ifndef GK_INTERNAL_CUH_
 #define GK_INTERNAL_CUH_
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <mutex>
 #include <type_traits>
 #include <string>
+#include <vector>
 
 #include "../../include/gk_bfs.h"
 
@@ -39,21 +46,25 @@ enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend
                    kOwnCount = 7, kSlots = 8 };
 
 struct Ctrl {
+  // ---- cleared before every launch (kCtrlClear bytes) ----
   unsigned long long bar_count;  // monotonic grid-barrier arrivals
   int error;
   int pad0;
   long long num_steps;
   long long pad1;
   unsigned long long cnt[4][kSlots];
-  unsigned int cta_ph[2048];  // per-CTA barrier count (watchdog diagnostics)
-  // Trace: globaltimer at kernel start (ts[0]) and at the release of each
-  // of the first kTraceCap-1 grid barriers; tag[i] names the phase that
-  // barrier i ended (see PhaseTag).
-  unsigned long long ts[kTraceCap];
+  // Trace: tag[i] names the phase that grid barrier i ended (see PhaseTag),
+  // 0 past the last one.
   unsigned char tag[kTraceCap];
+  // ---- written before read ----
+  // globaltimer at kernel start (ts[0]) and at the release of each of the
+  // first kTraceCap-1 grid barriers.
+  unsigned long long ts[kTraceCap];
+  unsigned int cta_ph[2048];  // per-CTA barrier count (watchdog diagnostics; CTAs < grid)
 };
+constexpr size_t kCtrlClear = offsetof(Ctrl, ts);
 
-static_assert(sizeof(Ctrl) % 16 == 0, "control blocks are cleared with 16-byte stores and laid out in pairs");
+static_assert(sizeof(Ctrl) % 16 == 0 && kCtrlClear % 16 == 0, "control blocks are cleared with 16-byte stores");
 
 struct Chunk {
   uint32_t u;
@@ -61,36 +72,24 @@ struct Chunk {
   int64_t start;
 };
 
-// Head records: the first kHead in-neighbours of a vertex, kNoVertex-padded.
-constexpr int kHead = 4;
 constexpr uint32_t kNoVertex = 0xffffffffu;
-using HeadRec = std::conditional<kHead == 2, uint2, uint4>::type;
-static_assert(kHead == 2 || kHead == 4, "head records are uint2 or uint4");
-__host__ __device__ inline uint2 head_pack(const uint32_t* h, uint2*) { return make_uint2(h[0], h[1]); }
-__host__ __device__ inline uint4 head_pack(const uint32_t* h, uint4*) { return make_uint4(h[0], h[1], h[2], h[3]); }
-__host__ __device__ inline void head_unpack(const uint2& r, uint32_t* u) {
-  u[0] = r.x;
-  u[1] = r.y;
-  u[2] = u[3] = kNoVertex;
-}
-__host__ __device__ inline void head_unpack(const uint4& r, uint32_t* u) {
-  u[0] = r.x;
-  u[1] = r.y;
-  u[2] = r.z;
-  u[3] = r.w;
-}
+// Neighbour arrays are allocated with this many bytes past the last arc, so
+// a 32-byte-aligned sector load covering the last arcs stays inside the
+// allocation.
+constexpr size_t kNbPad = 32;
 
 // Owned-range hub expansion (large top-down steps): CTA r owns target ids
 // [r*span, (r+1)*span) (span = own_span_w*32) and stages that slice of the
-// next bitmap in shared memory; split[rank(u)*(R+1) + r] = first index in
-// u's (ascending) out-list whose target is >= r*span, for every vertex u of
-// out-degree >= own_dmin.  Claims are logged per window of own_span_w ids
-// (kOwnWin windows per range) in own_stage and their parents written window
-// by window in vertex order.
+// next bitmap in shared memory.  The step's hubs (frontier vertices of
+// out-degree >= own_dmin) are listed; each CTA finds the run of every hub's
+// ascending out-list that falls in its range by an interpolation search
+// inside the trial (no per-graph table).  Claims are logged per window of
+// 2^own_win_log ids (kOwnWin windows per range) in own_stage and their
+// parents written window by window in vertex order.
 constexpr int kOwnWin = 64;  // windows per owned range, at most
 struct OwnEnt {
   uint32_t u;
-  uint32_t rank;  // row of u in own_split
+  uint32_t deg;   // out-degree (< 2^32)
   int64_t base;   // out_off[u]
 };
 
@@ -115,30 +114,24 @@ struct BfsParams {
   uint32_t* visited;
   uint32_t* bm0;
   uint32_t* bm1;
-  const uint32_t* dead;  // in-degree-0 vertices (+ ids >= n): never reachable
-  const HeadRec* head;   // first kHead in-neighbours of every live vertex (kNoVertex-padded)
-  const HeadRec* head2;  // the next kHead in-neighbours (same index), or null
-  const uint32_t* hbase; // per bitmap word: index of its first live vertex's head
-  int64_t live;          // vertices with in-edges (not dead)
-  const uint16_t* deg16; // out-degree clamped to 65535 (65535: read out_off), padded to whole words
+  const uint32_t* dead;  // graph: in-degree-0 vertices (+ ids >= n), never reachable
+  int64_t live;          // graph: vertices with in-edges (not dead)
   uint32_t* queue;
   Chunk* chunks;
   int64_t chunk_cap;
   Ctrl* ctrl;
-  Ctrl* ctrl_next;      // the other control block: zeroed by this launch for the next one
   gk_step* steps;
   int64_t step_cap;
   unsigned long long timeout_ns;
   unsigned stop_after;  // leave after this many grid barriers (profiling only)
-  const uint32_t* own_split;  // null: owned-range expansion off
-  const uint32_t* hv_bits;    // vertices with a split row
-  const uint32_t* hv_base;    // per bitmap word: rank of its first split row
-  OwnEnt* own_list;           // the step's frontier vertices with split rows
+  OwnEnt* own_list;           // the step's hubs (null: owned-range expansion off)
+  int64_t own_cap;            // capacity of own_list
   uint2* own_stage;           // [R][windows][2^own_win_log] logged claims {id - window start, parent}
   int32_t own_r;              // ranges = CTAs of the launch
   int32_t own_span_w;         // bitmap words per range (multiple of 4)
   int32_t own_win_log;        // ids per claim-log window = 2^own_win_log <= own_span_w
-  int64_t own_dmin;           // out-degree that gets a split row
+  int64_t own_dmin;           // out-degree that counts as a hub
+  int32_t bu_tw_log_max;  // bottom-up task = 2^this bitmap words (5 unless overridden for A/B)
   int32_t td_passes;    // large top-down steps: target-range passes (1 when next fits L2)
   int64_t td_span;      // ids per pass (multiple of 32)
   // Brandes (betweenness.hpp:38-80), bc_persistent only
@@ -172,26 +165,13 @@ cudaError_t bc_launch(const BfsParams& p, int device, cudaStream_t s);
 // scores /= max(scores) when the max is > 0 (betweenness.hpp:136-143).
 cudaError_t bc_normalize(float* scores, int64_t n, float* scratch_max, cudaStream_t s);
 
-// Auxiliary (untimed) kernels.
-cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, cudaStream_t s);
-cudaError_t build_deg16(const int64_t* off, int64_t n, uint16_t* deg16, cudaStream_t s);
-// Owned-range split rows (see OwnEnt) for out-degree >= dmin, ranges of
-// span_w bitmap words.  *nh = rows built; 0 rows (and null arrays) when no
-// vertex qualifies, a qualifying out-list is not ascending, or the table
-// would exceed max_bytes.
-cudaError_t build_own(const int64_t* out_off, const uint32_t* out_nb, int64_t n, int64_t dmin, int r,
-                      int64_t span_w, size_t max_bytes, uint32_t** hv_bits, uint32_t** hv_base,
-                      uint32_t** split, int64_t* nh, cudaStream_t s);
+// Graph layout (built with the graph, shared by BFS and Brandes): dead =
+// in-degree-0 vertices and ids >= n; *live = vertices with in-edges.
+cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, int64_t* live, cudaStream_t s);
 // CSR invariants: n rows with offsets monotone from 0 to m, neighbour ids < id_bound.
+// *sorted (may be null: not checked) = every list strictly ascending.
 cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int64_t m, int64_t id_bound,
-                         bool* offsets_ok, bool* ids_ok, cudaStream_t s);
-// head[v] = the first kHead in-neighbours of v in CSR (ascending) order,
-// padded with kNoVertex: the bottom-up sweep's first round reads this dense
-// array (sequential in v) instead of one random sector of in_nb per vertex.
-// hbase[w] = live (non-dead) vertices in words < w; head is allocated here
-// with one record per live vertex.
-cudaError_t build_head(const int64_t* in_off, const uint32_t* in_nb, int64_t n, const uint32_t* dead,
-                       uint32_t* hbase, HeadRec** head, HeadRec** head2, int64_t* nlive, cudaStream_t s);
+                         bool* offsets_ok, bool* ids_ok, bool* sorted, cudaStream_t s);
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s);
 cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
@@ -222,6 +202,19 @@ cudaError_t build_grid(int64_t rows, int64_t cols, double p_delete, double p_dia
 
 }  // namespace gk
 
+// Scratch of one traversal (gk_bfs / one gk_bfs_batch trial), carved from
+// the graph's memory pool inside the timed region and returned at its end.
+struct gk_trial {
+  int32_t* parent = nullptr;   // the result; outlives the trial until the next one
+  uint32_t* bits = nullptr;    // visited | bm0 | bm1
+  uint32_t* queue = nullptr;
+  gk::Chunk* chunks = nullptr;
+  gk::OwnEnt* own_list = nullptr;
+  uint2* own_stage = nullptr;
+  gk::Ctrl* ctrl = nullptr;
+  gk_step* steps = nullptr;
+};
+
 struct gk_graph {
   int device = 0;
   int64_t n = 0;
@@ -231,48 +224,29 @@ struct gk_graph {
   uint32_t* out_nb = nullptr;
   int64_t* in_off = nullptr;  // == out_off when undirected
   uint32_t* in_nb = nullptr;
-  // workspace
-  int32_t* parent = nullptr;
-  int32_t* depth = nullptr;
-  uint32_t* bits = nullptr;  // one block: visited | bm0 | bm1 | dead
-  uint32_t* visited = nullptr;
-  uint32_t* bm0 = nullptr;
-  uint32_t* bm1 = nullptr;
-  uint32_t* dead = nullptr;  // graph property, computed once by finish_graph
-  uint32_t* hv_bits = nullptr;   // owned-range hub expansion (see OwnEnt), null when off
-  uint32_t* hv_base = nullptr;
-  uint32_t* own_split = nullptr;
-  gk::OwnEnt* own_list = nullptr;
-  uint2* own_stage = nullptr;
-  int own_r = 0;
-  int64_t own_span_w = 0, own_dmin = 0;
-  int own_win_log = 0;
-  int64_t live = 0;  // vertices with in-edges
-  uint16_t* deg16 = nullptr;  // out-degree clamped to 65535, for the claim sweep
-  gk::HeadRec* head = nullptr;  // ditto: the first kHead entries of every live in-list
-  gk::HeadRec* head2 = nullptr; // ditto: entries kHead..2*kHead-1 (optional)
-  uint32_t* hbase = nullptr; // ditto: head index of each word's first live vertex
-  // Brandes workspace, allocated on first use
-  double2* bc_sd = nullptr;
-  uint32_t* bc_succ = nullptr;
-  float* bc_scores = nullptr;
-  int64_t* bc_bounds = nullptr;
-  int64_t bc_bounds_cap = 0;
-  uint32_t* bc_lv = nullptr;
-  long long* bc_lvdeg = nullptr;
-  uint32_t* queue = nullptr;
-  gk::Chunk* chunks = nullptr;
+  // graph layout shared by the traversal kernels (BFS, Brandes), built with the graph
+  uint32_t* dead = nullptr;  // in-degree 0 (never reachable) + ids >= n
+  int64_t live = 0;          // vertices with in-edges
+  // per-trial scratch comes from this pool (stream-ordered, kept warm between
+  // trials so an allocation is a pointer bump, not an OS call)
+  cudaMemPool_t pool = nullptr;
   int64_t chunk_cap = 0;
-  gk::Ctrl* ctrl = nullptr;   // two control blocks, used alternately (no per-launch memset)
-  int ctrl_epoch = 0;
-  gk_step* steps = nullptr;
   int64_t step_cap = 0;
+  int own_r = 0;  // owned-range hub expansion geometry (0: off for this graph)
+  int64_t own_span_w = 0, own_dmin = 0, own_cap = 0;
+  int own_win_log = 0;
+  size_t own_stage_bytes = 0;
+  // the last traversal's result, kept for gk_bfs_device_parent / verify / model
+  int32_t* parent = nullptr;
+  int32_t* depth = nullptr;  // diagnostic depth array (parity / model runs), lazily
   unsigned long long* acc = nullptr;  // aux accumulators
   int32_t keep_depth = 0;
   int32_t depth_valid = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t cstream = nullptr;  // D2H stream of gk_bfs_batch (created on first use)
-  int32_t* parent2 = nullptr;      // second parent buffer of gk_bfs_batch's 2-deep pipeline
+  int* batch_err = nullptr;        // pinned: per-trial kernel error codes of gk_bfs_batch
+  int32_t batch_err_cap = 0;
+  std::vector<cudaEvent_t> batch_ev;  // gk_bfs_batch's events, grown on demand
   cudaEvent_t ev0 = nullptr;
   cudaEvent_t ev1 = nullptr;
   gk::BfsLaunch launch;

@@ -20,6 +20,17 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef GK_PARENT_HINTS
 #define GK_PARENT_HINTS 1  // evict_first on random parent stores
 #endif
+#ifndef GK_LD_CLOBBER
+#define GK_LD_CLOBBER 1  // "memory" clobber on the bitmap loads (A/B switch)
+#endif
+#if GK_LD_CLOBBER
+#define GK_MEMCLOB : "memory"
+#else
+#define GK_MEMCLOB
+#endif
+#ifndef GK_FRONT_NC
+#define GK_FRONT_NC 0  // A/B only: the non-coherent path for front loads (not legal for kernel-written data)
+#endif
 #ifndef GK_STREAM_HINTS
 #define GK_STREAM_HINTS 1  // evict_first on top-down adjacency loads
 #endif
@@ -38,7 +49,7 @@ struct __align__(16) SmemT {
     uint32_t t_u[kBlock];
   } td;
   union {
-    uint32_t bu_acc[kWarps][2][32];  // bottom-up: per-warp next/dead bits of a task
+    uint32_t bu_acc[kWarps][32];     // bottom-up: per-warp next bits of a task
     double bc_sig[kBlock];           // Brandes forward: sigma of the tile's frontier vertices
   };
   long long red[kWarps + 2];
@@ -79,9 +90,9 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 __device__ __forceinline__ uint32_t ld_bits(const uint32_t* p) {
   uint32_t v;
 #if GK_BITMAP_HINTS
-  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()) GK_MEMCLOB);
 #else
-  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p) GK_MEMCLOB);
 #endif
   return v;
 }
@@ -89,16 +100,25 @@ __device__ __forceinline__ uint32_t ld_bits(const uint32_t* p) {
 // are only ever set, so a stale 0 merely costs the atomic that follows).
 __device__ __forceinline__ uint32_t ld_bits_l1(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.global.ca.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+  asm volatile("ld.global.ca.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()) GK_MEMCLOB);
   return v;
 }
-// Read-only front bitmap word within a bottom-up phase: L1-cacheable, kept in L2.
+// Front bitmap word within a bottom-up phase: no thread writes it during the
+// phase, but the same kernel wrote it in an earlier one, so this is a weak
+// L1-cacheable load (not ld.global.nc, which PTX defines only for data that
+// is read-only for the kernel's whole lifetime).  Ordering: the grid
+// barrier's release-add / acquire-load pair (thread 0) plus bar.sync make
+// the earlier phase's stores visible; the acquire invalidates this SM's L1,
+// so no line cached before the barrier is served after it.  volatile +
+// "memory" keeps the compiler from moving the load across the barrier.
 __device__ __forceinline__ uint32_t ld_front(const uint32_t* p) {
   uint32_t v;
-#if GK_BITMAP_HINTS
-  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()));
+#if GK_FRONT_NC
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()) GK_MEMCLOB);
+#elif GK_BITMAP_HINTS
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy_evict_last()) GK_MEMCLOB);
 #else
-  asm("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.u32 %0, [%1];" : "=r"(v) : "l"(p) GK_MEMCLOB);
 #endif
   return v;
 }
@@ -190,14 +210,6 @@ __device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& ph, unsigned c
   ph++;
   // Profiling aid (GK_STOP_AFTER): every CTA leaves after the same barrier.
   return s.ok != 0 && ph < P.stop_after;
-}
-
-// The next launch's control block (launches alternate between two) is
-// cleared here, so no memset has to run between launches.
-__device__ __forceinline__ void zero_next_ctrl(const BfsParams& P, long long gtid, long long gthreads) {
-  if (!P.ctrl_next) return;
-  uint4* c = reinterpret_cast<uint4*>(P.ctrl_next);
-  for (long long i = gtid; i < (long long)(sizeof(Ctrl) / sizeof(uint4)); i += gthreads) c[i] = make_uint4(0, 0, 0, 0);
 }
 
 // Exclusive scan of one int64 per thread across the CTA; *total gets the sum.

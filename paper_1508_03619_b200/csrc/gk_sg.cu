@@ -128,7 +128,7 @@ int sg_load(const char* path, int64_t* n_out, int64_t* m_out, int* directed_out,
     if (actual < expected) fail(4, "file shorter than its declared arrays");  // io.hpp:415-421
   }
   if (!code && st.init() != cudaSuccess) fail(7, "cannot allocate staging buffers");
-  const size_t ob = (n + 1) * 8 + 16, nbb = (m ? m : 1) * 4;
+  const size_t ob = (n + 1) * 8 + 16, nbb = (m ? m : 1) * 4 + kNbPad;
   if (!code && (cudaMalloc(off, ob) || cudaMalloc(nb, nbb))) fail(8, "device allocation failed");
   std::string e;
   if (!code && !(e = stream_in(f, st, (char*)*off, (n + 1) * 8)).empty()) fail(4, e);

@@ -56,8 +56,6 @@ struct ShardParams {
   int big;    // large top-down step: owned claims go to `next`, then k_sh_sweep
   uint32_t* next;        // owned next bitmap (big top-down steps), starts as visited
   const uint32_t* dead;  // owned never-reachable bitmap
-  const HeadRec* head;   // head records of the owned live vertices
-  const uint32_t* hbase; // head index of each owned word's first live vertex
   uint32_t* longq;       // bottom-up long-list scratch (aliases pairs)
   int64_t long_cap;
 };
@@ -555,9 +553,9 @@ __global__ void k_sh_q2b(ShardParams P, unsigned long long qs, unsigned long lon
 // Bottom-up sweep of the owned vertices against the replicated front
 // (bfs.hpp:47-66), the persistent kernel's bu_step on owned rows: a warp
 // task is 32 owned words; pending (not visited, not dead) vertices are
-// numbered by a warp prefix sum; 2 slots per lane refilled as they resolve;
-// round 1 reads the vertex's head record, later rounds 4 in-neighbours of
-// the list; after kLaneRounds rounds a vertex is deferred to k_sh_bu_long.
+// numbered by a warp prefix sum; 2 slots per lane refilled as they resolve,
+// each round tests 4 in-neighbours of the list; after kShRounds rounds a
+// vertex is deferred to k_sh_bu_long.
 // Parent = first in-neighbour (ascending) with its front bit, as the
 // reference picks.
 constexpr int kShSlots = 2;
@@ -577,11 +575,9 @@ __global__ void __launch_bounds__(kSB) k_sh_bu(ShardParams P, const uint32_t* fr
   for (long long t = gw; t < ntasks; t += nw) {
     const long long tbase = t << tw_log;
     const long long w = tbase + lane;
-    uint32_t vis = 0xffffffffu, pad = 0u, live = 0u, hb = 0u;
+    uint32_t vis = 0xffffffffu, pad = 0u;
     if (lane < tw && w < w32) {
       vis = __ldcg(P.visited + w);
-      live = ~__ldg(P.dead + w);
-      hb = __ldg(P.hbase + w);
       const int64_t rem = P.nloc - w * 32;
       if (rem < 32) pad = 0xffffffffu << rem;
     }
@@ -599,7 +595,7 @@ __global__ void __launch_bounds__(kSB) k_sh_bu(ShardParams P, const uint32_t* fr
     int next_c = 0;
     uint32_t r[kShSlots], d[kShSlots], rounds[kShSlots];
     int64_t b[kShSlots];
-    int st[kShSlots];  // 0 empty, 1 head round, 2 list rounds
+    int st[kShSlots];  // 0 empty, 2 list rounds
 #pragma unroll
     for (int k = 0; k < kShSlots; k++) {
       st[k] = 0;
@@ -621,14 +617,13 @@ __global__ void __launch_bounds__(kSB) k_sh_bu(ShardParams P, const uint32_t* fr
         }
         const uint32_t m = __shfl_sync(kFullMask, pm, lo);
         const int ex = __shfl_sync(kFullMask, excl, lo);
-        const uint32_t lv = __shfl_sync(kFullMask, live, lo);
-        const uint32_t hbl = __shfl_sync(kFullMask, hb, lo);
         if (need && c < total) {
           const uint32_t bit = __fns(m, 0, c - ex + 1);
           r[k] = (uint32_t)((tbase + lo) * 32 + (int)bit);
-          b[k] = (int64_t)hbl + __popc(lv & ((1u << bit) - 1u));
+          b[k] = P.off[r[k]];
+          d[k] = (uint32_t)(P.off[r[k] + 1] - b[k]);
           rounds[k] = 0;
-          st[k] = 1;
+          st[k] = d[k] ? 2 : 0;
         }
       }
       bool active = false;
@@ -640,14 +635,9 @@ __global__ void __launch_bounds__(kSB) k_sh_bu(ShardParams P, const uint32_t* fr
       }
       uint32_t u[kShSlots][4];
 #pragma unroll
-      for (int k = 0; k < kShSlots; k++) {
-        if (st[k] == 1) {
-          head_unpack(__ldg(P.head + b[k]), u[k]);
-        } else {
+      for (int k = 0; k < kShSlots; k++)
 #pragma unroll
-          for (int j = 0; j < 4; j++) u[k][j] = (st[k] && d[k] > (uint32_t)j) ? __ldg(P.nb + b[k] + j) : kNoVertex;
-        }
-      }
+        for (int j = 0; j < 4; j++) u[k][j] = (st[k] && d[k] > (uint32_t)j) ? __ldg(P.nb + b[k] + j) : kNoVertex;
 #pragma unroll
       for (int k = 0; k < kShSlots; k++) {
         if (!st[k]) continue;
@@ -665,15 +655,6 @@ __global__ void __launch_bounds__(kSB) k_sh_bu(ShardParams P, const uint32_t* fr
           if (P.want_depth) P.depth[r[k]] = lvl + 1;
           atomicOr(&acc[(r[k] >> 5) - tbase], 1u << (r[k] & 31u));
           st[k] = 0;
-        } else if (st[k] == 1) {
-          if (u[k][kHead - 1] == kNoVertex) {
-            st[k] = 0;  // the list ended inside the head
-          } else {
-            b[k] = P.off[r[k]] + kHead;
-            d[k] = (uint32_t)(P.off[r[k] + 1] - b[k]);
-            rounds[k] = 1;
-            st[k] = d[k] ? 2 : 0;
-          }
         } else {
           const uint32_t tk = d[k] < 4u ? d[k] : 4u;
           b[k] += tk;
@@ -702,7 +683,7 @@ __global__ void __launch_bounds__(kSB) k_sh_bu(ShardParams P, const uint32_t* fr
 }
 
 // Long in-lists deferred by k_sh_bu: one warp per vertex, ballot over 32
-// neighbours, resuming after the head and the kShRounds-1 list rounds.
+// neighbours, resuming after the kShRounds list rounds.
 __global__ void __launch_bounds__(kSB) k_sh_bu_long(ShardParams P, const uint32_t* front, uint32_t* next_slice,
                                                     unsigned long long count, int lvl) {
   const int lane = threadIdx.x & 31;
@@ -712,7 +693,7 @@ __global__ void __launch_bounds__(kSB) k_sh_bu_long(ShardParams P, const uint32_
   for (long long i = gw; i < (long long)count; i += nw) {
     const uint32_t r = P.longq[i];
     const int64_t le = P.off[r + 1];
-    for (int64_t j = P.off[r] + kHead + 4 * (kShRounds - 1); j < le; j += 32) {
+    for (int64_t j = P.off[r] + 4 * kShRounds; j < le; j += 32) {
       const int64_t jj = j + lane;
       bool h = false;
       uint32_t u = 0;
@@ -815,8 +796,6 @@ struct gk_shard {
   int big = 0;                  // the current top-down step is a large one
   uint32_t* next = nullptr;     // owned next bitmap for large top-down steps
   uint32_t* dead = nullptr;     // owned never-reachable bitmap (built once)
-  gk::HeadRec* head = nullptr;  // head records of owned live vertices (built once)
-  uint32_t* hbase = nullptr;
   long long launches = 0;  // kernels launched on this shard (telemetry)
 };
 
@@ -860,8 +839,6 @@ gk::ShardParams params(const gk_shard* s) {
   p.big = s->big;
   p.next = s->next;
   p.dead = s->dead;
-  p.head = s->head;
-  p.hbase = s->hbase;
   p.longq = reinterpret_cast<uint32_t*>(s->pairs);
   p.long_cap = 2 * s->pair_cap;
   return p;
@@ -870,7 +847,7 @@ gk::ShardParams params(const gk_shard* s) {
 gk_status shard_alloc(gk_shard* s) {
   {  // the owned rows must be a valid CSR over global neighbour ids
     bool off_ok = true, ids_ok = true;
-    SCK(gk::validate_csr(s->off, s->nb, s->nloc, s->m, s->n, &off_ok, &ids_ok, nullptr), "validate shard CSR");
+    SCK(gk::validate_csr(s->off, s->nb, s->nloc, s->m, s->n, &off_ok, &ids_ok, nullptr, nullptr), "validate shard CSR");
     if (!off_ok) return shard_fail(GK_ERR_INVALID, "invalid shard: offsets not monotone from 0 to m");
     if (!ids_ok) return shard_fail(GK_ERR_INVALID, "invalid shard: neighbour id out of range");
   }
@@ -888,12 +865,9 @@ gk_status shard_alloc(gk_shard* s) {
   SCK(cudaMalloc(&s->acc, sizeof(unsigned long long) * 4), "alloc acc");
   SCK(cudaMalloc(&s->next, sizeof(uint32_t) * wl), "alloc next");
   SCK(cudaMalloc(&s->dead, sizeof(uint32_t) * wl), "alloc dead");
-  SCK(cudaMalloc(&s->hbase, sizeof(uint32_t) * wl), "alloc head index");
-  // graph-derived, once: never-reachable owned vertices, head records
-  SCK(gk::dead_bitmap(s->off, s->nloc, s->dead, nullptr), "dead bitmap");
+  // graph layout, once: never-reachable owned vertices
   int64_t nlive = 0;
-  SCK(gk::build_head(s->off, s->nb, s->nloc, s->dead, s->hbase, &s->head, nullptr, &nlive, nullptr), "head records");
-  SCK(cudaStreamSynchronize(nullptr), "shard derived data");
+  SCK(gk::dead_bitmap(s->off, s->nloc, s->dead, &nlive, nullptr), "dead bitmap");
   return GK_OK;
 }
 
@@ -902,8 +876,7 @@ void shard_free(gk_shard* s) {
   cudaSetDevice(s->device);
   for (void* p : {(void*)s->off, (void*)s->nb, (void*)s->parent, (void*)s->depth, (void*)s->visited,
                   (void*)s->sent, (void*)s->queue, (void*)s->pairs, (void*)s->chunks,
-                  (void*)s->ctr, (void*)s->acc, (void*)s->next, (void*)s->dead, (void*)s->head,
-                  (void*)s->hbase})
+                  (void*)s->ctr, (void*)s->acc, (void*)s->next, (void*)s->dead})
     cudaFree(p);
   delete s;
 }
@@ -983,7 +956,7 @@ GK_API gk_status gk_shard_upload(int64_t n, int rank, int nranks, const int64_t*
   s->m = local_offsets[s->nloc];
   cudaError_t e;
   if ((e = cudaMalloc(&s->off, sizeof(int64_t) * (s->nloc + 3))) ||
-      (e = cudaMalloc(&s->nb, sizeof(uint32_t) * std::max<int64_t>(s->m, 1))) ||
+      (e = cudaMalloc(&s->nb, sizeof(uint32_t) * std::max<int64_t>(s->m, 1) + gk::kNbPad)) ||
       (e = cudaMemcpy(s->off, local_offsets, sizeof(int64_t) * (s->nloc + 1), cudaMemcpyHostToDevice)) ||
       (s->m && (e = cudaMemcpy(s->nb, neighbors, sizeof(uint32_t) * s->m, cudaMemcpyHostToDevice)))) {
     shard_free(s);

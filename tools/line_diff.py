@@ -19,14 +19,21 @@ def per_line(rep, lib, col, kname="bfs_persistent"):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[1]
+    # the page holds one section per function ("Kernel Name", name / header / rows)
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+    sec = next(i for i in starts[:-1] if kname in rows[i][1])
+    h = rows[sec + 1]
     ia, ic = h.index("Address"), h.index(col)
-    data = rows[2:]
+    data = [r for r in rows[sec + 2:starts[starts.index(sec) + 1]] if r and r[ia].startswith("0x")]
     base = min(int(r[ia], 16) for r in data)
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=d, capture_output=True)
-        cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-        dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True, text=True).stdout
+        dis = ""
+        for cub in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):
+            t = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True, text=True).stdout
+            if kname in t:
+                dis = t
+                break
     in_k, line, off2line = False, None, {}
     for l in dis.splitlines():
         if l.startswith("//---") and ".text." in l:
