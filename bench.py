@@ -61,6 +61,11 @@ CONFIGS = {
                               "2% diagonal shortcuts"),
 }
 SEED = 24601
+# One metric string for both arms (ours and --impl reference): the driver
+# pairs the two lines by it.  The HBM-roofline half of BASELINE.json's metric
+# is the line's "roofline" object.
+METRIC = "BFS GTEPS (harmonic mean over sources)"
+L2_NOTE = "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)"
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
@@ -75,6 +80,15 @@ def parse_config(name: str) -> dict:
             return dict(kind=kind, scale=sc, degree=16, permute=(kind == "kron"), name=name,
                         workload=f"{kind} 2^{sc} vertices, edge factor 16" + (", permuted" if kind == "kron" else ""))
     raise SystemExit(f"unknown config {name}")
+
+
+def line_config(cfg: dict, n: int, arcs: int, K: int) -> dict:
+    """The workload both arms print (identical keys and values)."""
+    csr = arcs * 4 + n * 8
+    l2 = (L2_NOTE % (csr / 1e9)) if csr > 126e6 else \
+        f"graph L2-resident (CSR {csr / 1e6:.0f} MB < 126 MB L2), as a loaded graph stays between GAP trials"
+    return {"workload": cfg["workload"], "name": cfg["name"], "n": int(n), "arcs": int(arcs), "seed": SEED,
+            "sources": K, "alpha": 15, "beta": 18, "l2": l2}
 
 
 def hmean(xs):
@@ -197,6 +211,42 @@ def cpu_reference(g, sources, warmup, budget_s, label, m_of=None):
             "mean_ms": 1e3 * sum(secs) / max(len(secs), 1), "setup_s": round(tstart - t0, 2)}
 
 
+def reference_arm(args, cfg, K, W):
+    """--impl reference: the UNMODIFIED reference on the host cores, nothing
+    of ours on the path.  Graph: the reference's generator (or the grid),
+    the ID permutation and a 64-bit BuildCsr on the host (oracle/ref_bench.cc,
+    pinned byte-identical to BuildCsr); sources: PickSources
+    (source_picker.hpp:47-54); trials: RunBenchmark's BFS loop
+    (benchmark.hpp:178-185) around gapkit::Bfs.  libgk_bfs.so is never loaded."""
+    from oracle import oracle as O
+    R = O.RefLib()
+    t0 = time.time()
+    if cfg["kind"] == "grid":
+        rg = R.bench_graph("grid", seed=SEED, rows=cfg["rows"], cols=cfg["cols"], p_delete=cfg["p_delete"],
+                           p_diag=cfg["p_diag"])
+    else:
+        rg = R.bench_graph(cfg["kind"], cfg["scale"], cfg["degree"], SEED, permute=cfg["permute"])
+    build_s = time.time() - t0
+    sources = rg.pick_sources(K, SEED)
+    if W:
+        rg.trials((list(sources) * (W // max(K, 1) + 1))[:W])
+    secs, mcc = rg.trials(sources)
+    value = hmean([m / t / 1e9 for m, t in zip(mcc, secs)])
+    threads = R.L.gkr_max_threads()
+    sample = (f"{cfg['name']}: all {K} picked sources, gapkit::Bfs (unmodified reference headers, "
+              f"oracle/_ref), OpenMP {threads} threads, OMP_WAIT_POLICY=active, OMP_PROC_BIND=spread; "
+              f"graph built on the host (reference generator + 64-bit BuildCsr) in {build_s:.0f} s")
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": args.gpus,
+            "steps": K, "warmup": W, "ms_per_step": 1e3 * statistics.mean(secs), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (seeded generator, no dataset)",
+            "config": line_config(cfg, rg.n, rg.m, K),
+            "run": {"host_cpu": cpu_model(), "nproc": os.cpu_count(), "host_build_s": round(build_s, 1)},
+            "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -283,7 +333,7 @@ def run_sharded(args, cfg, rank, world, local, dist):
                            "bytes_in_per_bfs_max_rank": sum(nvl) / len(nvl),
                            "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}}
     line = {
-        "metric": "BFS GTEPS (harmonic mean over sources) and % of HBM roofline",
+        "metric": METRIC,
         "value": value, "unit": "GTEPS", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": statistics.mean(dev_ms), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generator, no dataset)",
@@ -328,6 +378,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = parse_config(args.config)
     K, W = args.steps, max(args.warmup, 0)
+    if args.impl == "reference":  # rank 0 alone; no NCCL, no GPU, no libgk_bfs.so
+        if rank == 0:
+            print(json.dumps(reference_arm(args, cfg, K, W)), flush=True)
+        return
     dist = None
     if world > 1:
         import torch
@@ -336,27 +390,6 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_1508_03619_b200 import PinnedBuffer
-
-    if args.impl == "reference":
-        if rank != 0:
-            if dist:
-                dist.destroy_process_group()
-            return
-        g, build_s = build_graph(cfg, local)
-        sources = g.pick_sources(K, SEED)
-        res = cpu_reference(g, sources, W, budget_s=1e9, label=cfg["name"])
-        line = {"impl": "reference", "metric": "BFS GTEPS (harmonic mean over sources)", "value": res["value"],
-                "unit": "GTEPS", "n_gpus": args.gpus, "steps": K, "warmup": W,
-                "ms_per_step": res["mean_ms"], "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generator, no dataset)",
-                "config": {"workload": cfg["workload"], "name": cfg["name"], "n": g.n, "arcs": g.m,
-                           "host_cpu": cpu_model(), "nproc": os.cpu_count()},
-                "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": res["value"], "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        if dist:
-            dist.destroy_process_group()
-        return
 
     # ---------------- our arm ----------------
     if cfg["kind"] != "grid" and args.multi == "sharded" and (world > 1 or args.force_sharded):
@@ -468,26 +501,26 @@ def main():
     scheds = sorted(set(v if len(v) <= 48 else f"{v[:40]}...({len(v)} steps)" for v in sched_of.values()),
                     key=len)
     line = {
-        "metric": "BFS GTEPS (harmonic mean over sources) and % of HBM roofline",
+        "metric": METRIC,
         "value": value, "unit": "GTEPS", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": statistics.mean(step_ms), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generator, no dataset)",
-        "config": {"workload": cfg["workload"], "name": cfg["name"], "n": g.n, "arcs": g.m, "seed": SEED,
-                   "sources": K, "alpha": 15, "beta": 18,
-                   "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % ((g.m * 4 + g.n * 8) / 1e9),
-                   "parallelism": "single GPU" if world == 1 else
-                   f"{world} source-parallel replicas (whole graph per GPU, no data-path collective)",
-                   "device_build_s": round(build_s, 2), "timed_region_wall_s": round(wall, 4),
-                   "schedules": scheds[:4], "mean_m_cc": statistics.mean(step_m),
-                   "verified": (f"{verified}/{len(sources)} sources pass the device BFS certificate "
-                                "(depths exact, parents valid)") if not args.no_model else "not run"},
-        "e2e": {"value": e2e_val, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * g.n,
+        "config": line_config(cfg, g.n, g.m, K),
+        "run": {"parallelism": "single GPU" if world == 1 else
+                f"{world} source-parallel replicas (whole graph per GPU, no data-path collective)",
+                "trial": "one gk_bfs: pool allocation of the result and all scratch, their initialisation, "
+                         "the traversal kernel, scratch release -- CUDA events around all of it",
+                "device_build_s": round(build_s, 2), "timed_region_wall_s": round(wall, 4),
+                "schedules": scheds[:4], "mean_m_cc": statistics.mean(step_m),
+                "verified": (f"{verified}/{len(sources)} sources pass the device BFS certificate "
+                             "(depths exact, parents valid)") if not args.no_model else "not run"},
+        "e2e": {"value": e2e_val, "unit": "GTEPS", "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4 * g.n,
                 "one_call_per_source": hmean([m_of[s] / t / 1e9 for s, t in zip(sources, single_s)]),
                 "note": "gk_bfs_batch over the K sources, every source's parent array copied to pinned host "
                         "memory inside the timed region (copy of result i overlaps traversal i+1); "
                         "one_call_per_source = gk_bfs per source without overlap (first 8 sources); graph "
                         "resident (uploaded once, untimed, as the reference harness builds it untimed); "
-                        "per-step input is the source id passed by value"},
+                        "the per-step input is the 4-byte source id (a kernel argument)"},
         "gpu_launches": K,
         "clocks": clocks,
         "roofline": roof,

@@ -86,7 +86,9 @@ typedef struct {
   int32_t max_steps;       /* capacity of steps */
   int32_t want_counts;     /* fill reached / component_edges (untimed pass) */
   /* out */
-  float device_ms;         /* CUDA-event time of the traversal kernel */
+  float device_ms;         /* CUDA-event time of the whole trial: pool allocation of the result
+                              and all scratch, their initialisation, the traversal kernel,
+                              release of the scratch */
   int32_t num_steps;       /* steps executed (may exceed max_steps) */
   int64_t reached;         /* vertices with parent >= 0 */
   int64_t component_edges; /* sum of out-degree over reached / (directed?1:2) */
@@ -151,10 +153,11 @@ GK_API gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t bet
 
 /* gk_bfs over count sources (same validation, results and errors) with
  * parents_out[i] (host, ideally pinned; may repeat or be NULL) receiving
- * traversal i's ParentArray.  The copy of result i overlaps traversal i+1
- * (two device parent buffers, a second stream), as the reference harness's
- * trial loop would if it could (benchmark.hpp:178-185).  device_ms[i]
- * (may be NULL) = CUDA-event time of traversal i's kernel. */
+ * traversal i's ParentArray.  The copy of result i (on a second stream)
+ * overlaps traversal i+1, as the reference harness's trial loop would if it
+ * could (benchmark.hpp:178-185); each trial takes its result and scratch
+ * from the handle's pool.  device_ms[i] (may be NULL) = CUDA-event time of
+ * trial i, as gk_bfs_stats.device_ms. */
 GK_API gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int64_t alpha,
                               int64_t beta, int32_t strategy, int32_t* const* parents_out,
                               float* device_ms);
@@ -162,6 +165,11 @@ GK_API gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t coun
 /* Device pointer to the parent array of the last gk_bfs on this handle
  * (valid until the next call / free). */
 GK_API const int32_t* gk_bfs_device_parent(const gk_graph* g);
+
+/* Device pointer to the depth array the last gk_bfs recorded (it must have
+ * requested depth_out or gk_bfs_keep_depth), or NULL.  Test hook for the
+ * certificate's tamper tests. */
+GK_API int32_t* gk_bfs_device_depth(const gk_graph* g);
 
 /* Phase trace of the last gk_bfs: ts_ns[0] = kernel start, ts_ns[i] = release
  * of grid barrier i (globaltimer ns) and tags[i] the phase it ended: 'I' init,

@@ -309,6 +309,17 @@ class RefLib:
         L.gkr_brandes.restype = C.c_int
         L.gkr_verify_bc.argtypes = [vp, _U32P, C.c_int64, C.POINTER(C.c_float), C.c_char_p, C.c_int]
         L.gkr_verify_bc.restype = C.c_int
+        # ref_bench.cc: bench-configuration graphs, the 64-bit builder, trial loop
+        L.gkr_bench_graph.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_int, C.c_double, C.c_double,
+                                      C.c_char_p, C.c_int]
+        L.gkr_bench_graph.restype = vp
+        L.gkr_build64.argtypes = [C.c_int64, _U32P, C.c_int64]
+        L.gkr_build64.restype = vp
+        L.gkr_graph_views.argtypes = [vp, C.POINTER(vp), C.POINTER(vp)]
+        L.gkr_component_edges.argtypes = [vp, _I32P]
+        L.gkr_component_edges.restype = C.c_int64
+        L.gkr_bfs_trials.argtypes = [vp, _U32P, C.c_int, C.c_int64, C.c_int64,
+                                     np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS"), _I64]
         self.L = L
 
     def gen(self, kind: str, scale: int, degree: int = 16, seed: int = 24601) -> np.ndarray:
@@ -324,6 +335,24 @@ class RefLib:
         if not h:
             raise RuntimeError(err.value.decode())
         return RefGraph(self, h)
+
+    def bench_graph(self, kind: str, scale: int = 0, degree: int = 16, seed: int = 24601, permute: bool = True,
+                    rows: int = 0, cols: int = 0, p_delete: float = 0.15, p_diag: float = 0.02) -> "RefGraph":
+        """A bench configuration's graph built on the host: the reference's
+        generator (or the grid), the ID permutation, the 64-bit BuildCsr
+        (ref_bench.cc)."""
+        err = C.create_string_buffer(256)
+        k = {"kron": 0, "urand": 1, "grid": 2}[kind]
+        a, b = (rows, cols) if kind == "grid" else (scale, degree)
+        h = self.L.gkr_bench_graph(k, a, b, seed, int(permute), p_delete, p_diag, err, 256)
+        if not h:
+            raise RuntimeError(err.value.decode())
+        return RefGraph(self, h)
+
+    def build64(self, n: int, edges: np.ndarray) -> "RefGraph":
+        """ref_bench.cc's 64-bit OpenMP BuildCsr(el, false, true)."""
+        e = np.ascontiguousarray(edges, np.uint32)
+        return RefGraph(self, self.L.gkr_build64(n, e if e.size else np.zeros(2, np.uint32), e.size // 2))
 
     def read_sg(self, path: str) -> "RefGraph":
         err = C.create_string_buffer(256)
@@ -401,6 +430,27 @@ class RefGraph:
         secs = np.empty(s.size, np.float64)
         self.ref.L.gkr_bfs_timed(self.h, s, s.size, alpha, beta, secs, None)
         return secs
+
+    def trials(self, sources, alpha: int = 15, beta: int = 18) -> tuple[np.ndarray, np.ndarray]:
+        """RunBenchmark's BFS trials: seconds per Bfs call and the component
+        edges of each result."""
+        s = np.ascontiguousarray(sources, np.uint32)
+        secs = np.empty(s.size, np.float64)
+        mcc = np.empty(s.size, np.int64)
+        self.ref.L.gkr_bfs_trials(self.h, s, s.size, alpha, beta, secs, mcc)
+        return secs, mcc
+
+    def views(self) -> tuple[np.ndarray, np.ndarray]:
+        """(offsets, neighbours) of the out-CSR as read-only numpy views of
+        the reference's own vectors (valid while this object lives)."""
+        po, pn = C.c_void_p(), C.c_void_p()
+        self.ref.L.gkr_graph_views(self.h, C.byref(po), C.byref(pn))
+        off = np.frombuffer((C.c_int64 * (self.n + 1)).from_address(po.value), np.int64)
+        nb = np.frombuffer((C.c_uint32 * max(self.m, 1)).from_address(pn.value or po.value), np.uint32)[: self.m]
+        return off, nb
+
+    def component_edges(self, parent: np.ndarray) -> int:
+        return int(self.ref.L.gkr_component_edges(self.h, np.ascontiguousarray(parent, np.int32)))
 
     def schedule(self, src: int, alpha: int = 15, beta: int = 18, strategy: int = 0,
                  max_steps: int = 1 << 16) -> Replay:

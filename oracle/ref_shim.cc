@@ -23,21 +23,12 @@
 #include <vector>
 
 #include "gapkit/gapkit.hpp"
+#include "ref_graph.hpp"
 
 using namespace gapkit;
+using gkref::RefGraph;
 
 namespace {
-
-struct RefGraph {
-  bool directed = false;
-  int64_t n = 0;
-  std::vector<int64_t> off;
-  std::vector<NodeId> nb;
-  std::vector<int64_t> in_off;
-  std::vector<NodeId> in_nb;
-  CsrGraph g;
-  bool sealed = false;
-};
 
 void SetErr(char* err, int len, const std::string& s) {
   if (err && len > 0) {

@@ -265,6 +265,9 @@ class DeviceGraph:
     def device_parent_ptr(self) -> int:
         return int(_lib.load().gk_bfs_device_parent(self._h) or 0)
 
+    def device_depth_ptr(self) -> int:
+        return int(_lib.load().gk_bfs_device_depth(self._h) or 0)
+
     def bfs_batch(self, sources, outs=None, alpha: int = 15, beta: int = 18, strategy: int = 0) -> np.ndarray:
         """gk_bfs_batch: one traversal per source, parent array i copied into
         outs[i] (host int32 arrays of length n, ideally PinnedBuffer views;

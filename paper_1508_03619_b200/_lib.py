@@ -28,7 +28,7 @@ GK_ERR_LOAD = 10
 EXPORTED = (
     "gk_last_error", "gk_abi_version", "gk_device_count", "gk_graph_upload",
     "gk_graph_generate", "gk_graph_generate_grid", "gk_graph_free", "gk_graph_info",
-    "gk_graph_download", "gk_pick_sources", "gk_bfs", "gk_bfs_device_parent",
+    "gk_graph_download", "gk_pick_sources", "gk_bfs", "gk_bfs_device_parent", "gk_bfs_device_depth",
     "gk_bfs_byte_model", "gk_bfs_keep_depth", "gk_host_alloc", "gk_host_free", "gk_bfs_trace",
     "gk_shard_last_error", "gk_shard_generate", "gk_shard_upload", "gk_shard_free", "gk_shard_info",
     "gk_shard_set_stream", "gk_shard_degree", "gk_shard_begin", "gk_shard_td_expand", "gk_shard_td_apply",
@@ -84,6 +84,8 @@ def load() -> C.CDLL:
     L.gk_bfs.argtypes = [vp, u32, i64, i64, i32, vp, vp, C.POINTER(BfsStats)]
     L.gk_bfs_device_parent.argtypes = [vp]
     L.gk_bfs_device_parent.restype = vp
+    L.gk_bfs_device_depth.argtypes = [vp]
+    L.gk_bfs_device_depth.restype = vp
     L.gk_bfs_byte_model.argtypes = [vp, C.POINTER(Step), i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.gk_bfs_keep_depth.argtypes = [vp, i32]
     L.gk_bfs_verify.argtypes = [vp, u32, vp]
@@ -116,7 +118,7 @@ def load() -> C.CDLL:
     L.gk_host_free.restype = None
     for f in EXPORTED:
         if f not in ("gk_last_error", "gk_abi_version", "gk_device_count", "gk_graph_free",
-                     "gk_bfs_device_parent", "gk_host_alloc", "gk_host_free", "gk_shard_last_error",
+                     "gk_bfs_device_parent", "gk_bfs_device_depth", "gk_host_alloc", "gk_host_free", "gk_shard_last_error",
                      "gk_shard_free", "gk_shard_launches"):
             getattr(L, f).restype = C.c_int
     _lib = L

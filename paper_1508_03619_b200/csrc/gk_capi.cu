@@ -247,6 +247,10 @@ gk_status kernel_error(const gk::Ctrl& ctrl, const char* what) {
 }
 
 gk_status finish_graph(gk_graph* g, gk_graph** out) {
+  if (g->n > (int64_t(1) << 31)) {  // every construction path: parents and depths are int32
+    free_graph(g);
+    return fail(GK_ERR_INVALID, "invalid graph: more than 2^31 vertices (parents are int32)");
+  }
   // every kernel indexes with these arrays: reject a malformed CSR up front
   bool sorted = true;
   for (int pass = 0; pass < (g->directed ? 2 : 1); pass++) {
@@ -617,6 +621,7 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
 }
 
 const int32_t* gk_bfs_device_parent(const gk_graph* g) { return g ? g->parent : nullptr; }
+int32_t* gk_bfs_device_depth(const gk_graph* g) { return g && g->depth_valid ? g->depth : nullptr; }
 
 gk_status gk_bfs_trace(const gk_graph* g, uint64_t* ts_ns, char* tags, int32_t cap, int32_t* count) {
   if (!g || !count) return fail(GK_ERR_INVALID, "null argument");

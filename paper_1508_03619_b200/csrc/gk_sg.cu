@@ -120,6 +120,12 @@ int sg_load(const char* path, int64_t* n_out, int64_t* m_out, int* directed_out,
     weighted = hdr[5] & 2;
     memcpy(&n, hdr + 6, 8);
     memcpy(&m, hdr + 14, 8);
+  }
+  if (!code && n > (uint64_t(1) << 31)) {
+    fail(2, "more than 2^31 vertices (parents are int32)");
+  } else if (!code && m > (uint64_t(1) << 40)) {  // also keeps the size arithmetic below from overflowing
+    fail(4, "declared arc count out of range");
+  } else if (!code) {
     fseeko(f, 0, SEEK_END);
     const uint64_t actual = (uint64_t)ftello(f);
     fseeko(f, 22, SEEK_SET);

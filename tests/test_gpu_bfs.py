@@ -291,6 +291,26 @@ def test_device_certificate_rejects_tampering():
     assert not v["ok"] and v["errors"][1] == 1 and v["first_bad"] == 2
 
 
+def test_device_certificate_rejects_fake_root_directed():
+    """Directed graph 0->1, 2->3 from source 0: vertex 3 claimed at depth 0
+    with the unreached 2 as parent (depth[2] = -1 = 0 - 1) and no arc that
+    leaves a reached vertex toward it -- accepted before the certificate
+    required depth >= 1 off the source."""
+    g = O.build_csr(4, np.array([0, 1, 2, 3], np.uint32), symmetrize=False, directed=True)
+    dg = DeviceGraph.from_csr(g)
+    dg.keep_depth(True)
+    good = dg.bfs(0).parent.copy()
+    assert dg.verify(0)["ok"]
+    assert list(good) == [0, 0, -1, -1]
+    bad_p = good.copy()
+    bad_p[3] = 2
+    bad_d = np.array([0, 1, -1, 0], np.int32)
+    _cuda_memcpy_h2d(dg.device_parent_ptr(), bad_p)
+    _cuda_memcpy_h2d(dg.device_depth_ptr(), bad_d)
+    v = dg.verify(0)
+    assert not v["ok"] and v["errors"][3] == 1 and v["first_bad"] == 3, v
+
+
 @pytest.mark.parametrize("cfg", ["kron27", "urand27", "grid4900"])
 def test_full_size_configs_certificate(cfg):
     """BASELINE configs 2-4 at full size: the size-independent certificate

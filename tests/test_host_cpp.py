@@ -133,3 +133,42 @@ def test_cli_bc_verified(tools, tmp_path):
 def test_cli_bc_usage(tools):
     assert run(tools[1], "bc").returncode == 2
     assert run(tools[1], "bc", "-g", "8", "-i", "x").returncode == 2
+
+
+REF_BIN = os.path.join(BIN, "test_ref_binding")
+SNIPPET = os.path.join(BIN, "integration_snippet")
+
+
+def _ref_binaries():
+    if not (os.path.exists(REF_BIN) and os.path.exists(SNIPPET)):
+        subprocess.run(["make", "-C", ROOT, "lib", "host"], capture_output=True)
+    if not (os.path.exists(REF_BIN) and os.path.exists(SNIPPET)):
+        pytest.skip("reference-binding tests not built (built by `make host` where /root/reference exists)")
+    return REF_BIN, SNIPPET
+
+
+def test_reference_binding_builds_and_has_no_cpu_fallback():
+    """ref_binding.hpp compiles against the reference's own headers (the
+    INTEGRATION.md snippet included); without a device every call throws
+    gapkit::Error while argument errors still raise ConfigError first."""
+    ref, snip = _ref_binaries()
+    if HAS_GPU:
+        pytest.skip("CPU-only expectation")
+    r = run(ref)
+    assert r.returncode != 0
+    assert "PASS bfs rejects an out-of-range source" in r.stdout
+    assert "no CUDA device available" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_binding():
+    """The reference's BFS tests (test_kernels_source.cc:13-85, acceptance
+    criteria 1 and 7) through gapkit::b200::Bfs over the reference's
+    CsrGraph, and INTEGRATION.md's snippet."""
+    ref, snip = _ref_binaries()
+    r = run(ref)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 10
+    r = run(snip)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr

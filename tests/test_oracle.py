@@ -192,3 +192,34 @@ def test_oracle_matches_live_reference():
                 if c == "B":
                     sel = d == i + 1
                     assert (rp.parent[sel] == ref.parent[sel]).all()
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_reference_arm_builder_matches_buildcsr():
+    """ref_bench.cc's 64-bit OpenMP builder (the reference arm's, for graphs
+    past BuildCsr's 2^32-arc limit, builder.hpp:71-73) is byte-identical to
+    the reference's BuildCsr(el, false, true) where both run, and its
+    bench-configuration graphs equal the restated generator + builder."""
+    R = O.RefLib()
+    for kind, scale in (("kron", 14), ("urand", 13)):
+        e = R.gen(kind, scale, 16, SEED)
+        a = R.build(1 << scale, e).csr()
+        b = R.build64(1 << scale, e).csr()
+        assert (a.off == b.off).all() and (a.nb == b.nb).all(), kind
+    # with self-loops and duplicates in the input
+    e = np.array([0, 0, 1, 2, 2, 1, 1, 2, 3, 3, 4, 0, 0, 4], np.uint32)
+    a, b = R.build(6, e).csr(), R.build64(6, e).csr()
+    assert (a.off == b.off).all() and (a.nb == b.nb).all()
+    for kind, scale, permute in (("kron", 15, True), ("urand", 12, False)):
+        g = R.bench_graph(kind, scale, 16, SEED, permute=permute).csr()
+        h = O.make_graph(kind, scale, 16, SEED, permute=permute)
+        assert (g.off == h.off).all() and (g.nb == h.nb).all(), kind
+    g = R.bench_graph("grid", rows=40, cols=50).csr()
+    h = O.make_graph("grid", rows=40, cols=50)
+    assert (g.off == h.off).all() and (g.nb == h.nb).all()
+    rg = R.bench_graph("kron", 12, 16, SEED, permute=True)
+    src = rg.pick_sources(4, SEED)
+    secs, mcc = rg.trials(src)
+    assert (secs > 0).all()
+    for s, m in zip(src, mcc):
+        assert m == rg.component_edges(rg.bfs(int(s)))

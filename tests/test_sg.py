@@ -101,3 +101,12 @@ def test_load_errors(tmp_path):
         DeviceGraph.load_sg(str(trunc))
     with pytest.raises(GapkitError, match="cannot open"):
         DeviceGraph.load_sg(str(tmp_path / "missing.sg"))
+    # header past the int32 parent range: rejected before any size arithmetic
+    huge = tmp_path / "huge.sg"
+    huge.write_bytes(b"GAPB" + bytes([1, 0]) + struct.pack("<QQ", (1 << 31) + 1, 4) + bytes(64))
+    with pytest.raises(GapkitError, match="more than 2\\^31 vertices"):
+        DeviceGraph.load_sg(str(huge))
+    arcs = tmp_path / "arcs.sg"
+    arcs.write_bytes(b"GAPB" + bytes([1, 0]) + struct.pack("<QQ", 4, (1 << 62)) + bytes(64))
+    with pytest.raises(LoadError, match="arc count out of range"):
+        DeviceGraph.load_sg(str(arcs))
