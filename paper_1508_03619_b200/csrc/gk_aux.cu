@@ -81,6 +81,14 @@ __global__ void k_check_sorted(const int64_t* __restrict__ off, const uint32_t* 
 }
 
 
+__global__ void k_canary(const unsigned char* __restrict__ p, size_t len, unsigned char fill,
+                         unsigned long long* out) {
+  unsigned long long c = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x)
+    c += p[i] != fill;
+  if (c) atomicAdd(out, c);
+}
+
 __global__ void k_count_reached(const int32_t* __restrict__ parent, const int64_t* __restrict__ off,
                                 int64_t n, unsigned long long* out) {
   __shared__ unsigned long long sm[kAuxBlock / 32];
@@ -291,6 +299,13 @@ cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int6
   *ids_ok = hb[1] == 0;
   if (sorted) *sorted = hb[0] == 0 && hb[2] == 0;
   return e;
+}
+
+cudaError_t canary_count(const void* p, size_t len, unsigned char fill, unsigned long long* d_out, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), s);
+  if (e) return e;
+  k_canary<<<16, kAuxBlock, 0, s>>>(static_cast<const unsigned char*>(p), len, fill, d_out);
+  return cudaGetLastError();
 }
 
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,

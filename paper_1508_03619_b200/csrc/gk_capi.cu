@@ -12,9 +12,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "gk_internal.cuh"
 
 namespace {
+
+// NVTX ranges name the host-side phases (graph build, trial, batch, Brandes)
+// in nsys / ncu timelines; header-only, inert unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 thread_local std::string g_last_error;
 
@@ -88,6 +99,7 @@ gk_status setup_graph(gk_graph* g, bool sorted) {
   CK(cudaMalloc(&g->acc, sizeof(unsigned long long) * 8), "alloc acc");
   CK(gk::bfs_configure(g->device, &g->launch), "configure bfs kernel");
   if (getenv("GK_NO_FRONT_SMEM")) g->launch.smem_front_max = 0;  // tests: large-graph paths on small graphs
+  g->canary = getenv("GK_CANARY") && atoi(getenv("GK_CANARY")) != 0;
   CK(cudaMalloc(&g->dead, bitmap_bytes(n)), "alloc dead-vertex bitmap");
   CK(gk::dead_bitmap(g->in_off, n, g->dead, &g->live, g->stream), "dead-vertex bitmap");
   cudaMemPoolProps props{};
@@ -133,29 +145,73 @@ gk_status setup_graph(gk_graph* g, bool sorted) {
 struct TrialBlocks {
   void* work = nullptr;
   void* book = nullptr;
+  std::vector<std::pair<char*, const char*>> canaries;  // GK_CANARY: guard zones after each buffer
 };
+constexpr size_t kCanaryBytes = 4096;
+constexpr unsigned char kCanaryByte = 0xA5;
+
+// Carves consecutive buffers out of one pool block; in canary mode
+// (GK_CANARY=1, a debug aid standing in for compute-sanitizer's memcheck,
+// which this pool does not offer) every buffer is followed by a guard zone
+// that trial_check_canaries verifies untouched after the kernel.
+struct Carver {
+  char* base;
+  size_t at = 0;
+  size_t cz;
+  TrialBlocks* tb;
+  char* take(size_t sz, const char* name) {
+    char* r = base + at;
+    at += sz;
+    if (cz) {
+      tb->canaries.emplace_back(base + at, name);
+      at += cz;
+    }
+    return r;
+  }
+};
+
 cudaError_t trial_alloc(gk_graph* g, gk_trial* t, TrialBlocks* tb, cudaStream_t s, bool own) {
+  const size_t cz = g->canary ? kCanaryBytes : 0;
   const size_t wb = bitmap_bytes(g->n);
-  const size_t sz_bits = 3 * wb, sz_q = up(sizeof(uint32_t) * (g->n + 1)),
-               sz_ch = up(sizeof(gk::Chunk) * g->chunk_cap),
+  const size_t sz_par = up(sizeof(int32_t) * std::max<int64_t>(g->n, 4) + 16);
+  const size_t sz_q = up(sizeof(uint32_t) * (g->n + 1)), sz_ch = up(sizeof(gk::Chunk) * g->chunk_cap),
                sz_ol = own ? up(sizeof(gk::OwnEnt) * g->own_cap) : 0, sz_os = own ? up(g->own_stage_bytes) : 0;
   const size_t sz_ctrl = up(sizeof(gk::Ctrl)), sz_steps = up(sizeof(gk_step) * g->step_cap);
+  const size_t work = 3 * (wb + cz) + sz_q + sz_ch + sz_ol + sz_os + (own ? 4 : 2) * cz;
   cudaError_t e;
-  if ((e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&t->parent),
-                                   up(sizeof(int32_t) * std::max<int64_t>(g->n, 4) + 16), g->pool, s)))
-    return e;
-  if ((e = cudaMallocFromPoolAsync(&tb->work, sz_bits + sz_q + sz_ch + sz_ol + sz_os, g->pool, s))) return e;
-  if ((e = cudaMallocFromPoolAsync(&tb->book, sz_ctrl + sz_steps, g->pool, s))) return e;
-  char* w = static_cast<char*>(tb->work);
-  t->bits = reinterpret_cast<uint32_t*>(w);
-  t->queue = reinterpret_cast<uint32_t*>(w + sz_bits);
-  t->chunks = reinterpret_cast<gk::Chunk*>(w + sz_bits + sz_q);
-  t->own_list = own ? reinterpret_cast<gk::OwnEnt*>(w + sz_bits + sz_q + sz_ch) : nullptr;
-  t->own_stage = own ? reinterpret_cast<uint2*>(w + sz_bits + sz_q + sz_ch + sz_ol) : nullptr;
-  char* b = static_cast<char*>(tb->book);
-  t->ctrl = reinterpret_cast<gk::Ctrl*>(b);
-  t->steps = reinterpret_cast<gk_step*>(b + sz_ctrl);
+  if ((e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&t->parent), sz_par + cz, g->pool, s))) return e;
+  if ((e = cudaMallocFromPoolAsync(&tb->work, work, g->pool, s))) return e;
+  if ((e = cudaMallocFromPoolAsync(&tb->book, sz_ctrl + sz_steps + 2 * cz, g->pool, s))) return e;
+  if (cz) tb->canaries.emplace_back(reinterpret_cast<char*>(t->parent) + sz_par, "parent");
+  Carver w{static_cast<char*>(tb->work), 0, cz, tb};
+  t->bits = reinterpret_cast<uint32_t*>(w.take(wb, "visited"));
+  w.take(wb, "bm0");
+  w.take(wb, "bm1");
+  t->bits_stride = (wb + cz) / 4;
+  t->queue = reinterpret_cast<uint32_t*>(w.take(sz_q, "queue"));
+  t->chunks = reinterpret_cast<gk::Chunk*>(w.take(sz_ch, "chunks"));
+  t->own_list = own ? reinterpret_cast<gk::OwnEnt*>(w.take(sz_ol, "own_list")) : nullptr;
+  t->own_stage = own ? reinterpret_cast<uint2*>(w.take(sz_os, "own_stage")) : nullptr;
+  Carver b{static_cast<char*>(tb->book), 0, cz, tb};
+  t->ctrl = reinterpret_cast<gk::Ctrl*>(b.take(sz_ctrl, "ctrl"));
+  t->steps = reinterpret_cast<gk_step*>(b.take(sz_steps, "steps"));
+  for (auto& c : tb->canaries)
+    if ((e = cudaMemsetAsync(c.first, kCanaryByte, cz, s))) return e;
   return cudaSuccess;
+}
+
+// GK_CANARY: every guard zone still holds its fill byte (call after the
+// kernel, before the scratch is freed).
+gk_status trial_check_canaries(gk_graph* g, const TrialBlocks& tb, cudaStream_t s) {
+  for (const auto& c : tb.canaries) {
+    unsigned long long bad = 0;
+    CK(gk::canary_count(c.first, kCanaryBytes, kCanaryByte, g->acc, s), "canary check");
+    CK(cudaMemcpyAsync(&bad, g->acc, sizeof(bad), cudaMemcpyDeviceToHost, s), "canary check");
+    CK(cudaStreamSynchronize(s), "canary check");
+    if (bad) return fail(GK_ERR_CUDA, std::string("canary zone after '") + c.second + "' overwritten (" +
+                                          std::to_string(bad) + " bytes)");
+  }
+  return GK_OK;
 }
 
 // Kernel parameters of one traversal on g (tuning knobs read from the environment).
@@ -177,7 +233,7 @@ gk::BfsParams make_params(gk_graph* g, const gk_trial& t, uint32_t source, int64
   p.front_in_smem = ((size_t)p.w32 * 4 <= g->launch.smem_front_max) ? 1 : 0;
   p.parent = t.parent;
   p.depth = g->depth;
-  const size_t ww = bitmap_bytes(g->n) / 4;
+  const size_t ww = t.bits_stride;
   p.visited = t.bits;
   p.bm0 = t.bits + ww;
   p.bm1 = t.bits + 2 * ww;
@@ -288,6 +344,7 @@ int gk_device_count(void) {
 }
 
 gk_status gk_graph_upload(const gk_csr_view* csr, int device, gk_graph** out) {
+  NvtxRange nvtx_range("gk_graph_upload");
   if (!csr || !out || !csr->out_offsets || csr->num_nodes < 0)
     return fail(GK_ERR_INVALID, "gk_graph_upload: null argument");
   if (csr->num_nodes > (int64_t(1) << 31))
@@ -327,6 +384,7 @@ gk_status gk_graph_upload(const gk_csr_view* csr, int device, gk_graph** out) {
 
 gk_status gk_graph_generate(int kind, int scale, int degree, uint64_t seed, int permute,
                             int device, gk_graph** out) {
+  NvtxRange nvtx_range("gk_graph_generate");
   if (!out) return fail(GK_ERR_INVALID, "gk_graph_generate: null out");
   if (kind != 0 && kind != 1) return fail(GK_ERR_INVALID, "generator kind must be 0 (kron) or 1 (urand)");
   if (scale < 1 || scale > 31) return fail(GK_ERR_INVALID, "generator scale must be in [1, 31]");
@@ -348,6 +406,7 @@ gk_status gk_graph_generate(int kind, int scale, int degree, uint64_t seed, int 
 
 gk_status gk_graph_generate_grid(int64_t rows, int64_t cols, double p_delete, double p_diag,
                                  uint64_t seed, int device, gk_graph** out) {
+  NvtxRange nvtx_range("gk_graph_generate_grid");
   if (!out) return fail(GK_ERR_INVALID, "gk_graph_generate_grid: null out");
   if (rows < 1 || cols < 1 || rows * cols > (int64_t(1) << 31))
     return fail(GK_ERR_INVALID, "grid dimensions out of range");
@@ -369,6 +428,7 @@ gk_status gk_graph_generate_grid(int64_t rows, int64_t cols, double p_delete, do
 }
 
 gk_status gk_graph_load_sg(const char* path, int device, gk_graph** out) {
+  NvtxRange nvtx_range("gk_graph_load_sg");
   if (!path || !out) return fail(GK_ERR_INVALID, "gk_graph_load_sg: null argument");
   gk_status st = need_device(device);
   if (st != GK_OK) return st;
@@ -474,6 +534,7 @@ gk_status gk_bfs_keep_depth(gk_graph* g, int32_t keep) {
 
 gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int32_t strategy,
                  int32_t* parent_out, int32_t* depth_out, gk_bfs_stats* stats) {
+  NvtxRange nvtx_range("gk_bfs");
   if (!g) return fail(GK_ERR_INVALID, "null graph");
   // bfs.hpp:120-123, same order and messages
   if ((int64_t)source >= g->n) return fail(GK_ERR_SOURCE_RANGE, "bfs source out of range");
@@ -499,6 +560,10 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   g->parent = t.parent;
   gk::BfsParams p = make_params(g, t, source, alpha, beta, strategy, want_depth);
   CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
+  if (g->canary) {
+    const gk_status cst = trial_check_canaries(g, tb, s);
+    if (cst != GK_OK) return cst;
+  }
   CK(cudaFreeAsync(tb.work, s), "free trial scratch");
   CK(cudaEventRecord(g->ev1, s), "event record");
   gk::Ctrl& ctrl = g->last_ctrl;
@@ -547,6 +612,7 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
 // Same validation and results as gk_bfs.
 gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int64_t alpha, int64_t beta,
                        int32_t strategy, int32_t* const* parents_out, float* device_ms) {
+  NvtxRange nvtx_range("gk_bfs_batch");
   if (!g) return fail(GK_ERR_INVALID, "null graph");
   if (count < 0 || (count > 0 && !sources)) return fail(GK_ERR_INVALID, "null argument");
   for (int32_t i = 0; i < count; i++)
@@ -679,6 +745,7 @@ gk_status gk_bfs_verify(gk_graph* g, uint32_t source, int64_t* errors) {
 // the pool inside the timed region and returned at its end.
 gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, float* scores_out,
                      double* device_ms) {
+  NvtxRange nvtx_range("gk_brandes");
   if (!g) return fail(GK_ERR_INVALID, "null graph");
   if (!sources || num_sources <= 0) return fail(GK_ERR_BAD_PARAM, "betweenness requires at least one source");
   std::lock_guard<std::mutex> lock(g->mu);

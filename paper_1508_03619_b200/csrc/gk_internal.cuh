@@ -172,6 +172,8 @@ cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, int64_
 // *sorted (may be null: not checked) = every list strictly ascending.
 cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int64_t m, int64_t id_bound,
                          bool* offsets_ok, bool* ids_ok, bool* sorted, cudaStream_t s);
+// Bytes of p[0..len) that differ from fill, written to *d_out.
+cudaError_t canary_count(const void* p, size_t len, unsigned char fill, unsigned long long* d_out, cudaStream_t s);
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s);
 cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
@@ -206,7 +208,8 @@ cudaError_t build_grid(int64_t rows, int64_t cols, double p_delete, double p_dia
 // the graph's memory pool inside the timed region and returned at its end.
 struct gk_trial {
   int32_t* parent = nullptr;   // the result; outlives the trial until the next one
-  uint32_t* bits = nullptr;    // visited | bm0 | bm1
+  uint32_t* bits = nullptr;    // visited | bm0 | bm1, bits_stride words apart
+  size_t bits_stride = 0;
   uint32_t* queue = nullptr;
   gk::Chunk* chunks = nullptr;
   gk::OwnEnt* own_list = nullptr;
@@ -232,6 +235,7 @@ struct gk_graph {
   cudaMemPool_t pool = nullptr;
   int64_t chunk_cap = 0;
   int64_t step_cap = 0;
+  bool canary = false;  // GK_CANARY=1: guard zones after every trial buffer (debug)
   int own_r = 0;  // owned-range hub expansion geometry (0: off for this graph)
   int64_t own_span_w = 0, own_dmin = 0, own_cap = 0;
   int own_win_log = 0;

@@ -113,14 +113,21 @@ struct BenchPlan {  // benchmark.hpp:51-82 (BFS row of Table 1: 64 trials x 1 so
   int64_t beta = 18;
   uint64_t source_seed = kDefaultSeed;
   std::optional<NodeId> fixed_source;
+  // Measurement columns beyond the reference's report:
+  // the B_sec byte model of each trial (an untimed second traversal that
+  // records depths) and its HBM-roofline fraction against peak_gbs.
+  bool model = true;
+  double peak_gbs = 6550.7;  // MEASURED_PEAKS.json hbm_gbs of this pool's B200s
+  int gpus = 1;              // devices the traversal ran on
 };
 
 struct TrialResult {  // benchmark.hpp:84-90
   int trial = 0;
   NodeId source = 0;
   double seconds = 0;      // host wall clock around Bfs, parent array returned
-  double device_ms = 0;    // CUDA-event time of the traversal kernel
-  int64_t component_edges = 0;
+  double device_ms = 0;    // CUDA-event time of the trial (gk_bfs_stats.device_ms)
+  int64_t component_edges = 0;  // m_cc: undirected edges in the source's component
+  double bytes_model = 0;       // B_sec algorithmic bytes, 0 without plan.model
   std::string schedule;
   std::optional<bool> verified;
   uint64_t digest = 0;
@@ -180,6 +187,16 @@ inline BenchReport RunBenchmark(CsrGraph& g, const BenchPlan& plan, bool verify,
     tr.component_edges = tel.component_edges;
     tr.schedule = tel.schedule;
     tr.digest = HashBytes(parent.data(), parent.size() * sizeof(ParentEntry));
+    if (plan.model) {  // untimed: the same traversal again, recording depths, then the byte model
+      gk_graph* dev = g.device();
+      detail::CheckStatus(gk_bfs_keep_depth(dev, 1), "gk_bfs_keep_depth");
+      detail::CheckStatus(gk_bfs(dev, tr.source, plan.alpha, plan.beta, 0, nullptr, nullptr, nullptr), "gk_bfs");
+      double bs = 0, bu = 0;
+      detail::CheckStatus(gk_bfs_byte_model(dev, tel.steps.data(), static_cast<int32_t>(tel.steps.size()), &bs, &bu),
+                          "gk_bfs_byte_model");
+      detail::CheckStatus(gk_bfs_keep_depth(dev, 0), "gk_bfs_keep_depth");
+      tr.bytes_model = bs;
+    }
     if (verify) {
       VerifyReport r = VerifyBfs(g, tr.source, parent);
       tr.verified = r.ok;
@@ -191,13 +208,20 @@ inline BenchReport RunBenchmark(CsrGraph& g, const BenchPlan& plan, bool verify,
   return report;
 }
 
-inline void WriteCsv(std::ostream& out, const BenchReport& r) {  // benchmark.hpp:302-320 (+ device columns)
-  out << "kernel,graph,trial,source,elapsed_seconds,verified,device_ms,gteps,schedule\n";
+// benchmark.hpp:302-320 plus the device columns: device_ms, m_cc, GTEPS,
+// the B_sec byte model (bytes_model), roofline_frac = bytes_model /
+// device time / peak, gpus, and the executed direction schedule.
+inline void WriteCsv(std::ostream& out, const BenchReport& r, const BenchPlan& plan = {}) {
+  out << "kernel,graph,trial,source,elapsed_seconds,verified,device_ms,m_cc,gteps,bytes_model,roofline_frac,gpus,"
+         "schedule\n";
   for (const auto& t : r.trials) {
-    const double gteps = t.device_ms > 0 ? t.component_edges / (t.device_ms * 1e-3) / 1e9 : 0.0;
+    const double sec = t.device_ms * 1e-3;
+    const double gteps = sec > 0 ? t.component_edges / sec / 1e9 : 0.0;
+    const double frac = sec > 0 && t.bytes_model > 0 ? t.bytes_model / sec / 1e9 / plan.peak_gbs : 0.0;
     out << "bfs," << r.graph_name << "," << t.trial << "," << t.source << "," << t.seconds << ","
-        << (t.verified.has_value() ? (*t.verified ? "1" : "0") : "") << "," << t.device_ms << "," << gteps
-        << "," << (t.schedule.size() <= 64 ? t.schedule : t.schedule.substr(0, 61) + "...") << "\n";
+        << (t.verified.has_value() ? (*t.verified ? "1" : "0") : "") << "," << t.device_ms << ","
+        << t.component_edges << "," << gteps << "," << t.bytes_model << "," << frac << "," << plan.gpus << ","
+        << (t.schedule.size() <= 64 ? t.schedule : t.schedule.substr(0, 61) + "...") << "\n";
   }
 }
 

@@ -3,8 +3,14 @@
 // hand-rolled parser because CLI11 is not vendored).
 //
 //   gapkit_b200 bfs|bc (-f FILE.sg | -g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS]
-//               [-r SOURCE] [-i SOURCES_PER_TRIAL] [-v] [--seed S] [--no-permute] [--host-build]
-//               [--threads T] [-o FILE.csv]
+//               [-r SOURCE] [-i SOURCES_PER_TRIAL] [-v] [-s] [--seed S] [--no-permute] [--host-build]
+//               [--threads T] [--no-model] [--peak-gbs GB/s] [-o FILE.csv]
+//
+// -s/--symmetrize treats a file's graph as undirected (gapkit.cc:57-58;
+// LoadGraph, io.hpp:461-468: a directed .sg is flattened and rebuilt
+// symmetrized).  The CSV adds m_cc, the B_sec byte model, its roofline
+// fraction against --peak-gbs and the GPU count to the reference's columns
+// (--no-model skips the untimed model pass).
 //
 // bc follows the reference's plan (benchmark.hpp:75): 16 trials x 4 sources
 // by default, -i sets the sources per trial.
@@ -38,8 +44,8 @@ namespace {
 int Usage(const char* argv0) {
   std::fprintf(stderr,
                "usage: %s bfs|bc (-f FILE.sg | -g SCALE | -u SCALE | --grid RxC) [-k DEGREE] [-n TRIALS]\n"
-               "          [-r SOURCE] [-i SOURCES_PER_TRIAL] [-v] [--seed S] [--no-permute] [--host-build]\n"
-               "          [--threads T] [-o FILE.csv]\n",
+               "          [-r SOURCE] [-i SOURCES_PER_TRIAL] [-v] [-s] [--seed S] [--no-permute] [--host-build]\n"
+               "          [--threads T] [--no-model] [--peak-gbs GB/s] [-o FILE.csv]\n",
                argv0);
   return 2;
 }
@@ -58,7 +64,8 @@ int main(int argc, char** argv) {
   long long kron = -1, urand = -1, degree = 16, trials = bc ? 16 : 64, fixed = -1, threads = 0, per_trial = 4;
   long long rows = 0, cols = 0;
   unsigned long long seed = gapkit::kDefaultSeed;
-  bool verify = false, permute = true, host_build = false;
+  bool verify = false, permute = true, host_build = false, symmetrize = false, model = true;
+  double peak_gbs = 6550.7;
   std::string output, file;
   for (int i = 2; i < argc; i++) {
     std::string a = argv[i];
@@ -80,6 +87,11 @@ int main(int argc, char** argv) {
       need(&s);
       seed = static_cast<unsigned long long>(s);
     } else if (a == "-v") verify = true;
+    else if (a == "-s" || a == "--symmetrize") symmetrize = true;
+    else if (a == "--no-model") model = false;
+    else if (a == "--peak-gbs") {
+      if (i + 1 >= argc || std::sscanf(argv[++i], "%lf", &peak_gbs) != 1 || peak_gbs <= 0) return Usage(argv[0]);
+    }
     else if (a == "--no-permute") permute = false;
     else if (a == "--host-build") host_build = true;
     else if (a == "-f" || a == "--file") {
@@ -111,6 +123,15 @@ int main(int argc, char** argv) {
       name = file.substr(slash == std::string::npos ? 0 : slash + 1);
       name = name.substr(0, name.find_last_of('.'));
       g = gapkit::ReadSerializedOnDevice(file);
+      if (symmetrize && g.directed()) {  // io.hpp:466-467: BuildCsr(FlattenToEdgeList(g), false, true)
+        g.EnsureHostArrays();
+        gapkit::EdgeList el;
+        el.node_count = g.num_nodes();
+        for (int64_t u = 0; u < g.num_nodes(); u++)
+          for (gapkit::NodeId v : g.out_neigh(static_cast<gapkit::NodeId>(u)))
+            el.edges.push_back({static_cast<gapkit::NodeId>(u), v});
+        g = gapkit::BuildCsr(el, false, true);
+      }
     } else if (rows > 0) {
       name = "grid" + std::to_string(rows) + "x" + std::to_string(cols);
       g = host_build ? gapkit::BuildCsr(gapkit::GenerateGrid(rows, cols, 0.15, 0.02, seed), false, true)
@@ -157,6 +178,8 @@ int main(int argc, char** argv) {
     gapkit::BenchPlan plan;  // gapkit.cc:99-121
     plan.trials = static_cast<int>(trials);
     plan.source_seed = seed;
+    plan.model = model;
+    plan.peak_gbs = peak_gbs;
     if (fixed >= 0) {
       if (fixed >= g.num_nodes()) throw gapkit::ConfigError("-r source out of range");
       if (g.host_ready() && g.out_degree(static_cast<gapkit::NodeId>(fixed)) == 0)
@@ -167,9 +190,9 @@ int main(int argc, char** argv) {
     if (!output.empty()) {
       std::ofstream out(output);
       if (!out) throw gapkit::ConfigError("cannot open output file: " + output);
-      gapkit::WriteCsv(out, report);
+      gapkit::WriteCsv(out, report, plan);
     } else {
-      gapkit::WriteCsv(std::cout, report);
+      gapkit::WriteCsv(std::cout, report, plan);
     }
     std::printf("%s: n=%lld arcs=%lld trials=%d hmean %.2f GTEPS (device time)%s\n", name.c_str(),
                 static_cast<long long>(g.num_nodes()), static_cast<long long>(g.num_edges()), plan.trials,

@@ -93,6 +93,36 @@ def test_cli_bfs_verified(tools, graph, tmp_path):
 
 
 @pytest.mark.gpu
+def test_cli_csv_measurement_columns(tools, tmp_path):
+    """m_cc, the B_sec byte model, its roofline fraction and the GPU count
+    next to the reference's columns."""
+    out = tmp_path / "bfs.csv"
+    r = run(tools[1], "bfs", "-g", "14", "-n", "4", "-o", out)
+    assert r.returncode == 0, r.stderr
+    lines = out.read_text().strip().splitlines()
+    head = lines[0].split(",")
+    assert head == ["kernel", "graph", "trial", "source", "elapsed_seconds", "verified", "device_ms", "m_cc",
+                    "gteps", "bytes_model", "roofline_frac", "gpus", "schedule"]
+    for l in lines[1:]:
+        row = dict(zip(head, l.split(",")))
+        assert int(row["m_cc"]) > 0 and float(row["bytes_model"]) > 0 and int(row["gpus"]) == 1
+        frac = float(row["bytes_model"]) / (float(row["device_ms"]) * 1e-3) / 1e9 / 6550.7
+        assert abs(float(row["roofline_frac"]) - frac) <= 1e-6 + 1e-3 * frac
+
+
+@pytest.mark.gpu
+def test_cli_symmetrize_directed_file(tools, tmp_path):
+    """-s on a directed .sg (gapkit.cc:57-58; io.hpp:466-467): flattened and
+    rebuilt undirected, so BFS reaches along reversed arcs too."""
+    d = os.path.join(ROOT, "tests", "golden", "directed_1edge.sg")
+    plain = run(tools[1], "bfs", "-f", d, "-n", "1", "-r", "1", "--no-model")
+    sym = run(tools[1], "bfs", "-f", d, "-n", "1", "-r", "1", "--no-model", "-s")
+    assert sym.returncode == 0, sym.stderr
+    assert "arcs=2" in sym.stdout, sym.stdout
+    assert plain.returncode in (0, 2)  # vertex 1 has no out-arcs in the directed file
+
+
+@pytest.mark.gpu
 def test_cli_serialized_file(tools, tmp_path):
     out = tmp_path / "bfs.csv"
     r = run(tools[1], "bfs", "-f", os.path.join(ROOT, "tests", "golden", "kron10.sg"), "-n", "8", "-v", "-o", out)
