@@ -20,15 +20,15 @@ roofline  : algorithmic bytes B_sec (evaluated per source from
             measured HBM copy bandwidth (MEASURED_PEAKS.json).
 cpu_baseline : the reference's own OpenMP Bfs (oracle/_ref/libgapref.so, the
             unmodified headers) on the box's host cores, bounded sample.
-N > 1     : one process per GPU (torchrun).  Default (--multi replicas): the
-            benchmark's independent units -- its trials, one BFS per source --
-            are sharded over the ranks; every rank holds the whole graph (all
-            configs fit one B200, even kron30's 146 GB) and runs K sources of
-            its own (PickSources seeded by rank), no data-path collective,
-            weak scaling; per-step time = max over ranks, work summed.
-            --multi sharded: the 1D vertex-partitioned traversal of ONE graph
-            (NCCL per level, strong scaling) for graphs that
-            exceed one GPU.
+N > 1     : one process per GPU (torchrun).  Default (--multi sharded): the
+            1D vertex-partitioned traversal of ONE graph:
+            one persistent kernel per rank, the level loop on the device,
+            bitmap exchanges over NVLink peer memory, device-side cross-rank
+            barriers; strong scaling, step time = max over ranks; the line
+            adds the NVLink fraction.  --multi replicas: every rank holds the
+            whole graph and runs its own sources (weak scaling).
+            --emulate-ranks P at N=1: the sharded kernel with P ranks in one
+            launch on one GPU (its overhead against the single-device kernel).
 """
 from __future__ import annotations
 
@@ -270,21 +270,43 @@ def cpu_model():
 
 
 def run_sharded(args, cfg, rank, world, local, dist):
-    """N GPUs, one graph: 1D partition + per-level NCCL exchanges (dist.py)."""
+    """N GPUs, one graph, one persistent kernel per rank (dist.ShardedBfs:
+    1D vertex partition, device-driven level loop, exchanges over NVLink
+    peer memory); strong scaling.  --emulate-ranks P on one
+    GPU runs the same kernel with P ranks in one launch (dist.ShardGroup)."""
+    import numpy as np
     import torch
 
     from paper_1508_03619_b200 import DeviceGraph
-    from paper_1508_03619_b200.dist import GpuEngine, LocalComm, ShardedBfs, TorchComm, pick_sources_sharded
+    from paper_1508_03619_b200.dist import ShardedBfs, ShardGroup, pick_sources
     K, W = args.steps, max(args.warmup, 0)
+    P = world if world > 1 else max(1, args.emulate_ranks)
     t0 = time.time()
-    eng = GpuEngine.generate(cfg["kind"], cfg["scale"], cfg["degree"], SEED, cfg["permute"], rank, world, local)
+    if world > 1:
+        runner = ShardedBfs.generate(cfg["kind"], cfg["scale"], cfg["degree"], SEED, cfg["permute"], rank, world,
+                                     local)
+        shard = runner.shard
+        off = shard.local_offsets()
+        owned = (shard.lo, shard.hi)
+
+        def degree_of(v):  # PickSources over the partition: the owner answers
+            d = int(off[v - owned[0] + 1] - off[v - owned[0]]) if owned[0] <= v < owned[1] else 0
+            t = torch.tensor([d], dtype=torch.int64, device="cuda")
+            dist.all_reduce(t)
+            return int(t.item())
+    else:
+        runner = ShardGroup.generate(cfg["kind"], cfg["scale"], cfg["degree"], SEED, cfg["permute"], P, local)
+        offs = [sh.local_offsets() for sh in runner.shards]
+        deg = np.concatenate([np.diff(o) for o in offs])
+
+        def degree_of(v):
+            return int(deg[v])
     build_s = time.time() - t0
-    comm = TorchComm() if world > 1 else LocalComm(1)
-    sb = ShardedBfs([eng], comm)
-    sources = pick_sources_sharded(sb, K, SEED)
+    n = runner.n
+    sources = pick_sources(degree_of, n, K, SEED)
     for s in (sources * (W // max(K, 1) + 1))[:W]:
-        sb.run(s)
-    # algorithmic bytes: the single-device byte model of the same graph/sources (rank 0, untimed)
+        runner.run(s, parent=False)
+    # algorithmic bytes: the single-device byte model of the same graph (rank 0, untimed)
     bsec_of = {}
     if rank == 0 and not args.no_model:
         full = DeviceGraph.generate(cfg["kind"], cfg["scale"], cfg["degree"], SEED, permute=cfg["permute"],
@@ -295,73 +317,92 @@ def run_sharded(args, cfg, rank, world, local, dist):
             bsec_of[s] = full.byte_model(r.steps)[0]
         del full
         torch.cuda.empty_cache()
+    m_of, scheds = {}, {}
+    for s in sources:  # untimed: component edges
+        r = runner.run(s, parent=False, counts=True)
+        if world > 1:
+            t = torch.tensor([r.component_edges], dtype=torch.int64, device="cuda")
+            dist.all_reduce(t)
+            m_of[s] = int(t.item()) // 2
+        else:
+            m_of[s] = r.component_edges
+        scheds[s] = r.schedule
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.2)
-    dev_ms, m_of, nvl, scheds = [], {}, [], {}
-    launches0 = eng.launches()
+    dev_ms, nvl = [], []
+    launches0 = runner.launches()
     for s in sources:
         if dist:
             dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        res = sb.run(s)
-        e1.record()
-        torch.cuda.synchronize()
-        dev_ms.append(e0.elapsed_time(e1))
-        m_of[s] = res.component_edges
-        nvl.append(res.bytes_in)
-        scheds[s] = res.schedule
+        r = runner.run(s, parent=False)
+        dev_ms.append(r.device_ms)
+        nvl.append(max(r.bytes_in))
     clocks = clk.stop()
-    launches = eng.launches() - launches0
+    launches = runner.launches() - launches0
     e2e_s = []
-    for s in sources:
+    for s in sources:  # every rank's owned parents to host memory
         if dist:
             dist.barrier()
         t1 = time.perf_counter()
-        sb.run(s, gather=True)  # owned parent array D2H into host memory
+        runner.run(s, parent=True)
         e2e_s.append(time.perf_counter() - t1)
     if dist:
         t = torch.tensor(dev_ms + e2e_s + nvl, dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         vals = t.tolist()
         dev_ms, e2e_s, nvl = vals[:K], vals[K:2 * K], vals[2 * K:]
+    arcs = _arcs_of(runner, world, dist)
     if rank != 0:
         return
     ms = [m_of[s] for s in sources]
     value = hmean([m / (t * 1e-3) / 1e9 for m, t in zip(ms, dev_ms)])
     peak, peak_src = peaks()
     roof = None
+    tot_t = sum(dev_ms) * 1e-3
+    nvl_gbs = sum(nvl) / tot_t / 1e9
+    nvlink = {"achieved": nvl_gbs, "peak": 900.0, "unit": "GB/s", "frac": nvl_gbs / 900.0,
+              "bytes_in_per_bfs_max_rank": sum(nvl) / len(nvl),
+              "peak_source": "NVLink 5, 900 GB/s per direction per GPU (B200_PROFILING.md)",
+              "note": "exchange bytes received per rank: all-gather of next per step + claims reduce per "
+                      "top-down step" + ("" if world > 1 else "; ranks emulated on one GPU (no NVLink)")}
     if bsec_of:
-        tot_t = sum(dev_ms) * 1e-3
-        per_gpu = sum(bsec_of[s] for s in sources) / world / tot_t / 1e9
-        nvl_gbs = sum(nvl) / tot_t / 1e9
+        per_gpu = sum(bsec_of[s] for s in sources) / P / tot_t / 1e9
         roof = {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s", "frac": per_gpu / peak,
                 "traffic": None, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": sum(bsec_of[s] for s in sources) / len(sources) / world,
+                "algorithmic_bytes_per_launch": sum(bsec_of[s] for s in sources) / len(sources) / P,
                 "note": "per-GPU share (B_sec / N) of the single-device byte model over the sharded step time",
-                "nvlink": {"achieved": nvl_gbs, "peak": 770.0, "unit": "GB/s", "frac": nvl_gbs / 770.0,
-                           "bytes_in_per_bfs_max_rank": sum(nvl) / len(nvl),
-                           "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}}
+                "kernel": "bfs_sharded (one persistent launch per rank per BFS)", "nvlink": nvlink}
     line = {
         "metric": METRIC,
         "value": value, "unit": "GTEPS", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": statistics.mean(dev_ms), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generator, no dataset)",
-        "config": {"workload": cfg["workload"], "name": cfg["name"], "n": eng.n, "seed": SEED, "sources": K,
-                   "alpha": 15, "beta": 18, "parallelism": f"1D vertex partition over {world} GPU(s), NCCL",
-                   "l2": "inputs larger than L2", "device_build_s": round(build_s, 2),
-                   "schedules": sorted(set(scheds.values()), key=len)[:4]},
+        "config": line_config(cfg, n, arcs, K),
+        "run": {"parallelism": f"1D vertex partition over {P} rank(s)" +
+                (", one per GPU, exchanges over NVLink peer memory" if world > 1 else ", emulated in one launch"),
+                "trial": "one persistent kernel per rank: allocation, initialisation, the level loop with "
+                         "device-side cross-rank barriers -- CUDA events around all of it, max over ranks",
+                "device_build_s": round(build_s, 2), "schedules": sorted(set(scheds.values()), key=len)[:4]},
         "e2e": {"value": hmean([m / t / 1e9 for m, t in zip(ms, e2e_s)]), "unit": "GTEPS",
-                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * eng.nloc,
-                "note": "sharded run + owned parent array D2H per rank (max over ranks)"},
+                "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4 * n // max(world, 1),
+                "note": "sharded run + each rank's owned parent array D2H (max over ranks)"},
         "gpu_launches": launches,
         "clocks": clocks,
         "roofline": roof,
+        "nvlink": nvlink,
         "cpu_baseline": None,
     }
     print(json.dumps(line), flush=True)
+
+
+def _arcs_of(runner, world, dist):
+    import torch
+    if world > 1:
+        t = torch.tensor([runner.shard.m], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        return int(t.item())
+    return sum(sh.m for sh in runner.shards)
 
 
 def main():
@@ -375,10 +416,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-model", action="store_true")
     ap.add_argument("--verbose", action="store_true", help="per-source times on stderr")
-    ap.add_argument("--multi", default="replicas", choices=["sharded", "replicas"],
-                    help="N>1: source-parallel replicas (default; weak scaling) or the 1D-partitioned "
-                         "traversal of one graph (strong scaling)")
-    ap.add_argument("--force-sharded", action="store_true", help="run the sharded path even at N=1")
+    ap.add_argument("--multi", default="sharded", choices=["sharded", "replicas"],
+                    help="N>1: the 1D-partitioned traversal of one graph (default; strong scaling) or "
+                         "source-parallel whole-graph replicas (weak scaling)")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="N=1: run the sharded kernel with this many ranks emulated in one launch")
     args = ap.parse_args()
     # OpenMP settings for the reference CPU legs (must precede libgomp init).
     os.environ.setdefault("OMP_WAIT_POLICY", "active")
@@ -404,7 +446,7 @@ def main():
     from paper_1508_03619_b200 import PinnedBuffer
 
     # ---------------- our arm ----------------
-    if cfg["kind"] != "grid" and args.multi == "sharded" and (world > 1 or args.force_sharded):
+    if cfg["kind"] != "grid" and args.multi == "sharded" and (world > 1 or args.emulate_ranks > 0):
         run_sharded(args, cfg, rank, world, local, dist)
         if dist:
             dist.destroy_process_group()

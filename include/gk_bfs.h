@@ -207,13 +207,24 @@ GK_API gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_so
                             float* scores_out, double* device_ms);
 
 /* ---- Sharded (1D-partitioned) traversal, SURVEY.md §8(e) ----------------
- * Rank r of P owns vertices [r*block, min(n, (r+1)*block)), block =
- * ceil(n/P) rounded up to a multiple of 32.  A gk_shard holds the owned CSR
- * rows (global neighbour ids) and owned BFS state.  The level loop of
- * bfs.hpp:139-169 and the exchanges between these calls (all-reduce of
- * counters, all-to-all of (v,u) claim pairs, all-gather of bitmap slices)
- * are run by the host orchestrator (paper_1508_03619_b200/dist.py).  All
- * kernels run on the stream set with gk_shard_set_stream.  1 <= P <= 64. */
+ * Rank r of P (P <= 8) owns vertices [r*block, min(n, (r+1)*block)), block =
+ * ceil(n/P) rounded up to 1024, and the CSR rows of those vertices (global
+ * neighbour ids; undirected graphs).  A traversal is ONE persistent kernel
+ * per rank: the level loop of bfs.hpp:139-169 runs on the device, the ranks
+ * exchange bitmap slices through peer memory and meet at a device-side
+ * cross-rank barrier that reduces the heuristic's counters -- no host round
+ * trip per level (gk_bfs_sharded.cu).  Parents: bottom-up as bfs.hpp:55-60
+ * (first in-neighbour in the frontier), top-down claims resolved by their
+ * owner the same way; depths exact.
+ *
+ * Wiring, either
+ *   - every rank in this process on ONE device: gk_shard_join_local, then
+ *     gk_shard_group_bfs on rank 0 runs all ranks in one cooperative launch
+ *     (the single-GPU emulation of the multi-device run), or
+ *   - one process per device: gk_shard_export on every rank, exchange the
+ *     blobs (gk_shard_handle_size() bytes each), gk_shard_connect with all
+ *     of them in rank order, a host barrier, gk_shard_gather_dead; then every
+ *     rank calls gk_shard_bfs with the same arguments. */
 typedef struct gk_shard gk_shard;
 GK_API const char* gk_shard_last_error(void);
 /* This rank's rows of the device-generated graph (same graph as
@@ -230,34 +241,41 @@ GK_API gk_status gk_shard_upload(int64_t num_nodes, int rank, int nranks,
 GK_API void gk_shard_free(gk_shard* s);
 GK_API gk_status gk_shard_info(const gk_shard* s, int64_t* num_nodes, int64_t* lo,
                                int64_t* hi, int64_t* local_arcs, int64_t* block);
-GK_API gk_status gk_shard_set_stream(gk_shard* s, void* cuda_stream);
 /* Kernels this shard has launched so far (telemetry for the bench line). */
 GK_API int64_t gk_shard_launches(const gk_shard* s);
-GK_API gk_status gk_shard_degree(const gk_shard* s, uint32_t v, int64_t* degree);
-GK_API gk_status gk_shard_begin(gk_shard* s, uint32_t source, int32_t strategy,
-                                int32_t want_depth);
-/* Top-down over the owned queue window [qs, qe): local[0..1] = claims made
- * in place and their scout; dest_counts[r] = claim pairs (v<<32|u) for rank
- * r, written contiguously by rank into pairs_out_dev (device, capacity
- * pairs_cap >= local arcs suffices).  dedup: send each remote target at most
- * once this level (clears an n-bit sent map; worth it for large frontiers). */
-GK_API gk_status gk_shard_td_expand(gk_shard* s, uint64_t qs, uint64_t qe,
-                                    int32_t level, int32_t dedup, int64_t* local,
-                                    int64_t* dest_counts, uint64_t* pairs_out_dev,
-                                    int64_t pairs_cap);
-GK_API gk_status gk_shard_td_apply(gk_shard* s, const uint64_t* pairs_dev,
-                                   int64_t npairs, int32_t level, int64_t* out);
-GK_API gk_status gk_shard_tail(gk_shard* s, uint64_t* tail);
-GK_API gk_status gk_shard_rescan(gk_shard* s, uint64_t qs, uint64_t qe,
-                                 int64_t* degree_total);
-GK_API gk_status gk_shard_q2b(gk_shard* s, uint64_t qs, uint64_t qe,
-                              uint32_t* slice_dev);
-GK_API gk_status gk_shard_bu(gk_shard* s, const uint32_t* front_dev,
-                             uint32_t* next_slice_dev, int32_t level,
-                             int64_t* awake);
-GK_API gk_status gk_shard_b2q(gk_shard* s, const uint32_t* slice_dev);
-GK_API gk_status gk_shard_result(gk_shard* s, int32_t* parent_out,
-                                 int32_t* depth_out, int64_t* counts);
+/* This rank's rows to host arrays (hi-lo+1 local offsets, local_arcs ids; either may be NULL). */
+GK_API gk_status gk_shard_download(const gk_shard* s, int64_t* local_offsets, uint32_t* neighbors);
+/* Stream of this shard's traversals (NULL: its own). */
+GK_API gk_status gk_shard_set_stream(gk_shard* s, void* cuda_stream);
+GK_API gk_status gk_shard_join_local(gk_shard* const* shards, int nranks);
+GK_API int64_t gk_shard_handle_size(void);
+GK_API gk_status gk_shard_export(const gk_shard* s, void* handle_out);
+GK_API gk_status gk_shard_connect(gk_shard* s, const void* handles);
+GK_API gk_status gk_shard_gather_dead(gk_shard* s);
+/* One traversal of a local group (call on rank 0).  parents_out[q] /
+ * depths_out[q]: rank q's owned vertices (host arrays; the arrays of
+ * pointers and their entries may be NULL).  stats: device_ms of the whole
+ * trial (allocation, initialisation, kernel), the step log, and (with
+ * want_counts) reached / component_edges of the whole graph. */
+GK_API gk_status gk_shard_group_bfs(gk_shard* rank0, uint32_t source, int64_t alpha,
+                                    int64_t beta, int32_t strategy,
+                                    int32_t* const* parents_out,
+                                    int32_t* const* depths_out, gk_bfs_stats* stats);
+/* One traversal, multi-device (collective: every rank, same arguments).
+ * parent_out / depth_out: this rank's owned vertices.  With want_counts,
+ * stats->reached counts this rank's reached vertices and
+ * stats->component_edges their out-arcs (sum over ranks, halve).
+ * *bytes_in (may be NULL) = exchange bytes this rank received. */
+GK_API gk_status gk_shard_bfs(gk_shard* s, uint32_t source, int64_t alpha, int64_t beta,
+                              int32_t strategy, int32_t* parent_out, int32_t* depth_out,
+                              gk_bfs_stats* stats, int64_t* bytes_in);
+/* Phase trace of the last traversal on this shard (rank 0 of a local
+ * group): as gk_bfs_trace. */
+GK_API gk_status gk_shard_trace(const gk_shard* s, uint64_t* ts_ns, char* tags, int32_t cap, int32_t* count);
+/* Exchange bytes rank `rank` received in a traversal with this step log
+ * (the all-gather of next per step, the claims reduce per top-down step). */
+GK_API gk_status gk_shard_bytes_in(const gk_shard* s, int32_t rank, const gk_step* steps,
+                                   int32_t num_steps, int64_t* out);
 
 /* Pinned host buffers for end-to-end transfers. */
 GK_API void* gk_host_alloc(int64_t bytes);

@@ -31,9 +31,9 @@ EXPORTED = (
     "gk_graph_download", "gk_pick_sources", "gk_bfs", "gk_bfs_device_parent", "gk_bfs_device_depth",
     "gk_bfs_byte_model", "gk_bfs_keep_depth", "gk_host_alloc", "gk_host_free", "gk_bfs_trace",
     "gk_shard_last_error", "gk_shard_generate", "gk_shard_upload", "gk_shard_free", "gk_shard_info",
-    "gk_shard_set_stream", "gk_shard_degree", "gk_shard_begin", "gk_shard_td_expand", "gk_shard_td_apply",
-    "gk_shard_tail", "gk_shard_rescan", "gk_shard_q2b", "gk_shard_bu", "gk_shard_b2q", "gk_shard_result",
-    "gk_shard_launches", "gk_bfs_verify", "gk_graph_load_sg", "gk_graph_save_sg", "gk_brandes",
+    "gk_shard_set_stream", "gk_shard_launches", "gk_shard_join_local", "gk_shard_handle_size",
+    "gk_shard_export", "gk_shard_connect", "gk_shard_gather_dead", "gk_shard_group_bfs", "gk_shard_bfs",
+    "gk_shard_bytes_in", "gk_shard_download", "gk_shard_trace", "gk_bfs_verify", "gk_graph_load_sg", "gk_graph_save_sg", "gk_brandes",
     "gk_bfs_batch",
 )
 
@@ -102,16 +102,16 @@ def load() -> C.CDLL:
     L.gk_shard_set_stream.argtypes = [vp, vp]
     L.gk_shard_launches.argtypes = [vp]
     L.gk_shard_launches.restype = i64
-    L.gk_shard_degree.argtypes = [vp, u32, C.POINTER(i64)]
-    L.gk_shard_begin.argtypes = [vp, u32, i32, i32]
-    L.gk_shard_td_expand.argtypes = [vp, u64, u64, i32, i32, vp, vp, vp, i64]
-    L.gk_shard_td_apply.argtypes = [vp, vp, i64, i32, vp]
-    L.gk_shard_tail.argtypes = [vp, C.POINTER(u64)]
-    L.gk_shard_rescan.argtypes = [vp, u64, u64, C.POINTER(i64)]
-    L.gk_shard_q2b.argtypes = [vp, u64, u64, vp]
-    L.gk_shard_bu.argtypes = [vp, vp, vp, i32, C.POINTER(i64)]
-    L.gk_shard_b2q.argtypes = [vp, vp]
-    L.gk_shard_result.argtypes = [vp, vp, vp, vp]
+    L.gk_shard_join_local.argtypes = [vp, C.c_int]
+    L.gk_shard_download.argtypes = [vp, vp, vp]
+    L.gk_shard_trace.argtypes = [vp, C.POINTER(C.c_uint64), C.c_char_p, i32, C.POINTER(i32)]
+    L.gk_shard_handle_size.restype = i64
+    L.gk_shard_export.argtypes = [vp, vp]
+    L.gk_shard_connect.argtypes = [vp, vp]
+    L.gk_shard_gather_dead.argtypes = [vp]
+    L.gk_shard_group_bfs.argtypes = [vp, u32, i64, i64, i32, vp, vp, C.POINTER(BfsStats)]
+    L.gk_shard_bfs.argtypes = [vp, u32, i64, i64, i32, vp, vp, C.POINTER(BfsStats), C.POINTER(i64)]
+    L.gk_shard_bytes_in.argtypes = [vp, i32, C.POINTER(Step), i32, C.POINTER(i64)]
     L.gk_host_alloc.argtypes = [i64]
     L.gk_host_alloc.restype = vp
     L.gk_host_free.argtypes = [vp]
@@ -119,7 +119,7 @@ def load() -> C.CDLL:
     for f in EXPORTED:
         if f not in ("gk_last_error", "gk_abi_version", "gk_device_count", "gk_graph_free",
                      "gk_bfs_device_parent", "gk_bfs_device_depth", "gk_host_alloc", "gk_host_free", "gk_shard_last_error",
-                     "gk_shard_free", "gk_shard_launches"):
+                     "gk_shard_free", "gk_shard_launches", "gk_shard_handle_size"):
             getattr(L, f).restype = C.c_int
     _lib = L
     return L

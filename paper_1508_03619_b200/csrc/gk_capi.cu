@@ -264,6 +264,8 @@ gk::BfsParams make_params(gk_graph* g, const gk_trial& t, uint32_t source, int64
   }
   if (const char* bt = getenv("GK_BITMAP_TD_MIN")) p.bitmap_td_min = strtoll(bt, nullptr, 10);
   p.bu_tw_log_max = 5;
+  p.w_lo = 0;  // one rank owns every word
+  p.w_hi = p.w32;
   if (const char* tw = getenv("GK_BU_TASK_LOG")) p.bu_tw_log_max = std::max(0, std::min(5, atoi(tw)));
   // kTopDownRescan re-reads every new frontier's queue (bfs.hpp:161-167):
   // its steps keep the queue path (large steps leave the frontier a bitmap)

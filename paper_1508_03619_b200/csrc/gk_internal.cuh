@@ -43,7 +43,15 @@ enum PhaseTag : unsigned char { kTagInit = 'I', kTagTD = 'T', kTagHeavy = 'H', k
                                 kTagBU = 'B', kTagB2Q = 'C', kTagRescan = 'R', kTagSweep = 'S', kTagLong = 'L',
                                 kTagBcBack = 'D', kTagBcChunk = 'E', kTagBcScore = 'F', kTagOwn = 'O', kTagPull = 'P' };
 enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend = 4, kLongCount = 5, kCount = 6,
-                   kOwnCount = 7, kSlots = 8 };
+                   kOwnCount = 7, kWork = 8, kSlots = 10 };
+// kSum, kCount and kWork are traversal-wide totals (kWork: hubs, heavy
+// chunks and long lists registered -- the sharded kernel skips a phase no
+// rank has work for); the other slots count work of one rank (tiles,
+// chunks, queue appends, long lists).  Ranks that share one
+// launch (the sharded traversal's single-device emulation) keep those in
+// Ctrl::rcnt; ranks on separate devices in their own Ctrl.
+__host__ __device__ constexpr bool global_slot(int k) { return k == kSum || k == kCount || k == kWork; }
+constexpr int kMaxRanks = 8;
 
 struct Ctrl {
   // ---- cleared before every launch (kCtrlClear bytes) ----
@@ -53,6 +61,10 @@ struct Ctrl {
   long long num_steps;
   long long pad1;
   unsigned long long cnt[4][kSlots];
+  unsigned long long rcnt[4][kMaxRanks][kSlots];  // per-rank slots when ranks share a launch
+  unsigned long long xsnap[kSlots];  // sharded, multi-device: traversal-wide totals of the last cross-rank barrier
+  unsigned long long xsyncs;         // sharded, multi-device: cross-rank barriers this traversal passed
+  unsigned long long pad2;
   // Trace: tag[i] names the phase that grid barrier i ended (see PhaseTag),
   // 0 past the last one.
   unsigned char tag[kTraceCap];
@@ -132,6 +144,14 @@ struct BfsParams {
   int32_t own_win_log;        // ids per claim-log window = 2^own_win_log <= own_span_w
   int64_t own_dmin;           // out-degree that counts as a hub
   int32_t bu_tw_log_max;  // bottom-up task = 2^this bitmap words (5 unless overridden for A/B)
+  // Sharded traversal (gk_bfs_sharded.cu); zero for a single-device traversal.
+  int32_t cpr;          // CTAs per rank when several ranks share one launch (emulation), else 0
+  int32_t rslot;        // 1 + this rank's slot in Ctrl::rcnt when ranks share a launch, else 0
+  int32_t sharded;      // bitmap top-down claims store parents to the target's owner (shard_parent)
+  int64_t shard_block;  // vertices per rank
+  uint32_t shard_recip; // ceil(2^32 / shard_block)
+  int32_t* shard_parent[kMaxRanks];  // per rank: parent array shifted so [v] is owned v's slot (peer-mapped)
+  int64_t w_lo, w_hi;   // owned bitmap words [w_lo, w_hi) (0, w32 unsharded)
   int32_t td_passes;    // large top-down steps: target-range passes (1 when next fits L2)
   int64_t td_span;      // ids per pass (multiple of 32)
   // Brandes (betweenness.hpp:38-80), bc_persistent only
@@ -160,6 +180,49 @@ struct BfsLaunch {
 };
 cudaError_t bfs_configure(int device, BfsLaunch* cfg);
 cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t s);
+// ---- sharded traversal (gk_bfs_sharded.cu) --------------
+// Rank r owns vertices [lo, hi) (hi - lo = block, a multiple of 1024 so a
+// 32-word bottom-up task never straddles two ranks) and the CSR rows of
+// those vertices (undirected: in = out).  Bitmaps (visited, front/next,
+// claims) are full-n and replicated; parent/depth cover the owned range.
+struct ShardView {
+  const int64_t* off;  // shifted: off[v] for owned v (row of v - lo)
+  const uint32_t* nb;  // neighbour ids are global
+  int32_t* parent;     // shifted like off; a registered buffer peers map (remote claims store here)
+  int32_t* depth;      // shifted, or null
+  uint32_t* queue;     // owned frontier windows + long-list scratch, 2*(hi-lo)+64
+  OwnEnt* own_list;    // owned-range hub expansion of this rank's hubs (null: off)
+  uint2* own_stage;
+  int64_t own_cap;
+  Chunk* chunks;
+  int64_t chunk_cap;
+  uint32_t* bm[4];     // full-n bitmaps: visited, front/next pair, claims
+  const uint32_t* dead;  // full-n, replicated graph layout
+  int64_t lo, hi;
+};
+// Cross-rank barrier and counter reduction of separate launches (one per
+// device); lives on rank 0, the others map it.
+struct XCtrl {
+  unsigned long long bar;
+  int error;
+  int pad;
+  unsigned long long cnt[4][kSlots];
+};
+struct ShardTab {
+  int32_t nranks;
+  int32_t emulated;  // 1: all ranks in this one launch, cpr CTAs each (one device)
+  int32_t rank;      // this launch's rank (emulated == 0)
+  int32_t force_x;   // test hook: the multi-device barrier protocol even for one rank
+  int64_t m_total;   // arcs of the whole graph (edges_to_check, bfs.hpp:139)
+  int64_t block;     // vertices per rank
+  int64_t live_total;
+  ShardView v[kMaxRanks];  // peers: only bm[] is dereferenced (peer-mapped in multi-device runs)
+  XCtrl* x;          // multi-device only
+  unsigned long long xbase;  // multi-device: cross-rank barriers completed by earlier traversals
+};
+cudaError_t shard_configure(int device, BfsLaunch* cfg);
+cudaError_t shard_launch(const BfsParams& p, const ShardTab& t, int grid, cudaStream_t s);
+
 // One source of Brandes' forward + backward pass (cooperative launch).
 cudaError_t bc_launch(const BfsParams& p, int device, cudaStream_t s);
 // scores /= max(scores) when the max is > 0 (betweenness.hpp:136-143).

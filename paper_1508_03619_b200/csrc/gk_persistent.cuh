@@ -60,6 +60,14 @@ struct __align__(16) SmemT {
 };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+// CTA index / count within this traversal's rank (ranks sharing one launch
+// take consecutive runs of P.cpr CTAs).
+__device__ __forceinline__ int cta_id(const BfsParams& P) { return P.cpr ? (int)(blockIdx.x % P.cpr) : (int)blockIdx.x; }
+__device__ __forceinline__ int cta_count(const BfsParams& P) { return P.cpr ? P.cpr : (int)gridDim.x; }
+// Counter set of phase ph for this rank's own work (see global_slot).
+__device__ __forceinline__ unsigned long long* rset(const BfsParams& P, unsigned ph) {
+  return P.rslot ? P.ctrl->rcnt[ph & 3][P.rslot - 1] : P.ctrl->cnt[ph & 3];
+}
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned r;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
@@ -194,12 +202,15 @@ __device__ bool grid_sync(const BfsParams& P, SmemT& s, unsigned& ph, unsigned c
     // One read of the ended phase's counters per CTA, shared through smem
     // (every thread reading them from L2 made a hot spot on one line).
     const volatile unsigned long long* cs = c->cnt[ph & 3];
+    const volatile unsigned long long* rs = rset(P, ph);
 #pragma unroll
-    for (int i = 0; i < kSlots; i++) s.snap[i] = cs[i];
+    for (int i = 0; i < kSlots; i++) s.snap[i] = global_slot(i) ? cs[i] : rs[i];
     if (blockIdx.x == 0) {  // recycle the counter set two phases ahead; trace
       unsigned long long* z = c->cnt[(ph + 3) & 3];
 #pragma unroll
       for (int i = 0; i < kSlots; i++) z[i] = 0;
+      if (P.cpr)
+        for (int i = 0; i < kMaxRanks * kSlots; i++) (&c->rcnt[(ph + 3) & 3][0][0])[i] = 0;
       if (ph + 1 < (unsigned)kTraceCap) {
         c->ts[ph + 1] = globaltimer();
         c->tag[ph + 1] = tag;
@@ -264,7 +275,7 @@ struct QApp {
   unsigned long long* ctr;
 };
 __device__ __forceinline__ QApp qapp(const BfsParams& P, unsigned ph, unsigned long long base) {
-  return QApp{base, &P.ctrl->cnt[ph & 3][kAppend]};
+  return QApp{base, &rset(P, ph)[kAppend]};
 }
 
 // Per-warp staging buffer flushed with one fetch-add (QueueBuffer,
