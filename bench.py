@@ -367,10 +367,10 @@ def run_sharded(args, cfg, rank, world, local, dist):
               "note": "exchange bytes received per rank: all-gather of next per step + claims reduce per "
                       "top-down step" + ("" if world > 1 else "; ranks emulated on one GPU (no NVLink)")}
     if bsec_of:
-        per_gpu = sum(bsec_of[s] for s in sources) / P / tot_t / 1e9
+        per_gpu = sum(bsec_of[s] for s in sources) / world / tot_t / 1e9  # emulated ranks share one GPU
         roof = {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s", "frac": per_gpu / peak,
                 "traffic": None, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": sum(bsec_of[s] for s in sources) / len(sources) / P,
+                "algorithmic_bytes_per_launch": sum(bsec_of[s] for s in sources) / len(sources) / world,
                 "note": "per-GPU share (B_sec / N) of the single-device byte model over the sharded step time",
                 "kernel": "bfs_sharded (one persistent launch per rank per BFS)", "nvlink": nvlink}
     line = {

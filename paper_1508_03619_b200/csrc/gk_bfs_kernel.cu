@@ -97,7 +97,12 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   long long reached = 1;  // vertices claimed so far (source included)
   long long dummy = 0;
   // sparse sweeps while few vertices are pending (and the list scratch holds them twice)
-  auto sparse_ok = [&](long long pend) { return !P.front_in_smem && GK_SPARSE && pend <= P.w32 && 2 * pend <= 4 * P.chunk_cap; };
+#ifndef GK_SPARSE_MUL
+#define GK_SPARSE_MUL 1  // sparse sweeps while pending <= GK_SPARSE_MUL * n/32
+#endif
+  auto sparse_ok = [&](long long pend) {
+    return !P.front_in_smem && GK_SPARSE && pend <= GK_SPARSE_MUL * P.w32 && 2 * pend <= 4 * P.chunk_cap;
+  };
   int lvl = 0;
   int qcnt = 0;
   bool front_ready = false;  // frontg holds exactly the current frontier

@@ -795,7 +795,9 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
             }
         }
         if (hit) {
+#ifndef GK_BU_NO_PARENT  // diagnostic A/B only (results invalid without it)
           P.parent[v[k]] = (int32_t)par;
+#endif
           if (P.want_depth) P.depth[v[k]] = lvl + 1;
           atomicOr(&acc_n[(v[k] >> 5) - tbase], 1u << (v[k] & 31u));
           st[k] = 0;
