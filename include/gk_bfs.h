@@ -73,8 +73,9 @@ typedef struct {
 typedef struct {
   int32_t dir;            /* 'T' top-down or 'B' bottom-up (the reference's schedule) */
   int32_t pad;            /* how the step ran when not as dir names: 0, 'P' bottom-up step
-                             executed as a push, 'U' top-down step executed as a pull (same
-                             claimed set and counters either way) */
+                             executed as a push, 'U' top-down step executed as a pull, 'K'
+                             top-down step run by the cluster kernel (same claimed set and
+                             counters either way) */
   int64_t frontier;       /* frontier size entering the step */
   int64_t result;         /* T: scout count after the step; B: awake count */
   int64_t edges_to_check; /* heuristic's unexplored-arc budget */

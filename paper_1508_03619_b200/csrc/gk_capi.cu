@@ -74,6 +74,7 @@ void free_graph(gk_graph* g) {
   cudaFree(g->acc);
   if (g->pool) cudaMemPoolDestroy(g->pool);
   if (g->batch_err) cudaFreeHost(g->batch_err);
+  if (g->cm_peek) cudaFreeHost(g->cm_peek);
   for (cudaEvent_t e : g->batch_ev) cudaEventDestroy(e);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
@@ -99,6 +100,15 @@ gk_status setup_graph(gk_graph* g, bool sorted) {
   CK(cudaMalloc(&g->acc, sizeof(unsigned long long) * 8), "alloc acc");
   CK(gk::bfs_configure(g->device, &g->launch), "configure bfs kernel");
   if (getenv("GK_NO_FRONT_SMEM")) g->launch.smem_front_max = 0;  // tests: large-graph paths on small graphs
+  // Cluster mode for chains of tiny top-down levels.  gk_bfs reads the
+  // hand-off state with the control block it reads anyway; gk_bfs_batch
+  // pays a host round trip per trial for it, so it checks only on sparse
+  // graphs (mean degree <= 8: road networks, meshes), where chains occur.
+  CK(gk::cluster_configure(g->device, &g->cm_cluster, &g->cm_max_scout), "configure cluster kernel");
+  if (g->cm_cluster) {
+    CK(cudaHostAlloc(&g->cm_peek, sizeof(gk::Ctrl), cudaHostAllocDefault), "cudaHostAlloc");
+    g->cm_batch = g->m <= 8 * g->n;
+  }
   g->canary = getenv("GK_CANARY") && atoi(getenv("GK_CANARY")) != 0;
   CK(cudaMalloc(&g->dead, bitmap_bytes(n)), "alloc dead-vertex bitmap");
   CK(gk::dead_bitmap(g->in_off, n, g->dead, &g->live, g->stream), "dead-vertex bitmap");
@@ -280,6 +290,8 @@ gk::BfsParams make_params(gk_graph* g, const gk_trial& t, uint32_t source, int64
   if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
   p.stop_after = 0xffffffffu;
   if (const char* sa = getenv("GK_STOP_AFTER")) p.stop_after = (unsigned)strtoul(sa, nullptr, 10);
+  p.cm_ok = g->cm_cluster > 0;
+  p.cm_max_scout = g->cm_max_scout;
   return p;
 }
 
@@ -302,6 +314,31 @@ gk_status kernel_error(const gk::Ctrl& ctrl, const char* what) {
     return fail(GK_ERR_TIMEOUT, buf);
   }
   return fail(GK_ERR_CUDA, std::string(what) + " kernel: scratch buffer overflow");
+}
+
+// Cluster-mode hand-offs (gk_bfs_cluster.cu): after the grid kernel of a
+// traversal handed off (h.mode != 0), runs whichever kernel the control
+// block names next until the traversal has finished.  Each hand-off costs a
+// host round trip (the next kernel is chosen here); a chain enters cluster
+// mode only after kCmEnter tiny levels, so the trips are few.  Stops early
+// on a kernel error, which the caller reads from the control block.
+cudaError_t run_handoffs(gk_graph* g, gk::BfsParams p, cudaStream_t s, gk::Hand h) {
+  while (h.mode != 0) {
+    cudaError_t e;
+    if (h.mode == 1) {
+      e = gk::cluster_launch(p, h, g->cm_cluster, s);
+    } else {
+      p.resume = 1;
+      p.rs = h;
+      e = gk::bfs_launch(p, g->launch, s);
+    }
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMemcpyAsync(g->cm_peek, p.ctrl, gk::kCtrlPeek, cudaMemcpyDeviceToHost, s))) return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    if (g->cm_peek->error) return cudaSuccess;
+    h = g->cm_peek->hand;
+  }
+  return cudaSuccess;
 }
 
 gk_status finish_graph(gk_graph* g, gk_graph** out) {
@@ -562,15 +599,22 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   g->parent = t.parent;
   gk::BfsParams p = make_params(g, t, source, alpha, beta, strategy, want_depth);
   CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
-  if (g->canary) {
-    const gk_status cst = trial_check_canaries(g, tb, s);
-    if (cst != GK_OK) return cst;
-  }
-  CK(cudaFreeAsync(tb.work, s), "free trial scratch");
   CK(cudaEventRecord(g->ev1, s), "event record");
   gk::Ctrl& ctrl = g->last_ctrl;
   CK(cudaMemcpyAsync(&ctrl, t.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
   CK(cudaStreamSynchronize(s), "bfs kernel");
+  if (!ctrl.error && ctrl.hand.mode != 0) {  // the grid kernel handed off to the cluster kernel
+    CK(run_handoffs(g, p, s, ctrl.hand), "cluster-mode hand-off");
+    CK(cudaEventRecord(g->ev1, s), "event record");
+    CK(cudaMemcpyAsync(&ctrl, t.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
+    CK(cudaStreamSynchronize(s), "bfs kernel");
+  }
+  if (g->canary) {
+    const gk_status cst = trial_check_canaries(g, tb, s);
+    if (cst != GK_OK) return cst;
+  }
+  // the scratch returns to the pool (stream-ordered bookkeeping, no device work)
+  CK(cudaFreeAsync(tb.work, s), "free trial scratch");
   if (ctrl.error) {
     cudaFreeAsync(tb.book, s);
     return kernel_error(ctrl, "bfs");
@@ -657,7 +701,13 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     if ((e = cudaEventRecord(ev[3 * i], s))) break;
     if ((e = trial_alloc(g, &t, &tb, s, own))) break;
     gk::BfsParams p = make_params(g, t, sources[i], alpha, beta, strategy, 0);
+    p.cm_ok = g->cm_batch ? p.cm_ok : 0;
     if ((e = gk::bfs_launch(p, g->launch, s))) break;
+    if (p.cm_ok) {  // hand-offs are decided on the host: wait for the grid kernel
+      if ((e = cudaMemcpyAsync(g->cm_peek, p.ctrl, gk::kCtrlPeek, cudaMemcpyDeviceToHost, s))) break;
+      if ((e = cudaStreamSynchronize(s))) break;
+      if (!g->cm_peek->error && g->cm_peek->hand.mode != 0 && (e = run_handoffs(g, p, s, g->cm_peek->hand))) break;
+    }
     if ((e = cudaFreeAsync(tb.work, s))) break;
     if ((e = cudaEventRecord(ev[3 * i + 1], s))) break;
     if ((e = cudaMemcpyAsync(errs + i, &t.ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;

@@ -53,8 +53,20 @@ enum CounterSlot { kSum = 0, kTile = 1, kChunkCount = 2, kChunkNext = 3, kAppend
 __host__ __device__ constexpr bool global_slot(int k) { return k == kSum || k == kCount || k == kWork; }
 constexpr int kMaxRanks = 8;
 
+// Hand-off between the grid kernel and the cluster kernel (long chains of
+// tiny top-down levels, gk_bfs_cluster.cu): where the traversal stands.
+struct Hand {
+  long long mode;  // 0 finished, 1 continue in the cluster kernel, 2 continue in the grid kernel
+  long long qs, qe, qtail;  // the frontier's queue window, queue entries written so far
+  long long etc, scout, nsteps, reached, lvl;
+  unsigned long long qfill;  // cluster kernel: entries appended after qtail (overflow, exit)
+  long long swap;            // grid kernel: front/next bitmaps swapped (frontg == bm1)
+  long long pad;
+};
+
 struct Ctrl {
   // ---- cleared before every launch (kCtrlClear bytes) ----
+  Hand hand;
   unsigned long long bar_count;  // monotonic grid-barrier arrivals
   int error;
   int pad0;
@@ -75,6 +87,7 @@ struct Ctrl {
   unsigned int cta_ph[2048];  // per-CTA barrier count (watchdog diagnostics; CTAs < grid)
 };
 constexpr size_t kCtrlClear = offsetof(Ctrl, ts);
+constexpr size_t kCtrlPeek = offsetof(Ctrl, num_steps);  // hand, bar_count, error
 
 static_assert(sizeof(Ctrl) % 16 == 0 && kCtrlClear % 16 == 0, "control blocks are cleared with 16-byte stores");
 
@@ -152,6 +165,11 @@ struct BfsParams {
   uint32_t shard_recip; // ceil(2^32 / shard_block)
   int32_t* shard_parent[kMaxRanks];  // per rank: parent array shifted so [v] is owned v's slot (peer-mapped)
   int64_t w_lo, w_hi;   // owned bitmap words [w_lo, w_hi) (0, w32 unsharded)
+  // Cluster mode for long chains of tiny top-down levels (gk_bfs_cluster.cu)
+  int32_t cm_ok;         // the cluster kernel is available for this traversal
+  int32_t resume;        // this launch continues a traversal from rs (skip init)
+  int64_t cm_max_scout;  // a top-down step stays in cluster mode while scout <= this
+  Hand rs;               // resume state
   int32_t td_passes;    // large top-down steps: target-range passes (1 when next fits L2)
   int64_t td_span;      // ids per pass (multiple of 32)
   // Brandes (betweenness.hpp:38-80), bc_persistent only
@@ -180,6 +198,7 @@ struct BfsLaunch {
 };
 cudaError_t bfs_configure(int device, BfsLaunch* cfg);
 cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t s);
+const void* bfs_resume_fn();  // the grid kernel continuing a handed-back traversal (gk_bfs_resume.cu)
 // ---- sharded traversal (gk_bfs_sharded.cu) --------------
 // Rank r owns vertices [lo, hi) (hi - lo = block, a multiple of 1024 so a
 // 32-word bottom-up task never straddles two ranks) and the CSR rows of
@@ -221,6 +240,10 @@ struct ShardTab {
   unsigned long long xbase;  // multi-device: cross-rank barriers completed by earlier traversals
 };
 cudaError_t shard_configure(int device, BfsLaunch* cfg);
+// Cluster kernel: *cluster = CTAs per cluster (0: unavailable), *max_scout =
+// the largest step it takes.
+cudaError_t cluster_configure(int device, int* cluster, int64_t* max_scout);
+cudaError_t cluster_launch(const BfsParams& p, const Hand& h, int cluster, cudaStream_t s);
 cudaError_t shard_launch(const BfsParams& p, const ShardTab& t, int grid, cudaStream_t s);
 
 // One source of Brandes' forward + backward pass (cooperative launch).
@@ -317,6 +340,12 @@ struct gk_graph {
   cudaEvent_t ev0 = nullptr;
   cudaEvent_t ev1 = nullptr;
   gk::BfsLaunch launch;
+  // cluster mode (gk_bfs_cluster.cu): CTAs per cluster (0: off), largest step it takes,
+  // pinned copy of the control block's head (hand-off state + error) read between kernels
+  int cm_cluster = 0;
+  int64_t cm_max_scout = 0;
+  bool cm_batch = false;  // gk_bfs_batch checks for hand-offs after every trial (sparse graphs)
+  gk::Ctrl* cm_peek = nullptr;
   gk::Ctrl last_ctrl;  // host copy of the last traversal's control block
   int32_t last_valid = 0;
   std::mutex mu;

@@ -245,6 +245,56 @@ def test_grid_high_diameter():
         assert res.schedule == O.bfs_replay(g, s).dirs
 
 
+@pytest.fixture(scope="module")
+def chain_graphs():
+    """High-diameter graphs whose traversals are long chains of tiny
+    top-down levels (the cluster kernel's domain): a road-like grid and a
+    path with a few branches."""
+    out = {}
+    h = O.make_graph("grid", rows=300, cols=257, seed=99)
+    out["grid300x257"] = (h, DeviceGraph.from_csr(h))
+    n = 6000
+    e = [(i, i + 1) for i in range(n - 1)] + [(i, (i * 7919) % n) for i in range(0, n, 97)]
+    p = O.build_csr(n, np.array(e, np.uint32).reshape(-1))
+    out["path6000"] = (p, DeviceGraph.from_csr(p))
+    return out
+
+
+@pytest.mark.parametrize("strategy", [0, 1, 2])
+def test_cluster_mode_parity(chain_graphs, strategy):
+    """Chains of tiny top-down levels run in the cluster kernel (steps tagged
+    'K', gk_bfs_cluster.cu) and hand back to the grid kernel: depths exact,
+    parents valid, schedule and every step counter equal the reference's."""
+    for name, (g, dg) in chain_graphs.items():
+        seen_k = False
+        for s in O.pick_sources(g, 3, 5):
+            s = int(s)
+            res = dg.bfs(s, strategy=strategy, depth=True, counts=True)
+            key = (name, s, strategy)
+            assert (res.depth == O.bfs_depths(g, s)).all(), key
+            assert O.verify_bfs(g, s, res.parent)[0], key
+            rp = O.bfs_replay(g, s, strategy=strategy)
+            assert res.schedule == rp.dirs, key
+            assert [x[1] for x in res.steps] == rp.frontier, key
+            assert [x[2] for x in res.steps] == rp.result, key
+            assert [x[3] for x in res.steps] == rp.edges_to_check, key
+            assert res.reached == int((res.depth >= 0).sum()), key
+            seen_k |= any(x[4] == "K" for x in res.steps)
+        assert seen_k, name  # the cluster kernel ran
+
+
+def test_cluster_mode_batch(chain_graphs):
+    """gk_bfs_batch on a sparse graph checks for hand-offs after each trial:
+    every parent array valid and equal-depth to the single-source call."""
+    g, dg = chain_graphs["grid300x257"]
+    srcs = [int(s) for s in O.pick_sources(g, 4, 9)]
+    outs = [np.empty(g.n, np.int32) for _ in srcs]
+    ms = dg.bfs_batch(srcs, outs)
+    assert (ms > 0).all()
+    for s, par in zip(srcs, outs):
+        assert O.verify_bfs(g, s, par)[0], s
+
+
 # ---------------------------------------------------------------- certificate
 def _cuda_memcpy_h2d(dst_ptr, arr):
     """Tamper with a device array (test only) through the system CUDA runtime."""
