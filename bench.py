@@ -477,9 +477,11 @@ def main():
         dist.barrier()
     tw0 = time.time()
     dev_ms = []
+    launches0 = g.launches()
     for s in sources:
         r = g.bfs(s, parent=False)
         dev_ms.append(r.device_ms)
+    launches = g.launches() - launches0
     wall = time.time() - tw0
     clocks = clk.stop()
     if args.verbose:
@@ -542,7 +544,10 @@ def main():
                 "algorithmic_bytes_per_launch": tot_b / len(sources),
                 "b_use_frac": (sum(buse_of[s] for s in sources) / tot_t / 1e9) / peak,
                 "frac_of_8TBs_nominal": ach / 8000.0,
-                "kernel": "bfs_persistent (one launch per BFS)"}
+                "kernel": ("bfs_persistent (one launch per BFS)" if launches == len(sources) else
+                           f"bfs_persistent + bfs_cluster ({launches} launches for {len(sources)} BFS: "
+                           "chains of tiny top-down levels run in the cluster kernel)"),
+                "per": "BFS (all of its launches)"}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -575,7 +580,7 @@ def main():
                         "one_call_per_source = gk_bfs per source without overlap (first 8 sources); graph "
                         "resident (uploaded once, untimed, as the reference harness builds it untimed); "
                         "the per-step input is the 4-byte source id (a kernel argument)"},
-        "gpu_launches": K,
+        "gpu_launches": launches,
         "clocks": clocks,
         "roofline": roof,
         "cpu_baseline": cpu,

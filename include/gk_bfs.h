@@ -172,6 +172,12 @@ GK_API const int32_t* gk_bfs_device_parent(const gk_graph* g);
  * certificate's tamper tests. */
 GK_API int32_t* gk_bfs_device_depth(const gk_graph* g);
 
+/* Traversal kernels launched on g so far (grid kernel launches, cluster
+   kernel launches and grid-kernel resumptions of gk_bfs / gk_bfs_batch):
+   the difference around a timed region is the number of this library's
+   kernels it ran.  Memsets and the pool's bookkeeping are not counted. */
+GK_API int64_t gk_bfs_launches(const gk_graph* g);
+
 /* Phase trace of the last gk_bfs: ts_ns[0] = kernel start, ts_ns[i] = release
  * of grid barrier i (globaltimer ns) and tags[i] the phase it ended: 'I' init,
  * 'T' top-down, 'H' heavy-vertex chunks, 'Z' front clear, 'Q' queue->bitmap,

@@ -253,6 +253,10 @@ class DeviceGraph:
         e = list(errs)
         return {"ok": sum(e[:7]) == 0, "errors": e[:7], "first_bad": e[7]}
 
+    def launches(self) -> int:
+        """Traversal kernels launched on this graph so far (gk_bfs_launches)."""
+        return int(_lib.load().gk_bfs_launches(self._h))
+
     def trace(self):
         """[(tag, t_ms_since_kernel_start)] for the phases of the last bfs."""
         cap = 4096

@@ -43,6 +43,16 @@ struct CmEnt {
   int64_t off;
 };
 
+constexpr uint32_t kCmLight = 16;  // lists up to this long are expanded by their own lane
+constexpr int kCmW = 4;            // arcs per lane in flight
+constexpr int kCmSub = 4;          // sub-regions per (sender, destination) region
+
+struct CmArc {  // one arc of a flattened short list: parent, position in the neighbour array
+  uint32_t u;
+  uint32_t pad;
+  int64_t pos;
+};
+
 // Messages between the CTAs of the cluster (DSMEM, no cluster barrier per
 // level).  During level L every CTA sends each CTA d (itself included):
 //   * the claimed vertices whose home is d, as 16-byte entries stored with
@@ -60,32 +70,39 @@ struct __align__(16) CmShared {
   uint4 hdr[2][16];            // [parity][sender]
   unsigned long long mbar[2];  // per parity, C arrivals per phase
   unsigned long long ctot[2][2];  // this CTA's level totals by send parity: claims, scout
-  unsigned lc[2][16];          // entries sent per destination, by send parity
+  unsigned lc[2][16][kCmSub];  // entries sent per destination and sub-region, by send parity
   unsigned lovf[2];            // an entry of this CTA went to the global queue
   // kTopDownRescan's extra pass (bfs.hpp:161-167): per-CTA degree totals of
   // the new frontier, exchanged like the headers on their own barriers
   uint4 rmsg[2][16];
   unsigned long long rbar[2];
   unsigned long long rsum[2];
+  CmArc arc[kCmBlock / 32][32 * kCmW];  // per warp: the short lists being claimed
+  unsigned dbg[2][4];  // GK_CM_TRACE == 2: per-level warp timing of CTA 0
+  unsigned dbs[2][4];  // sub-phases of a warp's first round
 };
 
-constexpr uint32_t kCmLight = 16;  // lists up to this long are expanded by their own lane
-constexpr int kCmW = 8;            // arcs per lane in flight (a mesh vertex's list in one round)
 
 #ifndef GK_CM_TRACE
-#define GK_CM_TRACE 0  // 1: CTA 0 logs per-level phase cycles of the first levels in the trace (diagnostic)
+#define GK_CM_TRACE 0  // diagnostics: 1 CTA 0 logs per-level phase cycles in the trace, 2 its warp timing
 #endif
-#define CM_MARK(i) CM_MARKD(i, 0u)
+#if GK_CM_TRACE == 1
 // the clock is read once dep (a register) is available
 #define CM_MARKD(i, dep)                                                                    \
   do {                                                                                      \
-    if (GK_CM_TRACE && c == 0 && t == 0 && L < 120) {                                      \
+    if (c == 0 && t == 0 && L < 120) {                                                      \
       unsigned long long ck_;                                                               \
       asm volatile("mov.u64 %0, %%clock64;" : "=l"(ck_) : "r"((unsigned)(dep)));            \
       P.ctrl->ts[L * 4 + (i)] = ck_;                                                        \
       P.ctrl->tag[L * 4 + (i)] = 'a' + (i);                                                 \
     }                                                                                       \
   } while (0)
+#else
+#define CM_MARKD(i, dep) \
+  do {                   \
+  } while (0)
+#endif
+#define CM_MARK(i) CM_MARKD(i, 0u)
 
 __device__ __forceinline__ unsigned cm_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ unsigned cm_mapa(unsigned a, int rank) {
@@ -147,7 +164,7 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
   const long long base = H.qtail;  // hand-back window starts here
   const unsigned f_sa = cm_saddr(&S.f[0][0]), hdr_sa = cm_saddr(&S.hdr[0][0]), bar_sa = cm_saddr(&S.mbar[0]);
   if (t < 4) (&S.ctot[0][0])[t] = 0ull;
-  if (t < 32) (&S.lc[0][0])[t] = 0u;
+  if (t < 2 * 16 * kCmSub) (&S.lc[0][0][0])[t] = 0u;
   const unsigned rmsg_sa = cm_saddr(&S.rmsg[0][0]), rbar_sa = cm_saddr(&S.rbar[0]);
   if (t < 2) {
     S.lovf[t] = 0u;
@@ -164,18 +181,24 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
   unsigned long long t0 = 0;
   if (t == 0) t0 = globaltimer();
 
-  // a claimed (or loaded) vertex to its home CTA's region for this sender
-  auto push = [&](int dp, uint32_t v, uint32_t deg, int64_t off) {
-    const int home = cm_home(v, lgc);
-    const unsigned idx = atomicAdd(&S.lc[dp][home], 1u);
-    if (idx < (unsigned)R) {
-      const unsigned slot = (unsigned)(dp * kCmCap + c * R + (int)idx);
+  // a claimed (or loaded) vertex to its home CTA's region for this sender:
+  // slot idx of sub-region sub (warps w with w % kCmSub == sub share one, so
+  // fewer warps contend for each local counter)
+  const int R4 = R / kCmSub;
+  const int sub = (int)warp & (kCmSub - 1);
+  auto push_at = [&](int dp, int home, unsigned idx, uint32_t v, uint32_t deg, int64_t off) {
+    if (idx < (unsigned)R4) {
+      const unsigned slot = (unsigned)(dp * kCmCap + c * R + sub * R4 + (int)idx);
       cm_st_async(cm_mapa(f_sa + slot * (unsigned)sizeof(CmEnt), home), v, deg, (uint32_t)off,
                   (uint32_t)((uint64_t)off >> 32), cm_mapa(bar_sa + 8u * dp, home));
     } else {  // region full: to the global queue; the traversal returns to the grid kernel
       P.queue[base + atomicAdd(&P.ctrl->hand.qfill, 1ull)] = v;
       S.lovf[dp] = 1u;
     }
+  };
+  auto push = [&](int dp, uint32_t v, uint32_t deg, int64_t off) {
+    const int home = cm_home(v, lgc);
+    push_at(dp, home, atomicAdd(&S.lc[dp][home][sub], 1u), v, deg, off);
   };
   // after every warp's pushes and totals of send parity dp: headers + arrivals to every CTA
   auto send = [&](int dp) {
@@ -184,12 +207,18 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
       const unsigned long long cc = S.ctot[dp][0], sc = S.ctot[dp][1];
       const unsigned of = S.lovf[dp];
       if ((int)lane < C) {
-        const unsigned n = S.lc[dp][lane];
+        unsigned packed = 0, sent = 0;
+#pragma unroll
+        for (int k = 0; k < kCmSub; k++) {
+          const unsigned n = S.lc[dp][lane][k];
+          packed |= min(n, 255u) << (8 * k);
+          sent += min(n, (unsigned)R4);
+          S.lc[dp][lane][k] = 0u;
+        }
         const unsigned rbar = cm_mapa(bar_sa + 8u * dp, (int)lane);
-        cm_st_async(cm_mapa(hdr_sa + (unsigned)(dp * 16 + c) * 16u, (int)lane), n, (uint32_t)cc,
+        cm_st_async(cm_mapa(hdr_sa + (unsigned)(dp * 16 + c) * 16u, (int)lane), packed, (uint32_t)cc,
                     (uint32_t)(sc & 0xffff), (uint32_t)(sc >> 16) | (of << 31), rbar);
-        cm_arrive_tx(rbar, 16u * (1u + min(n, (unsigned)R)));
-        S.lc[dp][lane] = 0u;
+        cm_arrive_tx(rbar, 16u * (1u + sent));
       }
       __syncwarp();
       if (lane == 0) {
@@ -213,10 +242,16 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
     send(0);
   }
 
-  long long fsize = 0;
-  int nr = 0;
   // warp w walks sender region w % C, every wpr-th group of 32 entries
   const int reg = (int)warp % C, wpr = (kCmBlock / 32) / C, g0 = ((int)warp / C) * 32;
+  long long fsize = 0;
+  int nr = 0, p1 = 0, p2 = 0, p3 = 0;  // entries of this warp's region at the current level, sub-region prefixes
+  // entry e of this warp's region -> its slot in f[parity]
+  auto eslot = [&](int e) {
+    const int k = (e >= p1) + (e >= p2) + (e >= p3);
+    const int b = k == 0 ? 0 : k == 1 ? p1 : k == 2 ? p2 : p3;
+    return reg * R + k * R4 + (e - b);
+  };
 #ifdef GK_CM_EXITTAG
   unsigned dbg_maxn = 0, dbg_bit = 0;
 #endif  // entries of this warp's region at the current level
@@ -234,6 +269,29 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
       }
     }
     CM_MARK(0);
+#if GK_CM_TRACE == 2
+    unsigned xs = 0;
+    if (c == 0 && t == 0) {
+      const unsigned now = (unsigned)clock64();
+      if (L == 0) P.ctrl->ts[0] = 0;
+      if (L > 0 && L <= 120) {
+        const unsigned* d = S.dbg[(L - 1) & 1];
+        P.ctrl->ts[(L - 1) * 4 + 0] = (L == 1 ? 0 : d[0]);
+        P.ctrl->ts[(L - 1) * 4 + 1] = d[1] / (kCmBlock / 32);
+        const unsigned* d2 = S.dbs[(L - 1) & 1];
+        P.ctrl->ts[(L - 1) * 4 + 1] = d2[0];
+        P.ctrl->ts[(L - 1) * 4 + 2] = d2[1];
+        P.ctrl->ts[(L - 1) * 4 + 3] = d2[2];
+        for (int i = 0; i < 4; i++) P.ctrl->tag[(L - 1) * 4 + i] = 'a' + i;
+      }
+      unsigned* e = S.dbg[(L + 1) & 1];
+      e[0] = e[1] = e[2] = 0;
+      unsigned* e2 = S.dbs[(L + 1) & 1];
+      e2[0] = e2[1] = e2[2] = 0;
+    }
+    xs = (unsigned)clock64();
+    if (c == 0 && t == 0) S.dbg[L & 1][3] = xs;
+#endif
     // headers: lane j holds sender j's; totals by warp reductions (same in every warp)
     bool ovf;
     long long claims, sc_next;
@@ -242,12 +300,21 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
       claims = (long long)__reduce_add_sync(kFull, h.y);
       const unsigned lo = __reduce_add_sync(kFull, h.z), hi = __reduce_add_sync(kFull, h.w & 0x7fffffffu);
       sc_next = ((long long)hi << 16) + (long long)lo;
-      ovf = __any_sync(kFull, (h.w >> 31) != 0u || h.x > (unsigned)R);
+      bool full = false;  // a sub-region overflowed
+#pragma unroll
+      for (int k = 0; k < kCmSub; k++) full |= ((h.x >> (8 * k)) & 0xffu) > (unsigned)R4;
+      ovf = __any_sync(kFull, (h.w >> 31) != 0u || full);
 #ifdef GK_CM_EXITTAG
-      dbg_maxn = __reduce_max_sync(kFull, h.x);
+      dbg_maxn = __reduce_max_sync(kFull, h.x & 0xffu);
       dbg_bit = __reduce_or_sync(kFull, h.w >> 31);
 #endif
-      nr = (int)min(__shfl_sync(kFull, h.x, reg), (unsigned)R);
+      const unsigned pk = __shfl_sync(kFull, h.x, reg);
+      const int n0 = (int)min(pk & 0xffu, (unsigned)R4), n1 = (int)min((pk >> 8) & 0xffu, (unsigned)R4),
+                n2 = (int)min((pk >> 16) & 0xffu, (unsigned)R4), n3 = (int)min(pk >> 24, (unsigned)R4);
+      p1 = n0;
+      p2 = n0 + n1;
+      p3 = p2 + n2;
+      nr = p3 + n3;
     }
     if (!encode && L > 0) {
       // kTopDownRescan (bfs.hpp:161-167): the new frontier's degree total by
@@ -255,7 +322,7 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
       const unsigned q = L - 1u, rp = q & 1u;
       unsigned long long mine = 0;
       for (int i = g0 + (int)lane; i < nr; i += wpr * 32) {
-        const uint32_t v = S.f[cur][reg * R + i].v;
+        const uint32_t v = S.f[cur][eslot(i)].v;
         mine += (unsigned long long)(ld_off(P.out_off + v + 1) - ld_off(P.out_off + v));
       }
       const unsigned lo = __reduce_add_sync(kFull, (unsigned)(mine & 0xffff));
@@ -321,6 +388,10 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
     // issued together (bfs.hpp:77-84); the claimed vertex's degree is read
     // with the claim and travels with its frontier entry.
     auto claimw = [&](const uint32_t (&u)[kCmW], const uint32_t (&w)[kCmW], const bool (&ok)[kCmW]) {
+#if GK_CM_TRACE == 2
+      unsigned t_a = 0;
+      asm volatile("mov.u32 %0, %%clock;" : "=r"(t_a) : "r"(w[0] + w[1] + w[kCmW - 1]));
+#endif
       int64_t o0[kCmW], o1[kCmW];
 #pragma unroll
       for (int q = 0; q < kCmW; q++) {
@@ -330,15 +401,31 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
           o1[q] = ld_off(P.out_off + w[q] + 1);
         }
       }
-      bool cl4[kCmW];
+      // every claim atomic in flight at once: each result has its own
+      // register and is looked at only after the last one was issued
+      uint32_t old[kCmW];
 #pragma unroll
       for (int q = 0; q < kCmW; q++) {
-        const uint32_t bit = 1u << (w[q] & 31u);
-        cl4[q] = ok[q] && !(atomicOr(P.visited + (w[q] >> 5), bit) & bit);
+        old[q] = ~0u;  // predicated atomic: its result stays in its own register
+        asm volatile(
+            "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p atom.global.or.b32 %0, [%1], %3;\n }"
+            : "+r"(old[q])
+            : "l"(P.visited + (w[q] >> 5)), "r"((unsigned)ok[q]), "r"(1u << (w[q] & 31u))
+            : "memory");
       }
+#if GK_CM_TRACE == 2
+      unsigned t_b = 0, t_c = 0;
+      asm volatile("mov.u32 %0, %%clock;" : "=r"(t_b) : "r"(old[0] + old[kCmW - 1] + (unsigned)(o1[0] + o1[kCmW - 1])));
+#endif
+      bool cl[kCmW];
+      int home[kCmW];
+      unsigned idx[kCmW];
 #pragma unroll
       for (int q = 0; q < kCmW; q++) {
-        if (!cl4[q]) continue;
+        cl[q] = !((old[q] >> (w[q] & 31u)) & 1u);
+        home[q] = 0;
+        idx[q] = 0;
+        if (!cl[q]) continue;
         P.parent[w[q]] = (int32_t)u[q];
         if (P.want_depth) P.depth[w[q]] = lvl + 1;
         const int64_t dg = o1[q] - o0[q];
@@ -346,29 +433,71 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
         // counts the new frontier's degrees in a separate pass)
         sc += encode ? (dg ? dg : 1) : 0;
         cc++;
-        if (dg) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.out_nb + o0[q]));
-        push(nxt, w[q], (uint32_t)dg, o0[q]);
+        if (dg) {
+#if GK_CM_TOUCH  // A/B: a discarded load instead of the L2 prefetch
+          uint32_t dummy;
+          asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(dummy) : "l"(P.out_nb + o0[q]));
+#else
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(P.out_nb + o0[q]));
+#endif
+        }
+        home[q] = cm_home(w[q], lgc);
+        idx[q] = atomicAdd(&S.lc[nxt][home[q]][sub], 1u);
       }
+#pragma unroll
+      for (int q = 0; q < kCmW; q++)
+        if (cl[q]) push_at(nxt, home[q], idx[q], w[q], (uint32_t)(o1[q] - o0[q]), o0[q]);
+#if GK_CM_TRACE == 2
+      asm volatile("mov.u32 %0, %%clock;" : "=r"(t_c) : "r"((unsigned)cc));
+      if (c == 0) {
+        const unsigned m = __activemask();
+        const unsigned da = __reduce_max_sync(m, t_a - xs), db = __reduce_max_sync(m, t_b - t_a),
+                       dc = __reduce_max_sync(m, t_c - t_b);
+        if ((threadIdx.x & 31u) == (unsigned)(__ffs(m) - 1)) {
+          atomicMax(&S.dbs[L & 1][0], da);
+          atomicMax(&S.dbs[L & 1][1], db);
+          atomicMax(&S.dbs[L & 1][2], dc);
+        }
+      }
+#endif
     };
     // Expansion: warp w walks region w % C (every wpr-th group of 32
-    // entries); a lane walks its own entry's list when it is short, the warp
-    // walks the long ones together.
-    const CmEnt* fe = &S.f[cur][reg * R];
+    // entries).  The short lists of a group are flattened into the warp's
+    // arc buffer (each lane scatters its own, at its prefix) and claimed
+    // kCmW arcs per lane at a time, so every lane carries the same load; the
+    // long lists are walked by the whole warp together.
+    CmArc* ab = S.arc[warp];
     for (int e0 = g0; e0 < nr; e0 += wpr * 32) {
       const int ei = e0 + (int)lane;
       CmEnt en{0u, 0u, 0};
-      if (ei < nr) en = fe[ei];
+      if (ei < nr) en = S.f[cur][eslot(ei)];
       const bool heavy = en.deg > kCmLight;
-      const uint32_t dl = heavy ? 0u : en.deg;
-      for (uint32_t d0 = 0; d0 < dl; d0 += kCmW) {
+      const int dl = heavy ? 0 : (int)en.deg;
+      int incl = dl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if ((int)lane >= o) incl += y;
+      }
+      const int excl = incl - dl, tot = __shfl_sync(kFull, incl, 31);
+      for (int b = 0; b < tot; b += 32 * kCmW) {
+        const int lo = max(0, b - excl), hi = min(dl, b + 32 * kCmW - excl);
+        for (int d = lo; d < hi; d++) ab[excl + d - b] = CmArc{en.v, 0u, en.off + d};
+        __syncwarp();
         uint32_t u[kCmW], w[kCmW];
         bool ok[kCmW];
 #pragma unroll
         for (int q = 0; q < kCmW; q++) {
-          ok[q] = d0 + q < dl;
-          u[q] = en.v;
-          w[q] = ok[q] ? ld_nb(P.out_nb + en.off + d0 + q) : 0u;
+          const int j = q * 32 + (int)lane;
+          ok[q] = b + j < tot;
+          u[q] = w[q] = 0u;
+          if (ok[q]) {
+            const CmArc a = ab[j];
+            u[q] = a.u;
+            w[q] = ld_nb(P.out_nb + a.pos);
+          }
         }
+        __syncwarp();
         claimw(u, w, ok);
       }
       for (unsigned hm = __ballot_sync(kFull, heavy); hm; hm &= hm - 1) {
@@ -390,6 +519,15 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
       }
     }
     CM_MARKD(2, (unsigned)sc);
+#if GK_CM_TRACE == 2
+    if (c == 0 && lane == 0) {
+      unsigned now;
+      asm volatile("mov.u32 %0, %%clock;" : "=r"(now) : "r"((unsigned)sc));
+      atomicMax(&S.dbg[L & 1][0], now - xs);
+      atomicAdd(&S.dbg[L & 1][1], now - xs);
+      atomicMax(&S.dbg[L & 1][2], now);
+    }
+#endif
     {  // this CTA's totals: warp reductions, shared atomics
       const unsigned wc = __reduce_add_sync(kFull, cc);
       const unsigned lo = __reduce_add_sync(kFull, (unsigned)(sc & 0xffff));
@@ -405,9 +543,8 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
   }
   // hand back: the current entries join the global queue after the overflow
   {
-    const CmEnt* fe = &S.f[L & 1u][reg * R];
     for (int i = g0 + (int)lane; i < nr; i += wpr * 32)
-      P.queue[base + atomicAdd(&P.ctrl->hand.qfill, 1ull)] = fe[i].v;
+      P.queue[base + atomicAdd(&P.ctrl->hand.qfill, 1ull)] = S.f[L & 1u][eslot(i)].v;
   }
   cl.sync();
   if (c == 0 && t == 0) {
@@ -438,7 +575,9 @@ cudaError_t cluster_configure(int device, int* cluster, int64_t* max_scout) {
   if ((e = cudaFuncSetAttribute(bfs_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
   cudaFuncSetAttribute(bfs_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaGetLastError();
-  for (int cs = 16; cs >= 8; cs /= 2) {
+  int cs_max = 16;
+  if (const char* e = getenv("GK_CM_CLUSTER")) cs_max = atoi(e) >= 16 ? 16 : atoi(e) >= 8 ? 8 : 4;  // A/B
+  for (int cs = cs_max; cs >= 4; cs /= 2) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -5,6 +5,7 @@
 // CPU path: without a device, compute entry points fail with
 // GK_ERR_NO_DEVICE.
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -332,11 +333,19 @@ cudaError_t run_handoffs(gk_graph* g, gk::BfsParams p, cudaStream_t s, gk::Hand 
       p.rs = h;
       e = gk::bfs_launch(p, g->launch, s);
     }
+    g->launches++;
     if (e != cudaSuccess) return e;
     if ((e = cudaMemcpyAsync(g->cm_peek, p.ctrl, gk::kCtrlPeek, cudaMemcpyDeviceToHost, s))) return e;
     if ((e = cudaStreamSynchronize(s))) return e;
     if (g->cm_peek->error) return cudaSuccess;
     h = g->cm_peek->hand;
+#ifdef GK_CM_DEBUG
+    {
+      static auto t00 = std::chrono::steady_clock::now();
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t00).count();
+      fprintf(stderr, "%.3f handoff: mode %lld nsteps %lld qs %lld qe %lld\n", ms, h.mode, h.nsteps, h.qs, h.qe);
+    }
+#endif
   }
   return cudaSuccess;
 }
@@ -599,6 +608,7 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   g->parent = t.parent;
   gk::BfsParams p = make_params(g, t, source, alpha, beta, strategy, want_depth);
   CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
+  g->launches++;
   CK(cudaEventRecord(g->ev1, s), "event record");
   gk::Ctrl& ctrl = g->last_ctrl;
   CK(cudaMemcpyAsync(&ctrl, t.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
@@ -693,6 +703,23 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
   }
   const bool own = use_own(g);
   cudaError_t e = cudaSuccess;
+  if (!g->batch_warm && count > 1) {
+    // Up to three trials' blocks are live at once here (a result is freed
+    // only after its copy); grow the pool to that once, so no trial pays
+    // for the pool's first mapping of the memory.
+    gk_trial tw[3];
+    TrialBlocks bw[3];
+    int k = 0;
+    for (; k < 3 && e == cudaSuccess; k++) e = trial_alloc(g, &tw[k], &bw[k], s, own);
+    for (int j = 0; j < k; j++) {
+      if (tw[j].parent) cudaFreeAsync(tw[j].parent, s);
+      if (bw[j].work) cudaFreeAsync(bw[j].work, s);
+      if (bw[j].book) cudaFreeAsync(bw[j].book, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(GK_ERR_CUDA, std::string("bfs batch: ") + cudaGetErrorString(e));
+    g->batch_warm = true;
+  }
   for (int32_t i = 0; i < count && e == cudaSuccess; i++) {
     gk_trial t;
     TrialBlocks tb;
@@ -703,9 +730,19 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     gk::BfsParams p = make_params(g, t, sources[i], alpha, beta, strategy, 0);
     p.cm_ok = g->cm_batch ? p.cm_ok : 0;
     if ((e = gk::bfs_launch(p, g->launch, s))) break;
+    g->launches++;
     if (p.cm_ok) {  // hand-offs are decided on the host: wait for the grid kernel
       if ((e = cudaMemcpyAsync(g->cm_peek, p.ctrl, gk::kCtrlPeek, cudaMemcpyDeviceToHost, s))) break;
+#ifdef GK_CM_DEBUG
+      static auto t00 = std::chrono::steady_clock::now();
+      const double ms0 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t00).count();
+#endif
       if ((e = cudaStreamSynchronize(s))) break;
+#ifdef GK_CM_DEBUG
+      const double ms1 = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t00).count();
+      fprintf(stderr, "trial %d: grid kernel enqueued %.3f synced %.3f mode %lld nsteps %lld\n", i, ms0, ms1,
+              g->cm_peek->hand.mode, g->cm_peek->hand.nsteps);
+#endif
       if (!g->cm_peek->error && g->cm_peek->hand.mode != 0 && (e = run_handoffs(g, p, s, g->cm_peek->hand))) break;
     }
     if ((e = cudaFreeAsync(tb.work, s))) break;
@@ -739,6 +776,7 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
 }
 
 const int32_t* gk_bfs_device_parent(const gk_graph* g) { return g ? g->parent : nullptr; }
+int64_t gk_bfs_launches(const gk_graph* g) { return g ? (int64_t)g->launches : 0; }
 int32_t* gk_bfs_device_depth(const gk_graph* g) { return g && g->depth_valid ? g->depth : nullptr; }
 
 gk_status gk_bfs_trace(const gk_graph* g, uint64_t* ts_ns, char* tags, int32_t cap, int32_t* count) {

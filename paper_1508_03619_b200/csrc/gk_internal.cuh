@@ -335,6 +335,7 @@ struct gk_graph {
   cudaStream_t stream = nullptr;
   cudaStream_t cstream = nullptr;  // D2H stream of gk_bfs_batch (created on first use)
   int* batch_err = nullptr;        // pinned: per-trial kernel error codes of gk_bfs_batch
+  bool batch_warm = false;         // the pool holds three trials' blocks (gk_bfs_batch)
   int32_t batch_err_cap = 0;
   std::vector<cudaEvent_t> batch_ev;  // gk_bfs_batch's events, grown on demand
   cudaEvent_t ev0 = nullptr;
@@ -342,6 +343,7 @@ struct gk_graph {
   gk::BfsLaunch launch;
   // cluster mode (gk_bfs_cluster.cu): CTAs per cluster (0: off), largest step it takes,
   // pinned copy of the control block's head (hand-off state + error) read between kernels
+  long long launches = 0;  // traversal kernels launched (gk_bfs_launches)
   int cm_cluster = 0;
   int64_t cm_max_scout = 0;
   bool cm_batch = false;  // gk_bfs_batch checks for hand-offs after every trial (sparse graphs)

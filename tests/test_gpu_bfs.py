@@ -156,6 +156,19 @@ def test_directed_bottom_up_uses_in_edges():
     assert seen_b
 
 
+def test_launch_count(devs):
+    """gk_bfs_launches counts one grid-kernel launch per traversal that
+    never leaves the grid kernel (kron: no chain of tiny levels)."""
+    dg = devs["kron16p"]
+    l0 = dg.launches()
+    srcs = [int(s) for s in dg.pick_sources(3, SEED)]
+    for s in srcs:
+        dg.bfs(s, parent=False)
+    assert dg.launches() - l0 == 3
+    dg.bfs_batch(srcs)
+    assert dg.launches() - l0 == 6
+
+
 def test_graph_untouched_and_repeatable(hosts, devs):
     # test_kernels_source.cc:69-85 + acceptance criterion 3 (determinism)
     g, dg = hosts["kron16p"], devs["kron16p"]
@@ -269,7 +282,9 @@ def test_cluster_mode_parity(chain_graphs, strategy):
         seen_k = False
         for s in O.pick_sources(g, 3, 5):
             s = int(s)
+            l0 = dg.launches()
             res = dg.bfs(s, strategy=strategy, depth=True, counts=True)
+            nl = dg.launches() - l0
             key = (name, s, strategy)
             assert (res.depth == O.bfs_depths(g, s)).all(), key
             assert O.verify_bfs(g, s, res.parent)[0], key
@@ -279,7 +294,9 @@ def test_cluster_mode_parity(chain_graphs, strategy):
             assert [x[2] for x in res.steps] == rp.result, key
             assert [x[3] for x in res.steps] == rp.edges_to_check, key
             assert res.reached == int((res.depth >= 0).sum()), key
-            seen_k |= any(x[4] == "K" for x in res.steps)
+            k = any(x[4] == "K" for x in res.steps)
+            assert nl >= (2 if k else 1), (key, nl)  # grid kernel + cluster kernel (+ resumptions)
+            seen_k |= k
         assert seen_k, name  # the cluster kernel ran
 
 
