@@ -228,7 +228,8 @@ class DeviceGraph:
                "gk_bfs")
         k = min(st.num_steps, max_steps)
         # (direction, frontier, result, edges_to_check, executed-as: '' or 'P' pushed
-        # bottom-up / 'U' pulled top-down / 'K' top-down in the cluster kernel --
+        # bottom-up / 'U' pulled top-down / 'K' top-down in the cluster kernel /
+        # 'S' the whole traversal in the single-cluster small-graph kernel --
         # same claimed set and counters)
         sl = [(chr(steps[i].dir), steps[i].frontier, steps[i].result, steps[i].edges_to_check,
                chr(steps[i].pad) if steps[i].pad else "") for i in range(k)]

@@ -1,0 +1,660 @@
+// gk_bfs_small.cu -- the whole traversal of a small graph inside ONE
+// thread-block cluster (config 1 regime: n <= 8192 x cluster CTAs, every
+// bitmap resident in shared memory).
+//
+// On a graph this small the grid kernel (bfs_persistent) pays a 296-CTA grid
+// barrier and several dependent L2 round trips per phase, 4-6 phases per
+// level: ~80 us per kron16 BFS for ~2 MB of traffic.  Here the cluster's CTAs
+// (16, or 8 if the device will not co-schedule 16) each hold a full copy of
+// the visited and frontier bitmaps in shared memory and own a slice of the
+// vertex ids (CTA c: bitmap words [c*Wc, (c+1)*Wc)).  One level is:
+//   top-down (bfs.hpp:68-91): the frontier is listed from the replicated
+//     front bitmap (every CTA lists it when it fits kSmCap entries and takes
+//     1/C of its edges; otherwise each CTA lists its own slice); an edge to a
+//     vertex unvisited in the local copy is claimed in the CTA's local next
+//     bitmap (shared-memory atomic) and the claimer stores the parent --
+//     racing claimers in different CTAs store valid parents, as on the CPU;
+//     cluster barrier; each CTA ORs the C next copies over its slice
+//     (DSMEM), keeps the unvisited bits, sums their degrees
+//     (max(deg,1) = -old of bfs.hpp:83, or deg for kTopDownRescan,
+//     bfs.hpp:161-167);
+//   bottom-up (bfs.hpp:47-66): each CTA scans its own pending vertices'
+//     in-lists in ascending order against the replicated front -- the first
+//     hit is the parent, exactly the reference's choice;
+//   then (both) cluster barrier, and every CTA gathers the C new slices over
+//     DSMEM into its front and visited copies and sums the C counter pairs,
+//     so every CTA takes the same alpha/beta decision (bfs.hpp:139-169).
+// The step log, counters and results are the grid kernel's; the launch is
+// one cudaLaunchKernelEx per trial (no memsets: the kernel initialises the
+// control block, the parent array and its bitmaps itself).
+#include <cooperative_groups.h>
+
+#include "gk_persistent.cuh"
+
+namespace gk {
+namespace {
+
+namespace cg = cooperative_groups;
+
+#ifndef GK_SM_BLOCK
+#define GK_SM_BLOCK 512  // kron16: 1024 threads -15%, 256 -5%
+#endif
+constexpr int kSmBlock = GK_SM_BLOCK;
+constexpr int kSmWarps = kSmBlock / 32;
+constexpr int kSmMaxW = 4096;  // bitmap words: n <= 2^17
+constexpr int kSmCap = 8192;   // list entries per CTA (>= one CTA's slice of ids)
+constexpr int kSmSlice = kSmCap / 32;  // owned bitmap words per CTA, at most
+constexpr int kSmWon = 2048;   // won-list entries per CTA (more: the next level lists from the bitmap)
+constexpr int kSmRounds = 4;
+#ifndef GK_SM_BUW
+#define GK_SM_BUW 4  // 512 threads x 4 in flight: 8 -10%, 16 -30% (kron16)
+#endif
+#ifndef GK_SM_TDW
+#define GK_SM_TDW 4
+#endif
+constexpr int kSmBuW = GK_SM_BUW;  // bottom-up: pending vertices per thread in flight
+constexpr int kSmTdW = GK_SM_TDW;  // top-down: edges per thread in flight   // bottom-up: 4-neighbour rounds per thread before the warp takes a list
+
+struct __align__(16) SmShared {
+  uint32_t vis[kSmMaxW];          // visited (replicated; starts as the dead set)
+  uint32_t front[kSmMaxW];        // current frontier (replicated)
+  uint32_t nxt[kSmMaxW];          // top-down: this CTA's claims (all ids)
+  uint32_t slice[3][kSmSlice];    // this CTA's slice of level L's new frontier in [L % 3]
+  uint32_t ids[kSmCap];           // listed vertices (frontier / pending)
+  uint32_t pre[kSmCap + 1];       // top-down: exclusive degree prefix; bottom-up: long list
+  uint32_t off[kSmCap];           // top-down: out_off of the listed vertex (m < 2^32)
+  uint4 wl[2][kSmWon];            // won lists by level parity: {vertex, out_off, out-degree, 0} of the
+                                  // vertices this CTA added to the frontier in a top-down level
+  unsigned long long cnt[3][4];   // level L in [L % 3]: {new vertices, degree total, a won list overflowed}
+  unsigned long long tot[4];      // cluster totals of the level just gathered
+  uint4 red4[2][kSmWarps];        // per-warp partial sums, two alternating slots
+  int wpre[17];                   // exclusive prefix of the C won-list lengths of the last level
+  unsigned nlong;
+  unsigned nwon;
+};
+
+// Block-wide exclusive scan / sums of 32-bit values with ONE barrier: warp
+// scans (shuffles) or REDUX sums, per-warp totals in smem slot rs (the two
+// slots alternate, so a slot is rewritten only after every thread passed
+// the barrier of the call in between), every thread sums the totals it needs.
+__device__ __forceinline__ unsigned sm_exscan(unsigned x, unsigned* total, SmShared& S, int& rs) {
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  unsigned incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, incl, o);
+    if ((int)lane >= o) incl += y;
+  }
+  uint4* r = S.red4[rs];
+  if (lane == 31) r[warp].x = incl;
+  rs ^= 1;
+  __syncthreads();
+  unsigned base = 0, tot = 0;
+#pragma unroll 8
+  for (int i = 0; i < kSmWarps; i++) {
+    const unsigned v = r[i].x;
+    base += (unsigned)i < warp ? v : 0u;
+    tot += v;
+  }
+  *total = tot;
+  return base + incl - x;
+}
+
+__device__ __forceinline__ uint3 sm_sum3(unsigned a, unsigned b, unsigned c, SmShared& S, int& rs) {
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  a = __reduce_add_sync(kFull, a);
+  b = __reduce_add_sync(kFull, b);
+  c = __reduce_add_sync(kFull, c);
+  uint4* r = S.red4[rs];
+  if (lane == 0) r[warp] = make_uint4(a, b, c, 0u);
+  rs ^= 1;
+  __syncthreads();
+  uint3 t = make_uint3(0u, 0u, 0u);
+#pragma unroll 8
+  for (int i = 0; i < kSmWarps; i++) {
+    const uint4 v = r[i];
+    t.x += v.x;
+    t.y += v.y;
+    t.z += v.z;
+  }
+  return t;
+}
+
+// List the set bits of words [wa, wb) of bm (complemented when kNot) into
+// S.ids in ascending id order; returns the count (uniform).
+template <bool kNot>
+__device__ int sm_list(SmShared& S, const uint32_t* bm, int wa, int wb, int& rs) {
+  const int nw = wb - wa;
+  const int q = (nw + kSmBlock - 1) / kSmBlock;
+  const int j0 = wa + (int)threadIdx.x * q, j1 = min(wb, j0 + q);
+  unsigned cnt = 0;
+  for (int j = j0; j < j1; j++) cnt += __popc(kNot ? ~bm[j] : bm[j]);
+  unsigned total;
+  int pos = (int)sm_exscan(cnt, &total, S, rs);
+  for (int j = j0; j < j1; j++) {
+    uint32_t w = kNot ? ~bm[j] : bm[j];
+    while (w) {
+      const int b = __ffs(w) - 1;
+      w &= w - 1;
+      S.ids[pos++] = (uint32_t)(j * 32 + b);
+    }
+  }
+  __syncthreads();
+  return (int)total;
+}
+
+// Gather the C new slices of level buffer p into front / visited, clear the
+// local claims, and read the C counter pairs (after the level's last cluster
+// barrier).  Leaves the cluster totals in S.tot.
+__device__ void sm_gather(SmShared& S, cg::cluster_group& cl, int C, int W, int Wc, int p) {
+  // 16-byte DSMEM loads (Wc is a multiple of 4; slice words past a CTA's
+  // range stay zero, so the words past W gathered here are zero too)
+  for (int j = 4 * (int)threadIdx.x; j < W; j += 4 * kSmBlock) {
+    const int k = j / Wc;
+    const uint4 w = *reinterpret_cast<const uint4*>(cl.map_shared_rank(&S.slice[p][0], k) + (j - k * Wc));
+    *reinterpret_cast<uint4*>(&S.front[j]) = w;
+    uint4 v = *reinterpret_cast<const uint4*>(&S.vis[j]);
+    v.x |= w.x;
+    v.y |= w.y;
+    v.z |= w.z;
+    v.w |= w.w;
+    *reinterpret_cast<uint4*>(&S.vis[j]) = v;
+    *reinterpret_cast<uint4*>(&S.nxt[j]) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (threadIdx.x < 32) {
+    unsigned long long a = 0, b = 0, f = 0;
+    if ((int)threadIdx.x < C) {
+      const unsigned long long* rc = cl.map_shared_rank(&S.cnt[p][0], (int)threadIdx.x);
+      a = rc[0];
+      b = rc[1];
+      f = rc[2];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_down_sync(kFull, a, o);
+      b += __shfl_down_sync(kFull, b, o);
+      f += __shfl_down_sync(kFull, f, o);
+    }
+    if (threadIdx.x == 0) {
+      S.tot[0] = a;
+      S.tot[1] = b;
+      S.tot[2] = f;
+    }
+    int nw = (int)threadIdx.x < C ? (int)cl.map_shared_rank(&S.cnt[p][0], (int)threadIdx.x)[3] : 0;
+    int incl = nw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if ((int)threadIdx.x >= o) incl += y;
+    }
+    if ((int)threadIdx.x <= C && threadIdx.x < 17) S.wpre[threadIdx.x] = incl - nw;
+  }
+  __syncthreads();
+}
+
+#ifndef GK_SM_TRACE
+#define GK_SM_TRACE 0  // diagnostics: CTA 0 logs sub-phase timestamps in the trace instead of one per level
+#endif
+#if GK_SM_TRACE
+#define SM_MARK(ch)                                      \
+  do {                                                   \
+    if (c == 0 && t == 0 && trace_i + 1 < kTraceCap) {   \
+      trace_i++;                                         \
+      P.ctrl->ts[trace_i] = clock64();                   \
+      P.ctrl->tag[trace_i] = (unsigned char)(ch);        \
+    }                                                    \
+  } while (0)
+#else
+#define SM_MARK(ch) \
+  do {              \
+  } while (0)
+#endif
+
+__device__ __forceinline__ bool sm_bit(const uint32_t* bm, uint32_t v) { return (bm[v >> 5] >> (v & 31u)) & 1u; }
+
+__device__ void sm_log(const BfsParams& P, int c, long long idx, int dir, long long frontier, long long result,
+                       long long etc) {
+  if (c == 0 && threadIdx.x == 0) {
+    if (idx < P.step_cap) {
+      gk_step st;
+      st.dir = dir;
+      st.pad = 'S';  // executed by the single-cluster kernel
+      st.frontier = frontier;
+      st.result = result;
+      st.edges_to_check = etc;
+      P.steps[idx] = st;
+    }
+    if (!GK_SM_TRACE && idx + 1 < kTraceCap) {
+      P.ctrl->ts[idx + 1] = globaltimer();
+      P.ctrl->tag[idx + 1] = (unsigned char)dir;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
+  extern __shared__ uint4 sm_raw[];
+  SmShared& S = *reinterpret_cast<SmShared*>(sm_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank(), C = (int)cl.num_blocks();
+  const int t = threadIdx.x;
+  const unsigned lane = t & 31u, warp = t >> 5;
+  const int W = (int)P.w32;
+  const int Wc = ((W + C - 1) / C + 3) & ~3;  // <= kSmSlice (checked by the host)
+  const int wlo = min(W, c * Wc), whi = min(W, wlo + Wc);
+  const uint32_t src = P.src;
+  const bool encode = P.strategy != GK_BFS_TOP_DOWN_RESCAN;
+  int rs = 0;  // reduction slot (sm_exscan / sm_sum3)
+#if GK_SM_TRACE
+  int trace_i = 0;
+  const unsigned long long t_entry = clock64();  // SM cycles in trace mode
+#endif
+
+  // ---- init (replaces bfs.hpp:126-138) ----
+  if (c == 0) {  // the control block: nothing of it survives from an earlier trial
+    uint4* z = reinterpret_cast<uint4*>(P.ctrl);
+    for (int i = t; i < (int)(kCtrlClear / 16); i += kSmBlock) z[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  {
+    const long long gt = (long long)c * kSmBlock + t, gn = (long long)C * kSmBlock;
+    for (long long i = gt; i < P.n; i += gn) P.parent[i] = -1;
+    if (P.want_depth)
+      for (long long i = gt; i < P.n; i += gn) P.depth[i] = -1;
+  }
+  for (int j = t; j < W; j += kSmBlock) {
+    S.vis[j] = __ldg(P.dead + j);  // never-reachable vertices and ids >= n start visited
+    S.front[j] = 0u;
+    S.nxt[j] = 0u;
+  }
+  for (int j = t; j < 3 * kSmSlice; j += kSmBlock) (&S.slice[0][0])[j] = 0u;
+  __syncthreads();
+  if (t == 0) {
+    S.vis[src >> 5] |= 1u << (src & 31u);
+    S.front[src >> 5] |= 1u << (src & 31u);
+  }
+  cl.sync();  // every -1 store is ordered before the source's entry
+  if (c == 0 && t == 0) {
+    P.ctrl->ts[0] = globaltimer();
+#if GK_SM_TRACE
+    P.ctrl->ts[0] = t_entry;
+#endif
+    P.ctrl->tag[0] = kTagInit;
+    P.parent[src] = (int32_t)src;
+    if (P.want_depth) P.depth[src] = 0;
+  }
+
+  SM_MARK('i');
+  long long etc = P.m;                                    // bfs.hpp:139
+  long long scout = P.out_off[src + 1] - P.out_off[src];  // bfs.hpp:140
+  long long fsz = 1, nsteps = 0;
+  int lvl = 0;
+  unsigned L = 0;  // levels done (parity of the slice / counter buffers)
+
+  bool lists = false;  // every CTA's won list holds its share of the current frontier (uniform)
+  while (fsz > 0) {  // bfs.hpp:142
+    if (P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha) {
+      long long awake = fsz, old_awake;  // bfs.hpp:146
+      do {                               // bfs.hpp:149-154
+        old_awake = awake;
+        const int q3 = (int)(L % 3u);
+        // ---- bottom-up over this CTA's pending vertices (slice[q3] is zero) ----
+        if (t == 0) S.nlong = 0u;
+        const int k = sm_list<true>(S, S.vis, wlo, whi, rs);  // (sm_list ends with a CTA barrier)
+        SM_MARK('p');
+        for (int base = t; base < k; base += kSmBuW * kSmBlock) {
+          uint32_t v[kSmBuW], b[kSmBuW], e[kSmBuW];
+          bool live[kSmBuW];
+#pragma unroll
+          for (int q = 0; q < kSmBuW; q++) {
+            const int i = base + q * kSmBlock;
+            live[q] = i < k;
+            v[q] = live[q] ? S.ids[i] : 0u;
+            b[q] = e[q] = 0u;
+            if (live[q]) {
+              b[q] = (uint32_t)P.in_off[v[q]];
+              e[q] = (uint32_t)P.in_off[v[q] + 1];
+            }
+          }
+#pragma unroll 1
+          for (int r = 0; r < kSmRounds; r++) {
+            uint32_t u[kSmBuW][4];
+#pragma unroll
+            for (int q = 0; q < kSmBuW; q++)
+#pragma unroll
+              for (int j = 0; j < 4; j++) u[q][j] = (live[q] && b[q] + j < e[q]) ? ld_nb(P.in_nb + b[q] + j) : kNoVertex;
+#pragma unroll
+            for (int q = 0; q < kSmBuW; q++) {
+              if (!live[q]) continue;
+              int hit = -1;
+#pragma unroll
+              for (int j = 3; j >= 0; j--)
+                if (u[q][j] != kNoVertex && sm_bit(S.front, u[q][j])) hit = j;
+              if (hit >= 0) {  // the first in-neighbour in the frontier (bfs.hpp:55-60)
+                const uint32_t par = hit == 0 ? u[q][0] : hit == 1 ? u[q][1] : hit == 2 ? u[q][2] : u[q][3];
+                P.parent[v[q]] = (int32_t)par;
+                if (P.want_depth) P.depth[v[q]] = lvl + 1;
+                atomicOr(&S.slice[q3][(v[q] >> 5) - wlo], 1u << (v[q] & 31u));
+                live[q] = false;
+              } else {
+                b[q] += 4;
+                if (b[q] >= e[q]) live[q] = false;  // whole list scanned: not reached at this level
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kSmBuW; q++)
+            if (live[q]) S.pre[atomicAdd(&S.nlong, 1u)] = v[q];  // resumes at in_off + 4 * kSmRounds
+        }
+        __syncthreads();
+        SM_MARK('q');
+        const int nl = (int)S.nlong;
+        for (int i = (int)warp; i < nl; i += kSmWarps) {  // long lists: a warp per vertex
+          const uint32_t v = S.pre[i];
+          const int64_t le = P.in_off[v + 1];
+          for (int64_t j = P.in_off[v] + 4 * kSmRounds; j < le; j += 32) {
+            const int64_t jj = j + lane;
+            uint32_t u = 0;
+            bool h = false;
+            if (jj < le) {
+              u = ld_nb(P.in_nb + jj);
+              h = sm_bit(S.front, u);
+            }
+            const unsigned bal = __ballot_sync(kFull, h);
+            if (bal) {
+              const uint32_t hu = __shfl_sync(kFull, u, __ffs(bal) - 1);
+              if (lane == 0) {
+                P.parent[v] = (int32_t)hu;
+                if (P.want_depth) P.depth[v] = lvl + 1;
+                atomicOr(&S.slice[q3][(v >> 5) - wlo], 1u << (v & 31u));
+              }
+              break;
+            }
+          }
+        }
+        __syncthreads();
+        unsigned mine = 0;
+        for (int j = t; j < whi - wlo; j += kSmBlock) {
+          mine += __popc(S.slice[q3][j]);
+          S.slice[(q3 + 1) % 3][j] = 0u;  // the next level's slice (last read two levels ago)
+        }
+        mine = sm_sum3(mine, 0u, 0u, S, rs).x;
+        if (t == 0) {
+          S.cnt[q3][0] = (unsigned long long)mine;
+          S.cnt[q3][1] = 0ull;
+          S.cnt[q3][2] = 1ull;  // no won lists after a bottom-up step
+          S.cnt[q3][3] = 0ull;
+        }
+        SM_MARK('r');
+        cl.sync();
+        SM_MARK('s');
+        sm_gather(S, cl, C, W, Wc, q3);
+        SM_MARK('t');
+        L++;
+        awake = (long long)S.tot[0];
+        sm_log(P, c, nsteps++, 'B', old_awake, awake, etc);
+        lvl++;
+      } while (awake >= old_awake || awake > P.n / P.beta);
+      fsz = awake;
+      scout = 1;  // bfs.hpp:156
+      lists = false;
+    } else {
+      etc -= scout;  // bfs.hpp:158
+      const int q3 = (int)(L % 3u), wp = (int)(L & 1u);
+      // Small frontiers (<= kSmWon vertices): every CTA lists the whole
+      // frontier and takes 1/C of its edges; claims go straight to the
+      // target's owner over DSMEM (one cluster barrier per level).  Larger
+      // ones: each CTA expands its own slice, claims in a local bitmap, and
+      // the owners merge the C copies (two barriers, no per-claim traffic).
+      const bool fewer = fsz <= kSmWon;  // uniform: fsz is a cluster total
+      int k;
+      if (fewer && lists) {  // the frontier = the C won lists of the last level (offsets, degrees known)
+        const int rp = wp ^ 1;
+        k = (int)fsz;
+        for (int i = t; i < k; i += kSmBlock) {
+          int r = 0;
+          while (r + 1 < C && S.wpre[r + 1] <= i) r++;
+          const int j = i - S.wpre[r];
+          const uint4 x = cl.map_shared_rank(&S.wl[rp][0], r)[j];
+          S.ids[i] = x.x;
+          S.off[i] = x.y;
+          S.pre[i] = x.z;
+        }
+      } else {  // from the replicated front: all of it, or this CTA's slice
+        k = fewer ? sm_list<false>(S, S.front, 0, W, rs) : sm_list<false>(S, S.front, wlo, whi, rs);
+        for (int i = t; i < k; i += kSmBlock) {
+          const uint32_t v = S.ids[i];
+          const int64_t o0 = P.out_off[v], o1 = P.out_off[v + 1];
+          S.off[i] = (uint32_t)o0;
+          S.pre[i] = (uint32_t)(o1 - o0);
+        }
+      }
+      SM_MARK('a');
+      __syncthreads();
+      if (t == 0) S.nwon = 0u;  // (ordered before the claims by the prefix's barriers)
+      long long E;
+      {  // exclusive prefix of the degrees, 8 consecutive entries per thread
+        constexpr int kPer = kSmCap / kSmBlock;
+        const int i0 = t * kPer;
+        uint32_t d[kPer];
+        unsigned sum = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; q++) {
+          d[q] = i0 + q < k ? S.pre[i0 + q] : 0u;
+          sum += d[q];
+        }
+        unsigned tot;
+        unsigned x = sm_exscan(sum, &tot, S, rs);
+#pragma unroll
+        for (int q = 0; q < kPer; q++) {
+          if (i0 + q < k) S.pre[i0 + q] = (uint32_t)x;
+          x += d[q];
+        }
+        if (t == 0) S.pre[k] = (uint32_t)tot;
+        E = tot;
+      }
+      __syncthreads();
+      SM_MARK('b');
+      // ---- claims (bfs.hpp:77-84) ----
+      const long long e0 = fewer ? E * c / C : 0, e1 = fewer ? E * (c + 1) / C : E;
+      long long cc = 0, sc = 0;
+      bool ovf = false;
+      for (long long eb = e0 + t; eb < e1; eb += kSmTdW * kSmBlock) {
+        uint32_t u[kSmTdW], w[kSmTdW];
+        bool ok[kSmTdW];
+#pragma unroll
+        for (int q = 0; q < kSmTdW; q++) {
+          const long long e = eb + (long long)q * kSmBlock;
+          ok[q] = e < e1;
+          u[q] = 0u;
+          w[q] = 0u;
+          if (ok[q]) {
+            int lo = 0, hi = k;  // last entry with pre[i] <= e (its range holds e)
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if ((long long)S.pre[mid] <= e) lo = mid;
+              else hi = mid;
+            }
+            u[q] = S.ids[lo];
+            w[q] = ld_nb(P.out_nb + (S.off[lo] + (uint32_t)(e - S.pre[lo])));
+          }
+        }
+        // first attempt on this target from this CTA (local claim bitmap)
+#pragma unroll
+        for (int q = 0; q < kSmTdW; q++) {
+          if (ok[q] && !sm_bit(S.vis, w[q]) && !sm_bit(S.nxt, w[q])) {
+            const uint32_t bit = 1u << (w[q] & 31u);
+            ok[q] = !(atomicOr(&S.nxt[w[q] >> 5], bit) & bit);
+          } else {
+            ok[q] = false;
+          }
+        }
+        if (!fewer) {  // large frontier: the local claimer stores a (valid) parent; owners merge later
+#pragma unroll
+          for (int q = 0; q < kSmTdW; q++)
+            if (ok[q]) P.parent[w[q]] = (int32_t)u[q];
+          continue;
+        }
+        // small frontier: the owner's slice decides the one winner, which
+        // stores the parent, keeps the degree (read with the claim) and
+        // lists the vertex for the next level
+        int64_t o0[kSmTdW], o1[kSmTdW];
+        uint32_t old[kSmTdW];
+#pragma unroll
+        for (int q = 0; q < kSmTdW; q++) {
+          o0[q] = o1[q] = 0;
+          old[q] = ~0u;
+          if (ok[q]) {
+            const uint32_t ww = w[q] >> 5;
+            const int home = (int)(ww / (uint32_t)Wc);
+            o0[q] = P.out_off[w[q]];
+            o1[q] = P.out_off[w[q] + 1];
+            old[q] = atomicOr(cl.map_shared_rank(&S.slice[q3][0], home) + (ww - (uint32_t)home * (uint32_t)Wc),
+                              1u << (w[q] & 31u));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kSmTdW; q++) {
+          if (!ok[q] || ((old[q] >> (w[q] & 31u)) & 1u)) continue;
+          P.parent[w[q]] = (int32_t)u[q];
+          if (P.want_depth) P.depth[w[q]] = lvl + 1;
+          const long long dg = o1[q] - o0[q];
+          sc += encode ? (dg ? dg : 1) : dg;  // -old of bfs.hpp:83 / the rescan pass of bfs.hpp:161-167
+          cc++;
+          const unsigned i = atomicAdd(&S.nwon, 1u);
+          if (i < (unsigned)kSmWon) {
+            S.wl[wp][i] = make_uint4(w[q], (uint32_t)o0[q], (uint32_t)dg, 0u);
+          } else {
+            ovf = true;
+          }
+        }
+      }
+      SM_MARK('c');
+      if (!fewer) {
+        cl.sync();  // every CTA's attempts are in its claim bitmap
+        SM_MARK('d');
+        // merge this CTA's slice of the C claim bitmaps (all C loads in flight)
+        for (int j = wlo + 4 * t; j < whi; j += 4 * kSmBlock) {  // 16-byte DSMEM loads, C in flight
+          uint4 x = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 1
+          for (int r0 = 0; r0 < C; r0 += 8) {
+            uint4 y[8];
+#pragma unroll
+            for (int r = 0; r < 8; r++)
+              y[r] = r0 + r < C ? *reinterpret_cast<const uint4*>(cl.map_shared_rank(&S.nxt[0], r0 + r) + j)
+                                : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int r = 0; r < 8; r++) {
+              x.x |= y[r].x;
+              x.y |= y[r].y;
+              x.z |= y[r].z;
+              x.w |= y[r].w;
+            }
+          }
+          const uint4 v = *reinterpret_cast<const uint4*>(&S.vis[j]);
+          *reinterpret_cast<uint4*>(&S.slice[q3][j - wlo]) =
+              make_uint4(x.x & ~v.x, x.y & ~v.y, x.z & ~v.z, x.w & ~v.w);
+        }
+        __syncthreads();
+        SM_MARK('e');
+        const int kn = sm_list<false>(S, S.slice[q3], 0, whi - wlo, rs);  // ids relative to wlo * 32
+        for (int i = t; i < kn; i += kSmBlock) {
+          const uint32_t v = S.ids[i] + (uint32_t)wlo * 32u;
+          const int64_t o0 = P.out_off[v], o1 = P.out_off[v + 1];
+          const long long dg = o1 - o0;
+          sc += encode ? (dg ? dg : 1) : dg;
+          if (P.want_depth) P.depth[v] = lvl + 1;
+          if (i < kSmWon) {  // this CTA's share of the next frontier
+            S.wl[wp][i] = make_uint4(v, (uint32_t)o0, (uint32_t)dg, 0u);
+          }
+        }
+        cc = kn;
+        ovf = kn > kSmWon;
+        if (t == 0) S.nwon = (unsigned)kn;
+      }
+      for (int j = t; j < whi - wlo; j += kSmBlock) S.slice[(q3 + 1) % 3][j] = 0u;
+      const uint3 sums = sm_sum3(fewer ? (unsigned)cc : 0u, (unsigned)sc, ovf ? 1u : 0u, S, rs);
+      if (fewer) cc = sums.x;
+      sc = sums.y;
+      const unsigned ovf_any = sums.z;
+      if (t == 0) {
+        S.cnt[q3][0] = (unsigned long long)cc;
+        S.cnt[q3][1] = (unsigned long long)sc;
+        S.cnt[q3][2] = ovf_any ? 1ull : 0ull;
+        S.cnt[q3][3] = (unsigned long long)min(S.nwon, (unsigned)kSmWon);
+      }
+      SM_MARK('f');
+      cl.sync();  // every claim has landed in its owner's slice
+      SM_MARK('g');
+      sm_gather(S, cl, C, W, Wc, q3);
+      SM_MARK('h');
+      L++;
+      const long long fsize = fsz;
+      fsz = (long long)S.tot[0];
+      scout = (long long)S.tot[1];
+      lists = S.tot[2] == 0;
+      sm_log(P, c, nsteps++, 'T', fsize, scout, etc);
+      lvl++;
+    }
+  }
+  if (c == 0 && t == 0) P.ctrl->num_steps = nsteps;
+  // bfs.hpp:171-175's final sweep: unreached slots were written -1 at init.
+  // No CTA may exit while a peer can still read its shared memory.
+  cl.sync();
+}
+
+}  // namespace
+
+// Cluster size for graphs with n <= 8192 x cluster (0: the small-graph
+// kernel is not used for this graph / device).  m < 2^32 keeps offsets in
+// 32 bits; the bound 2^25 keeps the regime where one cluster beats the grid.
+cudaError_t small_configure(int device, int64_t n, int64_t m, int* cluster) {
+  *cluster = 0;
+  if (n < 1 || m > (int64_t(1) << 25) || n > (int64_t)kSmMaxW * 32) return cudaSuccess;
+  cudaError_t e;
+  const size_t smem = sizeof(SmShared);
+  if ((e = cudaFuncSetAttribute(bfs_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+  cudaFuncSetAttribute(bfs_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaGetLastError();
+  const int64_t w = (n + 31) / 32;
+  int cs_max = 16;
+  if (const char* e = getenv("GK_SM_CLUSTER")) cs_max = atoi(e) >= 16 ? 16 : 8;  // A/B
+  for (int cs = cs_max; cs >= 8; cs /= 2) {
+    if ((((w + cs - 1) / cs + 3) & ~int64_t(3)) > kSmSlice) break;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kSmBlock);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, (void*)bfs_small, &cfg) == cudaSuccess && nc >= 1) {
+      *cluster = cs;
+      return cudaSuccess;
+    }
+    cudaGetLastError();
+  }
+  (void)device;
+  return cudaSuccess;
+}
+
+cudaError_t small_launch(const BfsParams& p, int cluster, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(cluster);
+  cfg.blockDim = dim3(kSmBlock);
+  cfg.dynamicSmemBytes = sizeof(SmShared);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, bfs_small, p);
+}
+
+}  // namespace gk

@@ -110,6 +110,9 @@ gk_status setup_graph(gk_graph* g, bool sorted) {
     CK(cudaHostAlloc(&g->cm_peek, sizeof(gk::Ctrl), cudaHostAllocDefault), "cudaHostAlloc");
     g->cm_batch = g->m <= 8 * g->n;
   }
+  // Small graphs (n <= 8192 x cluster CTAs): one cluster runs the whole
+  // traversal with its bitmaps in shared memory (gk_bfs_small.cu).
+  CK(gk::small_configure(g->device, n, g->m, &g->small_cluster), "configure small-graph kernel");
   g->canary = getenv("GK_CANARY") && atoi(getenv("GK_CANARY")) != 0;
   CK(cudaMalloc(&g->dead, bitmap_bytes(n)), "alloc dead-vertex bitmap");
   CK(gk::dead_bitmap(g->in_off, n, g->dead, &g->live, g->stream), "dead-vertex bitmap");
@@ -181,7 +184,10 @@ struct Carver {
   }
 };
 
-cudaError_t trial_alloc(gk_graph* g, gk_trial* t, TrialBlocks* tb, cudaStream_t s, bool own) {
+void carve_work(gk_graph* g, gk_trial* t, TrialBlocks* tb, size_t cz, size_t wb, size_t sz_q, size_t sz_ch,
+                size_t sz_ol, size_t sz_os, bool own);
+
+cudaError_t trial_alloc(gk_graph* g, gk_trial* t, TrialBlocks* tb, cudaStream_t s, bool own, bool small = false) {
   const size_t cz = g->canary ? kCanaryBytes : 0;
   const size_t wb = bitmap_bytes(g->n);
   const size_t sz_par = up(sizeof(int32_t) * std::max<int64_t>(g->n, 4) + 16);
@@ -190,10 +196,31 @@ cudaError_t trial_alloc(gk_graph* g, gk_trial* t, TrialBlocks* tb, cudaStream_t 
   const size_t sz_ctrl = up(sizeof(gk::Ctrl)), sz_steps = up(sizeof(gk_step) * g->step_cap);
   const size_t work = 3 * (wb + cz) + sz_q + sz_ch + sz_ol + sz_os + (own ? 4 : 2) * cz;
   cudaError_t e;
-  if ((e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&t->parent), sz_par + cz, g->pool, s))) return e;
-  if ((e = cudaMallocFromPoolAsync(&tb->work, work, g->pool, s))) return e;
-  if ((e = cudaMallocFromPoolAsync(&tb->book, sz_ctrl + sz_steps + 2 * cz, g->pool, s))) return e;
+  // The small-graph kernel needs no device scratch (its bitmaps and lists
+  // live in shared memory): ONE pool block holds the result and the
+  // bookkeeping, which then lives as long as the result.
+  const size_t sz_book = sz_ctrl + sz_steps + 2 * cz;
+  if ((e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&t->parent), sz_par + cz + (small ? sz_book : 0), g->pool,
+                                   s)))
+    return e;
+  if (small) tb->book = nullptr;
+  else if ((e = cudaMallocFromPoolAsync(&tb->book, sz_book, g->pool, s))) return e;
   if (cz) tb->canaries.emplace_back(reinterpret_cast<char*>(t->parent) + sz_par, "parent");
+  Carver b{small ? reinterpret_cast<char*>(t->parent) + sz_par + cz : static_cast<char*>(tb->book), 0, cz, tb};
+  t->ctrl = reinterpret_cast<gk::Ctrl*>(b.take(sz_ctrl, "ctrl"));
+  t->steps = reinterpret_cast<gk_step*>(b.take(sz_steps, "steps"));
+  // the small-graph kernel keeps its bitmaps and lists in shared memory
+  if (!small) {
+    if ((e = cudaMallocFromPoolAsync(&tb->work, work, g->pool, s))) return e;
+    carve_work(g, t, tb, cz, wb, sz_q, sz_ch, sz_ol, sz_os, own);
+  }
+  for (auto& c : tb->canaries)
+    if ((e = cudaMemsetAsync(c.first, kCanaryByte, cz, s))) return e;
+  return cudaSuccess;
+}
+
+void carve_work(gk_graph* g, gk_trial* t, TrialBlocks* tb, size_t cz, size_t wb, size_t sz_q, size_t sz_ch,
+                size_t sz_ol, size_t sz_os, bool own) {
   Carver w{static_cast<char*>(tb->work), 0, cz, tb};
   t->bits = reinterpret_cast<uint32_t*>(w.take(wb, "visited"));
   w.take(wb, "bm0");
@@ -203,12 +230,6 @@ cudaError_t trial_alloc(gk_graph* g, gk_trial* t, TrialBlocks* tb, cudaStream_t 
   t->chunks = reinterpret_cast<gk::Chunk*>(w.take(sz_ch, "chunks"));
   t->own_list = own ? reinterpret_cast<gk::OwnEnt*>(w.take(sz_ol, "own_list")) : nullptr;
   t->own_stage = own ? reinterpret_cast<uint2*>(w.take(sz_os, "own_stage")) : nullptr;
-  Carver b{static_cast<char*>(tb->book), 0, cz, tb};
-  t->ctrl = reinterpret_cast<gk::Ctrl*>(b.take(sz_ctrl, "ctrl"));
-  t->steps = reinterpret_cast<gk_step*>(b.take(sz_steps, "steps"));
-  for (auto& c : tb->canaries)
-    if ((e = cudaMemsetAsync(c.first, kCanaryByte, cz, s))) return e;
-  return cudaSuccess;
 }
 
 // GK_CANARY: every guard zone still holds its fill byte (call after the
@@ -223,6 +244,30 @@ gk_status trial_check_canaries(gk_graph* g, const TrialBlocks& tb, cudaStream_t 
                                           std::to_string(bad) + " bytes)");
   }
   return GK_OK;
+}
+
+// The trial's buffers in the kernel parameters (after trial_alloc).
+void set_trial_ptrs(const gk_graph* g, const gk_trial& t, gk::BfsParams& p) {
+  p.parent = t.parent;
+  const size_t ww = t.bits_stride;
+  p.visited = t.bits;
+  p.bm0 = t.bits ? t.bits + ww : nullptr;
+  p.bm1 = t.bits ? t.bits + 2 * ww : nullptr;
+  p.queue = t.queue;
+  p.chunks = t.chunks;
+  p.ctrl = t.ctrl;
+  p.steps = t.steps;
+  if (t.own_list && !p.front_in_smem) {
+    p.own_list = t.own_list;
+    p.own_cap = g->own_cap;
+    p.own_stage = t.own_stage;
+    p.own_r = g->own_r;
+    p.own_span_w = (int32_t)g->own_span_w;
+    p.own_win_log = g->own_win_log;
+    p.own_dmin = g->own_dmin;
+  } else {
+    p.own_list = nullptr;
+  }
 }
 
 // Kernel parameters of one traversal on g (tuning knobs read from the environment).
@@ -242,23 +287,10 @@ gk::BfsParams make_params(gk_graph* g, const gk_trial& t, uint32_t source, int64
   p.beta = beta;
   p.want_depth = want_depth;
   p.front_in_smem = ((size_t)p.w32 * 4 <= g->launch.smem_front_max) ? 1 : 0;
-  p.parent = t.parent;
   p.depth = g->depth;
-  const size_t ww = t.bits_stride;
-  p.visited = t.bits;
-  p.bm0 = t.bits + ww;
-  p.bm1 = t.bits + 2 * ww;
   p.dead = g->dead;
   p.live = g->live;
-  if (t.own_list && !p.front_in_smem) {
-    p.own_list = t.own_list;
-    p.own_cap = g->own_cap;
-    p.own_stage = t.own_stage;
-    p.own_r = g->own_r;
-    p.own_span_w = (int32_t)g->own_span_w;
-    p.own_win_log = g->own_win_log;
-    p.own_dmin = g->own_dmin;
-  }
+  set_trial_ptrs(g, t, p);
   // Large top-down steps additionally clear and fill the n/8-byte next
   // bitmap and sum degrees in a separate pass; worth it above ~n/16 edges.
   p.bitmap_td_min = std::max<int64_t>(4096, g->n / 16);
@@ -281,11 +313,7 @@ gk::BfsParams make_params(gk_graph* g, const gk_trial& t, uint32_t source, int64
   // kTopDownRescan re-reads every new frontier's queue (bfs.hpp:161-167):
   // its steps keep the queue path (large steps leave the frontier a bitmap)
   if (strategy == GK_BFS_TOP_DOWN_RESCAN) p.bitmap_td_min = INT64_MAX;
-  p.queue = t.queue;
-  p.chunks = t.chunks;
   p.chunk_cap = g->chunk_cap;
-  p.ctrl = t.ctrl;
-  p.steps = t.steps;
   p.step_cap = g->step_cap;
   p.timeout_ns = 20ull * 1000 * 1000 * 1000;
   if (const char* w = getenv("GK_WATCHDOG_MS")) p.timeout_ns = strtoull(w, nullptr, 10) * 1000000ull;
@@ -295,6 +323,10 @@ gk::BfsParams make_params(gk_graph* g, const gk_trial& t, uint32_t source, int64
   p.cm_max_scout = g->cm_max_scout;
   return p;
 }
+
+// The single-cluster kernel for this graph (GK_NO_SMALL=1: the grid kernel
+// instead -- tests run both on the same small graphs).
+bool use_small(const gk_graph* g) { return g->small_cluster > 0 && !getenv("GK_NO_SMALL"); }
 
 bool use_own(const gk_graph* g) {
   return g->own_r > 0 && (size_t)((g->n + 31) / 32) * 4 > g->launch.smem_front_max;
@@ -603,11 +635,16 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   // initialisation, the traversal, the release of the scratch.
   gk_trial t;
   TrialBlocks tb;
-  CK(cudaEventRecord(g->ev0, s), "event record");
-  CK(trial_alloc(g, &t, &tb, s, use_own(g)), "allocate trial scratch");
-  g->parent = t.parent;
+  const bool small = use_small(g);
+  // kernel arguments (host work, the environment's tuning switches) ahead of
+  // the trial; the trial's own buffers are filled in after its allocation
   gk::BfsParams p = make_params(g, t, source, alpha, beta, strategy, want_depth);
-  CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
+  CK(cudaEventRecord(g->ev0, s), "event record");
+  CK(trial_alloc(g, &t, &tb, s, !small && use_own(g), small), "allocate trial scratch");
+  g->parent = t.parent;
+  set_trial_ptrs(g, t, p);
+  if (small) CK(gk::small_launch(p, g->small_cluster, s), "launch small-graph bfs kernel");
+  else CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
   g->launches++;
   CK(cudaEventRecord(g->ev1, s), "event record");
   gk::Ctrl& ctrl = g->last_ctrl;
@@ -624,9 +661,9 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
     if (cst != GK_OK) return cst;
   }
   // the scratch returns to the pool (stream-ordered bookkeeping, no device work)
-  CK(cudaFreeAsync(tb.work, s), "free trial scratch");
+  if (tb.work) CK(cudaFreeAsync(tb.work, s), "free trial scratch");
   if (ctrl.error) {
-    cudaFreeAsync(tb.book, s);
+    if (tb.book) cudaFreeAsync(tb.book, s);
     return kernel_error(ctrl, "bfs");
   }
   g->last_valid = 1;
@@ -651,7 +688,7 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
       stats->component_edges = (int64_t)(g->directed ? two[1] : two[1] / 2);
     }
   }
-  CK(cudaFreeAsync(tb.book, s), "free trial bookkeeping");
+  if (tb.book) CK(cudaFreeAsync(tb.book, s), "free trial bookkeeping");
   if (parent_out && g->n)
     CK(cudaMemcpyAsync(parent_out, g->parent, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, s), "D2H parent");
   if (depth_out && g->n)
@@ -701,7 +738,8 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     CK(cudaFreeAsync(g->parent, s), "free previous result");
     g->parent = nullptr;
   }
-  const bool own = use_own(g);
+  const bool small = use_small(g);
+  const bool own = !small && use_own(g);
   cudaError_t e = cudaSuccess;
   if (!g->batch_warm && count > 1) {
     // Up to three trials' blocks are live at once here (a result is freed
@@ -710,7 +748,7 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     gk_trial tw[3];
     TrialBlocks bw[3];
     int k = 0;
-    for (; k < 3 && e == cudaSuccess; k++) e = trial_alloc(g, &tw[k], &bw[k], s, own);
+    for (; k < 3 && e == cudaSuccess; k++) e = trial_alloc(g, &tw[k], &bw[k], s, own, small);
     for (int j = 0; j < k; j++) {
       if (tw[j].parent) cudaFreeAsync(tw[j].parent, s);
       if (bw[j].work) cudaFreeAsync(bw[j].work, s);
@@ -726,10 +764,10 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     // the copy of trial i-2 has returned its result to the pool
     if (i >= 2 && (e = cudaStreamWaitEvent(s, ev[3 * (i - 2) + 2], 0))) break;
     if ((e = cudaEventRecord(ev[3 * i], s))) break;
-    if ((e = trial_alloc(g, &t, &tb, s, own))) break;
+    if ((e = trial_alloc(g, &t, &tb, s, own, small))) break;
     gk::BfsParams p = make_params(g, t, sources[i], alpha, beta, strategy, 0);
-    p.cm_ok = g->cm_batch ? p.cm_ok : 0;
-    if ((e = gk::bfs_launch(p, g->launch, s))) break;
+    p.cm_ok = g->cm_batch && !small ? p.cm_ok : 0;
+    if ((e = small ? gk::small_launch(p, g->small_cluster, s) : gk::bfs_launch(p, g->launch, s))) break;
     g->launches++;
     if (p.cm_ok) {  // hand-offs are decided on the host: wait for the grid kernel
       if ((e = cudaMemcpyAsync(g->cm_peek, p.ctrl, gk::kCtrlPeek, cudaMemcpyDeviceToHost, s))) break;
@@ -745,10 +783,10 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
 #endif
       if (!g->cm_peek->error && g->cm_peek->hand.mode != 0 && (e = run_handoffs(g, p, s, g->cm_peek->hand))) break;
     }
-    if ((e = cudaFreeAsync(tb.work, s))) break;
+    if (tb.work && (e = cudaFreeAsync(tb.work, s))) break;
     if ((e = cudaEventRecord(ev[3 * i + 1], s))) break;
     if ((e = cudaMemcpyAsync(errs + i, &t.ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;
-    if ((e = cudaFreeAsync(tb.book, s))) break;
+    if (tb.book && (e = cudaFreeAsync(tb.book, s))) break;
     if ((e = cudaStreamWaitEvent(cs, ev[3 * i + 1], 0))) break;
     if (parents_out && parents_out[i] &&
         (e = cudaMemcpyAsync(parents_out[i], t.parent, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, cs)))

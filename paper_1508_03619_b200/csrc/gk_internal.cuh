@@ -244,6 +244,9 @@ cudaError_t shard_configure(int device, BfsLaunch* cfg);
 // the largest step it takes.
 cudaError_t cluster_configure(int device, int* cluster, int64_t* max_scout);
 cudaError_t cluster_launch(const BfsParams& p, const Hand& h, int cluster, cudaStream_t s);
+// Small graphs: the whole traversal inside one thread-block cluster (gk_bfs_small.cu).
+cudaError_t small_configure(int device, int64_t n, int64_t m, int* cluster);
+cudaError_t small_launch(const BfsParams& p, int cluster, cudaStream_t s);
 cudaError_t shard_launch(const BfsParams& p, const ShardTab& t, int grid, cudaStream_t s);
 
 // One source of Brandes' forward + backward pass (cooperative launch).
@@ -345,6 +348,7 @@ struct gk_graph {
   // pinned copy of the control block's head (hand-off state + error) read between kernels
   long long launches = 0;  // traversal kernels launched (gk_bfs_launches)
   int cm_cluster = 0;
+  int small_cluster = 0;  // gk_bfs_small.cu: CTAs of the single-cluster kernel for this graph (0: not used)
   int64_t cm_max_scout = 0;
   bool cm_batch = false;  // gk_bfs_batch checks for hand-offs after every trial (sparse graphs)
   gk::Ctrl* cm_peek = nullptr;

@@ -37,6 +37,23 @@ def _has_gpu():
 HAS_GPU = _has_gpu()
 
 
+@pytest.fixture(params=["small", "grid"])
+def both_kernels(request, monkeypatch):
+    """Run the test through the single-cluster kernel (graphs with n <= 2^17,
+    gk_bfs_small.cu) and again through the grid kernel (GK_NO_SMALL=1)."""
+    if request.param == "grid":
+        monkeypatch.setenv("GK_NO_SMALL", "1")
+    else:
+        monkeypatch.delenv("GK_NO_SMALL", raising=False)
+    return request.param
+
+
+@pytest.fixture
+def grid_kernel(monkeypatch):
+    """Tests of the grid kernel's own phases on small graphs."""
+    monkeypatch.setenv("GK_NO_SMALL", "1")
+
+
 def pytest_collection_modifyitems(config, items):
     if HAS_GPU:
         return

@@ -79,7 +79,7 @@ def test_pick_sources(golden, devs):
         assert devs[name].pick_sources(64, SEED).tolist() == ent["sources"], name
 
 
-def test_bfs_parity_against_reference(golden, hosts, devs):
+def test_bfs_parity_against_reference(golden, hosts, devs, both_kernels):
     """Every golden run: depths, parents, schedule and counters."""
     for name, ent in golden["graphs"].items():
         g, dg = hosts[name], devs[name]
@@ -102,7 +102,7 @@ def test_bfs_parity_against_reference(golden, hosts, devs):
                     assert (res.parent[sel] == rp.parent[sel]).all(), (key, "bottom-up parent", i)
 
 
-def test_known_answers():
+def test_known_answers(both_kernels):
     # test_kernels_source.cc:13-29
     path = DeviceGraph.from_csr(O.build_csr(3, np.array([0, 1, 1, 2], np.uint32)))
     assert Bfs(path, 0).tolist() == [0, 0, 1]
@@ -116,7 +116,7 @@ def test_known_answers():
         Bfs(path, 0, BfsOptions(beta=-1))
 
 
-def test_single_vertex_and_edgeless():
+def test_single_vertex_and_edgeless(both_kernels):
     one = DeviceGraph.upload(1, np.zeros(2, np.int64), np.zeros(0, np.uint32))
     assert Bfs(one, 0).tolist() == [0]
     none = DeviceGraph.upload(5, np.zeros(6, np.int64), np.zeros(0, np.uint32))
@@ -125,7 +125,7 @@ def test_single_vertex_and_edgeless():
         none.pick_sources(1)
 
 
-def test_strategies_agree(hosts, devs):
+def test_strategies_agree(hosts, devs, both_kernels):
     # test_kernels_source.cc:42-53 on a larger graph
     g, dg = hosts["kron16p"], devs["kron16p"]
     for s in O.pick_sources(g, 6, 3):
@@ -138,7 +138,7 @@ def test_strategies_agree(hosts, devs):
             assert res.schedule == rp.dirs and [x[2] for x in res.steps] == rp.result
 
 
-def test_directed_bottom_up_uses_in_edges():
+def test_directed_bottom_up_uses_in_edges(both_kernels):
     # test_kernels_source.cc:55-67 (alpha = beta = 1)
     e = O.gen_kron(12, 16, 11)
     g = O.build_csr(1 << 12, e, symmetrize=False, directed=True)
@@ -156,9 +156,10 @@ def test_directed_bottom_up_uses_in_edges():
     assert seen_b
 
 
-def test_launch_count(devs):
-    """gk_bfs_launches counts one grid-kernel launch per traversal that
-    never leaves the grid kernel (kron: no chain of tiny levels)."""
+def test_launch_count(devs, both_kernels):
+    """gk_bfs_launches counts one launch per traversal that never leaves its
+    kernel (kron: no chain of tiny levels; the small-graph kernel is one
+    launch by construction)."""
     dg = devs["kron16p"]
     l0 = dg.launches()
     srcs = [int(s) for s in dg.pick_sources(3, SEED)]
@@ -222,6 +223,39 @@ def _check_bfs_properties(off, nb, src, depth, parent):
     assert (pos < key.size).all() and (key[np.minimum(pos, key.size - 1)] == q).all()
 
 
+def test_small_graph_kernel_selected(devs, both_kernels):
+    """Graphs with n <= 2^17 run in the single-cluster kernel (every step
+    tagged 'S'); GK_NO_SMALL=1 sends them to the grid kernel."""
+    dg = devs["kron16p"]
+    for s in dg.pick_sources(3, SEED):
+        pads = {x[4] for x in dg.bfs(int(s), parent=False).steps}
+        assert pads == {"S"} if both_kernels == "small" else "S" not in pads
+
+
+@pytest.mark.parametrize("kind,scale,perm", [("kron", 17, True), ("urand", 17, False), ("kron", 18, True)])
+def test_small_kernel_size_limit(kind, scale, perm, both_kernels):
+    """At the small kernel's limit (2^17 vertices: 256 bitmap words per CTA
+    of a 16-CTA cluster) and just past it (2^18: grid kernel): depths,
+    parents, schedule, counters and bottom-up parents against the oracle."""
+    g = O.make_graph(kind, scale, permute=perm)
+    dg = DeviceGraph.from_csr(g)
+    for s in O.pick_sources(g, 4, 3):
+        s = int(s)
+        for st in (0, 1, 2):
+            res = dg.bfs(s, strategy=st, depth=True, counts=True)
+            assert (res.depth == O.bfs_depths(g, s)).all(), (s, st)
+            assert O.verify_bfs(g, s, res.parent)[0], (s, st)
+            rp = O.bfs_replay(g, s, strategy=st)
+            assert res.schedule == rp.dirs and [x[2] for x in res.steps] == rp.result, (s, st)
+            assert [x[3] for x in res.steps] == rp.edges_to_check, (s, st)
+            for i, c in enumerate(res.schedule):
+                if c == "B" and res.steps[i][4] != "P":
+                    sel = res.depth == i + 1
+                    assert (res.parent[sel] == rp.parent[sel]).all(), (s, st, i)
+            if scale > 17:
+                assert "S" not in {x[4] for x in res.steps}
+
+
 @pytest.mark.parametrize("kind,scale", [("kron", 21), ("urand", 20)])
 def test_medium_scale_against_oracle(kind, scale):
     dg = DeviceGraph.generate(kind, scale, 16, SEED)
@@ -274,7 +308,7 @@ def chain_graphs():
 
 
 @pytest.mark.parametrize("strategy", [0, 1, 2])
-def test_cluster_mode_parity(chain_graphs, strategy):
+def test_cluster_mode_parity(chain_graphs, strategy, grid_kernel):
     """Chains of tiny top-down levels run in the cluster kernel (steps tagged
     'K', gk_bfs_cluster.cu) and hand back to the grid kernel: depths exact,
     parents valid, schedule and every step counter equal the reference's."""
@@ -300,7 +334,7 @@ def test_cluster_mode_parity(chain_graphs, strategy):
         assert seen_k, name  # the cluster kernel ran
 
 
-def test_cluster_mode_batch(chain_graphs):
+def test_cluster_mode_batch(chain_graphs, grid_kernel):
     """gk_bfs_batch on a sparse graph checks for hand-offs after each trial:
     every parent array valid and equal-depth to the single-source call."""
     g, dg = chain_graphs["grid300x257"]

@@ -33,7 +33,7 @@ def check(g, dg, s, alpha=15, beta=18, strategy=0):
 
 
 @pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 63, 65, 1000, 1025])
-def test_ragged_vertex_counts(n):
+def test_ragged_vertex_counts(n, both_kernels):
     rng = np.random.default_rng(n)
     m = 3 * n
     e = rng.integers(0, n, size=2 * m, dtype=np.uint64).astype(np.uint32)
@@ -45,7 +45,7 @@ def test_ragged_vertex_counts(n):
                 check(g, dg, s, a, b, int(st))
 
 
-def test_heavy_hub_small_graph():
+def test_heavy_hub_small_graph(both_kernels):
     # one vertex of degree 6000 (> the 1024-edge chunk), plus a sparse ring:
     # heavy chunks, a large (bitmap) top-down step and head/list rounds
     n = 6001
@@ -57,7 +57,7 @@ def test_heavy_hub_small_graph():
             check(g, dg, s, a, b)
 
 
-def test_isolated_source_and_dead_vertices():
+def test_isolated_source_and_dead_vertices(both_kernels):
     # vertices 5..9 have no edges at all; BFS from one of them reaches only it
     e = np.array([0, 1, 1, 2, 2, 3, 3, 4], np.uint32)
     g = O.build_csr(10, e)
@@ -68,7 +68,7 @@ def test_isolated_source_and_dead_vertices():
     check(g, dg, 0, 1, 1)
 
 
-def test_directed_source_without_in_edges():
+def test_directed_source_without_in_edges(both_kernels):
     # vertex 0 only has out-edges: it is "dead" for the bottom-up sweep but a
     # valid source; vertex 4 has in-edges only
     e = np.array([0, 1, 0, 2, 1, 3, 2, 3, 3, 4, 1, 4], np.uint32)
@@ -82,7 +82,7 @@ def test_directed_source_without_in_edges():
 
 
 @pytest.mark.parametrize("passes", ["2", "3", "7"])
-def test_large_step_range_passes(passes, monkeypatch):
+def test_large_step_range_passes(passes, monkeypatch, grid_kernel):
     # GK_TD_PASSES forces the target-range passes of large top-down steps
     # that kick in by themselves only when the next bitmap exceeds 64 MB
     monkeypatch.setenv("GK_TD_PASSES", passes)
@@ -96,7 +96,7 @@ def test_large_step_range_passes(passes, monkeypatch):
         check(gu, dgu, int(s))
 
 
-def test_handle_state_across_kernels():
+def test_handle_state_across_kernels(both_kernels):
     # BFS, Brandes, BFS again on one handle: per-call state is re-initialised
     g = O.make_graph("kron", 12, permute=True)
     dg = DeviceGraph.from_csr(g)
@@ -109,7 +109,7 @@ def test_handle_state_across_kernels():
         assert (r.depth == d).all()
 
 
-def test_batch_matches_single_calls():
+def test_batch_matches_single_calls(both_kernels):
     # gk_bfs_batch: per-source results identical in depth, all parents valid,
     # copies overlapped with the next traversal
     from paper_1508_03619_b200 import ConfigError, PinnedBuffer
@@ -152,7 +152,7 @@ def test_malformed_csr_rejected():
 
 
 @pytest.mark.parametrize("dmin", ["1", "40", "300"])
-def test_owned_range_hub_expansion(dmin, monkeypatch):
+def test_owned_range_hub_expansion(dmin, monkeypatch, grid_kernel):
     # GK_OWN_DMIN makes small graphs' hubs take the owned-range expansion of
     # large top-down steps (td_own) that kron scale >= 21 uses by itself;
     # GK_NO_FRONT_SMEM keeps the bitmaps in global memory as at that size
@@ -178,7 +178,7 @@ def test_owned_range_hub_expansion(dmin, monkeypatch):
 
 
 @pytest.mark.parametrize("no_head2", ["0", "1"])
-def test_bottom_up_rounds_with_and_without_second_head(no_head2, monkeypatch):
+def test_bottom_up_rounds_with_and_without_second_head(no_head2, monkeypatch, grid_kernel):
     # the second head record (in-neighbours 4..7) replaces the first in_nb
     # round; without it (GK_NO_HEAD2) round 2 reads in_off/in_nb as before.
     # Lists of every length around the 4/8 boundaries, bottom-up parents
@@ -200,7 +200,7 @@ def test_bottom_up_rounds_with_and_without_second_head(no_head2, monkeypatch):
         check(gu, dgu, int(s))
 
 
-def test_rescan_strategy_on_fresh_handle():
+def test_rescan_strategy_on_fresh_handle(both_kernels):
     # kTopDownRescan re-reads each new frontier's queue (bfs.hpp:161-167):
     # its large steps must write that queue even when no earlier traversal
     # on the handle left the same entries behind
@@ -210,7 +210,7 @@ def test_rescan_strategy_on_fresh_handle():
         check(g, dg, int(s), strategy=int(BfsStrategy.kTopDownRescan))
 
 
-def test_sparse_sweeps_and_pulled_top_down(monkeypatch):
+def test_sparse_sweeps_and_pulled_top_down(monkeypatch, grid_kernel):
     # Once few vertices are unreached, bottom-up steps scan a list of them
     # and a top-down step whose frontier outnumbers them runs as a pull
     # ('P' in the trace): same claimed set and counters as the reference's
@@ -232,7 +232,7 @@ def test_sparse_sweeps_and_pulled_top_down(monkeypatch):
     assert "P" in seen
 
 
-def test_pushed_bottom_up_step(monkeypatch):
+def test_pushed_bottom_up_step(monkeypatch, grid_kernel):
     # A bottom-up step entered with a frontier whose out-degree total is small
     # against the pending vertices runs as a push ('P' in the step log): the
     # same claimed set and awake count as the reference's bottom-up step, so
