@@ -398,7 +398,24 @@ __device__ __forceinline__ void split_run(const uint32_t* a, uint32_t d, uint32_
   }
 }
 
+#ifndef GK_OWN_TRACE
+#define GK_OWN_TRACE 0  // diagnostics: CTA 0 stamps td_own's sub-phases into ctrl->ts[400..]
+#endif
+#if GK_OWN_TRACE
+#define OWN_MARK(i)                                                                      \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                           \
+      P.ctrl->ts[400 + (i)] = globaltimer();                                             \
+      P.ctrl->tag[400 + (i)] = 'o';                                                      \
+    }                                                                                    \
+  } while (0)
+#else
+#define OWN_MARK(i) \
+  do {              \
+  } while (0)
+#endif
 __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, uint32_t* nextbm, uint32_t* sm) {
+  OWN_MARK(0);
   constexpr int kE = GK_OWN_KE;  // arcs per lane in flight
   const int r = cta_id(P);
   const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -427,8 +444,10 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
       b = e.base + s0;
       len = (int64_t)s1 - s0;
     }
+    if (g0 == 0) OWN_MARK(1);
     int64_t tot;
     const int64_t pre = block_exscan(len, &tot, s);
+    if (g0 == 0) OWN_MARK(2);
     s.td.t_u[threadIdx.x] = u;
     s.td.t_b[threadIdx.x] = b - pre;  // arc of concatenated position e is t_b[o] + e
     s.td.t_pre[threadIdx.x] = pre;
@@ -488,8 +507,16 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
     }
     __syncthreads();
   }
+  OWN_MARK(3);
+#if GK_OWN_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 290) {
+    P.ctrl->ts[100 + blockIdx.x] = globaltimer();
+    P.ctrl->tag[100 + blockIdx.x] = 'g';
+  }
+#endif
   for (int i = threadIdx.x; i < nw; i += kBlock) atomicOr(nextbm + w0 + i, sm[i]);
   __syncthreads();
+  OWN_MARK(4);
   // Parents, window by window: gather the window's logged claims into
   // shared memory (the slice's space), then store them in vertex order
   // (coalesced: measured faster than storing the log entries directly).
@@ -513,6 +540,12 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
       if (pv != -2) *parent_slot(P, (uint32_t)(lo + i)) = pv;
     }
     __syncthreads();
+  }
+  OWN_MARK(5);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && GK_OWN_TRACE) {
+    P.ctrl->ts[410] = nown;
+    P.ctrl->ts[411] = (unsigned long long)nwin;
+    P.ctrl->tag[410] = P.ctrl->tag[411] = 'n';
   }
 }
 

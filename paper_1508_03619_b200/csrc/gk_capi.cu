@@ -820,9 +820,15 @@ int32_t* gk_bfs_device_depth(const gk_graph* g) { return g && g->depth_valid ? g
 gk_status gk_bfs_trace(const gk_graph* g, uint64_t* ts_ns, char* tags, int32_t cap, int32_t* count) {
   if (!g || !count) return fail(GK_ERR_INVALID, "null argument");
   if (!g->last_valid) return fail(GK_ERR_INVALID, "no completed gk_bfs on this handle");
+  // entries up to the first untagged one (diagnostic builds may tag entries
+  // past a gap: GK_TRACE_ALL=1 returns every slot up to the last tagged one)
+  int32_t last = gk::kTraceCap;
+  if (getenv("GK_TRACE_ALL")) {
+    while (last > 1 && g->last_ctrl.tag[last - 1] == 0) last--;
+  }
   int32_t k = 0;
-  for (int32_t i = 0; i < gk::kTraceCap; i++) {
-    if (i > 0 && g->last_ctrl.tag[i] == 0) break;
+  for (int32_t i = 0; i < last; i++) {
+    if (i > 0 && g->last_ctrl.tag[i] == 0 && !getenv("GK_TRACE_ALL")) break;
     if (k < cap) {
       if (ts_ns) ts_ns[k] = g->last_ctrl.ts[i];
       if (tags) tags[k] = i == 0 ? 'S' : (char)g->last_ctrl.tag[i];

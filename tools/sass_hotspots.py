@@ -22,8 +22,15 @@ def main():
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[1]
-    data = rows[2:]
+    # one section per function ("Kernel Name", name / header / rows)
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"] + [len(rows)]
+    sec = next((i for i in starts[:-1] if kname in rows[i][1]), None)
+    if sec is None:
+        h, data = rows[1], rows[2:]
+    else:
+        h = rows[sec + 1]
+        data = rows[sec + 2:starts[starts.index(sec) + 1]]
+    data = [r for r in data if r and r[h.index("Address")].startswith("0x")]
     ia, iw = h.index("Address"), h.index("Warp Stall Sampling (All Samples)")
     stall_cols = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
     base = min(int(r[ia], 16) for r in data)
@@ -31,9 +38,13 @@ def main():
                for r in data}
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=d, capture_output=True)
-        cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-        dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True,
-                             text=True).stdout
+        dis = ""
+        for cub in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):
+            t = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True,
+                               text=True).stdout
+            if kname in t:
+                dis = t
+                break
     # walk the kernel's section; track the current "//## File ..., line N" annotation
     in_k, line, off2line = False, None, {}
     for l in dis.splitlines():
