@@ -254,7 +254,28 @@ int aux_grid(int64_t n) {
   return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
+// Compact offsets: low 32 bits of every offset; the first vertex of each
+// 2^32 block of arcs goes to hi[block - 1] (one vertex's list is shorter
+// than 2^32 arcs, so consecutive offsets cross at most one block edge).
+__global__ void k_off32(const int64_t* off, int64_t n, uint32_t* off32, uint32_t* hi, int nhi) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = t; v <= n; v += nt) {
+    const int64_t o = off[v];
+    off32[v] = (uint32_t)o;
+    if (v > 0) {
+      const int64_t b = o >> 32, a = off[v - 1] >> 32;
+      for (int64_t k = a; k < b && k < nhi; k++) hi[k] = (uint32_t)v;
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t compact_offsets(const int64_t* off, int64_t n, uint32_t* off32, uint32_t* hi, int nhi, cudaStream_t s) {
+  k_off32<<<aux_grid(n + 1), kAuxBlock, 0, s>>>(off, n, off32, hi, nhi);
+  return cudaGetLastError();
+}
 
 cudaError_t dead_bitmap(const int64_t* in_off, int64_t n, uint32_t* dead, int64_t* live, cudaStream_t s) {
   const int64_t w32 = (n + 31) / 32;

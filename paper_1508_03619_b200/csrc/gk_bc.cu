@@ -75,9 +75,9 @@ __device__ void bc_forward_light(const BfsParams& P, SmemT& s, unsigned ph, cons
     double su = 0.0;
     if (i < qe) {
       u = __ldcg(P.queue + i);
-      b = P.out_off[u];
+      b = offv(P, P.out_off, u);
       su = __ldcg(&P.bc_sd[u].x);
-      const int64_t d = P.out_off[u + 1] - b;
+      const int64_t d = offv(P, P.out_off, u + 1) - b;
       if (d > kBcChunk) {
         const int64_t nch = (d + kBcChunk - 1) / kBcChunk;
         const unsigned long long base = atomicAdd(&cnt[kChunkCount], (unsigned long long)nch);
@@ -185,9 +185,9 @@ __device__ void bc_backward_level(const BfsParams& P, SmemT& s, unsigned ph, uns
     bool heavy = false;
     if (i < b1) {
       u = __ldcg(P.queue + i);
-      b = P.out_off[u];
+      b = offv(P, P.out_off, u);
       su = __ldcg(&P.bc_sd[u].x);
-      const int64_t d = P.out_off[u + 1] - b;
+      const int64_t d = offv(P, P.out_off, u + 1) - b;
       if (d > kBcChunk) {
         heavy = true;
         const int64_t nch = (d + kBcChunk - 1) / kBcChunk;
@@ -312,8 +312,8 @@ __device__ void bc_pull_level(const BfsParams& P, SmemT& s, unsigned ph, const Q
       vis = __ldcg(P.visited + w) | __ldg(P.dead + w);
       pend = !((vis >> (v & 31)) & 1u);
       if (pend) {
-        b = P.in_off[v];
-        dl = P.in_off[v + 1] - b;
+        b = offv(P, P.in_off, v);
+        dl = offv(P, P.in_off, v + 1) - b;
       }
     }
     s.td.t_b[threadIdx.x] = b;
@@ -391,8 +391,8 @@ __device__ void bc_push_level(const BfsParams& P, SmemT& s, unsigned long long b
     double t = 0.0;
     if (i < b1) {
       const uint32_t v = __ldcg(P.queue + i);
-      b = P.in_off[v];
-      dl = P.in_off[v + 1] - b;
+      b = offv(P, P.in_off, v);
+      dl = offv(P, P.in_off, v + 1) - b;
       const double2 sd = __ldcg(P.bc_sd + v);
       t = (1.0 + sd.y) / sd.x;
     }
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
       long long dsum = 0;
       for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
         const uint32_t u = __ldcg(P.queue + i);
-        dsum += P.out_off[u + 1] - P.out_off[u];
+        dsum += offv(P, P.out_off, u + 1) - offv(P, P.out_off, u);
       }
       const unsigned set = ph & 3;
       block_add(dsum, &P.ctrl->cnt[set][kSum], s);
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(kBlock, 2) bc_persistent(BfsParams P) {
         long long sum = 0;
         for (unsigned long long i = b0 + gtid; i < b1; i += gthreads) {
           const uint32_t u = __ldcg(P.queue + i);
-          sum += P.out_off[u + 1] - P.out_off[u];
+          sum += offv(P, P.out_off, u + 1) - offv(P, P.out_off, u);
         }
         const unsigned set = ph & 3;
         block_add(sum, &P.ctrl->cnt[set][kSum], s);

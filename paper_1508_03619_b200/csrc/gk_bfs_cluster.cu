@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
     unsigned loaded = 0;
     for (long long i = H.qs + (long long)c * kCmBlock + t; i < H.qe; i += (long long)C * kCmBlock) {
       const uint32_t v = __ldcg(P.queue + i);
-      const int64_t o0 = ld_off(P.out_off + v), o1 = ld_off(P.out_off + v + 1);
+      const int64_t o0 = offv(P, P.out_off, v), o1 = offv(P, P.out_off, v + 1);
       push(0, v, (uint32_t)(o1 - o0), o0);
       loaded++;
     }
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
       unsigned long long mine = 0;
       for (int i = g0 + (int)lane; i < nr; i += wpr * 32) {
         const uint32_t v = S.f[cur][eslot(i)].v;
-        mine += (unsigned long long)(ld_off(P.out_off + v + 1) - ld_off(P.out_off + v));
+        mine += (unsigned long long)(offv(P, P.out_off, v + 1) - offv(P, P.out_off, v));
       }
       const unsigned lo = __reduce_add_sync(kFull, (unsigned)(mine & 0xffff));
       const unsigned hi = __reduce_add_sync(kFull, (unsigned)(mine >> 16));
@@ -397,8 +397,8 @@ __global__ void __launch_bounds__(kCmBlock, 1) bfs_cluster(BfsParams P, Hand H) 
       for (int q = 0; q < kCmW; q++) {
         o0[q] = o1[q] = 0;
         if (ok[q]) {
-          o0[q] = ld_off(P.out_off + w[q]);
-          o1[q] = ld_off(P.out_off + w[q] + 1);
+          o0[q] = offv(P, P.out_off, w[q]);
+          o1[q] = offv(P, P.out_off, w[q] + 1);
         }
       }
       // every claim atomic in flight at once: each result has its own

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
   unsigned long long qs = 0, qe = 1;
   unsigned long long qtail = 1;  // queue entries written so far (uniform)
   long long etc = P.m;                                  // bfs.hpp:139
-  long long scout = P.out_off[src + 1] - P.out_off[src];  // bfs.hpp:140
+  long long scout = offv(P, P.out_off, src + 1) - offv(P, P.out_off, src);  // bfs.hpp:140
   long long nsteps = 0;
   long long reached = 1;  // vertices claimed so far (source included)
   long long dummy = 0;
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
         long long tot = 0;
         for (unsigned long long i = qs + gtid; i < qe; i += gthreads) {
           const uint32_t u = __ldcg(P.queue + i);
-          tot += P.out_off[u + 1] - P.out_off[u];
+          tot += offv(P, P.out_off, u + 1) - offv(P, P.out_off, u);
         }
         set = ph & 3;
         block_add(tot, &P.ctrl->cnt[set][kSum], s);

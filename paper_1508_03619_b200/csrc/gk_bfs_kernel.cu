@@ -28,6 +28,7 @@
 //             parent exactly as bfs.hpp:55-60 picks it
 //   b2q       BitmapToQueue (bfs.hpp:99-113), CTA-aggregated appends
 //   rescan    kTopDownRescan's extra degree pass (bfs.hpp:161-167)
+#define GK_OFFMODE 0  // int64 offsets; gk_bfs_kernel_c.cu: the compact ones
 #include "gk_bfs_grid.cuh"
 
 namespace gk {
@@ -57,16 +58,15 @@ cudaError_t bfs_configure(int device, BfsLaunch* cfg) {
   // static part at 1 CTA/SM; otherwise it is read through L1/L2.
   const size_t budget = (size_t)optin > cfg->smem_static + 1024 ? optin - cfg->smem_static - 1024 : 0;
   cfg->smem_front_max = budget & ~size_t(15);
-  if ((e = cudaFuncSetAttribute(bfs_persistent<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)cfg->smem_front_max)) ||
-      (e = cudaFuncSetAttribute(bfs_resume_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)cfg->smem_front_max)))
-    return e;
-  int occ = 0;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bfs_persistent<false>, kBlock, 0))) return e;
-  int occ_r = 0;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, bfs_resume_fn(), kBlock, 0))) return e;
-  occ = std::min(occ, occ_r);
+  const void* fns[4] = {(const void*)bfs_persistent<false>, bfs_resume_fn(), bfs_fresh_c_fn(), bfs_resume_c_fn()};
+  int occ = 1 << 30;
+  for (const void* f : fns) {
+    if ((e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg->smem_front_max)))
+      return e;
+    int o = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, f, kBlock, 0))) return e;
+    occ = std::min(occ, o);
+  }
   if (occ < 1) return cudaErrorInvalidConfiguration;
   cfg->grid = sms * occ;
   cfg->block = kBlock;
@@ -77,6 +77,8 @@ cudaError_t bfs_configure(int device, BfsLaunch* cfg) {
 }
 
 cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st) {
+  const void* fn = p.off32 ? (p.resume ? bfs_resume_c_fn() : bfs_fresh_c_fn())
+                           : (p.resume ? bfs_resume_fn() : (const void*)bfs_persistent<false>);
   size_t dyn = 0;
   int grid = cfg.grid;
   if (p.front_in_smem) {
@@ -84,7 +86,7 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st
     int occ = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bfs_persistent<false>, kBlock, dyn);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, dyn);
     if (e) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     grid = sms * occ;
@@ -123,7 +125,6 @@ cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t st
     local.parent_preset = 1;
   }
   void* args[] = {&local};
-  const void* fn = p.resume ? bfs_resume_fn() : (const void*)bfs_persistent<false>;
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(cfg.block), args, dyn, st);
 }
 

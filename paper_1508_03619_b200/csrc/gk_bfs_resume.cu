@@ -1,5 +1,6 @@
 // gk_bfs_resume.cu -- the grid kernel instantiated for a traversal that
 // continues after the cluster kernel handed it back (see gk_bfs_grid.cuh).
+#define GK_OFFMODE 0
 #include "gk_bfs_grid.cuh"
 
 namespace gk {

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
 
   SM_MARK('i');
   long long etc = P.m;                                    // bfs.hpp:139
-  long long scout = P.out_off[src + 1] - P.out_off[src];  // bfs.hpp:140
+  long long scout = offv(P, P.out_off, src + 1) - offv(P, P.out_off, src);  // bfs.hpp:140
   long long fsz = 1, nsteps = 0;
   int lvl = 0;
   unsigned L = 0;  // levels done (parity of the slice / counter buffers)
@@ -310,8 +310,8 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
             v[q] = live[q] ? S.ids[i] : 0u;
             b[q] = e[q] = 0u;
             if (live[q]) {
-              b[q] = (uint32_t)P.in_off[v[q]];
-              e[q] = (uint32_t)P.in_off[v[q] + 1];
+              b[q] = (uint32_t)offv(P, P.in_off, v[q]);
+              e[q] = (uint32_t)offv(P, P.in_off, v[q] + 1);
             }
           }
 #pragma unroll 1
@@ -349,8 +349,8 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
         const int nl = (int)S.nlong;
         for (int i = (int)warp; i < nl; i += kSmWarps) {  // long lists: a warp per vertex
           const uint32_t v = S.pre[i];
-          const int64_t le = P.in_off[v + 1];
-          for (int64_t j = P.in_off[v] + 4 * kSmRounds; j < le; j += 32) {
+          const int64_t le = offv(P, P.in_off, v + 1);
+          for (int64_t j = offv(P, P.in_off, v) + 4 * kSmRounds; j < le; j += 32) {
             const int64_t jj = j + lane;
             uint32_t u = 0;
             bool h = false;
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
         k = fewer ? sm_list<false>(S, S.front, 0, W, rs) : sm_list<false>(S, S.front, wlo, whi, rs);
         for (int i = t; i < k; i += kSmBlock) {
           const uint32_t v = S.ids[i];
-          const int64_t o0 = P.out_off[v], o1 = P.out_off[v + 1];
+          const int64_t o0 = offv(P, P.out_off, v), o1 = offv(P, P.out_off, v + 1);
           S.off[i] = (uint32_t)o0;
           S.pre[i] = (uint32_t)(o1 - o0);
         }
@@ -505,8 +505,8 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
           if (ok[q]) {
             const uint32_t ww = w[q] >> 5;
             const int home = (int)(ww / (uint32_t)Wc);
-            o0[q] = P.out_off[w[q]];
-            o1[q] = P.out_off[w[q] + 1];
+            o0[q] = offv(P, P.out_off, w[q]);
+            o1[q] = offv(P, P.out_off, w[q] + 1);
             old[q] = atomicOr(cl.map_shared_rank(&S.slice[q3][0], home) + (ww - (uint32_t)home * (uint32_t)Wc),
                               1u << (w[q] & 31u));
           }
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
         const int kn = sm_list<false>(S, S.slice[q3], 0, whi - wlo, rs);  // ids relative to wlo * 32
         for (int i = t; i < kn; i += kSmBlock) {
           const uint32_t v = S.ids[i] + (uint32_t)wlo * 32u;
-          const int64_t o0 = P.out_off[v], o1 = P.out_off[v + 1];
+          const int64_t o0 = offv(P, P.out_off, v), o1 = offv(P, P.out_off, v + 1);
           const long long dg = o1 - o0;
           sc += encode ? (dg ? dg : 1) : dg;
           if (P.want_depth) P.depth[v] = lvl + 1;

@@ -43,7 +43,7 @@ __device__ __forceinline__ void on_claim(const BfsParams& P, uint32_t u, uint32_
   P.parent[v] = (int32_t)u;
   if (P.want_depth) P.depth[v] = lvl + 1;
   if (encode) {
-    long long d = P.out_off[v + 1] - P.out_off[v];
+    long long d = offv(P, P.out_off, v + 1) - offv(P, P.out_off, v);
     scout += d ? d : 1;  // -old of the degree-encoded slot (bfs.hpp:83,130)
   } else {
     scout += 1;  // unencoded slot is -1 (bfs.hpp:129-130 with encode off)
@@ -74,8 +74,8 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
     for (int k = 0; k < 4; k++) {
       o0[k] = o1[k] = 0;
       if (ok[k] && encode) {
-        o0[k] = P.out_off[v[k]];
-        o1[k] = P.out_off[v[k] + 1];
+        o0[k] = offv(P, P.out_off, v[k]);
+        o1[k] = offv(P, P.out_off, v[k] + 1);
       }
     }
 #pragma unroll
@@ -155,8 +155,8 @@ __device__ void td_light(const BfsParams& P, SmemT& s, unsigned ph, const QApp& 
     int64_t b = 0, dl = 0;
     if ((int)threadIdx.x < tile_sz && i < qe) {
       u = __ldcg(P.queue + i);
-      b = P.out_off[u];
-      const int64_t d = P.out_off[u + 1] - b;
+      b = offv(P, P.out_off, u);
+      const int64_t d = offv(P, P.out_off, u + 1) - b;
       if (own && d >= P.own_dmin) {  // expanded range by range in td_own
         OwnEnt e;
         e.u = u;
@@ -584,8 +584,8 @@ __device__ __forceinline__ long long claim_degrees(const BfsParams& P, long long
       o0[k] = o1[k] = -1;
       if (c < total) {
         const int64_t v = (w0 + lo) * 32 + (int64_t)__fns(m, 0, c - ex + 1);
-        o0[k] = ld_off(P.out_off + v);
-        o1[k] = ld_off(P.out_off + v + 1);
+        o0[k] = offv(P, P.out_off, v);
+        o1[k] = offv(P, P.out_off, v + 1);
       }
     }
 #pragma unroll
@@ -769,8 +769,8 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
           if (need && c < total) {
             const uint32_t en = lst[c];
             v[k] = (uint32_t)((tbase + (en >> 5)) * 32 + (en & 31u));
-            b[k] = ld_off(P.in_off + v[k]);
-            e[k] = ld_off(P.in_off + v[k] + 1);
+            b[k] = offv(P, P.in_off, v[k]);
+            e[k] = offv(P, P.in_off, v[k] + 1);
             st[k] = 1;
           }
           continue;
@@ -785,8 +785,8 @@ __device__ void bu_step(const BfsParams& P, SmemT& s, unsigned ph, const uint32_
         const int ex = __shfl_sync(kFull, excl, lo);
         if (need && c < total) {
           v[k] = (uint32_t)((tbase + lo) * 32 + (int)__fns(m, 0, c - ex + 1));
-          b[k] = ld_off(P.in_off + v[k]);
-          e[k] = ld_off(P.in_off + v[k] + 1);
+          b[k] = offv(P, P.in_off, v[k]);
+          e[k] = offv(P, P.in_off, v[k] + 1);
           st[k] = 1;
         }
       }
@@ -880,8 +880,9 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
   const long long nw = ((long long)cta_count(P) * kBlock) >> 5;
   for (long long i = gw; i < (long long)count; i += nw) {
     const uint32_t v = __ldcg(lst + i);
-    const int64_t le = P.in_off[v + 1];
-    for (int64_t j = kSparse ? P.in_off[v] + kSparseScan : bu_resume(P.in_off[v]); j < le; j += 32) {
+    const int64_t le = offv(P, P.in_off, v + 1);
+    const int64_t lb = offv(P, P.in_off, v);
+    for (int64_t j = kSparse ? lb + kSparseScan : bu_resume(lb); j < le; j += 32) {
       const int64_t jj = j + lane;
       bool h = false;
       uint32_t u = 0;
@@ -899,7 +900,7 @@ __device__ void bu_long(const BfsParams& P, const uint32_t* front, uint32_t* nex
           atomicOr(P.visited + (v >> 5), 1u << (v & 31u));
           awake++;
           if constexpr (kPull) {  // top-down result of the claim (bfs.hpp:83)
-            const int64_t dg = P.out_off[v + 1] - P.out_off[v];
+            const int64_t dg = offv(P, P.out_off, v + 1) - offv(P, P.out_off, v);
             scout += dg ? dg : 1;
           }
         }
@@ -990,8 +991,8 @@ __device__ void sp_scan(const BfsParams& P, unsigned ph, const uint32_t* front, 
     }
 #pragma unroll
     for (int k = 0; k < kS; k++) {
-      o0[k] = act[k] ? ld_off(P.in_off + v[k]) : 0;
-      o1[k] = act[k] ? ld_off(P.in_off + v[k] + 1) : 0;
+      o0[k] = act[k] ? offv(P, P.in_off, v[k]) : 0;
+      o1[k] = act[k] ? offv(P, P.in_off, v[k] + 1) : 0;
       lim[k] = o1[k] - o0[k] > kSparseScan ? o0[k] + kSparseScan : o1[k];
       j[k] = o0[k];
       act[k] = act[k] && j[k] < lim[k];
@@ -1028,7 +1029,7 @@ __device__ void sp_scan(const BfsParams& P, unsigned ph, const uint32_t* front, 
         atomicOr(P.visited + (vv >> 5), 1u << (vv & 31u));
         found++;
         if constexpr (kPull) {
-          const int64_t dg = P.out_off[vv + 1] - P.out_off[vv];
+          const int64_t dg = offv(P, P.out_off, vv + 1) - offv(P, P.out_off, vv);
           scout += dg ? dg : 1;
         }
       } else if (i0 + k * gthreads < (long long)cnt && o1[k] - o0[k] > kSparseScan) {

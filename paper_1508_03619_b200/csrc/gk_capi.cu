@@ -71,6 +71,7 @@ void free_graph(gk_graph* g) {
   cudaFree(g->out_off);
   cudaFree(g->out_nb);
   cudaFree(g->dead);
+  cudaFree(g->off32);
   cudaFree(g->depth);
   cudaFree(g->acc);
   if (g->pool) cudaMemPoolDestroy(g->pool);
@@ -116,6 +117,22 @@ gk_status setup_graph(gk_graph* g, bool sorted) {
   g->canary = getenv("GK_CANARY") && atoi(getenv("GK_CANARY")) != 0;
   CK(cudaMalloc(&g->dead, bitmap_bytes(n)), "alloc dead-vertex bitmap");
   CK(gk::dead_bitmap(g->in_off, n, g->dead, &g->live, g->stream), "dead-vertex bitmap");
+  // The offsets' compact form (graph layout read by the BFS and Brandes
+  // kernels, built with the graph like the dead bitmap): 4 bytes per vertex
+  // instead of 8 on every offset read; undirected graphs up to 2^28
+  // vertices (memory headroom at 2^30) and 2^33 arcs (one carry bit).
+  if (!g->directed && n <= (int64_t(1) << 28) && g->m < (int64_t(2) << 32) && !getenv("GK_NO_OFF32")) {
+    const int nhi = (int)(g->m >> 32);  // 0 or 1
+    uint32_t* hi = nullptr;
+    CK(cudaMalloc(&g->off32, sizeof(uint32_t) * (size_t)(n + 1) + 64), "alloc compact offsets");
+    CK(cudaMalloc(&hi, sizeof(g->off_hi)), "alloc compact offsets");
+    CK(cudaMemsetAsync(hi, 0xFF, sizeof(g->off_hi), g->stream), "compact offsets");
+    cudaError_t e = gk::compact_offsets(g->out_off, n, g->off32, hi, nhi, g->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->off_hi, hi, sizeof(g->off_hi), cudaMemcpyDeviceToHost, g->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+    cudaFree(hi);
+    CK(e, "compact offsets");
+  }
   cudaMemPoolProps props{};
   props.allocType = cudaMemAllocationTypePinned;
   props.location.type = cudaMemLocationTypeDevice;
@@ -246,6 +263,11 @@ gk_status trial_check_canaries(gk_graph* g, const TrialBlocks& tb, cudaStream_t 
   return GK_OK;
 }
 
+void set_compact_offsets(const gk_graph* g, gk::BfsParams& p) {
+  p.off32 = g->off32;
+  p.off_hi[0] = g->off_hi[0];
+}
+
 // The trial's buffers in the kernel parameters (after trial_alloc).
 void set_trial_ptrs(const gk_graph* g, const gk_trial& t, gk::BfsParams& p) {
   p.parent = t.parent;
@@ -290,6 +312,7 @@ gk::BfsParams make_params(gk_graph* g, const gk_trial& t, uint32_t source, int64
   p.depth = g->depth;
   p.dead = g->dead;
   p.live = g->live;
+  set_compact_offsets(g, p);
   set_trial_ptrs(g, t, p);
   // Large top-down steps additionally clear and fill the n/8-byte next
   // bitmap and sum degrees in a separate pass; worth it above ~n/16 edges.
@@ -943,6 +966,7 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
   p.stop_after = 0xffffffffu;
   p.dead = g->dead;
   p.live = g->live;
+  set_compact_offsets(g, p);
   if (getenv("GK_BC_NO_PULL")) p.bc_lv = nullptr;  // top-down only (the reference's forward)
   gk_status st = GK_OK;
   cudaError_t e = cudaMemsetAsync(p.bc_scores, 0, sizeof(float) * n, s);

@@ -139,6 +139,11 @@ struct BfsParams {
   uint32_t* visited;
   uint32_t* bm0;
   uint32_t* bm1;
+  // graph: the offsets' compact form (undirected graphs up to 2^28 vertices
+  // and 2^33 arcs, else null): off[v] = off32[v] + 2^32 * (v >= off_hi[0]),
+  // off_hi[0] = first vertex whose offset is >= 2^32 (0xffffffff: none)
+  const uint32_t* off32;
+  uint32_t off_hi[1];
   const uint32_t* dead;  // graph: in-degree-0 vertices (+ ids >= n), never reachable
   int64_t live;          // graph: vertices with in-edges (not dead)
   uint32_t* queue;
@@ -199,6 +204,9 @@ struct BfsLaunch {
 cudaError_t bfs_configure(int device, BfsLaunch* cfg);
 cudaError_t bfs_launch(const BfsParams& p, const BfsLaunch& cfg, cudaStream_t s);
 const void* bfs_resume_fn();  // the grid kernel continuing a handed-back traversal (gk_bfs_resume.cu)
+// the same two instantiations reading the compact offsets (gk_bfs_kernel_c.cu, gk_bfs_resume_c.cu)
+const void* bfs_fresh_c_fn();
+const void* bfs_resume_c_fn();
 // ---- sharded traversal (gk_bfs_sharded.cu) --------------
 // Rank r owns vertices [lo, hi) (hi - lo = block, a multiple of 1024 so a
 // 32-word bottom-up task never straddles two ranks) and the CSR rows of
@@ -246,6 +254,9 @@ cudaError_t cluster_configure(int device, int* cluster, int64_t* max_scout);
 cudaError_t cluster_launch(const BfsParams& p, const Hand& h, int cluster, cudaStream_t s);
 // Small graphs: the whole traversal inside one thread-block cluster (gk_bfs_small.cu).
 cudaError_t small_configure(int device, int64_t n, int64_t m, int* cluster);
+// Compact offsets: off32[v] = low 32 bits of off[v]; hi[k] = first v with off[v] >= (k+1) 2^32 (gk_aux.cu).
+cudaError_t compact_offsets(const int64_t* off, int64_t n, uint32_t* off32, uint32_t* hi, int nhi,
+                            cudaStream_t s);
 cudaError_t small_launch(const BfsParams& p, int cluster, cudaStream_t s);
 cudaError_t shard_launch(const BfsParams& p, const ShardTab& t, int grid, cudaStream_t s);
 
@@ -318,6 +329,8 @@ struct gk_graph {
   uint32_t* in_nb = nullptr;
   // graph layout shared by the traversal kernels (BFS, Brandes), built with the graph
   uint32_t* dead = nullptr;  // in-degree 0 (never reachable) + ids >= n
+  uint32_t* off32 = nullptr;  // compact offsets (BfsParams::off32), undirected graphs <= 2^28 vertices
+  uint32_t off_hi[1] = {0xffffffffu};
   int64_t live = 0;          // vertices with in-edges
   // per-trial scratch comes from this pool (stream-ordered, kept warm between
   // trials so an allocation is a pointer bump, not an OS call)

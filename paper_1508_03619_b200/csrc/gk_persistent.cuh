@@ -157,6 +157,20 @@ __device__ __forceinline__ void st_parent(int32_t* p, int32_t v) {
 #endif
 }
 __device__ __forceinline__ int64_t ld_off(const int64_t* p) { return __ldg(p); }
+// Offset v of the CSR: from the compact form when the graph has one (4
+// bytes per vertex instead of 8 -- the bottom-up sweep reads one per pending
+// vertex), else the int64 array base (out_off or in_off; they are the same
+// array whenever off32 exists).
+// GK_OFFMODE fixes the choice at compile time for the grid kernel's two
+// instantiations (the run-time test costs registers in its hot loops).
+#ifndef GK_OFFMODE
+#define GK_OFFMODE 2  // 0: int64 offsets, 1: compact offsets (P.off32 set), 2: chosen at run time
+#endif
+__device__ __forceinline__ int64_t offv(const BfsParams& P, const int64_t* base, int64_t v) {
+  if (GK_OFFMODE == 1 || (GK_OFFMODE == 2 && P.off32))
+    return (int64_t)__ldg(P.off32 + v) + ((int64_t)(v >= (int64_t)P.off_hi[0]) << 32);
+  return __ldg(base + v);
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
   unsigned long long v;
