@@ -244,6 +244,9 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
   const uint32_t src = P.src;
   const bool encode = P.strategy != GK_BFS_TOP_DOWN_RESCAN;
   int rs = 0;  // reduction slot (sm_exscan / sm_sum3)
+#if GK_SM_SPAN  // diagnostics: kernel entry / exit times (globaltimer) in ts[510] / ts[511]
+  const unsigned long long t_in = globaltimer();
+#endif
 #if GK_SM_TRACE
   int trace_i = 0;
   const unsigned long long t_entry = clock64();  // SM cycles in trace mode
@@ -300,22 +303,37 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
         if (t == 0) S.nlong = 0u;
         const int k = sm_list<true>(S, S.vis, wlo, whi, rs);  // (sm_list ends with a CTA barrier)
         SM_MARK('p');
-        for (int base = t; base < k; base += kSmBuW * kSmBlock) {
-          uint32_t v[kSmBuW], b[kSmBuW], e[kSmBuW];
+        // the pending vertices' in-offsets into shared memory (one round
+        // trip for all of them), then kSmBuW slots per thread over this
+        // thread's entries (i = t mod kSmBlock): a slot whose vertex resolves
+        // (or is deferred) takes the next entry at once
+        for (int i = t; i < k; i += kSmBlock) {
+          const uint32_t v = S.ids[i];
+          S.off[i] = (uint32_t)offv(P, P.in_off, v);
+          S.pre[i] = (uint32_t)offv(P, P.in_off, v + 1);
+        }
+        __syncthreads();
+        uint32_t* longl = reinterpret_cast<uint32_t*>(&S.wl[0][0]);  // free during bottom-up levels
+        {
+          uint32_t v[kSmBuW], b[kSmBuW], e[kSmBuW], rounds[kSmBuW];
           bool live[kSmBuW];
+          int nexti = t;
 #pragma unroll
           for (int q = 0; q < kSmBuW; q++) {
-            const int i = base + q * kSmBlock;
-            live[q] = i < k;
-            v[q] = live[q] ? S.ids[i] : 0u;
-            b[q] = e[q] = 0u;
+            live[q] = nexti < k;
+            v[q] = b[q] = e[q] = rounds[q] = 0u;
             if (live[q]) {
-              b[q] = (uint32_t)offv(P, P.in_off, v[q]);
-              e[q] = (uint32_t)offv(P, P.in_off, v[q] + 1);
+              v[q] = S.ids[nexti];
+              b[q] = S.off[nexti];
+              e[q] = S.pre[nexti];
+              nexti += kSmBlock;
             }
           }
-#pragma unroll 1
-          for (int r = 0; r < kSmRounds; r++) {
+          for (;;) {
+            bool any = false;
+#pragma unroll
+            for (int q = 0; q < kSmBuW; q++) any |= live[q];
+            if (!any) break;
             uint32_t u[kSmBuW][4];
 #pragma unroll
             for (int q = 0; q < kSmBuW; q++)
@@ -328,27 +346,40 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
 #pragma unroll
               for (int j = 3; j >= 0; j--)
                 if (u[q][j] != kNoVertex && sm_bit(S.front, u[q][j])) hit = j;
+              bool done = false;
               if (hit >= 0) {  // the first in-neighbour in the frontier (bfs.hpp:55-60)
                 const uint32_t par = hit == 0 ? u[q][0] : hit == 1 ? u[q][1] : hit == 2 ? u[q][2] : u[q][3];
                 P.parent[v[q]] = (int32_t)par;
                 if (P.want_depth) P.depth[v[q]] = lvl + 1;
                 atomicOr(&S.slice[q3][(v[q] >> 5) - wlo], 1u << (v[q] & 31u));
-                live[q] = false;
+                done = true;
               } else {
                 b[q] += 4;
-                if (b[q] >= e[q]) live[q] = false;  // whole list scanned: not reached at this level
+                if (b[q] >= e[q]) {
+                  done = true;  // whole list scanned: not reached at this level
+                } else if (++rounds[q] == kSmRounds) {
+                  longl[atomicAdd(&S.nlong, 1u)] = v[q];  // resumes at in_off + 4 * kSmRounds
+                  done = true;
+                }
+              }
+              if (done) {  // next entry of this thread
+                live[q] = nexti < k;
+                if (live[q]) {
+                  v[q] = S.ids[nexti];
+                  b[q] = S.off[nexti];
+                  e[q] = S.pre[nexti];
+                  rounds[q] = 0u;
+                  nexti += kSmBlock;
+                }
               }
             }
           }
-#pragma unroll
-          for (int q = 0; q < kSmBuW; q++)
-            if (live[q]) S.pre[atomicAdd(&S.nlong, 1u)] = v[q];  // resumes at in_off + 4 * kSmRounds
         }
         __syncthreads();
         SM_MARK('q');
         const int nl = (int)S.nlong;
         for (int i = (int)warp; i < nl; i += kSmWarps) {  // long lists: a warp per vertex
-          const uint32_t v = S.pre[i];
+          const uint32_t v = longl[i];
           const int64_t le = offv(P, P.in_off, v + 1);
           for (int64_t j = offv(P, P.in_off, v) + 4 * kSmRounds; j < le; j += 32) {
             const int64_t jj = j + lane;
@@ -596,6 +627,13 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
     }
   }
   if (c == 0 && t == 0) P.ctrl->num_steps = nsteps;
+#if GK_SM_SPAN
+  if (c == 0 && t == 0) {
+    P.ctrl->ts[510] = t_in;
+    P.ctrl->ts[511] = globaltimer();
+    P.ctrl->tag[510] = P.ctrl->tag[511] = 'x';
+  }
+#endif
   // bfs.hpp:171-175's final sweep: unreached slots were written -1 at init.
   // No CTA may exit while a peer can still read its shared memory.
   cl.sync();

@@ -520,26 +520,54 @@ __device__ void td_own(const BfsParams& P, SmemT& s, unsigned long long nown, ui
   // Parents, window by window: gather the window's logged claims into
   // shared memory (the slice's space), then store them in vertex order
   // (coalesced: measured faster than storing the log entries directly).
+  // The next window's log entries are loaded while this window is written
+  // back (kOwnPf per thread in registers, the rest of a full window read
+  // directly): the log's DRAM round trip leaves the per-window critical path.
   int32_t* par = reinterpret_cast<int32_t*>(sm);
   const long long id0 = w0 * 32;
   const int ws = 1 << wlog;
-  for (int win = 0; win < nwin; win++) {
+  constexpr int kOwnPf = 4;
+  auto next_win = [&](int w) {
+    while (w < nwin && s.own_cnt[w] == 0) w++;  // uniform
+    return w;
+  };
+  uint2 pf[kOwnPf];
+  auto fetch = [&](int w) {
+    const unsigned cnt = w < nwin ? s.own_cnt[w] : 0u;
+    const uint2* st = stage + ((int64_t)w << wlog);
+#pragma unroll
+    for (int k = 0; k < kOwnPf; k++) {
+      const unsigned j = threadIdx.x + k * kBlock;
+      pf[k] = j < cnt ? __ldcg(st + j) : make_uint2(0xffffffffu, 0u);
+    }
+  };
+  int win = next_win(0);
+  fetch(win);
+  for (int i = threadIdx.x; i < ws; i += kBlock) par[i] = -2;
+  __syncthreads();
+  while (win < nwin) {
     const unsigned cnt = s.own_cnt[win];
-    if (cnt == 0) continue;  // uniform
     const long long lo = id0 + ((long long)win << wlog);
-    for (int i = threadIdx.x; i < ws; i += kBlock) par[i] = -2;
-    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kOwnPf; k++)
+      if (pf[k].x != 0xffffffffu) par[pf[k].x] = (int32_t)pf[k].y;
     const uint2* st = stage + ((int64_t)win << wlog);
-    for (unsigned j = threadIdx.x; j < cnt; j += kBlock) {
+    for (unsigned j = threadIdx.x + kOwnPf * kBlock; j < cnt; j += kBlock) {
       const uint2 c = __ldcg(st + j);
       par[c.x] = (int32_t)c.y;
     }
+    const int nwin2 = next_win(win + 1);
+    fetch(nwin2);
     __syncthreads();
     for (int i = threadIdx.x; i < ws; i += kBlock) {
       const int32_t pv = par[i];
-      if (pv != -2) *parent_slot(P, (uint32_t)(lo + i)) = pv;
+      if (pv != -2) {
+        *parent_slot(P, (uint32_t)(lo + i)) = pv;
+        par[i] = -2;
+      }
     }
     __syncthreads();
+    win = nwin2;
   }
   OWN_MARK(5);
   if (blockIdx.x == 0 && threadIdx.x == 0 && GK_OWN_TRACE) {
