@@ -78,6 +78,8 @@ void free_graph(gk_graph* g) {
   if (g->batch_err) cudaFreeHost(g->batch_err);
   if (g->cm_peek) cudaFreeHost(g->cm_peek);
   for (cudaEvent_t e : g->batch_ev) cudaEventDestroy(e);
+  if (g->sg_exec) cudaGraphExecDestroy(g->sg_exec);
+  if (g->sg_graph) cudaGraphDestroy(g->sg_graph);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->stream) cudaStreamDestroy(g->stream);
@@ -220,17 +222,21 @@ cudaError_t trial_alloc(gk_graph* g, gk_trial* t, TrialBlocks* tb, cudaStream_t 
   if ((e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&t->parent), sz_par + cz + (small ? sz_book : 0), g->pool,
                                    s)))
     return e;
-  if (small) tb->book = nullptr;
-  else if ((e = cudaMallocFromPoolAsync(&tb->book, sz_book, g->pool, s))) return e;
   if (cz) tb->canaries.emplace_back(reinterpret_cast<char*>(t->parent) + sz_par, "parent");
-  Carver b{small ? reinterpret_cast<char*>(t->parent) + sz_par + cz : static_cast<char*>(tb->book), 0, cz, tb};
-  t->ctrl = reinterpret_cast<gk::Ctrl*>(b.take(sz_ctrl, "ctrl"));
-  t->steps = reinterpret_cast<gk_step*>(b.take(sz_steps, "steps"));
-  // the small-graph kernel keeps its bitmaps and lists in shared memory
+  // the small-graph kernel keeps its bitmaps and lists in shared memory: no
+  // scratch block.  (Order of the blocks: result, scratch, bookkeeping --
+  // gk_bfs_batch's overlapped trials reuse the pool's blocks in that order;
+  // allocating the small bookkeeping block second fragmented the pool and
+  // cost the batch a third of its rate.)
   if (!small) {
     if ((e = cudaMallocFromPoolAsync(&tb->work, work, g->pool, s))) return e;
     carve_work(g, t, tb, cz, wb, sz_q, sz_ch, sz_ol, sz_os, own);
   }
+  if (small) tb->book = nullptr;
+  else if ((e = cudaMallocFromPoolAsync(&tb->book, sz_book, g->pool, s))) return e;
+  Carver b{small ? reinterpret_cast<char*>(t->parent) + sz_par + cz : static_cast<char*>(tb->book), 0, cz, tb};
+  t->ctrl = reinterpret_cast<gk::Ctrl*>(b.take(sz_ctrl, "ctrl"));
+  t->steps = reinterpret_cast<gk_step*>(b.take(sz_steps, "steps"));
   for (auto& c : tb->canaries)
     if ((e = cudaMemsetAsync(c.first, kCanaryByte, cz, s))) return e;
   return cudaSuccess;
@@ -403,6 +409,56 @@ cudaError_t run_handoffs(gk_graph* g, gk::BfsParams p, cudaStream_t s, gk::Hand 
 #endif
   }
   return cudaSuccess;
+}
+
+// The small-graph trial as a CUDA graph: [pool allocation of result +
+// bookkeeping] -> [bfs_small].  Captured once per handle; the result's
+// address is the graph's (freed by the next trial before the relaunch).
+// Returns false when it cannot be built (the stream path runs instead).
+bool small_graph_ready(gk_graph* g, const gk::BfsParams& p, cudaStream_t s) {
+  if (g->sg_exec) return true;
+  if (g->sg_failed) return false;
+  g->sg_failed = true;
+  gk_trial t;
+  TrialBlocks tb;
+  gk::BfsParams q = p;
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaError_t e = trial_alloc(g, &t, &tb, s, false, true);
+  if (e == cudaSuccess) {
+    set_trial_ptrs(g, t, q);
+    e = gk::small_launch(q, g->small_cluster, s);
+  }
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(s, &graph);
+  if (e != cudaSuccess || ec != cudaSuccess || !graph) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return false;
+  }
+  cudaGraphNode_t nodes[16];
+  size_t nn = 16;
+  cudaGraphNode_t kn = nullptr;
+  if (cudaGraphGetNodes(graph, nodes, &nn) == cudaSuccess) {
+    for (size_t i = 0; i < nn; i++) {
+      cudaGraphNodeType ty;
+      if (cudaGraphNodeGetType(nodes[i], &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) kn = nodes[i];
+    }
+  }
+  cudaGraphExec_t exec = nullptr;
+  if (!kn || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return false;
+  }
+  g->sg_graph = graph;
+  g->sg_exec = exec;
+  g->sg_kernel = kn;
+  g->sg_trial = t;
+  g->sg_failed = false;
+  return true;
 }
 
 gk_status finish_graph(gk_graph* g, gk_graph** out) {
@@ -662,14 +718,41 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
   // kernel arguments (host work, the environment's tuning switches) ahead of
   // the trial; the trial's own buffers are filled in after its allocation
   gk::BfsParams p = make_params(g, t, source, alpha, beta, strategy, want_depth);
+  static const bool host_timing = getenv("GK_HOST_TIMING") != nullptr;  // diagnostics
+  // small graphs: the trial is one CUDA graph launch (allocation node +
+  // kernel); its arguments are set here, before the timed region
+  const bool as_graph = small && !g->canary && !getenv("GK_NO_SMALL_GRAPH") && small_graph_ready(g, p, s);
+  if (as_graph) {
+    set_trial_ptrs(g, g->sg_trial, p);
+    cudaKernelNodeParams kp{};
+    CK(cudaGraphKernelNodeGetParams(g->sg_kernel, &kp), "small-graph kernel node");
+    void* args[] = {&p};
+    kp.kernelParams = args;
+    kp.extra = nullptr;
+    CK(cudaGraphExecKernelNodeSetParams(g->sg_exec, g->sg_kernel, &kp), "small-graph kernel arguments");
+  }
+  const auto h0 = std::chrono::steady_clock::now();
   CK(cudaEventRecord(g->ev0, s), "event record");
-  CK(trial_alloc(g, &t, &tb, s, !small && use_own(g), small), "allocate trial scratch");
+  const auto h1 = std::chrono::steady_clock::now();
+  if (as_graph) {
+    t = g->sg_trial;
+  } else {
+    CK(trial_alloc(g, &t, &tb, s, !small && use_own(g), small), "allocate trial scratch");
+    set_trial_ptrs(g, t, p);
+  }
   g->parent = t.parent;
-  set_trial_ptrs(g, t, p);
-  if (small) CK(gk::small_launch(p, g->small_cluster, s), "launch small-graph bfs kernel");
+  const auto h2 = std::chrono::steady_clock::now();
+  if (as_graph) CK(cudaGraphLaunch(g->sg_exec, s), "launch small-graph trial");
+  else if (small) CK(gk::small_launch(p, g->small_cluster, s), "launch small-graph bfs kernel");
   else CK(gk::bfs_launch(p, g->launch, s), "launch bfs kernel");
   g->launches++;
+  const auto h3 = std::chrono::steady_clock::now();
   CK(cudaEventRecord(g->ev1, s), "event record");
+  if (host_timing) {
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    fprintf(stderr, "gk_bfs host: record ev0 %.1f us, alloc %.1f us, launch %.1f us\n", us(h0, h1), us(h1, h2),
+            us(h2, h3));
+  }
   gk::Ctrl& ctrl = g->last_ctrl;
   CK(cudaMemcpyAsync(&ctrl, t.ctrl, sizeof(ctrl), cudaMemcpyDeviceToHost, s), "read ctrl");
   CK(cudaStreamSynchronize(s), "bfs kernel");

@@ -362,6 +362,14 @@ struct gk_graph {
   long long launches = 0;  // traversal kernels launched (gk_bfs_launches)
   int cm_cluster = 0;
   int small_cluster = 0;  // gk_bfs_small.cu: CTAs of the single-cluster kernel for this graph (0: not used)
+  // gk_bfs on a small graph: one CUDA graph per handle holding the trial's
+  // allocation node and the cluster kernel (the kernel arguments are set
+  // per trial, ahead of the timed region)
+  cudaGraph_t sg_graph = nullptr;
+  cudaGraphExec_t sg_exec = nullptr;
+  cudaGraphNode_t sg_kernel = nullptr;
+  gk_trial sg_trial;
+  bool sg_failed = false;
   int64_t cm_max_scout = 0;
   bool cm_batch = false;  // gk_bfs_batch checks for hand-offs after every trial (sparse graphs)
   gk::Ctrl* cm_peek = nullptr;
