@@ -103,6 +103,14 @@ gk_status setup_graph(gk_graph* g, bool sorted) {
   CK(cudaEventCreate(&g->ev1), "event");
   CK(cudaMalloc(&g->acc, sizeof(unsigned long long) * 8), "alloc acc");
   CK(gk::bfs_configure(g->device, &g->launch), "configure bfs kernel");
+  if (const char* fg = getenv("GK_L2_FETCH")) {  // A/B: the L2's maximum fetch granularity (bytes)
+    size_t before = 0, after = 0;
+    cudaDeviceGetLimit(&before, cudaLimitMaxL2FetchGranularity);
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(fg));
+    cudaDeviceGetLimit(&after, cudaLimitMaxL2FetchGranularity);
+    fprintf(stderr, "L2 fetch granularity %zu -> %zu\n", before, after);
+    cudaGetLastError();
+  }
   if (getenv("GK_NO_FRONT_SMEM")) g->launch.smem_front_max = 0;  // tests: large-graph paths on small graphs
   // Cluster mode for chains of tiny top-down levels.  gk_bfs reads the
   // hand-off state with the control block it reads anyway; gk_bfs_batch

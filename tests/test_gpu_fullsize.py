@@ -112,7 +112,10 @@ def test_kron30_parity_vs_reference():
     assert R.L.gkr_graph_seal(h, 0, err, 256)
     rg = O.RefGraph(R, h)
     log = [f"kron30: n={rg.n} arcs={rg.m} (device graph in the reference's CsrGraph)"]
-    sources = rg.pick_sources(NSRC, SEED)
-    assert (sources == g.pick_sources(NSRC, SEED)).all()
+    # one source by default: the 145 GB graph, the reference's depth arrays
+    # and VerifyBfs's own BFS share the host's ~196 GB
+    ns = int(os.environ.get("GK_FULLSIZE_KRON30_NSRC", "1"))
+    sources = rg.pick_sources(max(ns, 1), SEED)
+    assert (sources == g.pick_sources(max(ns, 1), SEED)).all()
     _check_sources(rg, g, [int(s) for s in sources], log)
     print("\n".join(log))
