@@ -65,10 +65,9 @@ struct __align__(16) SmShared {
   uint32_t off[kSmCap];           // top-down: out_off of the listed vertex (m < 2^32)
   uint4 wl[2][kSmWon];            // won lists by level parity: {vertex, out_off, out-degree, 0} of the
                                   // vertices this CTA added to the frontier in a top-down level
-  unsigned long long cnt[3][4];   // level L in [L % 3]: {new vertices, degree total, a won list overflowed}
-  unsigned long long tot[4];      // cluster totals of the level just gathered
+  uint4 cin[3][16];               // level L in [L % 3], pushed by CTA r into every CTA's [r]:
+                                  // {new vertices, degree total, no won list, won-list length}
   uint4 red4[2][kSmWarps];        // per-warp partial sums, two alternating slots
-  int wpre[17];                   // exclusive prefix of the C won-list lengths of the last level
   unsigned nlong;
   unsigned nwon;
 };
@@ -143,52 +142,101 @@ __device__ int sm_list(SmShared& S, const uint32_t* bm, int wa, int wb, int& rs)
   return (int)total;
 }
 
-// Gather the C new slices of level buffer p into front / visited, clear the
-// local claims, and read the C counter pairs (after the level's last cluster
-// barrier).  Leaves the cluster totals in S.tot.
-__device__ void sm_gather(SmShared& S, cg::cluster_group& cl, int C, int W, int Wc, int p) {
-  // 16-byte DSMEM loads (Wc is a multiple of 4; slice words past a CTA's
-  // range stay zero, so the words past W gathered here are zero too)
-  for (int j = 4 * (int)threadIdx.x; j < W; j += 4 * kSmBlock) {
-    const int k = j / Wc;
-    const uint4 w = *reinterpret_cast<const uint4*>(cl.map_shared_rank(&S.slice[p][0], k) + (j - k * Wc));
-    *reinterpret_cast<uint4*>(&S.front[j]) = w;
-    uint4 v = *reinterpret_cast<const uint4*>(&S.vis[j]);
-    v.x |= w.x;
-    v.y |= w.y;
-    v.z |= w.z;
-    v.w |= w.w;
-    *reinterpret_cast<uint4*>(&S.vis[j]) = v;
-    *reinterpret_cast<uint4*>(&S.nxt[j]) = make_uint4(0u, 0u, 0u, 0u);
+// Level end, before the cluster barrier: this CTA's counters into every
+// CTA's cin[q][c] (DSMEM stores; the barrier's release / acquire orders
+// them), so after the barrier every CTA sums them locally.
+__device__ __forceinline__ void sm_push(SmShared& S, cg::cluster_group& cl, int C, int c, int q, uint4 v) {
+  if ((int)threadIdx.x < C) *cl.map_shared_rank(&S.cin[q][c], (int)threadIdx.x) = v;
+}
+
+struct SmTot {
+  long long cnt, sc;
+  bool lists;  // every CTA's won list holds its share of the new frontier
+};
+__device__ __forceinline__ SmTot sm_totals(const SmShared& S, int C, int q) {
+  SmTot r{0, 0, true};
+  for (int k = 0; k < C; k++) {
+    const uint4 v = S.cin[q][k];
+    r.cnt += v.x;
+    r.sc += v.y;
+    r.lists &= v.z == 0u;
   }
-  if (threadIdx.x < 32) {
-    unsigned long long a = 0, b = 0, f = 0;
-    if ((int)threadIdx.x < C) {
-      const unsigned long long* rc = cl.map_shared_rank(&S.cnt[p][0], (int)threadIdx.x);
-      a = rc[0];
-      b = rc[1];
-      f = rc[2];
-    }
+  return r;
+}
+
+// After the level's cluster barrier: gather the C new slices of level
+// buffer q into front / visited (16-byte DSMEM loads; Wc is a multiple of
+// 4 and slice words past a CTA's range stay zero), clear the local claims,
+// and -- when the next level is a top-down one over the won lists (wl
+// buffer rp, k entries) -- gather the lists too, in the same round trip:
+// thread t takes entries [4t, 4t+4), so one scan gives the degree prefix.
+__device__ void sm_gather(SmShared& S, cg::cluster_group& cl, int C, int W, int Wc, int q, bool with_list, int rp,
+                          int k, int& rs) {
+  const int t = threadIdx.x;
+  constexpr int kPerL = kSmWon / kSmBlock;
+  uint4 sl[kSmMaxW / 4 / kSmBlock];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_down_sync(kFull, a, o);
-      b += __shfl_down_sync(kFull, b, o);
-      f += __shfl_down_sync(kFull, f, o);
+  for (int i = 0; i < kSmMaxW / 4 / kSmBlock; i++) {
+    const int j = 4 * (t + i * kSmBlock);
+    sl[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (j < W) {
+      const int r = j / Wc;
+      sl[i] = *reinterpret_cast<const uint4*>(cl.map_shared_rank(&S.slice[q][0], r) + (j - r * Wc));
     }
-    if (threadIdx.x == 0) {
-      S.tot[0] = a;
-      S.tot[1] = b;
-      S.tot[2] = f;
-    }
-    int nw = (int)threadIdx.x < C ? (int)cl.map_shared_rank(&S.cnt[p][0], (int)threadIdx.x)[3] : 0;
-    int incl = nw;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(kFull, incl, o);
-      if ((int)threadIdx.x >= o) incl += y;
-    }
-    if ((int)threadIdx.x <= C && threadIdx.x < 17) S.wpre[threadIdx.x] = incl - nw;
   }
+  uint4 le[kPerL];
+  if (with_list) {
+    int pre[17];  // exclusive prefix of the C won-list lengths
+    pre[0] = 0;
+#pragma unroll
+    for (int r = 0; r < 16; r++) pre[r + 1] = pre[r] + (r < C ? (int)S.cin[q][r].w : 0);
+#pragma unroll
+    for (int e = 0; e < kPerL; e++) {
+      const int i = t * kPerL + e;
+      le[e] = make_uint4(0u, 0u, 0u, 0u);
+      if (i < k) {
+        int r = 0;
+#pragma unroll
+        for (int b = 8; b > 0; b >>= 1)
+          if (r + b < C && pre[r + b] <= i) r += b;
+        le[e] = cl.map_shared_rank(&S.wl[rp][0], r)[i - pre[r]];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kSmMaxW / 4 / kSmBlock; i++) {
+    const int j = 4 * (t + i * kSmBlock);
+    if (j < W) {
+      const uint4 w = sl[i];
+      *reinterpret_cast<uint4*>(&S.front[j]) = w;
+      uint4 v = *reinterpret_cast<const uint4*>(&S.vis[j]);
+      v.x |= w.x;
+      v.y |= w.y;
+      v.z |= w.z;
+      v.w |= w.w;
+      *reinterpret_cast<uint4*>(&S.vis[j]) = v;
+      *reinterpret_cast<uint4*>(&S.nxt[j]) = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  if (with_list) {  // ids, offsets and the exclusive degree prefix of the next frontier
+    unsigned sum = 0;
+#pragma unroll
+    for (int e = 0; e < kPerL; e++) sum += le[e].z;
+    unsigned tot;
+    unsigned x = sm_exscan(sum, &tot, S, rs);
+#pragma unroll
+    for (int e = 0; e < kPerL; e++) {
+      const int i = t * kPerL + e;
+      if (i < k) {
+        S.ids[i] = le[e].x;
+        S.off[i] = le[e].y;
+        S.pre[i] = x;
+      }
+      x += le[e].z;
+    }
+    if (t == 0) S.pre[k] = tot;
+  }
+  if (t == 0) S.nwon = 0u;  // the coming level's won list
   __syncthreads();
 }
 
@@ -269,6 +317,7 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
     S.nxt[j] = 0u;
   }
   for (int j = t; j < 3 * kSmSlice; j += kSmBlock) (&S.slice[0][0])[j] = 0u;
+  if (t == 0) S.nwon = 0u;  // the first level's won list (later levels: reset by sm_gather)
   __syncthreads();
   if (t == 0) {
     S.vis[src >> 5] |= 1u << (src & 31u);
@@ -292,7 +341,9 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
   int lvl = 0;
   unsigned L = 0;  // levels done (parity of the slice / counter buffers)
 
-  bool lists = false;  // every CTA's won list holds its share of the current frontier (uniform)
+  // the frontier list of the coming top-down level was gathered with the
+  // last level's slices (ids, offsets, degree prefix in ids / off / pre)
+  bool have_list = false;
   while (fsz > 0) {  // bfs.hpp:142
     if (P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha) {
       long long awake = fsz, old_awake;  // bfs.hpp:146
@@ -408,25 +459,20 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
           S.slice[(q3 + 1) % 3][j] = 0u;  // the next level's slice (last read two levels ago)
         }
         mine = sm_sum3(mine, 0u, 0u, S, rs).x;
-        if (t == 0) {
-          S.cnt[q3][0] = (unsigned long long)mine;
-          S.cnt[q3][1] = 0ull;
-          S.cnt[q3][2] = 1ull;  // no won lists after a bottom-up step
-          S.cnt[q3][3] = 0ull;
-        }
+        sm_push(S, cl, C, c, q3, make_uint4(mine, 0u, 1u, 0u));  // no won lists after a bottom-up step
         SM_MARK('r');
         cl.sync();
         SM_MARK('s');
-        sm_gather(S, cl, C, W, Wc, q3);
+        awake = sm_totals(S, C, q3).cnt;
+        sm_gather(S, cl, C, W, Wc, q3, false, 0, 0, rs);
         SM_MARK('t');
         L++;
-        awake = (long long)S.tot[0];
         sm_log(P, c, nsteps++, 'B', old_awake, awake, etc);
         lvl++;
       } while (awake >= old_awake || awake > P.n / P.beta);
       fsz = awake;
       scout = 1;  // bfs.hpp:156
-      lists = false;
+      have_list = false;
     } else {
       etc -= scout;  // bfs.hpp:158
       const int q3 = (int)(L % 3u), wp = (int)(L & 1u);
@@ -437,18 +483,8 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
       // the owners merge the C copies (two barriers, no per-claim traffic).
       const bool fewer = fsz <= kSmWon;  // uniform: fsz is a cluster total
       int k;
-      if (fewer && lists) {  // the frontier = the C won lists of the last level (offsets, degrees known)
-        const int rp = wp ^ 1;
+      if (have_list) {  // the C won lists of the last level, gathered after its barrier
         k = (int)fsz;
-        for (int i = t; i < k; i += kSmBlock) {
-          int r = 0;
-          while (r + 1 < C && S.wpre[r + 1] <= i) r++;
-          const int j = i - S.wpre[r];
-          const uint4 x = cl.map_shared_rank(&S.wl[rp][0], r)[j];
-          S.ids[i] = x.x;
-          S.off[i] = x.y;
-          S.pre[i] = x.z;
-        }
       } else {  // from the replicated front: all of it, or this CTA's slice
         k = fewer ? sm_list<false>(S, S.front, 0, W, rs) : sm_list<false>(S, S.front, wlo, whi, rs);
         for (int i = t; i < k; i += kSmBlock) {
@@ -459,10 +495,11 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
         }
       }
       SM_MARK('a');
-      __syncthreads();
-      if (t == 0) S.nwon = 0u;  // (ordered before the claims by the prefix's barriers)
       long long E;
-      {  // exclusive prefix of the degrees, 8 consecutive entries per thread
+      if (have_list) {
+        E = S.pre[k];  // the gather's scan wrote the prefix
+      } else {  // exclusive prefix of the degrees, kPer consecutive entries per thread
+        __syncthreads();
         constexpr int kPer = kSmCap / kSmBlock;
         const int i0 = t * kPer;
         uint32_t d[kPer];
@@ -481,8 +518,8 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
         }
         if (t == 0) S.pre[k] = (uint32_t)tot;
         E = tot;
+        __syncthreads();
       }
-      __syncthreads();
       SM_MARK('b');
       // ---- claims (bfs.hpp:77-84) ----
       const long long e0 = fewer ? E * c / C : 0, e1 = fewer ? E * (c + 1) / C : E;
@@ -606,22 +643,23 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
       if (fewer) cc = sums.x;
       sc = sums.y;
       const unsigned ovf_any = sums.z;
-      if (t == 0) {
-        S.cnt[q3][0] = (unsigned long long)cc;
-        S.cnt[q3][1] = (unsigned long long)sc;
-        S.cnt[q3][2] = ovf_any ? 1ull : 0ull;
-        S.cnt[q3][3] = (unsigned long long)min(S.nwon, (unsigned)kSmWon);
-      }
+      __syncthreads();  // S.nwon final
+      sm_push(S, cl, C, c, q3, make_uint4((unsigned)cc, (unsigned)sc, ovf_any ? 1u : 0u, min(S.nwon, (unsigned)kSmWon)));
       SM_MARK('f');
       cl.sync();  // every claim has landed in its owner's slice
       SM_MARK('g');
-      sm_gather(S, cl, C, W, Wc, q3);
+      const SmTot tt = sm_totals(S, C, q3);
+      // the next level's direction (the test at the top of the loop, same
+      // totals): a top-down level over a small frontier takes the won lists
+      // now, in the slices' round trip
+      const bool next_td = !(P.strategy == GK_BFS_DIRECTION_OPTIMIZING && tt.sc > etc / P.alpha);
+      have_list = next_td && tt.lists && tt.cnt > 0 && tt.cnt <= kSmWon;
+      sm_gather(S, cl, C, W, Wc, q3, have_list, wp, (int)tt.cnt, rs);
       SM_MARK('h');
       L++;
       const long long fsize = fsz;
-      fsz = (long long)S.tot[0];
-      scout = (long long)S.tot[1];
-      lists = S.tot[2] == 0;
+      fsz = tt.cnt;
+      scout = tt.sc;
       sm_log(P, c, nsteps++, 'T', fsize, scout, etc);
       lvl++;
     }
