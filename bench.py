@@ -446,11 +446,19 @@ def main():
     from paper_1508_03619_b200 import PinnedBuffer
 
     # ---------------- our arm ----------------
+    fallback = None
     if cfg["kind"] != "grid" and args.multi == "sharded" and (world > 1 or args.emulate_ranks > 0):
-        run_sharded(args, cfg, rank, world, local, dist)
-        if dist:
-            dist.destroy_process_group()
-        return
+        from paper_1508_03619_b200.dist import ShardConnectError
+        try:
+            run_sharded(args, cfg, rank, world, local, dist)
+            if dist:
+                dist.destroy_process_group()
+            return
+        except ShardConnectError as ex:  # raised on every rank together (dist.ShardedBfs)
+            fallback = f"sharded traversal unavailable ({ex}); ran source-parallel replicas instead"
+            print(f"rank {rank}: {fallback}", file=sys.stderr, flush=True)
+            import gc
+            gc.collect()
     g, build_s = build_graph(cfg, local)
     sources = [int(s) for s in g.pick_sources(K, SEED + rank)]
     warm = sources[: max(W, 0)] if W <= K else (sources * (W // K + 1))[:W]
@@ -567,7 +575,8 @@ def main():
         "vs_baseline": None, "dtype": "int32", "data": "synthetic (seeded generator, no dataset)",
         "config": line_config(cfg, g.n, g.m, K),
         "run": {"parallelism": "single GPU" if world == 1 else
-                f"{world} source-parallel replicas (whole graph per GPU, no data-path collective)",
+                f"{world} source-parallel replicas (whole graph per GPU, no data-path collective)"
+                + (f" -- {fallback}" if fallback else ""),
                 "trial": "one gk_bfs: pool allocation of the result and all scratch, their initialisation, "
                          "the traversal kernel, scratch release -- CUDA events around all of it",
                 "device_build_s": round(build_s, 2), "timed_region_wall_s": round(wall, 4),

@@ -183,6 +183,11 @@ class ShardGroup:
         return [(tags.raw[i:i + 1].decode(), (ts[i] - ts[0]) * 1e-6) for i in range(k)]
 
 
+class ShardConnectError(GapkitError):
+    """The ranks could not map each other's buffers (peer access / CUDA IPC
+    unavailable); raised on every rank of the group together."""
+
+
 class ShardedBfs:
     """This process's rank of a multi-GPU group (one process per GPU;
     torch.distributed initialised).  The constructor wires the group: IPC
@@ -206,7 +211,16 @@ class ShardedBfs:
         blob = C.create_string_buffer(int(L.gk_shard_handle_size()))
         _check(L.gk_shard_export(shard._h, blob), "gk_shard_export")
         joined = b"".join(allgather(bytes(blob.raw)))
-        _check(L.gk_shard_connect(shard._h, joined), "gk_shard_connect")
+        # every rank reports whether it mapped its peers before anyone acts on
+        # it, so a rank that cannot (no peer access / IPC) fails the whole
+        # group together instead of leaving the others in a collective
+        st = L.gk_shard_connect(shard._h, joined)
+        why = b"" if st == 0 else (_lib.last_error() or f"status {st}").encode()[:200]
+        oks = allgather(b"ok" if st == 0 else b"fail:" + why)
+        bad = [i for i, o in enumerate(oks) if o != b"ok"]
+        if bad:
+            raise ShardConnectError(f"gk_shard_connect failed on rank(s) {bad}: "
+                                    + "; ".join(oks[i].decode(errors="replace") for i in bad))
         barrier()  # every rank has published its dead words (gk_shard_export)
         _check(L.gk_shard_gather_dead(shard._h), "gk_shard_gather_dead")
         barrier()
