@@ -46,6 +46,14 @@ constexpr int kSmCap = 8192;   // list entries per CTA (>= one CTA's slice of id
 constexpr int kSmSlice = kSmCap / 32;  // owned bitmap words per CTA, at most
 constexpr int kSmWon = 2048;   // won-list entries per CTA (more: the next level lists from the bitmap)
 constexpr int kSmRounds = 4;
+#ifndef GK_SM_REDE
+#define GK_SM_REDE 4096
+#endif
+// Top-down levels expanding at most this many edges run redundantly in
+// every CTA (no cluster barrier, no DSMEM); <= kSmCap, so the new frontier
+// list always fits.
+constexpr int kSmRedE = GK_SM_REDE;
+static_assert(kSmRedE <= kSmCap, "a redundant level's new frontier must fit the list");
 #ifndef GK_SM_BUW
 #define GK_SM_BUW 4  // 512 threads x 4 in flight: 8 -10%, 16 -30% (kron16)
 #endif
@@ -279,6 +287,47 @@ __device__ void sm_log(const BfsParams& P, int c, long long idx, int dir, long l
   }
 }
 
+// Back to cluster-wide levels after redundant ones: no CTA still reads an
+// earlier level's slices once all reached the first barrier; every slice
+// this CTA owns is zeroed; the second barrier orders that before the
+// level's claims.
+__device__ __forceinline__ void sm_resync(SmShared& S, cg::cluster_group& cl, bool& synced, int wlo, int whi) {
+  if (synced) return;
+  cl.sync();
+  for (int j = threadIdx.x; j < whi - wlo; j += kSmBlock) {
+    S.slice[0][j] = 0u;
+    S.slice[1][j] = 0u;
+    S.slice[2][j] = 0u;
+  }
+  cl.sync();
+  synced = true;
+}
+
+// Exclusive prefix of the k list degrees in S.pre (kPer consecutive entries
+// per thread), S.pre[k] = total; returns the total.  Ends with a barrier.
+__device__ long long sm_prefix(SmShared& S, int k, int& rs) {
+  __syncthreads();
+  constexpr int kPer = kSmCap / kSmBlock;
+  const int i0 = threadIdx.x * kPer;
+  uint32_t d[kPer];
+  unsigned sum = 0;
+#pragma unroll
+  for (int q = 0; q < kPer; q++) {
+    d[q] = i0 + q < k ? S.pre[i0 + q] : 0u;
+    sum += d[q];
+  }
+  unsigned tot;
+  unsigned x = sm_exscan(sum, &tot, S, rs);
+#pragma unroll
+  for (int q = 0; q < kPer; q++) {
+    if (i0 + q < k) S.pre[i0 + q] = (uint32_t)x;
+    x += d[q];
+  }
+  if (threadIdx.x == 0) S.pre[k] = (uint32_t)tot;
+  __syncthreads();
+  return tot;
+}
+
 __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
   extern __shared__ uint4 sm_raw[];
   SmShared& S = *reinterpret_cast<SmShared*>(sm_raw);
@@ -344,11 +393,15 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
   // the frontier list of the coming top-down level was gathered with the
   // last level's slices (ids, offsets, degree prefix in ids / off / pre)
   bool have_list = false;
+  // every CTA passed the last level's cluster barrier and gather (false after
+  // redundant levels: the slices are re-zeroed between two barriers first)
+  bool synced = true;
   while (fsz > 0) {  // bfs.hpp:142
     if (P.strategy == GK_BFS_DIRECTION_OPTIMIZING && scout > etc / P.alpha) {
       long long awake = fsz, old_awake;  // bfs.hpp:146
       do {                               // bfs.hpp:149-154
         old_awake = awake;
+        sm_resync(S, cl, synced, wlo, whi);
         const int q3 = (int)(L % 3u);
         // ---- bottom-up over this CTA's pending vertices (slice[q3] is zero) ----
         if (t == 0) S.nlong = 0u;
@@ -495,32 +548,80 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
         }
       }
       SM_MARK('a');
-      long long E;
-      if (have_list) {
-        E = S.pre[k];  // the gather's scan wrote the prefix
-      } else {  // exclusive prefix of the degrees, kPer consecutive entries per thread
-        __syncthreads();
-        constexpr int kPer = kSmCap / kSmBlock;
-        const int i0 = t * kPer;
-        uint32_t d[kPer];
-        unsigned sum = 0;
-#pragma unroll
-        for (int q = 0; q < kPer; q++) {
-          d[q] = i0 + q < k ? S.pre[i0 + q] : 0u;
-          sum += d[q];
-        }
-        unsigned tot;
-        unsigned x = sm_exscan(sum, &tot, S, rs);
-#pragma unroll
-        for (int q = 0; q < kPer; q++) {
-          if (i0 + q < k) S.pre[i0 + q] = (uint32_t)x;
-          x += d[q];
-        }
-        if (t == 0) S.pre[k] = (uint32_t)tot;
-        E = tot;
-        __syncthreads();
-      }
+      const long long E = have_list ? (long long)S.pre[k]  // the gather's (or last level's) scan wrote the prefix
+                                    : sm_prefix(S, k, rs);
       SM_MARK('b');
+      if (k == fsz && E <= kSmRedE) {  // uniform: the whole frontier is listed in every CTA
+        // ---- redundant level: every CTA expands the whole frontier against
+        // its own copy of visited (the copies are identical), so every CTA
+        // claims the same set; the owner of a claimed vertex stores its
+        // parent (one writer).  No cluster barrier, no DSMEM ----
+        for (long long eb = t; eb < E; eb += kSmTdW * kSmBlock) {
+          uint32_t u[kSmTdW], w[kSmTdW];
+          bool ok[kSmTdW];
+#pragma unroll
+          for (int q = 0; q < kSmTdW; q++) {
+            const long long e = eb + (long long)q * kSmBlock;
+            ok[q] = e < E;
+            u[q] = w[q] = 0u;
+            if (ok[q]) {
+              int lo = 0, hi = k;
+              while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if ((long long)S.pre[mid] <= e) lo = mid;
+                else hi = mid;
+              }
+              u[q] = S.ids[lo];
+              w[q] = ld_nb(P.out_nb + (S.off[lo] + (uint32_t)(e - S.pre[lo])));
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kSmTdW; q++) {
+            if (!ok[q] || sm_bit(S.vis, w[q]) || sm_bit(S.nxt, w[q])) continue;
+            const uint32_t bit = 1u << (w[q] & 31u), ww = w[q] >> 5;
+            if (!(atomicOr(&S.nxt[ww], bit) & bit) && (int)ww >= wlo && (int)ww < whi)
+              P.parent[w[q]] = (int32_t)u[q];  // bfs.hpp:77-84
+          }
+        }
+        __syncthreads();
+        // the new frontier (every vertex claimed here was unvisited): its
+        // list with offsets and degrees for the next level, the counters
+        const int kn = sm_list<false>(S, S.nxt, 0, W, rs);
+        unsigned scl = 0;
+        for (int i = t; i < kn; i += kSmBlock) {
+          const uint32_t v = S.ids[i];
+          const int64_t o0 = offv(P, P.out_off, v), o1 = offv(P, P.out_off, v + 1);
+          const uint32_t dg = (uint32_t)(o1 - o0);
+          S.off[i] = (uint32_t)o0;
+          S.pre[i] = dg;
+          scl += encode ? (dg ? dg : 1u) : dg;  // -old of bfs.hpp:83 / the rescan pass of bfs.hpp:161-167
+          const int vw = (int)(v >> 5);
+          if (P.want_depth && vw >= wlo && vw < whi) P.depth[v] = lvl + 1;
+        }
+        scl = sm_sum3(scl, 0u, 0u, S, rs).x;
+        for (int j = 4 * t; j < W; j += 4 * kSmBlock) {
+          const uint4 x = *reinterpret_cast<const uint4*>(&S.nxt[j]);
+          uint4 v = *reinterpret_cast<const uint4*>(&S.vis[j]);
+          v.x |= x.x;
+          v.y |= x.y;
+          v.z |= x.z;
+          v.w |= x.w;
+          *reinterpret_cast<uint4*>(&S.vis[j]) = v;
+          *reinterpret_cast<uint4*>(&S.front[j]) = x;
+          *reinterpret_cast<uint4*>(&S.nxt[j]) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        sm_prefix(S, kn, rs);
+        L++;
+        const long long fsize = fsz;
+        fsz = kn;
+        scout = scl;
+        have_list = true;
+        synced = false;
+        sm_log(P, c, nsteps++, 'T', fsize, scout, etc);
+        lvl++;
+        continue;
+      }
+      sm_resync(S, cl, synced, wlo, whi);
       // ---- claims (bfs.hpp:77-84) ----
       const long long e0 = fewer ? E * c / C : 0, e1 = fewer ? E * (c + 1) / C : E;
       long long cc = 0, sc = 0;
