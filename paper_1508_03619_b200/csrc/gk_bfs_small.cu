@@ -55,12 +55,16 @@ constexpr int kSmRounds = 4;
 constexpr int kSmRedE = GK_SM_REDE;
 static_assert(kSmRedE <= kSmCap, "a redundant level's new frontier must fit the list");
 #ifndef GK_SM_BUW
-#define GK_SM_BUW 4  // 512 threads x 4 in flight: 8 -10%, 16 -30% (kron16)
+#define GK_SM_BUW 2  // slots x in-neighbours per round: 2 x 8 (kron16 +2% over 4 x 4; 16 x 1, 3 x 8 equal, 2 x 16 -1%)
 #endif
 #ifndef GK_SM_TDW
 #define GK_SM_TDW 4
 #endif
 constexpr int kSmBuW = GK_SM_BUW;  // bottom-up: pending vertices per thread in flight
+#ifndef GK_SM_BUR
+#define GK_SM_BUR 8
+#endif
+constexpr int kSmBuR = GK_SM_BUR;  // bottom-up: in-neighbours per vertex per round
 constexpr int kSmTdW = GK_SM_TDW;  // top-down: edges per thread in flight   // bottom-up: 4-neighbour rounds per thread before the warp takes a list
 
 struct __align__(16) SmShared {
@@ -438,31 +442,35 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
 #pragma unroll
             for (int q = 0; q < kSmBuW; q++) any |= live[q];
             if (!any) break;
-            uint32_t u[kSmBuW][4];
+            uint32_t u[kSmBuW][kSmBuR];
 #pragma unroll
             for (int q = 0; q < kSmBuW; q++)
 #pragma unroll
-              for (int j = 0; j < 4; j++) u[q][j] = (live[q] && b[q] + j < e[q]) ? ld_nb(P.in_nb + b[q] + j) : kNoVertex;
+              for (int j = 0; j < kSmBuR; j++)
+                u[q][j] = (live[q] && b[q] + j < e[q]) ? ld_nb(P.in_nb + b[q] + j) : kNoVertex;
 #pragma unroll
             for (int q = 0; q < kSmBuW; q++) {
               if (!live[q]) continue;
               int hit = -1;
 #pragma unroll
-              for (int j = 3; j >= 0; j--)
+              for (int j = kSmBuR - 1; j >= 0; j--)
                 if (u[q][j] != kNoVertex && sm_bit(S.front, u[q][j])) hit = j;
               bool done = false;
               if (hit >= 0) {  // the first in-neighbour in the frontier (bfs.hpp:55-60)
-                const uint32_t par = hit == 0 ? u[q][0] : hit == 1 ? u[q][1] : hit == 2 ? u[q][2] : u[q][3];
+                uint32_t par = u[q][0];
+#pragma unroll
+                for (int j = 1; j < kSmBuR; j++)
+                  if (hit == j) par = u[q][j];
                 P.parent[v[q]] = (int32_t)par;
                 if (P.want_depth) P.depth[v[q]] = lvl + 1;
                 atomicOr(&S.slice[q3][(v[q] >> 5) - wlo], 1u << (v[q] & 31u));
                 done = true;
               } else {
-                b[q] += 4;
+                b[q] += kSmBuR;
                 if (b[q] >= e[q]) {
                   done = true;  // whole list scanned: not reached at this level
                 } else if (++rounds[q] == kSmRounds) {
-                  longl[atomicAdd(&S.nlong, 1u)] = v[q];  // resumes at in_off + 4 * kSmRounds
+                  longl[atomicAdd(&S.nlong, 1u)] = v[q];  // resumes at in_off + kSmBuR * kSmRounds
                   done = true;
                 }
               }
@@ -485,7 +493,7 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
         for (int i = (int)warp; i < nl; i += kSmWarps) {  // long lists: a warp per vertex
           const uint32_t v = longl[i];
           const int64_t le = offv(P, P.in_off, v + 1);
-          for (int64_t j = offv(P, P.in_off, v) + 4 * kSmRounds; j < le; j += 32) {
+          for (int64_t j = offv(P, P.in_off, v) + kSmBuR * kSmRounds; j < le; j += 32) {
             const int64_t jj = j + lane;
             uint32_t u = 0;
             bool h = false;
