@@ -8,24 +8,29 @@
 // (16, or 8 if the device will not co-schedule 16) each hold a full copy of
 // the visited and frontier bitmaps in shared memory and own a slice of the
 // vertex ids (CTA c: bitmap words [c*Wc, (c+1)*Wc)).  One level is:
-//   top-down (bfs.hpp:68-91): the frontier is listed from the replicated
-//     front bitmap (every CTA lists it when it fits kSmCap entries and takes
-//     1/C of its edges; otherwise each CTA lists its own slice); an edge to a
-//     vertex unvisited in the local copy is claimed in the CTA's local next
-//     bitmap (shared-memory atomic) and the claimer stores the parent --
-//     racing claimers in different CTAs store valid parents, as on the CPU;
-//     cluster barrier; each CTA ORs the C next copies over its slice
-//     (DSMEM), keeps the unvisited bits, sums their degrees
-//     (max(deg,1) = -old of bfs.hpp:83, or deg for kTopDownRescan,
-//     bfs.hpp:161-167);
+//   top-down (bfs.hpp:68-91), by the frontier's size:
+//     * <= kSmRedE edges: every CTA expands the whole frontier against its
+//       own (identical) visited copy -- the same claimed set everywhere, the
+//       owner of a vertex stores its parent; no barrier, no DSMEM;
+//     * <= kSmWon vertices: every CTA holds the whole frontier list (the
+//       won lists of the last level, gathered with its slices) and takes
+//       1/C of the edges; a claim goes to the owner's slice as one DSMEM
+//       atomicOr and the single winner stores the parent, keeps the degree
+//       it read with the claim (-old of bfs.hpp:83, or deg for
+//       kTopDownRescan, bfs.hpp:161-167) and lists the vertex;
+//     * larger: each CTA expands its own slice, claims in a local bitmap
+//       (racing claimers store valid parents, as on the CPU), and after a
+//       barrier the owners OR the C copies over DSMEM and sum the degrees;
 //   bottom-up (bfs.hpp:47-66): each CTA scans its own pending vertices'
 //     in-lists in ascending order against the replicated front -- the first
 //     hit is the parent, exactly the reference's choice;
-//   then (both) cluster barrier, and every CTA gathers the C new slices over
-//     DSMEM into its front and visited copies and sums the C counter pairs,
-//     so every CTA takes the same alpha/beta decision (bfs.hpp:139-169).
-// The step log, counters and results are the grid kernel's; the launch is
-// one cudaLaunchKernelEx per trial (no memsets: the kernel initialises the
+//   then: each CTA pushes its counters into every CTA (DSMEM stores), one
+//     cluster barrier, and every CTA gathers the C new slices (and the won
+//     lists, when a small top-down level follows) into its own copies and
+//     sums the counters, so every CTA takes the same alpha/beta decision
+//     (bfs.hpp:139-169).
+// The step log, counters and results are the grid kernel's; the trial is one
+// CUDA graph launch (pool allocation node + this kernel; it initialises the
 // control block, the parent array and its bitmaps itself).
 #include <cooperative_groups.h>
 
