@@ -84,6 +84,8 @@ void free_graph(gk_graph* g) {
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->stream) cudaStreamDestroy(g->stream);
   if (g->cstream) cudaStreamDestroy(g->cstream);
+  if (g->cstream2) cudaStreamDestroy(g->cstream2);
+  if (g->cs2_done) cudaEventDestroy(g->cs2_done);
   delete g;
 }
 
@@ -830,6 +832,11 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
   std::lock_guard<std::mutex> lock(g->mu);
   CK(cudaSetDevice(g->device), "cudaSetDevice");
   if (!g->cstream) CK(cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking), "stream");
+  const bool split = getenv("GK_BATCH_SPLIT") && atoi(getenv("GK_BATCH_SPLIT")) != 0;
+  if (split && !g->cstream2) {
+    CK(cudaStreamCreateWithFlags(&g->cstream2, cudaStreamNonBlocking), "stream");
+    CK(cudaEventCreateWithFlags(&g->cs2_done, cudaEventDisableTiming), "event");
+  }
   const size_t nev = 3 * (size_t)count;  // per trial: start, end, copy done
   while (g->batch_ev.size() < nev) {
     cudaEvent_t e;
@@ -902,9 +909,19 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     if ((e = cudaMemcpyAsync(errs + i, &t.ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;
     if (tb.book && (e = cudaFreeAsync(tb.book, s))) break;
     if ((e = cudaStreamWaitEvent(cs, ev[3 * i + 1], 0))) break;
-    if (parents_out && parents_out[i] &&
-        (e = cudaMemcpyAsync(parents_out[i], t.parent, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, cs)))
-      break;
+    if (parents_out && parents_out[i]) {
+      // GK_BATCH_SPLIT: the two halves on two copy streams (two DMA engines)
+      const size_t bytes = sizeof(int32_t) * g->n, half = split ? (bytes / 2 + 255) & ~size_t(255) : bytes;
+      if ((e = cudaMemcpyAsync(parents_out[i], t.parent, half, cudaMemcpyDeviceToHost, cs))) break;
+      if (half < bytes) {
+        if ((e = cudaStreamWaitEvent(g->cstream2, ev[3 * i + 1], 0))) break;
+        if ((e = cudaMemcpyAsync(reinterpret_cast<char*>(parents_out[i]) + half, reinterpret_cast<char*>(t.parent) + half,
+                                 bytes - half, cudaMemcpyDeviceToHost, g->cstream2)))
+          break;
+        if ((e = cudaEventRecord(g->cs2_done, g->cstream2))) break;
+        if ((e = cudaStreamWaitEvent(cs, g->cs2_done, 0))) break;
+      }
+    }
     if (i + 1 < count) {
       if ((e = cudaFreeAsync(t.parent, cs))) break;
     } else {
@@ -912,6 +929,7 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     }
     if ((e = cudaEventRecord(ev[3 * i + 2], cs))) break;
   }
+  if (g->cstream2) cudaStreamSynchronize(g->cstream2);
   cudaError_t e2 = cudaStreamSynchronize(s), e3 = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = e2 != cudaSuccess ? e2 : e3;
   if (e != cudaSuccess) return fail(GK_ERR_CUDA, std::string("bfs batch: ") + cudaGetErrorString(e));

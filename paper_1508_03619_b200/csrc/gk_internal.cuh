@@ -350,6 +350,8 @@ struct gk_graph {
   int32_t depth_valid = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t cstream = nullptr;  // D2H stream of gk_bfs_batch (created on first use)
+  cudaStream_t cstream2 = nullptr;  // second D2H stream (GK_BATCH_SPLIT)
+  cudaEvent_t cs2_done = nullptr;
   int* batch_err = nullptr;        // pinned: per-trial kernel error codes of gk_bfs_batch
   bool batch_warm = false;         // the pool holds three trials' blocks (gk_bfs_batch)
   int32_t batch_err_cap = 0;
