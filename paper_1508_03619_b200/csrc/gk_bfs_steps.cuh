@@ -111,7 +111,9 @@ __device__ __forceinline__ void claim4(const BfsParams& P, const QApp& qa, const
 #pragma unroll
     for (int k = 0; k < 4; k++) {
       if (!((x[k] >> (v[k] & 31u)) & 1u)) {
+#ifndef GK_TD_NO_PARENT  // diagnostic A/B only (results invalid without it)
         st_parent(parent_slot(P, v[k]), (int32_t)u[k]);
+#endif
         atomicOr(nextbm + (v[k] >> 5), 1u << (v[k] & 31u));  // result unused -> RED
       }
     }
