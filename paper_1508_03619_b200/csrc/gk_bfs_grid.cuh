@@ -30,7 +30,10 @@ constexpr long long kPushFactor = GK_PUSH_FACTOR;  // pushed bottom-up step when
 // kResume: the launch continues a traversal the cluster kernel handed back
 // (a separate instantiation, so the fresh traversal's code is unchanged).
 template <bool kResume>
-__global__ void __launch_bounds__(kBlock, 2) bfs_persistent(BfsParams P) {
+#ifndef GK_MINB
+#define GK_MINB 2  // CTAs per SM the register allocation must allow (64 registers at 2)
+#endif
+__global__ void __launch_bounds__(kBlock, GK_MINB) bfs_persistent(BfsParams P) {
   extern __shared__ uint4 dyn_smem[];
   __shared__ SmemT s;
   unsigned ph = 0;
