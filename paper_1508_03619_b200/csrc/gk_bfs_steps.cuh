@@ -699,8 +699,11 @@ constexpr int kBuSlots = GK_BU_SLOTS;
 #endif
 constexpr int kBuListWords = 512;  // per warp: 1024 uint16 pending ids
 constexpr size_t kBuListBytes = (size_t)kWarps * kBuListWords * 4;
-constexpr int kPerRound = 4;     // in-neighbours tested per slot per round
-constexpr int kLaneRounds = 12;  // rounds before a list is deferred to the long list
+#ifndef GK_BU_PER_ROUND
+#define GK_BU_PER_ROUND 4
+#endif
+constexpr int kPerRound = GK_BU_PER_ROUND;  // in-neighbours tested per slot per round
+constexpr int kLaneRounds = 48 / GK_BU_PER_ROUND;  // rounds before a list is deferred to the long list
 constexpr int kLaneScan = kPerRound * kLaneRounds;  // in-neighbours a lane tests (4-entry rounds)
 constexpr int kSparseScan = kLaneScan;  // entries sp_scan tests before deferring a list to bu_long
 
