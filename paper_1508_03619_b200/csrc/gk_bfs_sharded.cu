@@ -54,7 +54,8 @@ __device__ void rank_params(BfsParams& Q, const BfsParams& P0, const ShardTab& T
   Q = P0;
   const ShardView& v = T.v[r];
   Q.out_off = Q.in_off = v.off;
-  Q.off32 = nullptr;  // rank-local rows: the int64 offsets
+  Q.off32 = v.off32;  // the rank's rows in compact form (shifted like off), or null
+  Q.off_hi[0] = v.off_hi;
   Q.out_nb = Q.in_nb = v.nb;
   Q.parent = v.parent;
   Q.depth = v.depth;

@@ -214,6 +214,8 @@ const void* bfs_resume_c_fn();
 // claims) are full-n and replicated; parent/depth cover the owned range.
 struct ShardView {
   const int64_t* off;  // shifted: off[v] for owned v (row of v - lo)
+  const uint32_t* off32;  // shifted compact form of off (BfsParams::off32), or null
+  uint32_t off_hi;        // global id of the first owned vertex whose offset is >= 2^32
   const uint32_t* nb;  // neighbour ids are global
   int32_t* parent;     // shifted like off; a registered buffer peers map (remote claims store here)
   int32_t* depth;      // shifted, or null

@@ -37,6 +37,8 @@ struct gk_shard {
   int64_t n = 0, lo = 0, hi = 0, nloc = 0, block = 0, m = 0;
   int64_t m_total = 0, live_total = 0;
   int64_t* off = nullptr;  // owned rows, local offsets (row i = vertex lo + i)
+  uint32_t* off32 = nullptr;  // their compact form (m < 2^33), or null
+  uint32_t off_hi = 0xffffffffu;  // global id of the carry vertex
   uint32_t* nb = nullptr;
   uint32_t* bm = nullptr;    // 4 full-n bitmaps (visited, front/next pair, claims), peer-mapped
   uint32_t* dead = nullptr;  // full-n dead bitmap (replicated graph layout)
@@ -123,6 +125,19 @@ gk_status shard_setup(gk_shard* s) {
   // owned words from the owned rows (undirected: in-degree = out-degree)
   int64_t live = 0;
   SCK(gk::dead_bitmap(s->off, s->nloc, s->dead + s->lo / 32, &live, nullptr), "dead bitmap");
+  // the rows' compact offsets, read by the sharded kernel's offset loads
+  // like the single-device kernel's (gk_capi.cu setup_graph)
+  if (s->m < (int64_t(2) << 32) && !getenv("GK_NO_OFF32")) {
+    uint32_t* hi = nullptr;
+    SCK(cudaMalloc(&s->off32, sizeof(uint32_t) * (size_t)(s->nloc + 1) + 64), "alloc compact offsets");
+    SCK(cudaMalloc(&hi, sizeof(uint32_t)), "alloc compact offsets");
+    SCK(cudaMemset(hi, 0xff, sizeof(uint32_t)), "compact offsets");
+    SCK(gk::compact_offsets(s->off, s->nloc, s->off32, hi, (int)(s->m >> 32), nullptr), "compact offsets");
+    uint32_t hl = 0xffffffffu;
+    SCK(cudaMemcpy(&hl, hi, sizeof(hl), cudaMemcpyDeviceToHost), "compact offsets");
+    cudaFree(hi);
+    s->off_hi = hl == 0xffffffffu ? 0xffffffffu : (uint32_t)(s->lo + hl);
+  }
   if (s->rank == 0) {
     SCK(cudaMalloc(&s->x, sizeof(gk::XCtrl)), "alloc cross-rank control");
     SCK(cudaMemset(s->x, 0, sizeof(gk::XCtrl)), "cross-rank control");
@@ -142,8 +157,8 @@ void shard_free(gk_shard* s) {
   if (!s) return;
   cudaSetDevice(s->device);
   for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
-  for (void* p : {(void*)s->off, (void*)s->nb, (void*)s->bm, (void*)s->dead, (void*)s->parent, (void*)s->x,
-                  (void*)s->acc}) cudaFree(p);
+  for (void* p : {(void*)s->off, (void*)s->off32, (void*)s->nb, (void*)s->bm, (void*)s->dead, (void*)s->parent,
+                  (void*)s->x, (void*)s->acc}) cudaFree(p);
   if (s->pool) cudaMemPoolDestroy(s->pool);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
@@ -246,6 +261,8 @@ cudaError_t trial_alloc(gk_shard* s, ShardTrial* t, bool depth, int ctas, cudaSt
 gk::ShardView view_of(const gk_shard* s, const ShardTrial& t) {
   gk::ShardView v{};
   v.off = s->off - s->lo;  // shifted: off[v] for owned v
+  v.off32 = s->off32 ? s->off32 - s->lo : nullptr;
+  v.off_hi = s->off_hi;
   v.nb = s->nb;
   v.parent = s->parent - s->lo;
   v.depth = t.depth ? t.depth - s->lo : nullptr;
