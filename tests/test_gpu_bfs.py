@@ -334,6 +334,27 @@ def test_cluster_mode_parity(chain_graphs, strategy, grid_kernel):
         assert seen_k, name  # the cluster kernel ran
 
 
+@pytest.mark.parametrize("strategy", [0, 1, 2])
+def test_chains_in_small_kernel(chain_graphs, strategy, both_kernels):
+    """The same long chains of tiny levels through the single-cluster kernel
+    (thousands of redundant levels without a cluster barrier, then the way
+    back to cluster-wide levels) and through the grid kernel: depths,
+    parents, schedule and counters against the oracle."""
+    for name, (g, dg) in chain_graphs.items():
+        for s in O.pick_sources(g, 2, 7):
+            s = int(s)
+            res = dg.bfs(s, strategy=strategy, depth=True, counts=True)
+            key = (name, s, strategy, both_kernels)
+            assert (res.depth == O.bfs_depths(g, s)).all(), key
+            assert O.verify_bfs(g, s, res.parent)[0], key
+            rp = O.bfs_replay(g, s, strategy=strategy)
+            assert res.schedule == rp.dirs, key
+            assert [x[2] for x in res.steps] == rp.result, key
+            assert [x[3] for x in res.steps] == rp.edges_to_check, key
+            if both_kernels == "small":
+                assert {x[4] for x in res.steps} == {"S"}, key
+
+
 def test_cluster_mode_batch(chain_graphs, grid_kernel):
     """gk_bfs_batch on a sparse graph checks for hand-offs after each trial:
     every parent array valid and equal-depth to the single-source call."""
