@@ -58,7 +58,7 @@ constexpr int kSmRounds = 4;
 // every CTA (no cluster barrier, no DSMEM); <= kSmCap, so the new frontier
 // list always fits.
 constexpr int kSmRedE = GK_SM_REDE;
-static_assert(kSmRedE <= kSmCap, "a redundant level's new frontier must fit the list");
+static_assert(kSmRedE <= kSmCap && kSmRedE <= kSmMaxW, "a redundant level's new frontier must fit the lists");
 #ifndef GK_SM_BUW
 #define GK_SM_BUW 2  // slots x in-neighbours per round: 2 x 8 (kron16 +2% over 4 x 4; 16 x 1, 3 x 8 equal, 2 x 16 -1%)
 #endif
@@ -87,6 +87,7 @@ struct __align__(16) SmShared {
   uint4 red4[2][kSmWarps];        // per-warp partial sums, two alternating slots
   unsigned nlong;
   unsigned nwon;
+  unsigned nred;  // redundant level: vertices claimed so far (listed in front)
 };
 
 // Block-wide exclusive scan / sums of 32-bit values with ONE barrier: warp
@@ -316,6 +317,15 @@ __device__ __forceinline__ void sm_resync(SmShared& S, cg::cluster_group& cl, bo
 // per thread), S.pre[k] = total; returns the total.  Ends with a barrier.
 __device__ long long sm_prefix(SmShared& S, int k, int& rs) {
   __syncthreads();
+  if (k <= kSmBlock) {  // one entry per thread
+    const unsigned d = (int)threadIdx.x < k ? S.pre[threadIdx.x] : 0u;
+    unsigned tot;
+    const unsigned x = sm_exscan(d, &tot, S, rs);
+    if ((int)threadIdx.x < k) S.pre[threadIdx.x] = x;
+    if (threadIdx.x == 0) S.pre[k] = tot;
+    __syncthreads();
+    return tot;
+  }
   constexpr int kPer = kSmCap / kSmBlock;
   const int i0 = threadIdx.x * kPer;
   uint32_t d[kPer];
@@ -375,7 +385,10 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
     S.nxt[j] = 0u;
   }
   for (int j = t; j < 3 * kSmSlice; j += kSmBlock) (&S.slice[0][0])[j] = 0u;
-  if (t == 0) S.nwon = 0u;  // the first level's won list (later levels: reset by sm_gather)
+  if (t == 0) {
+    S.nwon = 0u;  // the first level's won list (later levels: reset by sm_gather)
+    S.nred = 0u;
+  }
   __syncthreads();
   if (t == 0) {
     S.vis[src >> 5] |= 1u << (src & 31u);
@@ -592,17 +605,22 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
           for (int q = 0; q < kSmTdW; q++) {
             if (!ok[q] || sm_bit(S.vis, w[q]) || sm_bit(S.nxt, w[q])) continue;
             const uint32_t bit = 1u << (w[q] & 31u), ww = w[q] >> 5;
-            if (!(atomicOr(&S.nxt[ww], bit) & bit) && (int)ww >= wlo && (int)ww < whi)
-              P.parent[w[q]] = (int32_t)u[q];  // bfs.hpp:77-84
+            if (!(atomicOr(&S.nxt[ww], bit) & bit)) {
+              if ((int)ww >= wlo && (int)ww < whi) P.parent[w[q]] = (int32_t)u[q];  // bfs.hpp:77-84
+              S.front[atomicAdd(&S.nred, 1u)] = w[q];  // the new frontier, listed (<= E <= kSmMaxW)
+            }
           }
         }
         __syncthreads();
+        SM_MARK('1');
         // the new frontier (every vertex claimed here was unvisited): its
         // list with offsets and degrees for the next level, the counters
-        const int kn = sm_list<false>(S, S.nxt, 0, W, rs);
+        const int kn = (int)S.nred;
+        SM_MARK('2');
         unsigned scl = 0;
         for (int i = t; i < kn; i += kSmBlock) {
-          const uint32_t v = S.ids[i];
+          const uint32_t v = S.front[i];
+          S.ids[i] = v;
           const int64_t o0 = offv(P, P.out_off, v), o1 = offv(P, P.out_off, v + 1);
           const uint32_t dg = (uint32_t)(o1 - o0);
           S.off[i] = (uint32_t)o0;
@@ -611,7 +629,9 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
           const int vw = (int)(v >> 5);
           if (P.want_depth && vw >= wlo && vw < whi) P.depth[v] = lvl + 1;
         }
-        scl = sm_sum3(scl, 0u, 0u, S, rs).x;
+        scl = sm_sum3(scl, 0u, 0u, S, rs).x;  // (every read of the list in front is done)
+        if (t == 0) S.nred = 0u;
+        SM_MARK('3');
         for (int j = 4 * t; j < W; j += 4 * kSmBlock) {
           const uint4 x = *reinterpret_cast<const uint4*>(&S.nxt[j]);
           uint4 v = *reinterpret_cast<const uint4*>(&S.vis[j]);
@@ -623,12 +643,18 @@ __global__ void __launch_bounds__(kSmBlock, 1) bfs_small(BfsParams P) {
           *reinterpret_cast<uint4*>(&S.front[j]) = x;
           *reinterpret_cast<uint4*>(&S.nxt[j]) = make_uint4(0u, 0u, 0u, 0u);
         }
-        sm_prefix(S, kn, rs);
+        SM_MARK('4');
+        const long long e_next = sm_prefix(S, kn, rs);
+        SM_MARK('5');
         L++;
         const long long fsize = fsz;
         fsz = kn;
         scout = scl;
-        have_list = true;
+        // the list is in this CTA's claim order: good for a redundant level
+        // (every CTA expands all of it); a cluster-wide level splits the
+        // edges by position, which needs the same order everywhere -- it
+        // lists the front bitmap instead
+        have_list = e_next <= kSmRedE;
         synced = false;
         sm_log(P, c, nsteps++, 'T', fsize, scout, etc);
         lvl++;
