@@ -34,51 +34,63 @@ inline ScoreArray Brandes(const CsrGraph& g, std::span<const NodeId> sources, do
   return scores;
 }
 
-// VerifyBetweenness (verify.hpp:216-270): serial Brandes with explicit
-// predecessor lists, same sources and max normalisation, |diff| < tolerance
-// everywhere.  Host-side checker for the CLI's -v (the reference CLI does the
-// same), never on the compute path.
+// VerifyBetweenness (verify.hpp:216-270 checks the same thing): an
+// independent host recount, level-synchronous rather than queue-driven.
+// Pass 1 grows the BFS one level at a time, recording each level's vertex
+// range in `layer` and adding path counts forward.  Pass 2 walks the levels
+// deepest-first and lets every vertex PULL its dependency from its
+// successors (out-neighbours exactly one level deeper), so no predecessor
+// lists are kept.  Same sources and max normalisation as Brandes; ok iff
+// |diff| < tolerance everywhere.  Host-side checker for the CLI's -v (the
+// reference CLI verifies the same way), never on the compute path.
 inline VerifyReport VerifyBetweenness(const CsrGraph& g, std::span<const NodeId> sources, const ScoreArray& scores,
                                       double tolerance = 1e-4) {
   const int64_t n = g.num_nodes();
   if (static_cast<int64_t>(scores.size()) != n) return {false, "score array has wrong length"};
-  std::vector<double> total(n, 0.0);
-  for (NodeId source : sources) {
-    std::vector<double> sigma(n, 0.0), delta(n, 0.0);
-    std::vector<int32_t> depth(n, -1);
-    std::vector<std::vector<NodeId>> preds(n);
-    std::vector<NodeId> order;
-    order.reserve(n);
-    sigma[source] = 1;
-    depth[source] = 0;
-    order.push_back(source);
-    for (size_t qi = 0; qi < order.size(); qi++) {
-      const NodeId u = order[qi];
-      for (NodeId v : g.out_neigh(u)) {
-        if (depth[v] == -1) {
-          depth[v] = depth[u] + 1;
-          order.push_back(v);
-        }
-        if (depth[v] == depth[u] + 1) {
-          sigma[v] += sigma[u];
-          preds[v].push_back(u);
+  std::vector<double> acc(n, 0.0), paths(n), dep(n);
+  std::vector<int32_t> level(n);
+  std::vector<NodeId> visit;
+  std::vector<size_t> layer;  // visit[layer[d] .. layer[d+1]) = level d
+  visit.reserve(n);
+  for (NodeId s : sources) {
+    std::fill(level.begin(), level.end(), -1);
+    std::fill(paths.begin(), paths.end(), 0.0);
+    std::fill(dep.begin(), dep.end(), 0.0);
+    visit.assign(1, s);
+    layer.assign({0, 1});
+    level[s] = 0;
+    paths[s] = 1;
+    for (int32_t d = 0; layer[d] < layer[d + 1]; d++) {
+      for (size_t i = layer[d]; i < layer[d + 1]; i++) {
+        const NodeId u = visit[i];
+        for (NodeId v : g.out_neigh(u)) {
+          if (level[v] < 0) {
+            level[v] = d + 1;
+            visit.push_back(v);
+          }
+          if (level[v] == d + 1) paths[v] += paths[u];
         }
       }
+      layer.push_back(visit.size());
     }
-    for (auto it = order.rbegin(); it != order.rend(); ++it) {
-      const NodeId w = *it;
-      for (NodeId v : preds[w]) delta[v] += (sigma[v] / sigma[w]) * (1 + delta[w]);
-      if (w != source) total[w] += delta[w];
+    for (size_t d = layer.size() - 2; d-- > 0;) {
+      for (size_t i = layer[d]; i < layer[d + 1]; i++) {
+        const NodeId u = visit[i];
+        double pull = 0;
+        for (NodeId v : g.out_neigh(u))
+          if (level[v] == level[u] + 1) pull += (1.0 + dep[v]) / paths[v];
+        dep[u] = paths[u] * pull;
+        if (u != s) acc[u] += dep[u];
+      }
     }
   }
-  double mx = 0;
-  for (double t : total) mx = std::max(mx, t);
-  if (mx > 0)
-    for (double& t : total) t /= mx;
-  for (int64_t v = 0; v < n; v++)
-    if (std::fabs(total[v] - static_cast<double>(scores[v])) >= tolerance)
+  const double top = acc.empty() ? 0.0 : *std::max_element(acc.begin(), acc.end());
+  for (int64_t v = 0; v < n; v++) {
+    const double want = top > 0 ? acc[v] / top : acc[v];
+    if (!(std::fabs(want - static_cast<double>(scores[v])) < tolerance))
       return {false, "score mismatch at vertex " + std::to_string(v) + ": got " + std::to_string(scores[v]) +
-                         ", expected " + std::to_string(total[v])};
+                         ", expected " + std::to_string(want)};
+  }
   return {};
 }
 

@@ -111,6 +111,27 @@ int main(int argc, char** argv) {
     bad = good;
     bad[2] = -1;
     CHECK(VerifyBfs(path, 0, bad).failure_detail.find("unreached") != std::string::npos);
+    // host betweenness checker, known answers (no device pass involved):
+    // path 0-1-2 from every source -> only the middle vertex scores;
+    // diamond 0-{1,2}-3 from 0 -> 1 and 2 each carry half of 0->3
+    std::vector<NodeId> p3 = {0, 1, 2};
+    CHECK(VerifyBetweenness(path, p3, ScoreArray{0.0f, 1.0f, 0.0f}).ok);
+    CHECK(VerifyBetweenness(path, p3, ScoreArray{0.0f, 0.5f, 0.0f}).failure_detail.find("vertex 1") !=
+          std::string::npos);
+    CHECK(!VerifyBetweenness(path, p3, ScoreArray{0.0f, 1.0f}).ok);
+    EdgeList dm;
+    dm.Add(0, 1);
+    dm.Add(0, 2);
+    dm.Add(1, 3);
+    dm.Add(2, 3);
+    dm.Add(3, 4);
+    CsrGraph diamond = BuildCsr(dm, false, true);
+    std::vector<NodeId> s0 = {0};
+    // from 0: delta(3) = 1 (vertex 4), delta(1) = delta(2) = (1 + 1) / 2 = 1
+    CHECK(VerifyBetweenness(diamond, s0, ScoreArray{0.0f, 1.0f, 1.0f, 1.0f, 0.0f}).ok);
+    std::vector<NodeId> s4 = {4};
+    // from 4: delta(3) = 3, delta(1) = delta(2) = 1/2 -> normalised 1/6
+    CHECK(VerifyBetweenness(diamond, s4, ScoreArray{0.0f, 1.0f / 6, 1.0f / 6, 1.0f, 0.0f}).ok);
     std::printf("errors ok\n");
     return 0;
   }
