@@ -222,7 +222,12 @@ class DeviceGraph:
 
         pa, pp = outbuf(parent)
         da, dp = outbuf(depth)
-        steps = (Step * max_steps)()
+        # the step log is read into `sl` before returning, so one buffer per
+        # handle serves every call (a fresh 1.5 MB ctypes array per call cost
+        # ~0.1 ms of host time on small graphs)
+        steps = self.__dict__.get("_steps_buf")
+        if steps is None or len(steps) < max_steps:
+            steps = self._steps_buf = (Step * max_steps)()
         st = BfsStats(C.cast(steps, C.POINTER(Step)), max_steps, 1 if counts else 0, 0.0, 0, -1, -1)
         _check(L.gk_bfs(self._h, int(source), int(alpha), int(beta), int(strategy), pp, dp, C.byref(st)),
                "gk_bfs")

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -84,6 +85,8 @@ void free_graph(gk_graph* g) {
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->stream) cudaStreamDestroy(g->stream);
   if (g->cstream) cudaStreamDestroy(g->cstream);
+  if (g->stage) cudaFreeHost(g->stage);
+  for (cudaEvent_t e : g->stage_ev) cudaEventDestroy(e);
   if (g->cstream2) cudaStreamDestroy(g->cstream2);
   if (g->cs2_done) cudaEventDestroy(g->cs2_done);
   delete g;
@@ -701,6 +704,67 @@ gk_status gk_bfs_keep_depth(gk_graph* g, int32_t keep) {
   return GK_OK;
 }
 
+// A result copied into caller memory.  Pinned destinations (and small
+// copies) take one cudaMemcpyAsync.  Pageable ones would go through the
+// driver's own staging at ~16 GB/s on the GPU box (tools/bench_mem/
+// hostcopy.cu); instead the array moves in 16 MiB chunks into a pinned
+// stage kept with the graph (~55 GB/s), and host threads copy each chunk out
+// as soon as its event fires, overlapping the next chunks' transfers.
+// Synchronous: the data is in `dst` on return.
+static cudaError_t copy_out(gk_graph* g, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  static const bool no_stage = getenv("GK_NO_STAGE") != nullptr;  // A/B switch
+  constexpr size_t kChunk = size_t(16) << 20;
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type != cudaMemoryTypeUnregistered;
+  cudaGetLastError();  // older drivers flag unregistered pointers
+  cudaError_t e;
+  if (pinned || no_stage || bytes < 2 * kChunk) {
+    if ((e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s))) return e;
+    return cudaStreamSynchronize(s);
+  }
+  if (g->stage_bytes < bytes) {
+    if (g->stage) cudaFreeHost(g->stage);
+    g->stage = nullptr;
+    g->stage_bytes = 0;
+    if ((e = cudaHostAlloc(&g->stage, bytes, cudaHostAllocDefault))) return e;
+    g->stage_bytes = bytes;
+  }
+  const size_t chunks = (bytes + kChunk - 1) / kChunk;
+  while (g->stage_ev.size() < chunks) {
+    cudaEvent_t ev;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming))) return e;
+    g->stage_ev.push_back(ev);
+  }
+  for (size_t k = 0; k < chunks; k++) {
+    const size_t a = k * kChunk, len = std::min(kChunk, bytes - a);
+    if ((e = cudaMemcpyAsync(g->stage + a, static_cast<const char*>(src) + a, len, cudaMemcpyDeviceToHost, s)))
+      return e;
+    if ((e = cudaEventRecord(g->stage_ev[k], s))) return e;
+  }
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int nt = (int)std::max(1u, std::min(16u, hw ? hw : 1u));
+  std::vector<cudaError_t> errs(nt, cudaSuccess);
+  auto work = [&](int t) {
+    cudaSetDevice(g->device);
+    for (size_t k = 0; k < chunks; k++) {
+      if (cudaError_t ee = cudaEventSynchronize(g->stage_ev[k])) {
+        errs[t] = ee;
+        return;
+      }
+      const size_t a = k * kChunk, len = std::min(kChunk, bytes - a);
+      const size_t lo = a + len * t / nt, hi = a + len * (t + 1) / nt;
+      memcpy(static_cast<char*>(dst) + lo, g->stage + lo, hi - lo);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; t++) pool.emplace_back(work, t);
+  work(0);
+  for (auto& th : pool) th.join();
+  for (cudaError_t ee : errs)
+    if (ee) return ee;
+  return cudaSuccess;
+}
+
 gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int32_t strategy,
                  int32_t* parent_out, int32_t* depth_out, gk_bfs_stats* stats) {
   NvtxRange nvtx_range("gk_bfs");
@@ -805,10 +869,8 @@ gk_status gk_bfs(gk_graph* g, uint32_t source, int64_t alpha, int64_t beta, int3
     }
   }
   if (tb.book) CK(cudaFreeAsync(tb.book, s), "free trial bookkeeping");
-  if (parent_out && g->n)
-    CK(cudaMemcpyAsync(parent_out, g->parent, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, s), "D2H parent");
-  if (depth_out && g->n)
-    CK(cudaMemcpyAsync(depth_out, g->depth, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, s), "D2H depth");
+  if (parent_out && g->n) CK(copy_out(g, parent_out, g->parent, sizeof(int32_t) * g->n, s), "D2H parent");
+  if (depth_out && g->n) CK(copy_out(g, depth_out, g->depth, sizeof(int32_t) * g->n, s), "D2H depth");
   CK(cudaStreamSynchronize(s), "D2H");
   return st;
 }
@@ -1095,7 +1157,7 @@ gk_status gk_brandes(gk_graph* g, const uint32_t* sources, int64_t num_sources, 
   if (!e && st == GK_OK) e = gk::bc_normalize(p.bc_scores, n, p.bc_scores + n, s);
   if (!e && st == GK_OK) e = cudaEventRecord(g->ev1, s);
   if (!e && st == GK_OK && scores_out)
-    e = cudaMemcpyAsync(scores_out, p.bc_scores, sizeof(float) * n, cudaMemcpyDeviceToHost, s);
+    e = copy_out(g, scores_out, p.bc_scores, sizeof(float) * n, s);
   cudaFreeAsync(w, s);
   const cudaError_t es = cudaStreamSynchronize(s);
   if (!e) e = es;

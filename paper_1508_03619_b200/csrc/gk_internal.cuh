@@ -354,6 +354,10 @@ struct gk_graph {
   cudaStream_t cstream = nullptr;  // D2H stream of gk_bfs_batch (created on first use)
   cudaStream_t cstream2 = nullptr;  // second D2H stream (GK_BATCH_SPLIT)
   cudaEvent_t cs2_done = nullptr;
+  // pinned staging for copies into pageable host memory (gk_capi.cu copy_out)
+  char* stage = nullptr;
+  size_t stage_bytes = 0;
+  std::vector<cudaEvent_t> stage_ev;
   int* batch_err = nullptr;        // pinned: per-trial kernel error codes of gk_bfs_batch
   bool batch_warm = false;         // the pool holds three trials' blocks (gk_bfs_batch)
   int32_t batch_err_cap = 0;

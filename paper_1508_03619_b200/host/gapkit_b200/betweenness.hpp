@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "gk_bfs.h"
+#include "gapkit_b200/fresh_vector.hpp"
 #include "gapkit_b200/graph.hpp"
 #include "gapkit_b200/harness.hpp"
 #include "gapkit_b200/types.hpp"
@@ -27,7 +28,7 @@ namespace gapkit {
 
 inline ScoreArray Brandes(const CsrGraph& g, std::span<const NodeId> sources, double* device_ms = nullptr) {
   if (sources.empty()) throw ConfigError("betweenness requires at least one source");
-  ScoreArray scores(g.num_nodes());
+  ScoreArray scores = gk_host::FreshVector<Score>(static_cast<size_t>(g.num_nodes()));
   detail::CheckStatus(gk_brandes(g.device(), sources.data(), static_cast<int64_t>(sources.size()),
                                  scores.data(), device_ms),
                       "gk_brandes");

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "gk_bfs.h"
+#include "gapkit_b200/fresh_vector.hpp"
 #include "gapkit_b200/graph.hpp"
 #include "gapkit_b200/types.hpp"
 
@@ -44,7 +45,7 @@ inline ParentArray Bfs(const CsrGraph& g, NodeId source, const BfsOptions& opts 
   if (static_cast<int64_t>(source) >= g.num_nodes()) throw ConfigError("bfs source out of range");
   if (opts.alpha <= 0 || opts.beta <= 0) throw ConfigError("bfs alpha and beta must be positive");
   gk_graph* dev = g.device();
-  ParentArray parent(g.num_nodes());
+  ParentArray parent = gk_host::FreshVector<ParentEntry>(static_cast<size_t>(g.num_nodes()));
   gk_bfs_stats st{};
   std::vector<gk_step> steps;
   if (telemetry) {

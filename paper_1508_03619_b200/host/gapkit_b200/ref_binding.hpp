@@ -44,6 +44,7 @@
 #include <vector>
 
 #include "gk_bfs.h"
+#include "gapkit_b200/fresh_vector.hpp"
 
 namespace gapkit::b200 {
 
@@ -134,7 +135,7 @@ inline ParentArray Bfs(const CsrGraph& g, NodeId source, const BfsOptions& opts 
   if (static_cast<int64_t>(source) >= g.num_nodes()) throw ConfigError("bfs source out of range");
   if (opts.alpha <= 0 || opts.beta <= 0) throw ConfigError("bfs alpha and beta must be positive");
   std::shared_ptr<detail::Handle> h = detail::DeviceGraph(g);
-  ParentArray parent(static_cast<size_t>(g.num_nodes()));
+  ParentArray parent = gk_host::FreshVector<ParentEntry>(static_cast<size_t>(g.num_nodes()));
   const gk_status st = gk_bfs(h->g, source, opts.alpha, opts.beta, static_cast<int32_t>(opts.strategy),
                               parent.data(), nullptr, nullptr);
   if (st != GK_OK) detail::Throw(st);
@@ -144,7 +145,7 @@ inline ParentArray Bfs(const CsrGraph& g, NodeId source, const BfsOptions& opts 
 // Drop-in for gapkit::Brandes (kernels/betweenness.hpp:84-145).
 inline ScoreArray Brandes(const CsrGraph& g, std::span<const NodeId> sources) {
   std::shared_ptr<detail::Handle> h = detail::DeviceGraph(g);
-  ScoreArray scores(static_cast<size_t>(g.num_nodes()));
+  ScoreArray scores = gk_host::FreshVector<Score>(static_cast<size_t>(g.num_nodes()));
   const gk_status st = gk_brandes(h->g, sources.data(), static_cast<int64_t>(sources.size()), scores.data(),
                                   nullptr);
   if (st != GK_OK) detail::Throw(st);
