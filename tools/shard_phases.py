@@ -43,3 +43,14 @@ for s in srcs:
     tot += agg(grp.trace())
     sch.append(r.schedule)
 show("sharded P=1", tot, len(srcs), sch[:3])
+
+if len(sys.argv) > 2:  # one source's phase sequence, both kernels
+    s = srcs[0]
+    r = grp.run(s, parent=False)
+    tr = grp.trace()
+    print("sharded seq:", " ".join(f"{t}{(b - a) * 1e3:.0f}" for (_, a), (t, b) in zip(tr, tr[1:])))
+    del grp
+    g, _ = bench.build_graph(cfg, 0)
+    g.bfs(s, parent=False)
+    tr = g.trace()
+    print("single  seq:", " ".join(f"{t}{(b - a) * 1e3:.0f}" for (_, a), (t, b) in zip(tr, tr[1:])))
