@@ -551,6 +551,7 @@ def main():
     g.bfs_batch(sources, [pins[i & 1].array for i in range(len(sources))])
     batch_s = time.perf_counter() - t0
     e2e_s = [batch_s / len(sources)] * len(sources)
+    d2h_total, d2h_packed = g.batch_d2h_bytes()
     single_s = []
     for s in sources[: min(8, len(sources))]:
         t0 = time.perf_counter()
@@ -627,10 +628,14 @@ def main():
                 "schedules": scheds[:4], "mean_m_cc": statistics.mean(step_m),
                 "verified": (f"{verified}/{len(sources)} sources pass the device BFS certificate "
                              "(depths exact, parents valid)") if not args.no_model else "not run"},
-        "e2e": {"value": e2e_val, "unit": "GTEPS", "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 4 * g.n,
+        "e2e": {"value": e2e_val, "unit": "GTEPS", "h2d_bytes_per_step": 4,
+                "d2h_bytes_per_step": d2h_total / len(sources),
+                "result_bytes_per_step": 4 * g.n, "compact_sources": d2h_packed,
                 "one_call_per_source": hmean([m_of[s] / t / 1e9 for s, t in zip(sources, single_s)]),
                 "note": "gk_bfs_batch over the K sources, every source's parent array copied to pinned host "
                         "memory inside the timed region (copy of result i overlaps traversal i+1); "
+                        "compact_sources of them travel as reached bitmap + packed parents and are "
+                        "expanded into the full ParentArray by host threads inside the timed region; "
                         "one_call_per_source = gk_bfs per source without overlap (first 8 sources); graph "
                         "resident (uploaded once, untimed, as the reference harness builds it untimed); "
                         "the per-step input is the 4-byte source id (a kernel argument)",

@@ -163,6 +163,14 @@ GK_API gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t coun
                               int64_t beta, int32_t strategy, int32_t* const* parents_out,
                               float* device_ms);
 
+/* Device->host result bytes the last gk_bfs_batch on this handle moved:
+ * from 2^22 vertices each ParentArray travels compact (per 1024-vertex block
+ * a reached count prefix, the reached bitmap, the reached vertices' parents)
+ * and is expanded into the caller's array on host threads; a source whose
+ * reached set leaves nothing to save travels raw (n int32).  *packed (may be
+ * NULL) = sources sent compact.  GK_BATCH_PACK=0 turns the compact form off. */
+GK_API int64_t gk_bfs_batch_d2h_bytes(const gk_graph* g, int64_t* packed);
+
 /* Device pointer to the parent array of the last gk_bfs on this handle
  * (valid until the next call / free). */
 GK_API const int32_t* gk_bfs_device_parent(const gk_graph* g);

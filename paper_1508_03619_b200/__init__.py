@@ -304,6 +304,13 @@ class DeviceGraph:
                                         ptrs, ms.ctypes.data), "gk_bfs_batch")
         return ms[:k]
 
+    def batch_d2h_bytes(self) -> tuple[int, int]:
+        """(device->host result bytes, sources sent compact) of the last
+        bfs_batch (gk_bfs_batch_d2h_bytes)."""
+        packed = C.c_int64(0)
+        total = int(_lib.load().gk_bfs_batch_d2h_bytes(self._h, C.byref(packed)))
+        return total, int(packed.value)
+
     def brandes(self, sources) -> tuple[np.ndarray, float]:
         """Betweenness scores over `sources` (gk_brandes) and the device ms."""
         src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64))

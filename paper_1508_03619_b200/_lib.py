@@ -34,7 +34,7 @@ EXPORTED = (
     "gk_shard_set_stream", "gk_shard_launches", "gk_shard_join_local", "gk_shard_handle_size",
     "gk_shard_export", "gk_shard_connect", "gk_shard_gather_dead", "gk_shard_group_bfs", "gk_shard_bfs",
     "gk_shard_bytes_in", "gk_shard_download", "gk_shard_trace", "gk_bfs_verify", "gk_graph_load_sg", "gk_graph_save_sg", "gk_brandes",
-    "gk_bfs_batch", "gk_bfs_launches",
+    "gk_bfs_batch", "gk_bfs_launches", "gk_bfs_batch_d2h_bytes",
 )
 
 
@@ -113,6 +113,8 @@ def load() -> C.CDLL:
     L.gk_bfs_batch.argtypes = [vp, vp, i32, i64, i64, i32, vp, vp]
     L.gk_bfs_launches.argtypes = [vp]
     L.gk_bfs_launches.restype = i64
+    L.gk_bfs_batch_d2h_bytes.argtypes = [vp, C.POINTER(i64)]
+    L.gk_bfs_batch_d2h_bytes.restype = i64
     L.gk_shard_last_error.restype = C.c_char_p
     L.gk_shard_generate.argtypes = [C.c_int, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(vp)]
@@ -140,7 +142,8 @@ def load() -> C.CDLL:
     for f in EXPORTED:
         if f not in ("gk_last_error", "gk_abi_version", "gk_device_count", "gk_graph_free",
                      "gk_bfs_device_parent", "gk_bfs_device_depth", "gk_host_alloc", "gk_host_free", "gk_shard_last_error",
-                     "gk_shard_free", "gk_shard_launches", "gk_shard_handle_size", "gk_bfs_launches"):
+                     "gk_shard_free", "gk_shard_launches", "gk_shard_handle_size", "gk_bfs_launches",
+                     "gk_bfs_batch_d2h_bytes"):
             getattr(L, f).restype = C.c_int
     _lib = L
     return L

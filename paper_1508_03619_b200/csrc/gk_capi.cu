@@ -79,6 +79,15 @@ void free_graph(gk_graph* g) {
   if (g->batch_err) cudaFreeHost(g->batch_err);
   if (g->cm_peek) cudaFreeHost(g->cm_peek);
   for (cudaEvent_t e : g->batch_ev) cudaEventDestroy(e);
+  for (int k = 0; k < 2; k++) {
+    if (g->pk_dev[k]) cudaFree(g->pk_dev[k]);
+    if (g->pk_host[k]) cudaFreeHost(g->pk_host[k]);
+    if (g->pk_sc[k]) cudaEventDestroy(g->pk_sc[k]);
+    if (g->pk_cp[k]) cudaEventDestroy(g->pk_cp[k]);
+  }
+  if (g->pk_cnt) cudaFree(g->pk_cnt);
+  if (g->pk_total) cudaFreeHost(g->pk_total);
+  if (g->pk_ev) cudaEventDestroy(g->pk_ev);
   if (g->sg_exec) cudaGraphExecDestroy(g->sg_exec);
   if (g->sg_graph) cudaGraphDestroy(g->sg_graph);
   if (g->ev0) cudaEventDestroy(g->ev0);
@@ -923,6 +932,41 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
   }
   const bool small = use_small(g);
   const bool own = !small && use_own(g);
+  // Compact transfer of the results (gk_pack.cu) on graphs from 2^22
+  // vertices; a source whose reached set makes it no smaller goes raw.
+  static const char* pk_env = getenv("GK_BATCH_PACK");
+  const bool pack = parents_out && g->n >= (int64_t(1) << 22) && !(pk_env && atoi(pk_env) == 0) && !split;
+  const int64_t nblk = (g->n + 1023) / 1024;
+  const size_t pk_bytes = sizeof(uint32_t) * gk::pack_words(g->n);
+  if (pack && !g->pk_dev[0]) {
+    for (int k = 0; k < 2; k++) {
+      CK(cudaMalloc(&g->pk_dev[k], pk_bytes), "alloc transfer buffer");
+      CK(cudaHostAlloc(&g->pk_host[k], pk_bytes, cudaHostAllocDefault), "cudaHostAlloc transfer stage");
+      CK(cudaEventCreateWithFlags(&g->pk_sc[k], cudaEventDisableTiming), "event");
+      CK(cudaEventCreateWithFlags(&g->pk_cp[k], cudaEventDisableTiming), "event");
+    }
+    CK(cudaMalloc(&g->pk_cnt, sizeof(uint32_t) * (nblk + 1)), "alloc block counts");
+    CK(cudaHostAlloc(&g->pk_total, sizeof(uint32_t) * 2, cudaHostAllocDefault), "cudaHostAlloc");
+    CK(cudaEventCreateWithFlags(&g->pk_ev, cudaEventDisableTiming | cudaEventBlockingSync), "event");
+  }
+  // GK_PACK_RAW_FRAC (A/B, default 0): blocks [0, raw_blk) travel raw
+  // straight into the caller's array after the compact rest.  Measured on
+  // kron27 (profiles/r02/e2e_compact_kron27.txt): raw shares 0 / 0.15 / 0.25
+  // / 0.35 give 245 / 236 / 227 / 213 GTEPS -- the DMA writes and the host
+  // expansion share the host's memory bandwidth, and DMA bytes cost more.
+  static const double raw_frac = getenv("GK_PACK_RAW_FRAC") ? atof(getenv("GK_PACK_RAW_FRAC")) : 0.0;
+  const int64_t raw_blk = std::min<int64_t>(nblk - 1, std::max<int64_t>(0, (int64_t)(raw_frac * nblk)));
+  static const int exp_threads = getenv("GK_EXPAND_THREADS") ? atoi(getenv("GK_EXPAND_THREADS"))
+                                                              : (int)std::thread::hardware_concurrency() - 1;
+  std::thread expander[2];  // host expansion of source i runs in expander[i & 1]
+  int exp_err[2] = {0, 0};
+  int32_t* exp_dst[2] = {nullptr, nullptr};
+  auto settle = [&](const int32_t* dst) {  // outputs may repeat: one writer per array at a time
+    for (int k = 0; k < 2; k++)
+      if (expander[k].joinable() && exp_dst[k] == dst) expander[k].join();
+  };
+  g->last_d2h_bytes = 0;
+  g->last_packed = 0;
   cudaError_t e = cudaSuccess;
   if (!g->batch_warm && count > 1) {
     // Up to three trials' blocks are live at once here (a result is freed
@@ -970,8 +1014,47 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     if ((e = cudaEventRecord(ev[3 * i + 1], s))) break;
     if ((e = cudaMemcpyAsync(errs + i, &t.ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;
     if (tb.book && (e = cudaFreeAsync(tb.book, s))) break;
+    bool packed = false;
+    if (pack && parents_out[i]) {
+      // the transfer buffer i & 1 is free: trial i waited for the copy of i - 2
+      const int k = i & 1;
+      if ((e = gk::pack_count(t.parent, g->n, g->pk_dev[k], g->pk_cnt, s))) break;
+      if ((e = cudaMemcpyAsync(g->pk_total, g->pk_dev[k] + nblk, sizeof(uint32_t), cudaMemcpyDeviceToHost, s))) break;
+      if ((e = cudaMemcpyAsync(g->pk_total + 1, g->pk_dev[k] + raw_blk, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)))
+        break;
+      if ((e = cudaEventRecord(g->pk_ev, s))) break;
+      if ((e = cudaEventSynchronize(g->pk_ev))) break;  // trial i is done and its reached count known
+      const size_t words = gk::pack_words(g->n) - (size_t)g->n + *g->pk_total;
+      if (words < (size_t)g->n) {
+        packed = true;
+        if ((e = gk::pack_scatter(t.parent, g->n, g->pk_dev[k], s))) break;
+        if ((e = cudaEventRecord(g->pk_sc[k], s))) break;
+        if (expander[k].joinable()) expander[k].join();  // stage k: source i - 2 expanded
+        if (exp_err[k]) break;
+        if ((e = cudaStreamWaitEvent(cs, g->pk_sc[k], 0))) break;
+        // offsets + bitmap, then the compact part's packed parents (same
+        // offsets in the stage), then the raw head into the caller's array
+        const size_t head = (size_t)(nblk + 1 + 32 * nblk), skip = g->pk_total[1];
+        if ((e = cudaMemcpyAsync(g->pk_host[k], g->pk_dev[k], sizeof(uint32_t) * head, cudaMemcpyDeviceToHost, cs)))
+          break;
+        if (words > head + skip &&
+            (e = cudaMemcpyAsync(g->pk_host[k] + head + skip, g->pk_dev[k] + head + skip,
+                                 sizeof(uint32_t) * (words - head - skip), cudaMemcpyDeviceToHost, cs)))
+          break;
+        if ((e = cudaEventRecord(g->pk_cp[k], cs))) break;
+        if (raw_blk > 0 && (e = cudaMemcpyAsync(parents_out[i], t.parent, sizeof(int32_t) * 1024 * raw_blk,
+                                                 cudaMemcpyDeviceToHost, cs)))
+          break;
+        g->last_d2h_bytes += (int64_t)(sizeof(uint32_t) * (words - skip) + sizeof(int32_t) * 1024 * raw_blk);
+        g->last_packed++;
+      }
+    }
     if ((e = cudaStreamWaitEvent(cs, ev[3 * i + 1], 0))) break;
-    if (parents_out && parents_out[i]) {
+    if (packed) {
+      // expanded by the host below, once this copy has landed
+    } else if (parents_out && parents_out[i]) {
+      settle(parents_out[i]);
+      g->last_d2h_bytes += (int64_t)(sizeof(int32_t) * g->n);
       // GK_BATCH_SPLIT: the two halves on two copy streams (two DMA engines)
       const size_t bytes = sizeof(int32_t) * g->n, half = split ? (bytes / 2 + 255) & ~size_t(255) : bytes;
       if ((e = cudaMemcpyAsync(parents_out[i], t.parent, half, cudaMemcpyDeviceToHost, cs))) break;
@@ -990,7 +1073,30 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
       g->parent = t.parent;  // the last result stays for gk_bfs_device_parent
     }
     if ((e = cudaEventRecord(ev[3 * i + 2], cs))) break;
+    if (packed) {
+      const int k = i & 1;
+      cudaEvent_t done = g->pk_cp[k];
+      const int64_t first = raw_blk;
+      int32_t* dst = parents_out[i];
+      const uint32_t* stage = g->pk_host[k];
+      const int64_t n = g->n;
+      const int dev = g->device;
+      int* err = &exp_err[k];
+      settle(dst);
+      exp_dst[k] = dst;
+      expander[k] = std::thread([=]() {
+        cudaSetDevice(dev);
+        if (cudaEventSynchronize(done) != cudaSuccess) {
+          *err = 1;
+          return;
+        }
+        gk::expand_parents(stage, n, dst, exp_threads, first);
+      });
+    }
   }
+  for (auto& th : expander)
+    if (th.joinable()) th.join();
+  if (e == cudaSuccess && (exp_err[0] || exp_err[1])) e = cudaErrorUnknown;
   if (g->cstream2) cudaStreamSynchronize(g->cstream2);
   cudaError_t e2 = cudaStreamSynchronize(s), e3 = cudaStreamSynchronize(cs);
   if (e == cudaSuccess) e = e2 != cudaSuccess ? e2 : e3;
@@ -1005,6 +1111,11 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     }
   }
   return GK_OK;
+}
+
+int64_t gk_bfs_batch_d2h_bytes(const gk_graph* g, int64_t* packed) {
+  if (packed) *packed = g ? g->last_packed : 0;
+  return g ? g->last_d2h_bytes : 0;
 }
 
 const int32_t* gk_bfs_device_parent(const gk_graph* g) { return g ? g->parent : nullptr; }

@@ -278,6 +278,14 @@ cudaError_t validate_csr(const int64_t* off, const uint32_t* nb, int64_t n, int6
 cudaError_t canary_count(const void* p, size_t len, unsigned char fill, unsigned long long* d_out, cudaStream_t s);
 cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
                           unsigned long long* d_out2, cudaStream_t s);
+// Compact ParentArray transfer (gk_pack.cu, gk_expand.cpp): words of the
+// transfer buffer, the count + scan pass (reached total lands in buf[nblk]),
+// the scatter of the reached parents, and the host expansion.
+size_t pack_words(int64_t n);
+cudaError_t pack_count(const int32_t* parent, int64_t n, uint32_t* buf, uint32_t* cnt, cudaStream_t s);
+cudaError_t pack_scatter(const int32_t* parent, int64_t n, uint32_t* buf, cudaStream_t s);
+void expand_parents(const uint32_t* buf, int64_t n, int32_t* dst, int threads, int64_t first_block);
+bool expand_uses_avx512();
 cudaError_t verify_bfs(const int64_t* off, const uint32_t* nb, const int32_t* parent, const int32_t* depth,
                        int64_t n, uint32_t src, long long* errs8, cudaStream_t s);
 cudaError_t byte_model(const BfsParams& p, const int32_t* depth, const char* dirs,
@@ -362,6 +370,18 @@ struct gk_graph {
   bool batch_warm = false;         // the pool holds three trials' blocks (gk_bfs_batch)
   int32_t batch_err_cap = 0;
   std::vector<cudaEvent_t> batch_ev;  // gk_bfs_batch's events, grown on demand
+  // gk_bfs_batch's compact ParentArray transfer (gk_pack.cu): two device
+  // transfer buffers and two pinned stages (source i uses i & 1), the block
+  // counts, the pinned reached total, count-ready / scatter-done events
+  uint32_t* pk_dev[2] = {nullptr, nullptr};
+  uint32_t* pk_host[2] = {nullptr, nullptr};
+  uint32_t* pk_cnt = nullptr;
+  uint32_t* pk_total = nullptr;
+  cudaEvent_t pk_ev = nullptr;
+  cudaEvent_t pk_sc[2] = {nullptr, nullptr};
+  cudaEvent_t pk_cp[2] = {nullptr, nullptr};  // compact part landed (the raw head may still be copying)
+  int64_t last_d2h_bytes = 0;  // device->host result bytes of the last gk_bfs_batch
+  int64_t last_packed = 0;     // sources of the last gk_bfs_batch sent compact
   cudaEvent_t ev0 = nullptr;
   cudaEvent_t ev1 = nullptr;
   gk::BfsLaunch launch;

@@ -134,6 +134,74 @@ def test_batch_matches_single_calls(both_kernels):
     assert dg.bfs_batch([]).size == 0
 
 
+def _device_parent(dg, n):
+    from cuda.bindings import runtime as rt
+    out = np.empty(n, np.int32)
+    err, = rt.cudaMemcpy(out.ctypes.data, dg.device_parent_ptr(), 4 * n, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+    assert int(err) == 0
+    return out
+
+
+def _sparse_upload(n, m, seed):
+    # mostly isolated vertices: a small reached set, so the result travels compact
+    rng = np.random.default_rng(seed)
+    e = rng.integers(0, n, size=2 * m, dtype=np.uint64).astype(np.uint32)
+    g = O.build_csr(n, e)
+    return g, DeviceGraph.from_csr(g)
+
+
+@pytest.mark.parametrize("n", [1 << 22, (1 << 22) + 77])
+def test_batch_compact_transfer(n):
+    # gk_bfs_batch from 2^22 vertices ships each ParentArray compact (reached
+    # bitmap + packed parents) and expands it on the host: every output must
+    # equal the device result bit for bit, ragged last block included, and
+    # the bytes moved must be the compact size
+    from paper_1508_03619_b200 import PinnedBuffer
+    g, dg = _sparse_upload(n, n, n)
+    srcs = [int(s) for s in O.pick_sources(g, 5)]
+    nblk = (n + 1023) // 1024
+    for s in srcs:
+        out = np.full(n, 7, np.int32)
+        dg.bfs_batch([s], [out])
+        ref = _device_parent(dg, n)
+        assert (out == ref).all()
+        ok, msg = O.verify_bfs(g, s, out)
+        assert ok, msg
+        total, packed = dg.batch_d2h_bytes()
+        reached = int((ref >= 0).sum())
+        # compact part (offsets, bitmap, packed parents) + the raw head blocks
+        assert packed == 1 and 4 * (nblk + 1 + 32 * nblk) <= total <= 4 * (nblk + 1 + 32 * nblk + reached) + 4 * n // 4
+    # several sources, repeated pinned outputs (the bench's use) and pageable ones
+    pins = [PinnedBuffer(n), PinnedBuffer(n)]
+    dg.bfs_batch(srcs, [pins[i & 1].array for i in range(len(srcs))])
+    assert (pins[(len(srcs) - 1) & 1].array == _device_parent(dg, n)).all()
+    assert O.verify_bfs(g, srcs[-2], pins[(len(srcs) - 2) & 1].array)[0]
+    outs = [np.empty(n, np.int32) for _ in srcs]
+    dg.bfs_batch(srcs, outs)
+    for s, p in zip(srcs, outs):
+        ok, msg = O.verify_bfs(g, s, p)
+        assert ok, msg
+    assert dg.batch_d2h_bytes()[1] == len(srcs)
+    # every output the same array: the last source's result lands last
+    same = np.empty(n, np.int32)
+    dg.bfs_batch(srcs, [same] * len(srcs))
+    assert (same == _device_parent(dg, n)).all()
+
+
+def test_batch_raw_when_compact_is_larger():
+    # a source reaching (nearly) every vertex gains nothing from the compact
+    # form: it travels raw (n int32), GK_BATCH_PACK-independent results
+    g = O.make_graph("urand", 22)
+    dg = DeviceGraph.from_csr(g)
+    srcs = [int(s) for s in O.pick_sources(g, 2)]
+    outs = [np.empty(g.n, np.int32) for _ in srcs]
+    dg.bfs_batch(srcs, outs)
+    assert dg.batch_d2h_bytes() == (4 * g.n * len(srcs), 0)
+    for s, p in zip(srcs, outs):
+        ok, msg = O.verify_bfs(g, s, p)
+        assert ok, msg
+
+
 def test_malformed_csr_rejected():
     # every kernel indexes with off/nb: a malformed CSR is refused at creation
     from paper_1508_03619_b200 import GapkitError
