@@ -943,7 +943,7 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
       CK(cudaMalloc(&g->pk_dev[k], pk_bytes), "alloc transfer buffer");
       CK(cudaHostAlloc(&g->pk_host[k], pk_bytes, cudaHostAllocDefault), "cudaHostAlloc transfer stage");
       CK(cudaEventCreateWithFlags(&g->pk_sc[k], cudaEventDisableTiming), "event");
-      CK(cudaEventCreateWithFlags(&g->pk_cp[k], cudaEventDisableTiming), "event");
+      CK(cudaEventCreateWithFlags(&g->pk_cp[k], cudaEventDisableTiming | cudaEventBlockingSync), "event");
     }
     CK(cudaMalloc(&g->pk_cnt, sizeof(uint32_t) * (nblk + 1)), "alloc block counts");
     CK(cudaHostAlloc(&g->pk_total, sizeof(uint32_t) * 2, cudaHostAllocDefault), "cudaHostAlloc");
