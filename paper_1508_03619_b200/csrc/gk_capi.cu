@@ -1015,17 +1015,25 @@ gk_status gk_bfs_batch(gk_graph* g, const uint32_t* sources, int32_t count, int6
     if ((e = cudaMemcpyAsync(errs + i, &t.ctrl->error, sizeof(int), cudaMemcpyDeviceToHost, s))) break;
     if (tb.book && (e = cudaFreeAsync(tb.book, s))) break;
     bool packed = false;
-    if (pack && parents_out[i]) {
+    if (pack && parents_out[i] && !g->pk_raw) {
       // the transfer buffer i & 1 is free: trial i waited for the copy of i - 2
       const int k = i & 1;
-      if ((e = gk::pack_count(t.parent, g->n, g->pk_dev[k], g->pk_cnt, s))) break;
+      // (the scan kernel can also store these two words into mapped pinned
+      // memory, bypassing the copy engine: kron27 e2e fell to 54 GTEPS with
+      // it -- the copies stay)
+      if ((e = gk::pack_count(t.parent, g->n, g->pk_dev[k], g->pk_cnt, raw_blk, nullptr, s))) break;
       if ((e = cudaMemcpyAsync(g->pk_total, g->pk_dev[k] + nblk, sizeof(uint32_t), cudaMemcpyDeviceToHost, s))) break;
       if ((e = cudaMemcpyAsync(g->pk_total + 1, g->pk_dev[k] + raw_blk, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)))
         break;
       if ((e = cudaEventRecord(g->pk_ev, s))) break;
       if ((e = cudaEventSynchronize(g->pk_ev))) break;  // trial i is done and its reached count known
       const size_t words = gk::pack_words(g->n) - (size_t)g->n + *g->pk_total;
-      if (words < (size_t)g->n) {
+      if (words >= (size_t)g->n) {
+        // this graph's sources reach (nearly) everything: its later results
+        // go raw without the count pass and its host round trip (urand27:
+        // 62 GTEPS e2e with a count per source, 159 without)
+        g->pk_raw = true;
+      } else {
         packed = true;
         if ((e = gk::pack_scatter(t.parent, g->n, g->pk_dev[k], s))) break;
         if ((e = cudaEventRecord(g->pk_sc[k], s))) break;

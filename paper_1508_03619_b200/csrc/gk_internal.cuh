@@ -282,7 +282,9 @@ cudaError_t count_reached(const int32_t* parent, const int64_t* off, int64_t n,
 // transfer buffer, the count + scan pass (reached total lands in buf[nblk]),
 // the scatter of the reached parents, and the host expansion.
 size_t pack_words(int64_t n);
-cudaError_t pack_count(const int32_t* parent, int64_t n, uint32_t* buf, uint32_t* cnt, cudaStream_t s);
+// host_out (mapped pinned, may be NULL): receives {reached total, off[probe]}.
+cudaError_t pack_count(const int32_t* parent, int64_t n, uint32_t* buf, uint32_t* cnt, int64_t probe,
+                       uint32_t* host_out, cudaStream_t s);
 cudaError_t pack_scatter(const int32_t* parent, int64_t n, uint32_t* buf, cudaStream_t s);
 void expand_parents(const uint32_t* buf, int64_t n, int32_t* dst, int threads, int64_t first_block);
 bool expand_uses_avx512();
@@ -382,6 +384,7 @@ struct gk_graph {
   cudaEvent_t pk_cp[2] = {nullptr, nullptr};  // compact part landed (the raw head may still be copying)
   int64_t last_d2h_bytes = 0;  // device->host result bytes of the last gk_bfs_batch
   int64_t last_packed = 0;     // sources of the last gk_bfs_batch sent compact
+  bool pk_raw = false;         // a result of this graph gained nothing compact: later ones go raw
   cudaEvent_t ev0 = nullptr;
   cudaEvent_t ev1 = nullptr;
   gk::BfsLaunch launch;

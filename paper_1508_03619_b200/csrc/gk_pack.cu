@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(kPkThreads) k_pack_count(const int32_t* __rest
 // Exclusive prefix of the block counts (nblk <= 2^21): each thread sums a
 // contiguous run, one block-wide scan, then writes its run's offsets.
 __global__ void __launch_bounds__(kScanThreads) k_pack_scan(const uint32_t* __restrict__ cnt, int64_t nblk,
-                                                            uint32_t* __restrict__ off) {
+                                                            uint32_t* __restrict__ off, int64_t probe,
+                                                            volatile uint32_t* host_out) {
   typedef cub::BlockScan<uint32_t, kScanThreads> Scan;
   __shared__ typename Scan::TempStorage tmp;
   const int64_t per = (nblk + kScanThreads - 1) / kScanThreads;
@@ -71,6 +72,15 @@ __global__ void __launch_bounds__(kScanThreads) k_pack_scan(const uint32_t* __re
     ex += cnt[i];
   }
   if (threadIdx.x == 0) off[nblk] = total;
+  if (host_out) {  // mapped pinned memory: the total and off[probe] reach the host without a copy-engine slot
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      host_out[0] = total;
+      host_out[1] = off[probe];
+      __threadfence_system();
+    }
+  }
 }
 
 // Same walk as k_pack_count: lane l of word k stores its parent at
@@ -117,11 +127,12 @@ size_t pack_words(int64_t n) {
   return (size_t)(nblk + 1 + 32 * nblk + n);
 }
 
-cudaError_t pack_count(const int32_t* parent, int64_t n, uint32_t* buf, uint32_t* cnt, cudaStream_t s) {
+cudaError_t pack_count(const int32_t* parent, int64_t n, uint32_t* buf, uint32_t* cnt, int64_t probe,
+                       uint32_t* host_out, cudaStream_t s) {
   const int64_t nblk = (n + 1023) / 1024;
-  if (nblk > (int64_t(1) << 21)) return cudaErrorInvalidValue;
+  if (nblk > (int64_t(1) << 21) || probe < 0 || probe > nblk) return cudaErrorInvalidValue;
   k_pack_count<<<pack_grid(nblk), kPkThreads, 0, s>>>(parent, n, nblk, buf + nblk + 1, cnt);
-  k_pack_scan<<<1, kScanThreads, 0, s>>>(cnt, nblk, buf);
+  k_pack_scan<<<1, kScanThreads, 0, s>>>(cnt, nblk, buf, probe, host_out);
   return cudaGetLastError();
 }
 
